@@ -1,0 +1,643 @@
+/*
+ * oracle/eq_oracle.cpp — CPU restatement of the EventQueues hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in paper_2512_05906_b200/ links, loads or
+ * calls this file; only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs do, and only as the checker.
+ *
+ * What it restates (file:line in /root/reference):
+ *   primal step ........ pkg/src/eventq/network.py:547-611 (PrimalRSNN.step),
+ *                        expression order copied term by term so that reference
+ *                        mode is bitwise identical to the Python reference
+ *   synapse ............ neuro.py:33-47 + jumps.py:116-126 + dual.py:72-84
+ *   LIF + crossing ..... neuro.py:125-210 (refractory gate before the crossing
+ *                        test :155-158, grazing error :194-199)
+ *   fan-out ............ network.py:412-443 with compose_delay / delivery_step
+ *                        (jumps.py:83-96) and exact-delivery payloads
+ *                        (network.py:429-437)
+ *   ring ............... queues.py:55-123 (slot = step % capacity, capability
+ *                        error when step - now >= capacity :94-98)
+ *   fifo/heap/sorted ... queues.py:184-260, 481-571, 308-403: all three drop the
+ *                        INCOMING event when full and pop every due event; their
+ *                        accepted sets are identical, so one
+ *                        "pool" restatement covers all three; FIFO keeps its
+ *                        tail-key capability check (queues.py:220-224)
+ *   donothing .......... queues.py:26-52 (drops everything)
+ *   reverse mode ....... SURVEY.md Appendix B — the transpose of the reference's
+ *                        forward-mode tangent recurrences (the reference has no
+ *                        VJP; its JVP, network.py:668-683, is the pin)
+ *
+ * Two arithmetic modes:
+ *   mode 0 "reference": double, glibc exp/log, slot sums in the reference's
+ *          insertion order (emit step, source ascending, CSR row order).  Pinned
+ *          bitwise against the Python reference in tests/test_oracle_pin.py.
+ *   mode 1 "device": T = float or double, exp/log from include/eq_math.h, slot
+ *          sums in fixed point (int32 for float, int64 for double) with
+ *          frac_bits fraction bits, which makes them order-independent.  This
+ *          is the arithmetic contract of the CUDA kernels; the GPU is compared
+ *          with this mode bit for bit.
+ */
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "../include/eq_math.h"
+
+namespace {
+
+enum Kind { K_RING = 0, K_FIFO = 1, K_HEAP = 2, K_SORTED = 3, K_DONOTHING = 5 };
+enum Status { OK = 0, E_CONFIG = 1, E_CAPABILITY = 2, E_CAUSALITY = 3, E_GRAZING = 4, E_INTERNAL = 5 };
+
+struct Cfg {
+  int32_t kind, n, n_trials, t_steps, refractory_steps, exact_delivery, capacity, frac_bits;
+  int32_t mode, precision, record_v, pad;
+  double dt, tau_m, tau_syn, v_th, v_reset;
+};
+
+struct Spike {
+  int32_t step, trial, neuron;
+  double t, a, vh;       // exact copies of the T values
+};
+
+template <typename T> struct FixedOf;
+template <> struct FixedOf<float> { typedef int32_t type; };
+template <> struct FixedOf<double> { typedef int64_t type; };
+
+struct Error {
+  int code = OK;
+  std::string msg;
+};
+
+template <typename T, bool DEV>
+struct Trial;
+
+struct Session {
+  Cfg cfg;
+  // network (double copies; cast to T at use)
+  std::vector<int64_t> rowptr;
+  std::vector<int32_t> col;
+  std::vector<double> w, d;
+  std::vector<uint32_t> mask;  // [B][T][W]
+  std::vector<double> amp;     // [N]
+  int words = 0;
+  int horizon = 0;
+  int capacity = 0;            // bounded kinds
+  // outputs
+  std::vector<double> v_out, i_out, v_trace;
+  std::vector<Spike> spikes;
+  std::vector<int64_t> counters;   // [B][3]
+  std::vector<int64_t> pending;    // [B][N][horizon][2] fixed (device mode)
+  std::vector<double> pending_ref; // [B][N][horizon][2] (reference mode)
+  std::string err;
+  bool forward_done = false;
+};
+
+inline bool drive_on(const Session& s, int b, int m, int j) {
+  const uint32_t* row = s.mask.data() + ((size_t)b * s.cfg.t_steps + m) * s.words;
+  return (row[j >> 5] >> (j & 31)) & 1u;
+}
+
+template <typename T, bool DEV> inline T xexp(T x) {
+  if (DEV) return eq_exp_t(x);
+  return (T)std::exp((double)x);
+}
+template <typename T, bool DEV> inline T xlog(T x) {
+  if (DEV) return eq_log_t(x);
+  return (T)std::log((double)x);
+}
+
+/*
+ * delivery_step (jumps.py:90-96) for a spike emitted in loop step m:
+ * max(ceil(t_post/dt), m+2).  In exact arithmetic ceil(t_post/dt) <= m+1+ceil(d/dt)
+ * because t_spk <= (m+1)dt; device mode clamps to that bound so that a rounding
+ * overshoot of t_post/dt (frequent in fp32 near the end of a step) cannot move
+ * an event one step past its edge's horizon.  Reference mode is literal.
+ */
+template <typename T, bool DEV>
+inline int32_t delivery(T t_post, T d, T dt, int m) {
+  int32_t q = (int32_t)std::ceil(t_post / dt);
+  if (DEV) {
+    int32_t hi = m + 1 + (int32_t)std::ceil(d / dt);
+    q = std::min(q, hi);
+  }
+  return std::max(q, (int32_t)(m + 2));
+}
+
+// fixed-point helpers (device mode): q = rint(v * 2^F), v = q * 2^-F
+template <typename A> inline A to_fixed(double v, int F) {
+  return (A)std::llrint(std::ldexp(v, F));
+}
+template <typename T, typename A> inline T from_fixed(A q, int F) {
+  return (T)std::ldexp((double)q, -F);
+}
+
+/* One trial of the primal simulation. */
+template <typename T, bool DEV>
+struct Trial {
+  typedef typename FixedOf<T>::type A;
+  struct Ev { int32_t due; A fs, fm; double rs, rm; };
+
+  const Session& S;
+  const Cfg& c;
+  int b;
+  int N, R;
+  std::vector<T> I, V;
+  std::vector<int32_t> refr;
+  // ring storage: [R][N] pairs
+  std::vector<A> ring_f;       // device mode
+  std::vector<double> ring_r;  // reference mode
+  std::vector<uint8_t> ring_occ;
+  // bounded storage
+  std::vector<std::vector<Ev>> pool;
+  std::vector<int32_t> tail_key;
+  int64_t n_spk = 0, n_enq = 0, n_drop = 0;
+  Error e;
+
+  Trial(const Session& s, int trial) : S(s), c(s.cfg), b(trial) {
+    N = c.n;
+    R = S.horizon;
+    I.assign(N, (T)0);
+    V.assign(N, (T)c.v_reset);
+    refr.assign(N, 0);
+    if (c.kind == K_RING) {
+      if (DEV) ring_f.assign((size_t)R * N * 2, 0);
+      else ring_r.assign((size_t)R * N * 2, 0.0);
+      ring_occ.assign((size_t)R * N, 0);
+    } else if (c.kind != K_DONOTHING) {
+      pool.resize(N);
+      tail_key.assign(N, -1);
+    }
+  }
+
+  // pop slot `now` for neuron j -> (ps, pm)
+  inline void pop(int j, int now, T& ps, T& pm) {
+    ps = (T)0; pm = (T)0;
+    if (c.kind == K_RING) {
+      size_t k = (size_t)(now % R) * N + j;
+      if (DEV) {
+        ps = from_fixed<T, A>(ring_f[2 * k], c.frac_bits);
+        pm = from_fixed<T, A>(ring_f[2 * k + 1], c.frac_bits);
+        ring_f[2 * k] = 0; ring_f[2 * k + 1] = 0;
+      } else {
+        ps = (T)ring_r[2 * k]; pm = (T)ring_r[2 * k + 1];
+        ring_r[2 * k] = 0.0; ring_r[2 * k + 1] = 0.0;
+      }
+      ring_occ[k] = 0;
+    } else if (c.kind != K_DONOTHING) {
+      std::vector<Ev>& q = pool[j];
+      A fs = 0, fm = 0;
+      double rs = 0.0, rm = 0.0;
+      size_t keep = 0;
+      for (size_t x = 0; x < q.size(); ++x) {
+        if (q[x].due == now) {   // merged in insertion order (= (due, seq) order)
+          fs += q[x].fs; fm += q[x].fm;
+          rs += q[x].rs; rm += q[x].rm;
+        } else {
+          q[keep++] = q[x];
+        }
+      }
+      q.resize(keep);
+      if (DEV) { ps = from_fixed<T, A>(fs, c.frac_bits); pm = from_fixed<T, A>(fm, c.frac_bits); }
+      else { ps = (T)rs; pm = (T)rm; }
+    }
+  }
+
+  // enqueue one event; returns false when dropped
+  inline bool enqueue(int j, int now, int32_t dstep, T ws, T wm) {
+    if (dstep < now) {
+      e.code = E_CAUSALITY;
+      e.msg = "event for step " + std::to_string(dstep) + " enqueued at step " + std::to_string(now);
+      return false;
+    }
+    if (c.kind == K_DONOTHING) return false;
+    if (c.kind == K_RING) {
+      if (dstep - now >= R) {
+        e.code = E_CAPABILITY;
+        e.msg = "ring: delay of " + std::to_string(dstep - now + 1) + " steps exceeds buffer capacity " + std::to_string(R);
+        return false;
+      }
+      size_t k = (size_t)(dstep % R) * N + j;
+      if (DEV) {
+        ring_f[2 * k] += to_fixed<A>((double)ws, c.frac_bits);
+        ring_f[2 * k + 1] += to_fixed<A>((double)wm, c.frac_bits);
+      } else {
+        ring_r[2 * k] += (double)ws;
+        ring_r[2 * k + 1] += (double)wm;
+      }
+      ring_occ[k] = 1;
+      return true;
+    }
+    if (c.kind == K_FIFO && dstep < tail_key[j]) {
+      e.code = E_CAPABILITY;
+      e.msg = "fiforing supports homogeneous delays only: event for step " + std::to_string(dstep) +
+              " arrived after one for step " + std::to_string(tail_key[j]);
+      return false;
+    }
+    std::vector<Ev>& q = pool[j];
+    if ((int)q.size() == S.capacity) return false;
+    Ev ev;
+    ev.due = dstep;
+    ev.fs = DEV ? to_fixed<A>((double)ws, c.frac_bits) : 0;
+    ev.fm = DEV ? to_fixed<A>((double)wm, c.frac_bits) : 0;
+    ev.rs = (double)ws; ev.rm = (double)wm;
+    q.push_back(ev);
+    if (c.kind == K_FIFO) tail_key[j] = dstep;
+    return true;
+  }
+
+  void run(std::vector<Spike>& out, double* vtrace) {
+    const T dt = (T)c.dt, tau_m = (T)c.tau_m, tau_s = (T)c.tau_syn;
+    const T v_th = (T)c.v_th, v_reset = (T)c.v_reset;
+    // constants as the reference computes them (network.py:527-528, 183-185)
+    const T k_m = (T)std::exp(-c.dt / c.tau_m);
+    const T k_s = (T)std::exp(-c.dt / c.tau_syn);
+    const T cc = c.exact_delivery ? (T)(c.tau_syn / (c.tau_m - c.tau_syn)) : (T)0;
+    const bool exact = c.exact_delivery != 0;
+    std::vector<int> crossing;
+    std::vector<T> cross_t;
+    for (int m = 0; m < c.t_steps && e.code == OK; ++m) {
+      crossing.clear(); cross_t.clear();
+      for (int j = 0; j < N; ++j) {
+        T ps, pm;
+        pop(j, m, ps, pm);
+        if (!exact) pm = (T)0;
+        T i = (I[j] + ps) * k_s;                              // network.py:559
+        I[j] = i;
+        T drive = drive_on(S, b, m, j) ? (T)S.amp[j] : (T)0;
+        T a = i + drive;                                       // :561
+        T v = V[j];
+        if (exact) v = v + cc * (pm - ps);                      // :564
+        T v_new = a + (v - a) * k_m;                            // :565
+        if (refr[j] > 0) {                                      // :566-567
+          refr[j] -= 1;
+        } else if (v < v_th && v_th <= v_new) {                 // :568
+          T v_dot = (a - v_th) / tau_m;                         // :569
+          if (v_dot < (T)1e-9) {
+            e.code = E_GRAZING;
+            e.msg = "grazing crossing at step " + std::to_string(m + 1);
+            return;
+          }
+          T r = (v_th - a) / (v - a);                           // :574
+          T t_spk = (T)m * dt - tau_m * xlog<T, DEV>(r);        // :575
+          T u = (T)(m + 1) * dt - t_spk;                        // :576
+          v_new = a + (v_reset - a) * xexp<T, DEV>(-u / tau_m); // :577
+          refr[j] = c.refractory_steps;                         // :578
+          crossing.push_back(j);
+          cross_t.push_back(t_spk);
+          Spike sp;
+          sp.step = m; sp.trial = b; sp.neuron = j;
+          sp.t = (double)t_spk; sp.a = (double)a; sp.vh = (double)v;
+          out.push_back(sp);
+        }
+        V[j] = v_new;                                           // :580
+      }
+      if (vtrace) for (int j = 0; j < N; ++j) vtrace[(size_t)m * N + j] = (double)V[j];
+      // fan-out in ascending source order, CSR row order (network.py:583-611)
+      const int now = m + 1;  // queues were popped for step m
+      for (size_t k = 0; k < crossing.size() && e.code == OK; ++k) {
+        int i = crossing[k];
+        T t_spk = cross_t[k];
+        n_spk += 1;
+        for (int64_t x = S.rowptr[i]; x < S.rowptr[i + 1]; ++x) {
+          int j = S.col[x];
+          T d = (T)S.d[x];
+          T t_post = t_spk + d;                                 // :588
+          int32_t dstep = delivery<T, DEV>(t_post, d, dt, m);   // jumps.py:96
+          n_enq += 1;
+          T w = (T)S.w[x];
+          T ws, wm;
+          if (exact) {
+            T phi = (T)dstep * dt - t_post;                     // :599
+            ws = w * xexp<T, DEV>(-phi / tau_s);                // :601
+            wm = w * xexp<T, DEV>(-phi / tau_m);                // :606
+          } else {
+            ws = w; wm = (T)0;
+          }
+          bool ok = enqueue(j, now, dstep, ws, wm);
+          if (e.code != OK) return;
+          if (!ok) n_drop += 1;
+        }
+      }
+    }
+  }
+};
+
+template <typename T, bool DEV>
+int run_forward(Session& s) {
+  const Cfg& c = s.cfg;
+  int B = c.n_trials, N = c.n;
+  s.v_out.assign((size_t)B * N, 0.0);
+  s.i_out.assign((size_t)B * N, 0.0);
+  s.counters.assign((size_t)B * 3, 0);
+  if (c.record_v) s.v_trace.assign((size_t)B * c.t_steps * N, 0.0);
+  else s.v_trace.clear();
+  s.pending.assign(DEV ? (size_t)B * N * s.horizon * 2 : 0, 0);
+  s.pending_ref.assign(DEV ? 0 : (size_t)B * N * s.horizon * 2, 0.0);
+  std::vector<std::vector<Spike>> per_trial(B);
+  std::vector<Error> errs(B);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int b = 0; b < B; ++b) {
+    Trial<T, DEV> tr(s, b);
+    tr.run(per_trial[b], c.record_v ? s.v_trace.data() + (size_t)b * c.t_steps * N : nullptr);
+    errs[b] = tr.e;
+    for (int j = 0; j < N; ++j) {
+      s.v_out[(size_t)b * N + j] = (double)tr.V[j];
+      s.i_out[(size_t)b * N + j] = (double)tr.I[j];
+    }
+    s.counters[3 * b] = tr.n_spk;
+    s.counters[3 * b + 1] = tr.n_enq;
+    s.counters[3 * b + 2] = tr.n_drop;
+    // canonical pending contents: due steps T .. T+horizon-1
+    int H = s.horizon;
+    for (int j = 0; j < N; ++j) {
+      for (int k = 0; k < H; ++k) {
+        int due = c.t_steps + k;
+        typename FixedOf<T>::type fs = 0, fm = 0;
+        double rs = 0.0, rm = 0.0;
+        if (c.kind == K_RING) {
+          size_t q = (size_t)(due % tr.R) * N + j;
+          if (DEV) { fs = tr.ring_f[2 * q]; fm = tr.ring_f[2 * q + 1]; }
+          else { rs = tr.ring_r[2 * q]; rm = tr.ring_r[2 * q + 1]; }
+        } else if (c.kind != K_DONOTHING) {
+          for (auto& ev : tr.pool[j]) if (ev.due == due) { fs += ev.fs; fm += ev.fm; rs += ev.rs; rm += ev.rm; }
+        }
+        size_t o = (((size_t)b * N + j) * H + k) * 2;
+        if (DEV) { s.pending[o] = fs; s.pending[o + 1] = fm; }
+        else { s.pending_ref[o] = rs; s.pending_ref[o + 1] = rm; }
+      }
+    }
+  }
+  for (int b = 0; b < B; ++b) {
+    if (errs[b].code != OK) { s.err = errs[b].msg; return errs[b].code; }
+  }
+  s.spikes.clear();
+  for (int b = 0; b < B; ++b) s.spikes.insert(s.spikes.end(), per_trial[b].begin(), per_trial[b].end());
+  s.forward_done = true;
+  return OK;
+}
+
+/*
+ * Reverse mode.  For each trial, walking m = T-1 .. 0:
+ *   R-fanout(m): every spike of step m gathers the reverse slot adjoints
+ *     Lambda_s, Lambda_m at its events' delivery steps s (zero for s >= T) and
+ *     produces dL/dw_e, dL/dd_e and dL/dt_spk.
+ *   R-neuron(m): per neuron, the adjoint of F1..F6 of PrimalRSNN.step.
+ * dL/dt_spk of one spike is reduced over its row with the same 32-lane
+ * partial + xor-butterfly order the GPU warp uses, so lambda_t matches bitwise.
+ * Gradients accumulate in double.
+ */
+template <typename T, bool DEV>
+int run_backward(Session& s, const double* vbar, const double* ibar, double* gw, double* gd, double* gamp) {
+  const Cfg& c = s.cfg;
+  if (c.kind != K_RING) { s.err = "backward is implemented for the ring kind"; return E_CONFIG; }
+  if (!c.exact_delivery) { s.err = "backward requires exact_delivery"; return E_CONFIG; }
+  int B = c.n_trials, N = c.n, TT = c.t_steps;
+  size_t E = s.col.size();
+  const T dt = (T)c.dt, tau_m = (T)c.tau_m, tau_s = (T)c.tau_syn;
+  const T v_th = (T)c.v_th, v_reset = (T)c.v_reset;
+  const T k_m = (T)std::exp(-c.dt / c.tau_m);
+  const T k_s = (T)std::exp(-c.dt / c.tau_syn);
+  const T cc = (T)(c.tau_syn / (c.tau_m - c.tau_syn));
+  const int R = s.horizon + 1;
+  std::fill(gw, gw + E, 0.0);
+  std::fill(gd, gd + E, 0.0);
+  std::fill(gamp, gamp + N, 0.0);
+  // spikes grouped by (trial, step)
+  std::vector<std::vector<std::vector<int>>> by(B, std::vector<std::vector<int>>(TT));
+  for (size_t k = 0; k < s.spikes.size(); ++k) by[s.spikes[k].trial][s.spikes[k].step].push_back((int)k);
+
+  int P = 1;
+#ifdef _OPENMP
+  P = omp_get_max_threads();
+#endif
+  std::vector<std::vector<double>> pw(P, std::vector<double>(E)), pd(P, std::vector<double>(E)),
+      pa(P, std::vector<double>(N));
+  for (int b0 = 0; b0 < B; b0 += P) {
+    int nb = std::min(P, B - b0);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int q = 0; q < nb; ++q) {
+      int b = b0 + q;
+      std::vector<double>& lw = pw[q];
+      std::vector<double>& ld = pd[q];
+      std::vector<double>& la_acc = pa[q];
+      std::fill(lw.begin(), lw.end(), 0.0);
+      std::fill(ld.begin(), ld.end(), 0.0);
+      std::fill(la_acc.begin(), la_acc.end(), 0.0);
+      std::vector<T> lV(N), lI(N);
+      for (int j = 0; j < N; ++j) {
+        lV[j] = (T)vbar[(size_t)b * N + j];
+        lI[j] = ibar ? (T)ibar[(size_t)b * N + j] : (T)0;
+      }
+      std::vector<T> Ls((size_t)R * N, (T)0), Lm((size_t)R * N, (T)0);
+      std::vector<T> spk_lt(N, (T)0);
+      std::vector<int> spk_of(N, -1);
+      for (int m = TT - 1; m >= 0; --m) {
+        const std::vector<int>& list = by[b][m];
+        // R-fanout(m)
+        for (int k : list) {
+          const Spike& sp = s.spikes[k];
+          int i = sp.neuron;
+          T t = (T)sp.t;
+          T part[32];
+          for (int l = 0; l < 32; ++l) part[l] = (T)0;
+          int64_t r0 = s.rowptr[i], r1 = s.rowptr[i + 1];
+          for (int64_t x = r0; x < r1; ++x) {
+            int lane = (int)((x - r0) & 31);
+            int j = s.col[x];
+            T w = (T)s.w[x];
+            T dd = (T)s.d[x];
+            T t_post = t + dd;
+            int32_t st = delivery<T, DEV>(t_post, dd, dt, m);
+            if (st >= TT) continue;
+            T phi = (T)st * dt - t_post;
+            T es = xexp<T, DEV>(-phi / tau_s);
+            T em = xexp<T, DEV>(-phi / tau_m);
+            size_t o = (size_t)(st % R) * N + j;
+            T as = Ls[o], am = Lm[o];
+            T g_w = es * as + em * am;
+            T g_tp = w * (es * as / tau_s + em * am / tau_m);
+            lw[x] += (double)g_w;
+            ld[x] += (double)g_tp;
+            part[lane] = part[lane] + g_tp;
+          }
+          for (int off = 16; off >= 1; off >>= 1)
+            for (int l = 0; l < off; ++l) part[l] = part[l] + part[l + off];
+          spk_lt[i] = part[0];
+          spk_of[i] = k;
+        }
+        // R-neuron(m)
+        for (int j = 0; j < N; ++j) {
+          T lv = lV[j];
+          T la, lvh;
+          if (spk_of[j] >= 0) {
+            const Spike& sp = s.spikes[spk_of[j]];
+            T t = (T)sp.t, a = (T)sp.a, vh = (T)sp.vh;
+            T u = (T)(m + 1) * dt - t;
+            T ku = xexp<T, DEV>(-u / tau_m);
+            T r = (v_th - a) / (vh - a);
+            T lt = spk_lt[j] + lv * (v_reset - a) * ku / tau_m;
+            T lr = -tau_m * lt / r;
+            T den = vh - a;
+            T den2 = den * den;
+            la = lv * ((T)1 - ku) + lr * (v_th - vh) / den2;
+            lvh = -lr * (v_th - a) / den2;
+            spk_of[j] = -1;
+          } else {
+            la = lv * ((T)1 - k_m);
+            lvh = lv * k_m;
+          }
+          T lip = lI[j] + la;
+          if (drive_on(s, b, m, j)) la_acc[j] += (double)la;
+          size_t o = (size_t)(m % R) * N + j;
+          Lm[o] = cc * lvh;
+          Ls[o] = k_s * lip - cc * lvh;
+          lI[j] = k_s * lip;
+          lV[j] = lvh;
+        }
+      }
+    }
+    // fixed-order reduction over trials (deterministic regardless of threads)
+#pragma omp parallel for schedule(static)
+    for (int64_t x = 0; x < (int64_t)E; ++x)
+      for (int q = 0; q < nb; ++q) { gw[x] += pw[q][x]; gd[x] += pd[q][x]; }
+    for (int j = 0; j < N; ++j)
+      for (int q = 0; q < nb; ++q) gamp[j] += pa[q][j];
+  }
+  return OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+struct eqo_cfg {
+  int32_t kind, n, n_trials, t_steps, refractory_steps, exact_delivery, capacity, frac_bits;
+  int32_t mode, precision, record_v, pad;
+  double dt, tau_m, tau_syn, v_th, v_reset;
+};
+
+void* eqo_create(const eqo_cfg* cfg) {
+  Session* s = new Session();
+  std::memcpy(&s->cfg, cfg, sizeof(Cfg));
+  s->words = (cfg->n + 31) / 32;
+  return s;
+}
+
+void eqo_destroy(void* h) { delete (Session*)h; }
+
+const char* eqo_error(void* h) { return ((Session*)h)->err.c_str(); }
+
+int eqo_set_network(void* h, const int64_t* rowptr, const int32_t* col, const double* w, const double* d) {
+  Session* s = (Session*)h;
+  const Cfg& c = s->cfg;
+  int N = c.n;
+  s->rowptr.assign(rowptr, rowptr + N + 1);
+  int64_t E = rowptr[N];
+  s->col.assign(col, col + E);
+  s->w.assign(w, w + E);
+  s->d.assign(d, d + E);
+  // horizon = max ceil(d/dt) + 1 in the working precision (network.py:188-198)
+  int hmax = 1;
+  for (int64_t x = 0; x < E; ++x) {
+    int q;
+    if (c.mode == 1 && c.precision == 32) q = (int)std::ceil((float)d[x] / (float)c.dt);
+    else q = (int)std::ceil(d[x] / c.dt);
+    hmax = std::max(hmax, q);
+  }
+  s->horizon = hmax + 1;
+  if (c.kind == K_FIFO || c.kind == K_HEAP || c.kind == K_SORTED)
+    s->capacity = c.capacity > 0 ? c.capacity : s->horizon * (N - 1) + 1;  // network.py:327
+  return OK;
+}
+
+int eqo_horizon(void* h) { return ((Session*)h)->horizon; }
+
+int eqo_set_drive(void* h, const uint32_t* mask, const double* amp) {
+  Session* s = (Session*)h;
+  const Cfg& c = s->cfg;
+  s->mask.assign(mask, mask + (size_t)c.n_trials * c.t_steps * s->words);
+  s->amp.assign(amp, amp + c.n);
+  return OK;
+}
+
+int eqo_forward(void* h) {
+  Session* s = (Session*)h;
+  const Cfg& c = s->cfg;
+  if (c.mode == 0) return run_forward<double, false>(*s);
+  if (c.precision == 32) return run_forward<float, true>(*s);
+  return run_forward<double, true>(*s);
+}
+
+int eqo_backward(void* h, const double* vbar, const double* ibar, double* gw, double* gd, double* gamp) {
+  Session* s = (Session*)h;
+  const Cfg& c = s->cfg;
+  if (!s->forward_done) { s->err = "backward before forward"; return E_CONFIG; }
+  if (c.mode == 0) return run_backward<double, false>(*s, vbar, ibar, gw, gd, gamp);
+  if (c.precision == 32) return run_backward<float, true>(*s, vbar, ibar, gw, gd, gamp);
+  return run_backward<double, true>(*s, vbar, ibar, gw, gd, gamp);
+}
+
+int64_t eqo_spike_count(void* h) { return (int64_t)((Session*)h)->spikes.size(); }
+
+void eqo_get_spikes(void* h, int32_t* step, int32_t* trial, int32_t* neuron, double* t, double* a, double* vh) {
+  Session* s = (Session*)h;
+  for (size_t k = 0; k < s->spikes.size(); ++k) {
+    const Spike& sp = s->spikes[k];
+    step[k] = sp.step; trial[k] = sp.trial; neuron[k] = sp.neuron;
+    t[k] = sp.t; a[k] = sp.a; vh[k] = sp.vh;
+  }
+}
+
+void eqo_get_state(void* h, double* v, double* i) {
+  Session* s = (Session*)h;
+  std::copy(s->v_out.begin(), s->v_out.end(), v);
+  std::copy(s->i_out.begin(), s->i_out.end(), i);
+}
+
+void eqo_get_vtrace(void* h, double* out) {
+  Session* s = (Session*)h;
+  std::copy(s->v_trace.begin(), s->v_trace.end(), out);
+}
+
+void eqo_get_counters(void* h, int64_t* out) {
+  Session* s = (Session*)h;
+  std::copy(s->counters.begin(), s->counters.end(), out);
+}
+
+void eqo_get_pending(void* h, int64_t* fixed_out, double* ref_out) {
+  Session* s = (Session*)h;
+  if (fixed_out) std::copy(s->pending.begin(), s->pending.end(), fixed_out);
+  if (ref_out) std::copy(s->pending_ref.begin(), s->pending_ref.end(), ref_out);
+}
+
+int eqo_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+}  // extern "C"
+
+extern "C" {
+/* Vectorised access to the shared eq_math.h functions (accuracy tests):
+ * which = 0 exp, 1 log (double); 2 expf, 3 logf (float, carried in double). */
+void eqo_math(int which, const double* in, double* out, int64_t n) {
+  for (int64_t k = 0; k < n; ++k) {
+    switch (which) {
+      case 0: out[k] = eq_exp(in[k]); break;
+      case 1: out[k] = eq_log(in[k]); break;
+      case 2: out[k] = (double)eq_expf((float)in[k]); break;
+      default: out[k] = (double)eq_logf((float)in[k]); break;
+    }
+  }
+}
+}
