@@ -1,0 +1,381 @@
+"""Benchmark: ring-buffer forward + reverse of the R-SNN hot path (BASELINE config C3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C3] [--trials B] [--precision 32]
+
+One bench step = one forward of T=1000 simulated steps plus its reverse pass
+for the B trials this rank owns (weak scaling: B trials per GPU, trials shard
+across ranks, a final NCCL all-reduce of dL/dw and dL/dd).  `value` is
+synaptic events per second (one event = one (spike, out-edge) pair, counted on
+the device, fwd+bwd counted once) over the whole job; `e2e` is the same metric
+through the public API with the drive mask copied from pinned host memory and
+the loss + gradients read back every step.
+
+--impl reference times the reference's CPU path on the host cores: the
+reference is pure Python and cannot travel to the GPU box, so this runs the
+C++ port of it (oracle/, pinned bitwise to the reference in
+tests/test_oracle_pin.py) with OpenMP over trials, on a bounded sample of the
+same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ---------------------------------------------------------------- algorithmic bytes
+# SURVEY.md §8(d) / BASELINE.md §4 (fp32, ring, exact delivery, reverse mode):
+#   per neuron-step 60 B = fwd 36 [slot 8 read + 8 clear, drive 4, I/V 16] + bwd 24 [adjoints 16, slot 8]
+#   per spike 32 B       = fwd 16 (record write) + bwd 16 (record read)
+#   per event 64 B       = fwd 28 [CSR 12, slot RMW 16] + bwd 36 [CSR 12, gather 8, (g_w,g_d) RMW 16]
+FWD_B = (36.0, 16.0, 28.0)
+BWD_B = (24.0, 16.0, 36.0)
+
+
+def alg_bytes(neuron_steps, spikes, events, which):
+    a = FWD_B if which == "fwd" else BWD_B
+    return a[0] * neuron_steps + a[1] * spikes + a[2] * events
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[3 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_inputs(cfg, trials, rank, seed=0):
+    from paper_2512_05906_b200 import workload as wl
+    n, k, drange, _, T = wl.CONFIGS[cfg]
+    net = wl.random_network(n, k, seed, delay_steps=drange)
+    # trial b of rank r has drive seed 1000 + r*trials + b
+    from concurrent.futures import ProcessPoolExecutor
+    seeds = [1000 + rank * trials + b for b in range(trials)]
+    workers = max(1, min(len(seeds), (os.cpu_count() or 2) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))))
+    with ProcessPoolExecutor(workers) as ex:
+        masks = list(ex.map(_one_mask, [(n, T, s) for s in seeds]))
+    mask = np.stack(masks)
+    return net, mask, np.full(n, 12.0), T
+
+
+def _one_mask(args):
+    from paper_2512_05906_b200 import workload as wl
+    n, T, s = args
+    return wl.pack_mask(wl.poisson_drive_mask(n, T, 1e-3, 16e-3, 12e-3, s))
+
+
+# ---------------------------------------------------------------- reference arm (CPU)
+
+def cpu_reference_sample(net, mask, amp, T, max_trials=None, steps=None):
+    """The oracle (C++ port of the reference path) on host cores: forward +
+    reverse over `trials` trials of the same network; returns (events/s, info)."""
+    from oracle import oracle as orc
+    threads = orc.threads()
+    B = max_trials or min(threads, 16)
+    B = min(B, mask.shape[0])
+    steps = steps or T
+    s = orc.OracleSession(n=net.n, n_trials=B, t_steps=steps, mode="device", precision=32,
+                          frac_bits=orc.frac_bits(float(np.bincount(net.col, weights=np.abs(net.weight),
+                                                                     minlength=net.n).max()), 32))
+    s.set_network(net.rowptr, net.col, net.weight, net.delay)
+    s.set_drive(np.ascontiguousarray(mask[:B, :steps]), amp)
+    t0 = time.perf_counter()
+    out = s.forward()
+    s.backward(2.0 * (out["v"] - 0.25))
+    dt = time.perf_counter() - t0
+    events = int(out["counters"][:, 1].sum())
+    return events / dt, dict(cores=threads, trials=B, steps=steps, seconds=dt, events=events,
+                             neuron_steps=B * steps * net.n)
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    trials = args.cpu_trials or min(orc.threads(), 16)
+    net, mask, amp, T = make_inputs(args.config, trials, 0)
+    vals = []
+    info = None
+    for it in range(args.warmup + args.steps):
+        v, info = cpu_reference_sample(net, mask, amp, T, max_trials=args.cpu_trials, steps=args.cpu_steps)
+        if it >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "synaptic events/sec (fwd+bwd)", "value": value,
+        "unit": "events/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{args.config} ring fwd+bwd (sample)", **info},
+        "cpu_baseline": {"value": value, "unit": "events/s", "cores": info["cores"], "kind": "port",
+                         "sample": f"{info['trials']} trials x {info['steps']} steps of {args.config}"},
+        "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_05906_b200.engine import Engine
+    from paper_2512_05906_b200 import workload as wl
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    net, mask, amp, T = make_inputs(args.config, args.trials, rank)
+    B = args.trials
+    if args.steps_per_pass:
+        T = args.steps_per_pass
+        mask = np.ascontiguousarray(mask[:, :T])
+    eng = Engine(net.n, B, T, precision=args.precision, device=local)
+    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+    mask_dev = torch.from_numpy(mask.view(np.int32)).to(dev)
+    amp_dev = torch.from_numpy(amp).to(dev, eng.dtype)
+    eng.set_drive(mask_dev, amp_dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        out = eng.forward()
+        vbar = (2.0 * (out["v"] - 0.25)).to(eng.dtype)
+        gw, gd, ga = eng.backward(vbar, want_amp=False)
+        if world > 1:
+            dist.all_reduce(gw)
+            dist.all_reduce(gd)
+        return out
+
+    # ---- device-resident timing, with per-kernel events
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    counters = eng.counters()
+    spikes = int(counters[:, 0].sum())
+    events = int(counters[:, 1].sum())
+    neuron_steps = B * T * net.n
+
+    fwd_ms, bwd_ms = [], []
+    launches0 = eng.launch_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = eng.forward()
+            e1.record(stream)
+            vbar = (2.0 * (out["v"] - 0.25)).to(eng.dtype)
+            gw, gd, _ = eng.backward(vbar, want_amp=False)
+            e2.record(stream)
+            if world > 1:
+                dist.all_reduce(gw)
+                dist.all_reduce(gd)
+            fwd_ms.append((e0, e1))
+            bwd_ms.append((e1, e2))
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = eng.launch_count - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    fwd = [a.elapsed_time(b) for a, b in fwd_ms]
+    bwd = [a.elapsed_time(b) for a, b in bwd_ms]
+    t = torch.tensor([total_ms], device=dev)
+    ev = torch.tensor([float(events)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ev)
+    ms_per_step = float(t.item()) / args.steps
+    total_events = float(ev.item())
+    value = total_events / (ms_per_step / 1e3)
+
+    # ---- end to end through the public API: pinned host drive in, loss + grads out
+    mask_host = torch.from_numpy(mask.view(np.int32)).pin_memory()
+    gw_host = torch.empty(net.n_edges, dtype=torch.float32).pin_memory()
+    gd_host = torch.empty_like(gw_host)
+    loss_host = torch.empty(1, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for it in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        mask_dev.copy_(mask_host, non_blocking=True)
+        eng.set_drive(mask_dev, amp_dev)
+        out = eng.forward()
+        loss = ((out["v"].double() - 0.25) ** 2).sum()
+        vbar = (2.0 * (out["v"] - 0.25)).to(eng.dtype)
+        gw, gd, _ = eng.backward(vbar, want_amp=False)
+        if world > 1:
+            dist.all_reduce(gw)
+            dist.all_reduce(gd)
+        gw_host.copy_(gw.float(), non_blocking=True)
+        gd_host.copy_(gd.float(), non_blocking=True)
+        loss_host.copy_(loss.reshape(1), non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    e2e_t = torch.tensor([statistics.mean(e2e_ms)], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = total_events / (float(e2e_t.item()) / 1e3)
+
+    peaks, peak_kind = read_peaks()
+    peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    fwd_avg, bwd_avg = statistics.mean(fwd), statistics.mean(bwd)
+    fwd_bytes = alg_bytes(neuron_steps, spikes, events, "fwd")
+    bwd_bytes = alg_bytes(neuron_steps, spikes, events, "bwd")
+    dom = ("k_forward", fwd_bytes, fwd_avg) if fwd_avg >= bwd_avg else ("k_backward", bwd_bytes, bwd_avg)
+    achieved = dom[1] / (dom[2] / 1e3) / 1e9
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            v, info = cpu_reference_sample(net, mask, amp, T, max_trials=args.cpu_trials, steps=args.cpu_steps)
+            cpu = {"value": v, "unit": "events/s", "cores": info["cores"], "kind": "port",
+                   "sample": f"{info['trials']} trials x {info['steps']} steps of {args.config}, "
+                             f"fwd+bwd, OpenMP over trials ({info['seconds']:.1f} s)"}
+        except Exception as exc:  # the checker must not sink the bench line
+            cpu = {"value": None, "unit": "events/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+    line = {
+        "metric": "synaptic events/sec (fwd+bwd)",
+        "value": value,
+        "unit": "events/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if args.precision == 32 else "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {net.n} LIF neurons, {net.n_edges // net.n} syn/neuron, "
+                               f"delay<=64 steps, ring, fwd+bwd T={T}",
+                   "trials_per_gpu": B, "global_trials": B * world, "neurons": net.n, "steps_per_pass": T,
+                   "spikes_per_gpu": spikes, "events_per_gpu": events,
+                   "neuron_steps_per_sec": neuron_steps * world / (ms_per_step / 1e3),
+                   "l2": "inputs larger than L2 (ring %.2f GB/GPU)" % (B * (eng.horizon + 1) * net.n * 8 / 1e9),
+                   "parallelism": f"trial-dp{world}"},
+        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": dom[1], "avg_launch_ms": dom[2],
+                     "fwd_ms": fwd_avg, "bwd_ms": bwd_avg},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "events/s", "h2d_bytes_per_step": int(mask.nbytes),
+                "d2h_bytes_per_step": int(2 * 4 * net.n_edges + 8)},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--trials", type=int, default=16)
+    ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--cpu-trials", type=int, default=0)
+    ap.add_argument("--cpu-steps", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--steps-per-pass", type=int, default=0, help="override T (debug)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,135 @@
+/*
+ * eventq_b200.h — C ABI of the B200 EventQueues hot path.
+ *
+ * One handle = one simulation configuration (network + drive + queue kind) for
+ * a batch of independent trials, living on one GPU.  All bulk data crosses the
+ * boundary as raw device pointers owned by the caller; the library owns only
+ * its internal queue storage, spike log and adjoint scratch.  Every call runs on
+ * the caller's CUDA stream (`stream` is a cudaStream_t, NULL = legacy default).
+ * A handle is not thread-safe.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   eq_create + eq_set_network  <- build_rsnn(params)          pkg/src/eventq/network.py:201-333
+ *                                  (validation :213-268, horizon :188-198,
+ *                                   queue wiring + capacities :321-332)
+ *   eq_set_drive                <- PoissonDrive.materialize    pkg/src/eventq/network.py:123-155
+ *   eq_run                      <- network_step(state, drive)  pkg/src/eventq/network.py:336-445
+ *                                  (n_steps calls, persistent on device)
+ *   eq_forward                  <- simulate(state, T, drive) / PrimalRSNN.run
+ *                                  pkg/src/eventq/network.py:458-497, :613-619
+ *   eq_backward                 <- (new) reverse mode through the same queues; the
+ *                                  reference only has forward mode,
+ *                                  forward_gradient network.py:668-683, whose
+ *                                  directional derivatives it reproduces
+ *   eq_counters                 <- SimResult.spike_count/enqueued_count/drop_count
+ *                                  pkg/src/eventq/network.py:448-455
+ *   eq_last_error / status      <- exception classes          pkg/src/eventq/errors.py:4-33
+ *   eq_queue_*                  <- make_queue / EventQueue.enqueue / pop_due / occupancy
+ *                                  pkg/src/eventq/queues.py:636-692, events.py:99-141
+ *
+ * Precision: eq_config.precision = 32 (float payloads, int32 fixed-point slot
+ * sums packed two per int64) or 64 (double payloads, int64 fixed point).  The
+ * arithmetic contract is restated on the CPU by oracle/eq_oracle.cpp (device
+ * mode) and is compared bit for bit.
+ */
+#ifndef EVENTQ_B200_H
+#define EVENTQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Queue kinds (reference QueueKind, pkg/src/eventq/events.py:71-86). */
+enum {
+  EQ_KIND_RING = 0,        /* RingQueue       queues.py:55-123  */
+  EQ_KIND_FIFORING = 1,    /* FIFORingQueue   queues.py:184-260 */
+  EQ_KIND_BINARYHEAP = 2,  /* BinaryHeapQueue queues.py:481-571 */
+  EQ_KIND_SORTEDARRAY = 3, /* SortedArrayQueue queues.py:308-403 */
+  EQ_KIND_DONOTHING = 5    /* DoNothingQueue  queues.py:26-52   */
+};
+
+/* Status codes; the Python layer raises the reference class of the same name. */
+enum {
+  EQ_OK = 0,
+  EQ_ERR_CONFIGURATION = 1, /* ConfigurationError */
+  EQ_ERR_CAPABILITY = 2,    /* CapabilityError    */
+  EQ_ERR_CAUSALITY = 3,     /* CausalityError     */
+  EQ_ERR_GRAZING = 4,       /* GrazingCrossingError */
+  EQ_ERR_CUDA = 5,          /* CUDA runtime failure / device timeout */
+  EQ_ERR_CAPACITY = 6       /* an internal buffer (spike log) is too small */
+};
+
+typedef struct eq_config {
+  int32_t kind;             /* EQ_KIND_* */
+  int32_t precision;        /* 32 or 64 */
+  int32_t n_neurons;        /* n >= 2 */
+  int32_t n_trials;         /* independent trials sharing the network */
+  int32_t t_steps;          /* steps the drive covers (and eq_forward runs) */
+  int32_t refractory_steps; /* NetworkParams.refractory_steps */
+  int32_t exact_delivery;   /* NetworkParams.exact_delivery (1 = default) */
+  int32_t capacity;         /* bounded kinds: events per queue; 0 = reference default */
+  int64_t max_spikes;       /* spike-log capacity over the run; 0 = default */
+  double dt, tau_m, tau_syn, v_th, v_reset;
+} eq_config;
+
+typedef struct eq_handle eq_handle;
+
+int eq_create(const eq_config* cfg, int device, eq_handle** out);
+int eq_destroy(eq_handle* h);
+const char* eq_last_error(const eq_handle* h);
+const char* eq_version(void);
+
+/* CSR out-edges (rows = presynaptic neuron, columns sorted ascending within a
+ * row).  rowptr int64[n+1], col int32[E], weight/delay float|double[E]: device
+ * pointers that must stay valid while the handle uses them. */
+int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, const void* weight,
+                   const void* delay, int64_t n_edges, void* stream);
+
+/* Drive: packed bit mask uint32[n_trials][t_steps][ceil(n/32)] (bit j%32 of
+ * word j/32 = neuron j receives `amplitude[j]` on that step) and amplitude
+ * float|double[n].  Device pointers. */
+int eq_set_drive(eq_handle* h, const uint32_t* mask, const void* amplitude, void* stream);
+
+/* Reset all state to rest (v = v_reset, i = 0, queues empty, step 0). */
+int eq_reset(eq_handle* h, void* stream);
+
+/* Advance n_steps steps from the current step.  v_trace (optional, device,
+ * float|double[n_steps][n_trials][n]) receives the membrane after each step. */
+int eq_run(eq_handle* h, int32_t n_steps, void* v_trace, void* stream);
+
+/* eq_reset + eq_run(t_steps) + copy final state: v_out/i_out float|double[n_trials][n]. */
+int eq_forward(eq_handle* h, void* v_out, void* i_out, void* v_trace, void* stream);
+
+/* Reverse mode over the steps run since the last reset.  v_bar/i_bar: cotangents of
+ * the final membrane / synaptic current, float|double[n_trials][n] (i_bar may be
+ * NULL).  Outputs (device, double): grad_w[E], grad_d[E] summed over trials,
+ * grad_amp[n] summed over trials. */
+int eq_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* grad_w, double* grad_d,
+                double* grad_amp, void* stream);
+
+/* Host-side queries (synchronise the stream). */
+int eq_counters(eq_handle* h, int64_t* out /* [n_trials][3] spikes, events, drops */, void* stream);
+int64_t eq_spike_count(eq_handle* h, void* stream);
+/* Spike records of the last run, device outputs of length eq_spike_count:
+ * step, trial, neuron (int32) and the crossing time t_spk (float|double);
+ * order is unspecified (sort by (trial, step, neuron) for a raster). */
+int eq_get_spikes(eq_handle* h, int32_t* step, int32_t* trial, int32_t* neuron, void* t_spk,
+                  void* stream);
+/* Queue contents still pending after the run, canonical form int64
+ * [n_trials][n][horizon][2]: fixed-point (synapse, membrane) sums per due step
+ * t_run .. t_run+horizon-1 (host pointer). */
+int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream);
+int eq_horizon(const eq_handle* h);
+int eq_frac_bits(const eq_handle* h);
+/* Launch geometry actually used: CTAs and threads per CTA of the persistent kernels. */
+int eq_geometry(const eq_handle* h, int32_t* ctas, int32_t* threads);
+/* Number of kernels this handle has launched (for launch accounting). */
+int64_t eq_launch_count(const eq_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVENTQ_B200_H */

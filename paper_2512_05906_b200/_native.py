@@ -1,0 +1,84 @@
+"""ctypes binding of the in-tree sm_100a library (lib/libeventq_b200.so).
+
+There is no fallback: if the library is missing or cannot load, importing the
+engine fails loudly (build it with ``python -m paper_2512_05906_b200.build`` or
+``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import STATUS_TO_ERROR, EventQError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libeventq_b200.so")
+
+KIND_IDS = {"ring": 0, "fiforing": 1, "binaryheap": 2, "sortedarray": 3, "donothing": 5}
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32), ("precision", ctypes.c_int32), ("n_neurons", ctypes.c_int32),
+        ("n_trials", ctypes.c_int32), ("t_steps", ctypes.c_int32), ("refractory_steps", ctypes.c_int32),
+        ("exact_delivery", ctypes.c_int32), ("capacity", ctypes.c_int32), ("max_spikes", ctypes.c_int64),
+        ("dt", ctypes.c_double), ("tau_m", ctypes.c_double), ("tau_syn", ctypes.c_double),
+        ("v_th", ctypes.c_double), ("v_reset", ctypes.c_double),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the B200 extension is not built "
+            "(run `python -m paper_2512_05906_b200.build`); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    H = ctypes.c_void_p
+    sig = {
+        "eq_create": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.c_int, ctypes.POINTER(H)]),
+        "eq_destroy": (ctypes.c_int, [H]),
+        "eq_last_error": (ctypes.c_char_p, [H]),
+        "eq_version": (ctypes.c_char_p, []),
+        "eq_set_network": (ctypes.c_int, [H, vp, vp, vp, vp, i64, vp]),
+        "eq_set_drive": (ctypes.c_int, [H, vp, vp, vp]),
+        "eq_reset": (ctypes.c_int, [H, vp]),
+        "eq_run": (ctypes.c_int, [H, i32, vp, vp]),
+        "eq_forward": (ctypes.c_int, [H, vp, vp, vp, vp]),
+        "eq_backward": (ctypes.c_int, [H, vp, vp, vp, vp, vp, vp]),
+        "eq_counters": (ctypes.c_int, [H, vp, vp]),
+        "eq_spike_count": (i64, [H, vp]),
+        "eq_get_spikes": (ctypes.c_int, [H, vp, vp, vp, vp, vp]),
+        "eq_get_pending": (ctypes.c_int, [H, vp, vp]),
+        "eq_horizon": (ctypes.c_int, [H]),
+        "eq_frac_bits": (ctypes.c_int, [H]),
+        "eq_geometry": (ctypes.c_int, [H, vp, vp]),
+        "eq_launch_count": (i64, [H]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive",
+            "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_counters", "eq_spike_count",
+            "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",
+            "eq_launch_count")
+
+
+def check(handle, code: int) -> None:
+    if code == 0:
+        return
+    msg = lib().eq_last_error(handle)
+    msg = msg.decode() if msg else ""
+    raise STATUS_TO_ERROR.get(code, EventQError)(msg)

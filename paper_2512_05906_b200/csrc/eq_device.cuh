@@ -1,0 +1,157 @@
+// eq_device.cuh — device primitives shared by the EventQueues kernels.
+//
+// Everything here is sm_100a-only code (no arch dispatch).  The arithmetic that
+// must agree bit-for-bit with the CPU oracle lives in include/eq_math.h and in
+// the step helpers below, compiled with -fmad=false so no a*b+c is fused
+// behind the source's back.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/eq_math.h"
+#include "../../include/eventq_b200.h"
+
+namespace eq {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------- precision
+
+template <typename T> struct Prec;
+
+// fp32: slot = one int64 holding two int32 fixed-point sums (membrane << 32 | synapse)
+template <> struct Prec<float> {
+  typedef float2 T2;
+  static constexpr int kSlotWords = 1;
+  __device__ __forceinline__ static long long q(float v, double scale) {
+    return (long long)__double2int_rn((double)v * scale);
+  }
+  __device__ __forceinline__ static float deq(long long q, double inv) {
+    return __double2float_rn((double)q * inv);
+  }
+};
+template <> struct Prec<double> {
+  typedef double2 T2;
+  static constexpr int kSlotWords = 2;
+  __device__ __forceinline__ static long long q(double v, double scale) {
+    return __double2ll_rn(v * scale);
+  }
+  __device__ __forceinline__ static double deq(long long q, double inv) {
+    return __ll2double_rn(q) * inv;
+  }
+};
+
+// pack/unpack the fp32 slot: P = qm * 2^32 + qs, summed mod 2^64; each field's
+// true sum fits int32 by the frac-bits bound, so the low word sign-extends to qs.
+__device__ __forceinline__ long long pack2(long long qs, long long qm) {
+  return qm * 4294967296LL + qs;
+}
+__device__ __forceinline__ void unpack2(long long p, long long& qs, long long& qm) {
+  int lo = (int)(unsigned int)(p & 0xffffffffLL);
+  qs = lo;
+  qm = (p - (long long)lo) >> 32;
+}
+
+// ---------------------------------------------------------------- memory
+
+__device__ __forceinline__ long long ld_cg(const long long* p) { return __ldcg(p); }
+__device__ __forceinline__ void st_cg(long long* p, long long v) { __stcg(p, v); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_volatile(const int* p) { return *(volatile const int*)p; }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void red_add(long long* p, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+// error word: [0] code, [1] step, [2] trial, [3] neuron
+__device__ __forceinline__ void raise_error(int* err, int code, int step, int trial, int neuron) {
+  if (atomicCAS(err, 0, code) == 0) {
+    err[1] = step;
+    err[2] = trial;
+    err[3] = neuron;
+  }
+}
+
+// Grid-wide barrier for a cooperative (co-resident) launch: sense by generation
+// counter, release/acquire at gpu scope, 20 s watchdog so a bug can never wedge
+// the GPU (the kernel then exits with EQ_ERR_CUDA).
+__device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* err) {
+  __shared__ int s_ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_ok = 1;
+    unsigned* count = bar;
+    unsigned* gen = bar + 1;
+    unsigned g = ld_acquire(gen);
+    __threadfence();
+    unsigned prev = atomicAdd(count, 1u);
+    if (prev == nblocks - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      st_release(gen, g + 1);
+    } else {
+      unsigned long long t0 = globaltimer();
+      while (ld_acquire(gen) == g) {
+        __nanosleep(40);
+        if (globaltimer() - t0 > 20000000000ULL) {
+          atomicCAS(err, 0, EQ_ERR_CUDA);
+          s_ok = 0;
+          break;
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return s_ok;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum_butterfly(T v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// ---------------------------------------------------------------- step math
+//
+// Mirrors network.py:547-611 (PrimalRSNN.step) with the device-mode delivery
+// clamp of oracle/eq_oracle.cpp::delivery.
+
+template <typename T>
+__device__ __forceinline__ int delivery_step(T t_post, T d, T dt, int m) {
+  int q = (int)ceil(t_post / dt);
+  int hi = m + 1 + (int)ceil(d / dt);
+  q = q < hi ? q : hi;
+  return q > m + 2 ? q : m + 2;
+}
+
+template <typename T>
+struct alignas(16) SpikeRec;
+template <>
+struct alignas(16) SpikeRec<float> {
+  int idx;      // trial * N + neuron
+  float t, a, vh;
+};
+template <>
+struct alignas(16) SpikeRec<double> {
+  int idx;
+  int pad;
+  double t, a, vh;
+};
+
+}  // namespace eq

@@ -1,0 +1,386 @@
+// eq_ring.cuh — persistent fused step kernels (forward + reverse) for the ring
+// queue (RingQueue, queues.py:55-123) and DoNothing (queues.py:26-52).
+//
+// Geometry: a cooperative grid of G CTAs.  Neuron-trials are flattened to
+// idx = trial*N + neuron and CTA c owns the contiguous range
+// [c*per, (c+1)*per).  One grid barrier per simulated step:
+//
+//   phase m (forward):  pop slot m + synapse + LIF for the owned neurons
+//                       (network.py:547-580), then fan the CTA's own crossings
+//                       out as fixed-point red.add into slot (dstep mod R) of
+//                       each target (network.py:583-611).
+//   phase m (reverse):  R-fanout(m) for the CTA's own spikes of step m (gather
+//                       of the reverse slots, dL/dw, dL/dd, dL/dt_spk), then
+//                       R-neuron(m) for the owned neurons.
+//
+// Ring rows are R = horizon + 1 slots: a fan-out of step m writes delivery
+// steps in [m+2, m+horizon] while other CTAs may still pop slot m in the same
+// phase, so (m+horizon) mod R must differ from m mod R.  Any R >= horizon gives
+// the reference's results (slot = step % capacity never aliases a live step).
+#pragma once
+
+#include "eq_device.cuh"
+
+namespace eq {
+
+template <typename T>
+struct StepConsts {
+  T dt, tau_m, tau_s, v_th, v_reset, k_m, k_s, cc;
+  double scale, inv_scale;  // 2^F, 2^-F
+};
+
+template <typename T>
+struct NetView {
+  const int64_t* rowptr;
+  const int32_t* col;
+  const T* w;
+  const T* d;
+  const uint32_t* mask;  // [B][t_mask][words]
+  const T* amp;          // [N]
+  int words, t_mask;
+};
+
+template <typename T>
+struct FwdArgs {
+  int N, B, G;
+  long long total, per;
+  int m0, m1;         // steps [m0, m1)
+  int R, kind, refractory, exact;
+  StepConsts<T> c;
+  NetView<T> net;
+  T* I;
+  T* V;
+  int32_t* refr;
+  long long* ring;    // fp32: [B][R][N]; fp64: [B][R][N][2]
+  SpikeRec<T>* scratch;  // [G][per] per-CTA spill area for the step's spikes
+  SpikeRec<T>* log;
+  long long log_cap;
+  unsigned long long* log_count;
+  long long* chunk_off;  // [m][G]
+  int* chunk_cnt;        // [m][G]
+  long long* counters;   // [B][3]
+  T* v_trace;            // [m1-m0][B][N] or null
+  int* err;
+  unsigned* bar;
+};
+
+template <int NT>
+struct FwdShared {
+  static constexpr int kCap = 1024;   // spikes staged in smem per step per CTA
+  static constexpr int kTrials = 8;   // per-CTA trial counters kept in smem
+};
+
+template <typename T>
+__device__ __forceinline__ bool drive_bit(const NetView<T>& net, int b, int m, int j) {
+  int mm = m < net.t_mask ? m : net.t_mask - 1;   // network.py:155 rows[-1]
+  const uint32_t* row = net.mask + ((size_t)b * net.t_mask + mm) * net.words;
+  return (__ldg(row + (j >> 5)) >> (j & 31)) & 1u;
+}
+
+template <typename T, int NT, int U>
+__global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
+  typedef Prec<T> P;
+  constexpr int kCap = FwdShared<NT>::kCap;
+  constexpr int kTr = FwdShared<NT>::kTrials;
+  __shared__ SpikeRec<T> s_spk[kCap];
+  __shared__ int s_n;
+  __shared__ long long s_off;
+  __shared__ unsigned long long s_ctr[kTr][2];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int cta = blockIdx.x;
+  const long long begin = (long long)cta * A.per;
+  const long long end = begin + A.per < A.total ? begin + A.per : A.total;
+  const int b_first = (int)(begin / A.N);
+  const StepConsts<T> c = A.c;
+  SpikeRec<T>* spill = A.scratch + (size_t)cta * A.per;
+
+  if (tid < kTr * 2) (&s_ctr[0][0])[tid] = 0ULL;
+
+  for (int m = A.m0; m < A.m1; ++m) {
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    // ---------------- neuron update: pop, synapse, membrane, crossing
+    for (long long base = begin; base < end; base += (long long)NT * U) {
+      long long slot_v[U][2];
+      T Iv[U], Vv[U];
+      int rf[U];
+      bool on[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long idx = base + (long long)u * NT + tid;
+        slot_v[u][0] = slot_v[u][1] = 0;
+        if (idx < end) {
+          int b = (int)(idx / A.N);
+          int j = (int)(idx - (long long)b * A.N);
+          size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
+          if (A.kind == EQ_KIND_RING) {
+            if (P::kSlotWords == 1) {
+              slot_v[u][0] = ld_cg(A.ring + so);
+              st_cg(A.ring + so, 0);
+            } else {
+              slot_v[u][0] = ld_cg(A.ring + 2 * so);
+              slot_v[u][1] = ld_cg(A.ring + 2 * so + 1);
+              st_cg(A.ring + 2 * so, 0);
+              st_cg(A.ring + 2 * so + 1, 0);
+            }
+          }
+          Iv[u] = A.I[idx];
+          Vv[u] = A.V[idx];
+          rf[u] = A.refractory ? A.refr[idx] : 0;
+          on[u] = drive_bit(A.net, b, m, j);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long idx = base + (long long)u * NT + tid;
+        if (idx >= end) continue;
+        int b = (int)(idx / A.N);
+        int j = (int)(idx - (long long)b * A.N);
+        T ps, pm;
+        if (P::kSlotWords == 1) {
+          long long qs, qm;
+          unpack2(slot_v[u][0], qs, qm);
+          ps = P::deq(qs, c.inv_scale);
+          pm = P::deq(qm, c.inv_scale);
+        } else {
+          ps = P::deq(slot_v[u][0], c.inv_scale);
+          pm = P::deq(slot_v[u][1], c.inv_scale);
+        }
+        if (!A.exact) pm = (T)0;
+        T i = (Iv[u] + ps) * c.k_s;                       // network.py:559
+        T drive = on[u] ? __ldg(A.net.amp + j) : (T)0;
+        T a = i + drive;                                   // :561
+        T v = Vv[u];
+        if (A.exact) v = v + c.cc * (pm - ps);             // :564
+        T v_new = a + (v - a) * c.k_m;                     // :565
+        if (rf[u] > 0) {                                   // :566-567
+          rf[u] -= 1;
+        } else if (v < c.v_th && c.v_th <= v_new) {        // :568
+          T v_dot = (a - c.v_th) / c.tau_m;
+          if (v_dot < (T)1e-9) {
+            raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, j);
+          } else {
+            T r = (c.v_th - a) / (v - a);                  // :574
+            T t_spk = (T)m * c.dt - c.tau_m * eq_log_t(r); // :575
+            T uu = (T)(m + 1) * c.dt - t_spk;              // :576
+            v_new = a + (c.v_reset - a) * eq_exp_t(-uu / c.tau_m);
+            rf[u] = A.refractory;
+            int pos = atomicAdd(&s_n, 1);
+            SpikeRec<T> rec;
+            rec.idx = (int)idx;
+            rec.t = t_spk;
+            rec.a = a;
+            rec.vh = v;
+            if (pos < kCap) s_spk[pos] = rec;
+            else spill[pos - kCap] = rec;
+          }
+        }
+        A.I[idx] = i;
+        A.V[idx] = v_new;
+        if (A.refractory) A.refr[idx] = rf[u];
+        if (A.v_trace) A.v_trace[(size_t)(m - A.m0) * A.total + idx] = v_new;
+      }
+    }
+    __syncthreads();
+    const int nspk = s_n;
+    // ---------------- fan-out (network.py:583-611): one warp per spike
+    for (int k = warp; k < nspk; k += NT / kWarp) {
+      SpikeRec<T> rec = k < kCap ? s_spk[k] : spill[k - kCap];
+      int b = rec.idx / A.N;
+      int i = rec.idx - b * A.N;
+      long long r0 = __ldg(A.net.rowptr + i), r1 = __ldg(A.net.rowptr + i + 1);
+      if (lane == 0) {
+        int tb = b - b_first;
+        unsigned long long ev = (unsigned long long)(r1 - r0);
+        if (tb < kTr) {
+          atomicAdd(&s_ctr[tb][0], 1ULL);
+          atomicAdd(&s_ctr[tb][1], ev);
+        } else {
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), ev);
+        }
+        if (A.kind == EQ_KIND_DONOTHING)
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), ev);
+      }
+      if (A.kind != EQ_KIND_RING) continue;
+      long long* ring_b = A.ring + (size_t)b * A.R * A.N * P::kSlotWords;
+      for (long long x = r0 + lane; x < r1; x += kWarp) {
+        int j = __ldg(A.net.col + x);
+        T w = __ldg(A.net.w + x);
+        T d = __ldg(A.net.d + x);
+        T t_post = rec.t + d;                              // :588
+        int ds = delivery_step(t_post, d, c.dt, m);        // jumps.py:96
+        T ws, wm;
+        if (A.exact) {
+          T phi = (T)ds * c.dt - t_post;                   // :599
+          ws = w * eq_exp_t(-phi / c.tau_s);               // :601
+          wm = w * eq_exp_t(-phi / c.tau_m);               // :606
+        } else {
+          ws = w;
+          wm = (T)0;
+        }
+        size_t so = (size_t)(ds % A.R) * A.N + j;
+        long long qs = P::q(ws, c.scale), qm = P::q(wm, c.scale);
+        if (P::kSlotWords == 1) {
+          red_add(ring_b + so, pack2(qs, qm));
+        } else {
+          red_add(ring_b + 2 * so, qs);
+          if (A.exact) red_add(ring_b + 2 * so + 1, qm);
+        }
+      }
+    }
+    // ---------------- spike log for the reverse pass: one chunk per (step, CTA)
+    if (tid == 0) {
+      unsigned long long off = nspk ? atomicAdd(A.log_count, (unsigned long long)nspk) : 0ULL;
+      if (nspk && (long long)(off + nspk) > A.log_cap) {
+        raise_error(A.err, EQ_ERR_CAPACITY, m, -1, -1);
+        off = 0;
+      }
+      s_off = (long long)off;
+      A.chunk_off[(size_t)m * A.G + cta] = (long long)off;
+      A.chunk_cnt[(size_t)m * A.G + cta] = nspk;
+    }
+    __syncthreads();
+    if (s_off + nspk <= A.log_cap) {
+      for (int k = tid; k < nspk; k += NT) A.log[s_off + k] = k < kCap ? s_spk[k] : spill[k - kCap];
+    }
+    if (!grid_sync(A.bar, A.G, A.err)) break;
+    if (ld_volatile(A.err) != 0) break;
+  }
+  __syncthreads();
+  if (tid < kTr) {
+    int b = b_first + tid;
+    if (b < A.B && (long long)b * A.N < end) {
+      if (s_ctr[tid][0]) atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), s_ctr[tid][0]);
+      if (s_ctr[tid][1]) atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), s_ctr[tid][1]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ reverse
+
+template <typename T>
+struct BwdArgs {
+  int N, B, G;
+  long long total, per;
+  int m_run;          // steps simulated since reset (reverse walks m_run-1 .. 0)
+  int R, refractory;
+  StepConsts<T> c;
+  NetView<T> net;
+  T* lamV;
+  T* lamI;
+  typename Prec<T>::T2* lam;   // [B][R][N] (Lambda_s, Lambda_m)
+  double* gw;
+  double* gd;
+  double* gamp_bt;             // [B][N] or null
+  const SpikeRec<T>* log;
+  T* lt_log;                   // dL/dt_spk per log record
+  const long long* chunk_off;
+  const int* chunk_cnt;
+  int* err;
+  unsigned* bar;
+};
+
+template <typename T, int NT, int U>
+__global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
+  typedef typename Prec<T>::T2 T2;
+  extern __shared__ unsigned int s_bits[];   // one bit per owned neuron-trial
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int cta = blockIdx.x;
+  const long long begin = (long long)cta * A.per;
+  const long long end = begin + A.per < A.total ? begin + A.per : A.total;
+  const int nwords = (int)((A.per + 31) / 32);
+  const StepConsts<T> c = A.c;
+  for (int k = tid; k < nwords; k += NT) s_bits[k] = 0u;
+  __syncthreads();
+
+  for (int m = A.m_run - 1; m >= 0; --m) {
+    const long long off = A.chunk_off[(size_t)m * A.G + cta];
+    const int cnt = A.chunk_cnt[(size_t)m * A.G + cta];
+    // ---------------- R-fanout(m): own spikes, one warp per spike
+    for (int k = warp; k < cnt; k += NT / kWarp) {
+      SpikeRec<T> rec = A.log[off + k];
+      int b = rec.idx / A.N;
+      int i = rec.idx - b * A.N;
+      long long r0 = __ldg(A.net.rowptr + i), r1 = __ldg(A.net.rowptr + i + 1);
+      const T2* lam_b = A.lam + (size_t)b * A.R * A.N;
+      T part = (T)0;
+      for (long long x = r0 + lane; x < r1; x += kWarp) {
+        int j = __ldg(A.net.col + x);
+        T w = __ldg(A.net.w + x);
+        T d = __ldg(A.net.d + x);
+        T t_post = rec.t + d;
+        int st = delivery_step(t_post, d, c.dt, m);
+        if (st >= A.m_run) continue;                       // never popped: no effect
+        T phi = (T)st * c.dt - t_post;
+        T es = eq_exp_t(-phi / c.tau_s);
+        T em = eq_exp_t(-phi / c.tau_m);
+        T2 L = __ldcg(lam_b + (size_t)(st % A.R) * A.N + j);
+        T g_w = es * L.x + em * L.y;
+        T g_tp = w * (es * L.x / c.tau_s + em * L.y / c.tau_m);
+        atomicAdd(A.gw + x, (double)g_w);
+        atomicAdd(A.gd + x, (double)g_tp);
+        part = part + g_tp;
+      }
+      part = warp_sum_butterfly(part);
+      if (lane == 0) {
+        A.lt_log[off + k] = part;
+        long long loc = (long long)rec.idx - begin;
+        atomicOr(&s_bits[loc >> 5], 1u << (loc & 31));
+      }
+    }
+    __syncthreads();
+    // ---------------- R-neuron(m)
+    for (long long base = begin; base < end; base += (long long)NT * U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long idx = base + (long long)u * NT + tid;
+        if (idx >= end) continue;
+        int b = (int)(idx / A.N);
+        int j = (int)(idx - (long long)b * A.N);
+        T lv = A.lamV[idx];
+        T la, lvh;
+        long long loc = idx - begin;
+        if ((s_bits[loc >> 5] >> (loc & 31)) & 1u) {
+          int k = 0;
+          while (k < cnt && A.log[off + k].idx != (int)idx) ++k;
+          SpikeRec<T> rec = A.log[off + k];
+          T lt0 = A.lt_log[off + k];
+          T t = rec.t, a = rec.a, vh = rec.vh;
+          T uu = (T)(m + 1) * c.dt - t;
+          T ku = eq_exp_t(-uu / c.tau_m);
+          T r = (c.v_th - a) / (vh - a);
+          T lt = lt0 + lv * (c.v_reset - a) * ku / c.tau_m;
+          T lr = -c.tau_m * lt / r;
+          T den = vh - a;
+          T den2 = den * den;
+          la = lv * ((T)1 - ku) + lr * (c.v_th - vh) / den2;
+          lvh = -lr * (c.v_th - a) / den2;
+        } else {
+          la = lv * ((T)1 - c.k_m);
+          lvh = lv * c.k_m;
+        }
+        T lip = A.lamI[idx] + la;
+        if (A.gamp_bt && drive_bit(A.net, b, m, j)) A.gamp_bt[idx] += (double)la;
+        T2 L;
+        L.x = c.k_s * lip - c.cc * lvh;
+        L.y = c.cc * lvh;
+        A.lam[((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j] = L;
+        A.lamI[idx] = c.k_s * lip;
+        A.lamV[idx] = lvh;
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < cnt; k += NT) {
+      long long loc = (long long)A.log[off + k].idx - begin;
+      s_bits[loc >> 5] = 0u;
+    }
+    if (!grid_sync(A.bar, A.G, A.err)) break;
+    if (ld_volatile(A.err) != 0) break;
+  }
+}
+
+}  // namespace eq

@@ -1,0 +1,740 @@
+// eventq.cu — the C ABI (include/eventq_b200.h) over the sm_100a kernels.
+//
+// Host code only orchestrates: validation of the network on the device
+// (reference checks of build_rsnn, network.py:213-268), buffer ownership, and
+// one cooperative launch of a persistent kernel per eq_run / eq_backward.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "eq_device.cuh"
+#include "eq_ring.cuh"
+
+using namespace eq;
+
+namespace {
+
+constexpr int kNT = 512;   // threads per CTA of the persistent kernels
+constexpr int kU = 4;      // neurons per thread in flight per round
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct eq_handle {
+  eq_config cfg{};
+  std::string err;
+  int device = 0;
+  int n_sm = 0;
+  int G = 0;
+  long long total = 0, per = 0;
+  int horizon = 0, R = 0, frac_bits = 0;
+  double scale = 1.0, inv_scale = 1.0;
+  int64_t E = 0;
+  const int64_t* rowptr = nullptr;
+  const int32_t* col = nullptr;
+  const void* w = nullptr;
+  const void* d = nullptr;
+  const uint32_t* mask = nullptr;
+  const void* amp = nullptr;
+  bool net_set = false, drive_set = false;
+  size_t tsize = 4;
+  // forward state
+  void* I = nullptr;
+  void* V = nullptr;
+  int32_t* refr = nullptr;
+  long long* ring = nullptr;
+  size_t ring_words = 0;
+  void* scratch = nullptr;
+  void* log = nullptr;
+  long long log_cap = 0;
+  unsigned long long* log_count = nullptr;
+  long long* chunk_off = nullptr;
+  int* chunk_cnt = nullptr;
+  int t_cap = 0;
+  long long* counters = nullptr;
+  int* err_dev = nullptr;
+  unsigned* bar = nullptr;
+  // reverse state
+  void* lamV = nullptr;
+  void* lamI = nullptr;
+  void* lam = nullptr;
+  void* lt_log = nullptr;
+  double* gamp_bt = nullptr;
+  int steps_done = 0;
+  long long launches = 0;
+  std::vector<void*> owned;
+};
+
+namespace {
+
+int fail(eq_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+int cuda_fail(eq_handle* h, cudaError_t e, const char* what) {
+  return fail(h, EQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define EQ_CUDA(h, call)                                   \
+  do {                                                     \
+    cudaError_t _e = (call);                               \
+    if (_e != cudaSuccess) return cuda_fail((h), _e, #call); \
+  } while (0)
+
+cudaError_t alloc(eq_handle* h, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess) h->owned.push_back(*p);
+  return e;
+}
+
+void release(eq_handle* h, void* p) {
+  if (!p) return;
+  cudaFree(p);
+  h->owned.erase(std::remove(h->owned.begin(), h->owned.end(), p), h->owned.end());
+}
+
+template <typename T>
+StepConsts<T> consts(const eq_handle* h) {
+  const eq_config& c = h->cfg;
+  StepConsts<T> k;
+  k.dt = (T)c.dt;
+  k.tau_m = (T)c.tau_m;
+  k.tau_s = (T)c.tau_syn;
+  k.v_th = (T)c.v_th;
+  k.v_reset = (T)c.v_reset;
+  // computed in double with libm and rounded once, exactly as the reference
+  // computes them (network.py:527-528, 183-185) and as the oracle does
+  k.k_m = (T)std::exp(-c.dt / c.tau_m);
+  k.k_s = (T)std::exp(-c.dt / c.tau_syn);
+  k.cc = c.exact_delivery ? (T)(c.tau_syn / (c.tau_m - c.tau_syn)) : (T)0;
+  k.scale = std::ldexp(1.0, h->frac_bits);
+  k.inv_scale = std::ldexp(1.0, -h->frac_bits);
+  return k;
+}
+
+template <typename T>
+NetView<T> netview(const eq_handle* h) {
+  NetView<T> n;
+  n.rowptr = h->rowptr;
+  n.col = h->col;
+  n.w = (const T*)h->w;
+  n.d = (const T*)h->d;
+  n.mask = h->mask;
+  n.amp = (const T*)h->amp;
+  n.words = (h->cfg.n_neurons + 31) / 32;
+  n.t_mask = h->cfg.t_steps;
+  return n;
+}
+
+// ------------------------------------------------------------ small kernels
+
+// Network validation + statistics, one thread per source row.
+// stats[0] = max ceil(d/dt); stats[1] = first bad edge (flat index) for
+// ConfigurationError, stats[2] = code of that error; insum = fixed-point
+// sum of |w| per target (2^-40 units; deterministic integer adds).
+template <typename T>
+__global__ void k_net_stats(int N, const int64_t* rowptr, const int32_t* col, const T* w, const T* d,
+                            T dt, int homogeneous_only, long long* insum, long long* stats) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  long long r0 = rowptr[i], r1 = rowptr[i + 1];
+  int hmax = 1;
+  T d0 = d[0];
+  int prev = -1;
+  for (long long x = r0; x < r1; ++x) {
+    int j = col[x];
+    int code = 0;
+    if (j < 0 || j >= N || j == i || j <= prev) code = 1;
+    else if (!(d[x] >= dt)) code = 2;
+    else if (homogeneous_only && d[x] != d0) code = 3;
+    if (code) {
+      // smallest offending edge wins: reference loops i, j row-major (network.py:225-240)
+      unsigned long long key = ((unsigned long long)x << 2) | (unsigned long long)code;
+      atomicMin(reinterpret_cast<unsigned long long*>(stats + 1), key);
+      return;
+    }
+    prev = j;
+    int q = (int)ceil(d[x] / dt);
+    hmax = q > hmax ? q : hmax;
+    atomicAdd(reinterpret_cast<unsigned long long*>(insum + j),
+              (unsigned long long)__double2ll_rn(fabs((double)w[x]) * 1099511627776.0));
+  }
+  atomicMax(stats, (long long)hmax);
+}
+
+__global__ void k_max_ll(const long long* a, long long n, long long* out) {
+  long long best = 0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    best = a[k] > best ? a[k] : best;
+  for (int off = 16; off; off >>= 1) {
+    long long o = __shfl_xor_sync(0xffffffffu, best, off);
+    best = o > best ? o : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+template <typename T>
+__global__ void k_fill(T* p, long long n, T v) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    p[k] = v;
+}
+
+template <typename T>
+__global__ void k_sum_trials(const double* bt, int B, int N, double* out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double s = 0.0;
+  for (int b = 0; b < B; ++b) s += bt[(size_t)b * N + j];
+  out[j] = s;
+}
+
+template <typename T>
+__global__ void k_decode_spikes(const SpikeRec<T>* log, const long long* chunk_off, const int* chunk_cnt,
+                                int n_chunks, int G, int N, int32_t* step, int32_t* trial,
+                                int32_t* neuron, T* t) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (wid >= n_chunks) return;
+  long long off = chunk_off[wid];
+  int cnt = chunk_cnt[wid];
+  int m = wid / G;
+  for (int k = lane; k < cnt; k += 32) {
+    SpikeRec<T> r = log[off + k];
+    step[off + k] = m;
+    trial[off + k] = r.idx / N;
+    neuron[off + k] = r.idx % N;
+    if (t) t[off + k] = r.t;
+  }
+}
+
+template <typename T>
+__global__ void k_pending(const long long* ring, int B, int R, int N, int H, int now, long long* out) {
+  long long total = (long long)B * N * H;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < total;
+       k += (long long)gridDim.x * blockDim.x) {
+    int hh = (int)(k % H);
+    long long bj = k / H;
+    int j = (int)(bj % N);
+    int b = (int)(bj / N);
+    size_t so = ((size_t)b * R + (size_t)((now + hh) % R)) * N + j;
+    long long qs, qm;
+    if (Prec<T>::kSlotWords == 1) {
+      unpack2(ring[so], qs, qm);
+    } else {
+      qs = ring[2 * so];
+      qm = ring[2 * so + 1];
+    }
+    out[2 * k] = qs;
+    out[2 * k + 1] = qm;
+  }
+}
+
+// ------------------------------------------------------------ launches
+
+int check_err(eq_handle* h, cudaStream_t s) {
+  int e[4];
+  EQ_CUDA(h, cudaMemcpyAsync(e, h->err_dev, sizeof e, cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  if (e[0] == 0) return EQ_OK;
+  char buf[256];
+  switch (e[0]) {
+    case EQ_ERR_GRAZING:
+      snprintf(buf, sizeof buf, "grazing crossing at step %d (trial %d, neuron %d): slope below 1e-09",
+               e[1], e[2], e[3]);
+      break;
+    case EQ_ERR_CAPACITY:
+      snprintf(buf, sizeof buf, "spike log capacity %lld exceeded at step %d; raise eq_config.max_spikes",
+               (long long)h->log_cap, e[1]);
+      break;
+    case EQ_ERR_CUDA:
+      snprintf(buf, sizeof buf, "device watchdog: grid barrier timed out");
+      break;
+    default:
+      snprintf(buf, sizeof buf, "device error %d at step %d (trial %d, neuron %d)", e[0], e[1], e[2], e[3]);
+  }
+  return fail(h, e[0], buf);
+}
+
+template <typename T>
+int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
+  FwdArgs<T> A;
+  A.N = h->cfg.n_neurons;
+  A.B = h->cfg.n_trials;
+  A.G = h->G;
+  A.total = h->total;
+  A.per = h->per;
+  A.m0 = h->steps_done;
+  A.m1 = h->steps_done + n_steps;
+  A.R = h->R;
+  A.kind = h->cfg.kind;
+  A.refractory = h->cfg.refractory_steps;
+  A.exact = h->cfg.exact_delivery;
+  A.c = consts<T>(h);
+  A.net = netview<T>(h);
+  A.I = (T*)h->I;
+  A.V = (T*)h->V;
+  A.refr = h->refr;
+  A.ring = h->ring;
+  A.scratch = (SpikeRec<T>*)h->scratch;
+  A.log = (SpikeRec<T>*)h->log;
+  A.log_cap = h->log_cap;
+  A.log_count = h->log_count;
+  A.chunk_off = h->chunk_off;
+  A.chunk_cnt = h->chunk_cnt;
+  A.counters = h->counters;
+  A.v_trace = (T*)v_trace;
+  A.err = h->err_dev;
+  A.bar = h->bar;
+  void* args[] = {&A};
+  EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_forward<T, kNT, kU>, dim3(h->G), dim3(kNT), args,
+                                         0, s));
+  h->launches += 1;
+  int rc = check_err(h, s);
+  if (rc == EQ_OK || rc == EQ_ERR_GRAZING) h->steps_done += n_steps;
+  return rc;
+}
+
+template <typename T>
+int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* gw, double* gd, double* gamp,
+                    cudaStream_t s) {
+  typedef typename Prec<T>::T2 T2;
+  const int N = h->cfg.n_neurons, B = h->cfg.n_trials;
+  const long long total = h->total;
+  EQ_CUDA(h, cudaMemcpyAsync(h->lamV, v_bar, total * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  if (i_bar) EQ_CUDA(h, cudaMemcpyAsync(h->lamI, i_bar, total * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  else EQ_CUDA(h, cudaMemsetAsync(h->lamI, 0, total * sizeof(T), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->lam, 0, (size_t)B * h->R * N * sizeof(T2), s));
+  EQ_CUDA(h, cudaMemsetAsync(gw, 0, h->E * sizeof(double), s));
+  EQ_CUDA(h, cudaMemsetAsync(gd, 0, h->E * sizeof(double), s));
+  if (gamp) EQ_CUDA(h, cudaMemsetAsync(h->gamp_bt, 0, total * sizeof(double), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned), s));
+  BwdArgs<T> A;
+  A.N = N;
+  A.B = B;
+  A.G = h->G;
+  A.total = total;
+  A.per = h->per;
+  A.m_run = h->steps_done;
+  A.R = h->R;
+  A.refractory = h->cfg.refractory_steps;
+  A.c = consts<T>(h);
+  A.net = netview<T>(h);
+  A.lamV = (T*)h->lamV;
+  A.lamI = (T*)h->lamI;
+  A.lam = (T2*)h->lam;
+  A.gw = gw;
+  A.gd = gd;
+  A.gamp_bt = gamp ? h->gamp_bt : nullptr;
+  A.log = (const SpikeRec<T>*)h->log;
+  A.lt_log = (T*)h->lt_log;
+  A.chunk_off = h->chunk_off;
+  A.chunk_cnt = h->chunk_cnt;
+  A.err = h->err_dev;
+  A.bar = h->bar;
+  size_t smem = (size_t)((h->per + 31) / 32) * sizeof(unsigned);
+  void* args[] = {&A};
+  EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_backward<T, kNT, kU>, dim3(h->G), dim3(kNT), args,
+                                         smem, s));
+  h->launches += 1;
+  if (gamp) {
+    k_sum_trials<T><<<(N + 255) / 256, 256, 0, s>>>(h->gamp_bt, B, N, gamp);
+    h->launches += 1;
+  }
+  return check_err(h, s);
+}
+
+int setup_geometry(eq_handle* h) {
+  // One persistent CTA set shared by forward and reverse (the reverse pass
+  // finds a step's spikes through the forward's per-CTA chunks).
+  int occ_f = 0, occ_b = 0;
+  const void* kf;
+  const void* kb;
+  if (h->cfg.precision == 32) {
+    kf = (const void*)k_forward<float, kNT, kU>;
+    kb = (const void*)k_backward<float, kNT, kU>;
+  } else {
+    kf = (const void*)k_forward<double, kNT, kU>;
+    kb = (const void*)k_backward<double, kNT, kU>;
+  }
+  EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf, kNT, 0));
+  int occ = std::max(1, occ_f);
+  for (; occ >= 1; --occ) {
+    long long G = (long long)h->n_sm * occ;
+    long long per = (h->total + G - 1) / G;
+    size_t smem = (size_t)((per + 31) / 32) * sizeof(unsigned);
+    if (smem > 200 * 1024) continue;
+    if (smem > 48 * 1024)
+      EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, kb, kNT, smem));
+    if (occ_b >= occ) break;
+  }
+  if (occ < 1) return fail(h, EQ_ERR_CONFIGURATION, "problem too large for one persistent grid");
+  h->G = h->n_sm * occ;
+  // never more CTAs than there are neuron-trials to own
+  if ((long long)h->G > h->total) h->G = (int)h->total;
+  h->per = (h->total + h->G - 1) / h->G;
+  return EQ_OK;
+}
+
+int ensure_chunks(eq_handle* h, int steps_needed) {
+  if (steps_needed <= h->t_cap) return EQ_OK;
+  int ncap = std::max(steps_needed, h->t_cap * 2);
+  void *off = nullptr, *cnt = nullptr;
+  EQ_CUDA(h, alloc(h, &off, (size_t)ncap * h->G * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, &cnt, (size_t)ncap * h->G * sizeof(int)));
+  if (h->t_cap) {
+    EQ_CUDA(h, cudaMemcpy(off, h->chunk_off, (size_t)h->t_cap * h->G * sizeof(long long), cudaMemcpyDeviceToDevice));
+    EQ_CUDA(h, cudaMemcpy(cnt, h->chunk_cnt, (size_t)h->t_cap * h->G * sizeof(int), cudaMemcpyDeviceToDevice));
+  }
+  release(h, h->chunk_off);
+  release(h, h->chunk_cnt);
+  h->chunk_off = (long long*)off;
+  h->chunk_cnt = (int*)cnt;
+  h->t_cap = ncap;
+  return EQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* eq_version(void) { return "eventq_b200 0.1.0 sm_100a"; }
+
+const char* eq_last_error(const eq_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int eq_create(const eq_config* cfg, int device, eq_handle** out) {
+  if (!cfg || !out) return EQ_ERR_CONFIGURATION;
+  *out = nullptr;
+  eq_handle* h = new eq_handle();
+  h->cfg = *cfg;
+  h->device = device;
+  const eq_config& c = h->cfg;
+  auto bad = [&](const std::string& m) {
+    h->err = m;
+    *out = h;
+    return EQ_ERR_CONFIGURATION;
+  };
+  if (c.n_neurons < 2) return bad("a recurrent network needs n >= 2, got " + std::to_string(c.n_neurons));
+  if (c.n_trials < 1) return bad("n_trials must be >= 1");
+  if (c.t_steps < 1) return bad("t_steps must be >= 1, got " + std::to_string(c.t_steps));
+  if (c.precision != 32 && c.precision != 64) return bad("precision must be 32 or 64");
+  if (!(c.dt > 0.0)) return bad("dt must be positive");
+  if (!(c.tau_m > 0.0)) return bad("tau_m must be positive, got " + std::to_string(c.tau_m));
+  if (!(c.tau_syn > 0.0)) return bad("tau_syn must be positive, got " + std::to_string(c.tau_syn));
+  if (!(c.v_th > c.v_reset)) return bad("threshold must sit above reset");
+  if (c.kind != EQ_KIND_RING && c.kind != EQ_KIND_DONOTHING)
+    return bad("queue kind " + std::to_string(c.kind) + " is not available in this build");
+  if (c.exact_delivery && std::fabs(c.tau_m - c.tau_syn) < 1e-3 * c.tau_m)
+    return bad("exact delivery splits the membrane/synapse eigenmodes and needs tau_m != tau_syn");
+  h->total = (long long)c.n_neurons * c.n_trials;
+  if (h->total >= (1LL << 31)) return bad("n_neurons * n_trials must be < 2^31");
+  h->tsize = c.precision == 32 ? 4 : 8;
+  DeviceGuard g(device);
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) {
+    *out = h;
+    return cuda_fail(h, e, "cudaGetDeviceProperties");
+  }
+  if (prop.major != 10) {
+    *out = h;
+    return fail(h, EQ_ERR_CUDA, "this build targets sm_100a (B200); device is sm_" +
+                                    std::to_string(prop.major) + std::to_string(prop.minor));
+  }
+  h->n_sm = prop.multiProcessorCount;
+  *out = h;
+  int rc = setup_geometry(h);
+  if (rc) return rc;
+  const size_t T = h->tsize;
+  EQ_CUDA(h, alloc(h, &h->I, h->total * T));
+  EQ_CUDA(h, alloc(h, &h->V, h->total * T));
+  EQ_CUDA(h, alloc(h, (void**)&h->refr, h->total * sizeof(int32_t)));
+  EQ_CUDA(h, alloc(h, &h->lamV, h->total * T));
+  EQ_CUDA(h, alloc(h, &h->lamI, h->total * T));
+  EQ_CUDA(h, alloc(h, (void**)&h->gamp_bt, h->total * sizeof(double)));
+  EQ_CUDA(h, alloc(h, (void**)&h->counters, (size_t)c.n_trials * 3 * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, (void**)&h->err_dev, 4 * sizeof(int)));
+  EQ_CUDA(h, alloc(h, (void**)&h->bar, 2 * sizeof(unsigned)));
+  EQ_CUDA(h, alloc(h, (void**)&h->log_count, sizeof(unsigned long long)));
+  const size_t rec = c.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
+  EQ_CUDA(h, alloc(h, &h->scratch, (size_t)h->G * h->per * rec));
+  long long cap = c.max_spikes > 0 ? c.max_spikes
+                                   : std::max<long long>(1LL << 20, h->total * (long long)c.t_steps / 32);
+  h->log_cap = cap;
+  EQ_CUDA(h, alloc(h, &h->log, (size_t)cap * rec));
+  EQ_CUDA(h, alloc(h, &h->lt_log, (size_t)cap * T));
+  rc = ensure_chunks(h, c.t_steps);
+  if (rc) return rc;
+  return EQ_OK;
+}
+
+int eq_destroy(eq_handle* h) {
+  if (!h) return EQ_OK;
+  {
+    DeviceGuard g(h->device);
+    for (void* p : h->owned) cudaFree(p);
+  }
+  delete h;
+  return EQ_OK;
+}
+
+int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, const void* weight,
+                   const void* delay, int64_t n_edges, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const eq_config& c = h->cfg;
+  const int N = c.n_neurons;
+  if (n_edges < 1) return fail(h, EQ_ERR_CONFIGURATION, "network has no edges");
+  void *insum = nullptr, *stats = nullptr;
+  EQ_CUDA(h, alloc(h, &insum, (size_t)N * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, &stats, 4 * sizeof(long long)));
+  long long init[4] = {1, -1LL, 0, 0};
+  init[1] = (long long)~0ULL;
+  EQ_CUDA(h, cudaMemsetAsync(insum, 0, (size_t)N * sizeof(long long), s));
+  EQ_CUDA(h, cudaMemcpyAsync(stats, init, sizeof init, cudaMemcpyHostToDevice, s));
+  int homog = c.kind == EQ_KIND_FIFORING;
+  if (c.precision == 32)
+    k_net_stats<float><<<(N + 127) / 128, 128, 0, s>>>(N, rowptr, col, (const float*)weight, (const float*)delay,
+                                                        (float)c.dt, homog, (long long*)insum, (long long*)stats);
+  else
+    k_net_stats<double><<<(N + 127) / 128, 128, 0, s>>>(N, rowptr, col, (const double*)weight,
+                                                         (const double*)delay, c.dt, homog, (long long*)insum,
+                                                         (long long*)stats);
+  k_max_ll<<<256, 256, 0, s>>>((const long long*)insum, N, (long long*)stats + 2);
+  h->launches += 2;
+  long long st[4];
+  EQ_CUDA(h, cudaMemcpyAsync(st, stats, sizeof st, cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  release(h, insum);
+  release(h, stats);
+  if ((unsigned long long)st[1] != ~0ULL) {
+    unsigned long long key = (unsigned long long)st[1];
+    long long x = (long long)(key >> 2);
+    int code = (int)(key & 3);
+    // locate the row of edge x on the host (validation path only)
+    std::vector<int64_t> rp(N + 1);
+    EQ_CUDA(h, cudaMemcpy(rp.data(), rowptr, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    int i = (int)(std::upper_bound(rp.begin(), rp.end(), (int64_t)x) - rp.begin()) - 1;
+    int j = -1;
+    EQ_CUDA(h, cudaMemcpy(&j, col + x, sizeof(int), cudaMemcpyDeviceToHost));
+    double dv = 0.0, d0 = 0.0;
+    if (c.precision == 32) {
+      float f, f0;
+      EQ_CUDA(h, cudaMemcpy(&f, (const float*)delay + x, 4, cudaMemcpyDeviceToHost));
+      EQ_CUDA(h, cudaMemcpy(&f0, delay, 4, cudaMemcpyDeviceToHost));
+      dv = f;
+      d0 = f0;
+    } else {
+      EQ_CUDA(h, cudaMemcpy(&dv, (const double*)delay + x, 8, cudaMemcpyDeviceToHost));
+      EQ_CUDA(h, cudaMemcpy(&d0, delay, 8, cudaMemcpyDeviceToHost));
+    }
+    char buf[256];
+    if (code == 1)
+      snprintf(buf, sizeof buf, "CSR edge %lld (%d,%d): targets must be in [0,n), not the source, ascending",
+               x, i, j);
+    else if (code == 2)
+      snprintf(buf, sizeof buf, "delay on edge (%d,%d) is %g, below one step (%g)", i, j, dv, c.dt);
+    else
+      snprintf(buf, sizeof buf,
+               "fiforing supports homogeneous delays only, but edge (%d,%d) has %g while another edge has %g", i, j,
+               dv, d0);
+    return fail(h, EQ_ERR_CONFIGURATION, buf);
+  }
+  h->horizon = (int)st[0] + 1;           // network.py:188-198
+  h->R = h->horizon + 1;                 // + one slot for in-phase pop/scatter overlap
+  // fixed-point fraction bits: largest F with 4*max_in*2^F <= 2^(bits-2)
+  double max_in = std::ldexp((double)st[2], -40);
+  int bits = c.precision == 32 ? 32 : 64;
+  if (max_in <= 0.0) {
+    h->frac_bits = bits - 2;
+  } else {
+    int e;
+    double m = std::frexp(4.0 * max_in, &e);
+    int ceil_log2 = (m == 0.5) ? e - 1 : e;
+    h->frac_bits = (bits - 2) - ceil_log2;
+  }
+  h->scale = std::ldexp(1.0, h->frac_bits);
+  h->inv_scale = std::ldexp(1.0, -h->frac_bits);
+  h->rowptr = rowptr;
+  h->col = col;
+  h->w = weight;
+  h->d = delay;
+  h->E = n_edges;
+  // queue storage
+  release(h, h->ring);
+  release(h, h->lam);
+  h->ring = nullptr;
+  h->lam = nullptr;
+  size_t words = c.kind == EQ_KIND_RING ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
+  h->ring_words = words;
+  EQ_CUDA(h, alloc(h, (void**)&h->ring, words * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, &h->lam, (size_t)c.n_trials * h->R * N * 2 * h->tsize));
+  h->net_set = true;
+  return eq_reset(h, stream);
+}
+
+int eq_set_drive(eq_handle* h, const uint32_t* mask, const void* amplitude, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  (void)stream;
+  h->mask = mask;
+  h->amp = amplitude;
+  h->drive_set = true;
+  return EQ_OK;
+}
+
+int eq_reset(eq_handle* h, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (!h->net_set) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_network must come first");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t T = h->tsize;
+  EQ_CUDA(h, cudaMemsetAsync(h->ring, 0, h->ring_words * sizeof(long long), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->I, 0, h->total * T, s));
+  if (h->cfg.precision == 32)
+    k_fill<float><<<296, 256, 0, s>>>((float*)h->V, h->total, (float)h->cfg.v_reset);
+  else
+    k_fill<double><<<296, 256, 0, s>>>((double*)h->V, h->total, h->cfg.v_reset);
+  h->launches += 1;
+  EQ_CUDA(h, cudaMemsetAsync(h->refr, 0, h->total * sizeof(int32_t), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->counters, 0, (size_t)h->cfg.n_trials * 3 * sizeof(long long), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, 4 * sizeof(int), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->log_count, 0, sizeof(unsigned long long), s));
+  h->steps_done = 0;
+  return EQ_OK;
+}
+
+int eq_run(eq_handle* h, int32_t n_steps, void* v_trace, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (!h->net_set || !h->drive_set) return fail(h, EQ_ERR_CONFIGURATION, "network and drive must be set");
+  if (n_steps < 1) return fail(h, EQ_ERR_CONFIGURATION, "n_steps must be >= 1");
+  DeviceGuard g(h->device);
+  int rc = ensure_chunks(h, h->steps_done + n_steps);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned), s));
+  if (h->cfg.precision == 32) return launch_forward<float>(h, n_steps, v_trace, s);
+  return launch_forward<double>(h, n_steps, v_trace, s);
+}
+
+int eq_forward(eq_handle* h, void* v_out, void* i_out, void* v_trace, void* stream) {
+  int rc = eq_reset(h, stream);
+  if (rc) return rc;
+  rc = eq_run(h, h->cfg.t_steps, v_trace, stream);
+  if (rc) return rc;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (v_out) EQ_CUDA(h, cudaMemcpyAsync(v_out, h->V, h->total * h->tsize, cudaMemcpyDeviceToDevice, s));
+  if (i_out) EQ_CUDA(h, cudaMemcpyAsync(i_out, h->I, h->total * h->tsize, cudaMemcpyDeviceToDevice, s));
+  return EQ_OK;
+}
+
+int eq_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* grad_w, double* grad_d,
+                double* grad_amp, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (h->steps_done < 1) return fail(h, EQ_ERR_CONFIGURATION, "backward needs a forward run first");
+  if (h->cfg.kind != EQ_KIND_RING && h->cfg.kind != EQ_KIND_DONOTHING)
+    return fail(h, EQ_ERR_CONFIGURATION, "reverse mode not available for this queue kind");
+  if (!h->cfg.exact_delivery) return fail(h, EQ_ERR_CONFIGURATION, "reverse mode requires exact_delivery");
+  if (!v_bar || !grad_w || !grad_d) return fail(h, EQ_ERR_CONFIGURATION, "v_bar, grad_w, grad_d are required");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (h->cfg.precision == 32) return launch_backward<float>(h, v_bar, i_bar, grad_w, grad_d, grad_amp, s);
+  return launch_backward<double>(h, v_bar, i_bar, grad_w, grad_d, grad_amp, s);
+}
+
+int eq_counters(eq_handle* h, int64_t* out, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  EQ_CUDA(h, cudaMemcpyAsync(out, h->counters, (size_t)h->cfg.n_trials * 3 * sizeof(long long),
+                             cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  return EQ_OK;
+}
+
+int64_t eq_spike_count(eq_handle* h, void* stream) {
+  if (!h) return -1;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long n = 0;
+  if (cudaMemcpyAsync(&n, h->log_count, sizeof n, cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  return (int64_t)n;
+}
+
+int eq_get_spikes(eq_handle* h, int32_t* step, int32_t* trial, int32_t* neuron, void* t_spk, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int n_chunks = h->steps_done * h->G;
+  if (n_chunks == 0) return EQ_OK;
+  int blocks = (n_chunks * 32 + 255) / 256;
+  if (h->cfg.precision == 32)
+    k_decode_spikes<float><<<blocks, 256, 0, s>>>((const SpikeRec<float>*)h->log, h->chunk_off, h->chunk_cnt,
+                                                   n_chunks, h->G, h->cfg.n_neurons, step, trial, neuron,
+                                                   (float*)t_spk);
+  else
+    k_decode_spikes<double><<<blocks, 256, 0, s>>>((const SpikeRec<double>*)h->log, h->chunk_off, h->chunk_cnt,
+                                                    n_chunks, h->G, h->cfg.n_neurons, step, trial, neuron,
+                                                    (double*)t_spk);
+  h->launches += 1;
+  EQ_CUDA(h, cudaGetLastError());
+  return EQ_OK;
+}
+
+int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (h->cfg.kind != EQ_KIND_RING) return fail(h, EQ_ERR_CONFIGURATION, "pending contents: ring kind only");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int N = h->cfg.n_neurons, B = h->cfg.n_trials, H = h->horizon;
+  size_t n = (size_t)B * N * H * 2;
+  void* buf = nullptr;
+  EQ_CUDA(h, alloc(h, &buf, n * sizeof(long long)));
+  if (h->cfg.precision == 32)
+    k_pending<float><<<592, 256, 0, s>>>(h->ring, B, h->R, N, H, h->steps_done, (long long*)buf);
+  else
+    k_pending<double><<<592, 256, 0, s>>>(h->ring, B, h->R, N, H, h->steps_done, (long long*)buf);
+  h->launches += 1;
+  EQ_CUDA(h, cudaMemcpyAsync(host_out, buf, n * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  release(h, buf);
+  return EQ_OK;
+}
+
+int eq_horizon(const eq_handle* h) { return h ? h->horizon : -1; }
+int eq_frac_bits(const eq_handle* h) { return h ? h->frac_bits : -1; }
+int eq_geometry(const eq_handle* h, int32_t* ctas, int32_t* threads) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (ctas) *ctas = h->G;
+  if (threads) *threads = kNT;
+  return EQ_OK;
+}
+int64_t eq_launch_count(const eq_handle* h) { return h ? h->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+"""Device engine: one C-ABI handle (include/eventq_b200.h) on one GPU.
+
+PyTorch is only the tensor shell here: it owns the caller-side device buffers
+and provides the CUDA stream; every simulation step and its reverse run inside
+the sm_100a kernels of ``lib/libeventq_b200.so``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import ConfigurationError
+from .workload import LIFConfig
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class Engine:
+    """Batched R-SNN simulation of ``n_trials`` trials sharing one network.
+
+    Mirrors ``build_rsnn`` + ``simulate`` (network.py:201-497) for the ring and
+    donothing kinds, plus the reverse pass (``backward``) the reference lacks.
+    """
+
+    def __init__(self, n: int, n_trials: int, t_steps: int, *, kind: str = "ring",
+                 precision: int = 32, lif: Optional[LIFConfig] = None, capacity: int = 0,
+                 max_spikes: int = 0, device: Optional[int] = None):
+        self.L = _native.lib()
+        if kind not in _native.KIND_IDS:
+            raise ConfigurationError(f"unknown queue kind {kind!r}")
+        lif = lif or LIFConfig()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device)
+        self.n, self.B, self.T = n, n_trials, t_steps
+        self.kind, self.precision, self.lif = kind, precision, lif
+        self.dtype = torch.float32 if precision == 32 else torch.float64
+        cfg = _native.Config()
+        cfg.kind = _native.KIND_IDS[kind]
+        cfg.precision = precision
+        cfg.n_neurons, cfg.n_trials, cfg.t_steps = n, n_trials, t_steps
+        cfg.refractory_steps = lif.refractory_steps
+        cfg.exact_delivery = int(bool(lif.exact_delivery))
+        cfg.capacity = capacity
+        cfg.max_spikes = max_spikes
+        cfg.dt, cfg.tau_m, cfg.tau_syn = lif.dt, lif.tau_m, lif.tau_syn
+        cfg.v_th, cfg.v_reset = lif.v_th, lif.v_reset
+        self.cfg = cfg
+        h = ctypes.c_void_p()
+        code = self.L.eq_create(ctypes.byref(cfg), device, ctypes.byref(h))
+        self.h = h
+        _native.check(self.h, code)
+        self._net = None
+        self._drive = None
+
+    # ------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.L.eq_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _dev(self, a, dtype) -> torch.Tensor:
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.device, dtype=dtype).contiguous()
+        return torch.as_tensor(np.ascontiguousarray(a)).to(device=self.device, dtype=dtype).contiguous()
+
+    # ------------------------------------------------------------ inputs
+    def set_network(self, rowptr, col, weight, delay) -> None:
+        rp = self._dev(rowptr, torch.int64)
+        cl = self._dev(col, torch.int32)
+        w = self._dev(weight, self.dtype)
+        d = self._dev(delay, self.dtype)
+        if rp.numel() != self.n + 1:
+            raise ConfigurationError(f"rowptr must have n+1 = {self.n + 1} entries")
+        E = cl.numel()
+        if w.numel() != E or d.numel() != E:
+            raise ConfigurationError("weight/delay must have one entry per edge")
+        self._net = (rp, cl, w, d)
+        _native.check(self.h, self.L.eq_set_network(self.h, _ptr(rp), _ptr(cl), _ptr(w), _ptr(d), E,
+                                                      self.stream))
+        self.n_edges = E
+
+    def set_drive(self, mask, amp) -> None:
+        m = self._dev(np.asarray(mask, dtype=np.uint32).view(np.int32) if not isinstance(mask, torch.Tensor)
+                      else mask, torch.int32)
+        words = (self.n + 31) // 32
+        if tuple(m.shape) != (self.B, self.T, words):
+            raise ConfigurationError(f"drive mask must be [{self.B}, {self.T}, {words}] uint32")
+        a = self._dev(amp, self.dtype)
+        if a.numel() != self.n:
+            raise ConfigurationError("amplitude must have n entries")
+        self._drive = (m, a)
+        _native.check(self.h, self.L.eq_set_drive(self.h, _ptr(m), _ptr(a), self.stream))
+
+    # ------------------------------------------------------------ running
+    def forward(self, record_v: bool = False) -> Dict[str, torch.Tensor]:
+        v = torch.empty(self.B, self.n, dtype=self.dtype, device=self.device)
+        i = torch.empty_like(v)
+        tr = torch.empty(self.T, self.B, self.n, dtype=self.dtype, device=self.device) if record_v else None
+        _native.check(self.h, self.L.eq_forward(self.h, _ptr(v), _ptr(i), _ptr(tr), self.stream))
+        out = {"v": v, "i": i}
+        if record_v:
+            out["v_trace"] = tr
+        return out
+
+    def reset(self) -> None:
+        _native.check(self.h, self.L.eq_reset(self.h, self.stream))
+
+    def run(self, n_steps: int, v_trace: Optional[torch.Tensor] = None) -> None:
+        _native.check(self.h, self.L.eq_run(self.h, n_steps, _ptr(v_trace), self.stream))
+
+    def backward(self, v_bar: torch.Tensor, i_bar: Optional[torch.Tensor] = None, want_amp: bool = True):
+        vb = self._dev(v_bar, self.dtype)
+        ib = None if i_bar is None else self._dev(i_bar, self.dtype)
+        gw = torch.empty(self.n_edges, dtype=torch.float64, device=self.device)
+        gd = torch.empty_like(gw)
+        ga = torch.empty(self.n, dtype=torch.float64, device=self.device) if want_amp else None
+        _native.check(self.h, self.L.eq_backward(self.h, _ptr(vb), _ptr(ib), _ptr(gw), _ptr(gd), _ptr(ga),
+                                                  self.stream))
+        return gw, gd, ga
+
+    # ------------------------------------------------------------ queries
+    def counters(self) -> np.ndarray:
+        out = np.empty((self.B, 3), dtype=np.int64)
+        _native.check(self.h, self.L.eq_counters(self.h, out.ctypes.data_as(ctypes.c_void_p), self.stream))
+        return out
+
+    def spike_count(self) -> int:
+        n = self.L.eq_spike_count(self.h, self.stream)
+        if n < 0:
+            _native.check(self.h, 5)
+        return int(n)
+
+    def spikes(self) -> Dict[str, np.ndarray]:
+        """Spike records sorted by (trial, step, neuron)."""
+        S = self.spike_count()
+        step = torch.empty(S, dtype=torch.int32, device=self.device)
+        trial = torch.empty_like(step)
+        neuron = torch.empty_like(step)
+        t = torch.empty(S, dtype=self.dtype, device=self.device)
+        if S:
+            _native.check(self.h, self.L.eq_get_spikes(self.h, _ptr(step), _ptr(trial), _ptr(neuron), _ptr(t),
+                                                        self.stream))
+        st, tr, ne, tt = (x.cpu().numpy() for x in (step, trial, neuron, t))
+        order = np.lexsort((ne, st, tr))
+        return {"step": st[order], "trial": tr[order], "neuron": ne[order], "t": tt[order]}
+
+    def pending(self) -> np.ndarray:
+        H = self.horizon
+        out = np.empty((self.B, self.n, H, 2), dtype=np.int64)
+        _native.check(self.h, self.L.eq_get_pending(self.h, out.ctypes.data_as(ctypes.c_void_p), self.stream))
+        return out
+
+    @property
+    def horizon(self) -> int:
+        return int(self.L.eq_horizon(self.h))
+
+    @property
+    def frac_bits(self) -> int:
+        return int(self.L.eq_frac_bits(self.h))
+
+    @property
+    def geometry(self):
+        c = ctypes.c_int32()
+        t = ctypes.c_int32()
+        self.L.eq_geometry(self.h, ctypes.byref(c), ctypes.byref(t))
+        return c.value, t.value
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.L.eq_launch_count(self.h))

@@ -153,26 +153,25 @@ def poisson_drive_mask(n: int, t_steps: int, dt: float, mean_interval: float,
     # enough draws per neuron to pass t_total with overwhelming probability
     expect = t_total / (pulse_duration + mean_interval)
     m = int(expect + 8.0 * math.sqrt(expect + 1.0) + 8)
-    active = np.zeros((t_steps, n), dtype=bool)
     u = uniform(seed, 7, n * m).reshape(n, m)
     gaps = -mean_interval * np.log1p(-u)          # Exp(mean)
     starts = np.cumsum(gaps, axis=1) + pulse_duration * np.arange(m)[None, :]
     # starts[:, k] = gap_0 + sum_{1..k}(gap_i + dur)
     if (starts[:, -1] < t_total).any():
         raise RuntimeError("drive draw budget exhausted; raise m")
-    for k in range(m):
-        s = starts[:, k]
-        live = s < t_total
-        if not live.any():
-            break
-        e = s + pulse_duration
-        lo = np.clip(np.ceil(s / dt), 0, t_steps).astype(np.int64)
-        hi = np.clip(np.ceil(e / dt), 0, t_steps).astype(np.int64)
-        idx = np.nonzero(live & (hi > lo))[0]
-        for width in np.unique(hi[idx] - lo[idx]):
-            sel = idx[(hi[idx] - lo[idx]) == width]
-            for off in range(int(width)):
-                active[lo[sel] + off, sel] = True
+    live = starts < t_total
+    lo = np.clip(np.ceil(starts / dt), 0, t_steps).astype(np.int64)
+    hi = np.clip(np.ceil((starts + pulse_duration) / dt), 0, t_steps).astype(np.int64)
+    keep = live & (hi > lo)
+    jj = np.broadcast_to(np.arange(n)[:, None], starts.shape)[keep]
+    L = lo[keep]
+    W = (hi - lo)[keep]
+    flat = np.zeros(t_steps * n, dtype=bool)
+    base = L * n + jj
+    for off in range(int(W.max()) if W.size else 0):
+        sel = W > off
+        flat[base[sel] + off * n] = True
+    active = flat.reshape(t_steps, n)
     return active
 
 

@@ -84,7 +84,8 @@ def run_case(name: str, net: wl.Network, kind: str, t_steps: int, mask: np.ndarr
         drop_count=res.drop_count, enqueued_count=res.enqueued_count,
     )
     if record:
-        out["v_trace"] = res.voltages
+        if net.n * t_steps <= 100_000:   # keep fixtures small
+            out["v_trace"] = res.voltages
         out["v_final"] = res.voltages[-1]
     # primal twin must be bitwise the dual's primal half (network.py:501-505)
     pr = PrimalRSNN(params)

@@ -1,0 +1,179 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+* device-mode oracle, same precision: BITWISE — raster, final V and I, pending
+  ring contents (fixed-point ints), counters; reverse pass: lambda-derived
+  gradients bitwise at one trial (same accumulation order), rtol 1e-12 across
+  trials (double atomics reorder the trial sum), grad_amp bitwise;
+* reference fixtures (Python reference outputs) in fp64: raster identical,
+  voltages within 1e-9 (SURVEY §8(c) precision contract);
+* fp32: the north-star tolerance rtol 1e-5 applies to floats vs an fp32
+  restatement — here the restatement is bitwise, which is stronger.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from golden_cases import BY_NAME, CASES, edge_index
+from oracle.oracle import OracleSession
+from paper_2512_05906_b200 import workload as wl
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _engine(net, mask, amp, B, T, precision, kind="ring", refractory=0, capacity=0):
+    from paper_2512_05906_b200.engine import Engine
+    lif = wl.LIFConfig(refractory_steps=refractory)
+    eng = Engine(net.n, B, T, kind=kind, precision=precision, lif=lif, capacity=capacity)
+    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+    eng.set_drive(mask, amp)
+    return eng
+
+
+def _oracle(net, mask, amp, B, T, precision, F, kind="ring", refractory=0, mode="device"):
+    s = OracleSession(n=net.n, n_trials=B, t_steps=T, kind=kind, mode=mode, precision=precision,
+                      frac_bits=F, refractory_steps=refractory)
+    s.set_network(net.rowptr, net.col, net.weight, net.delay)
+    s.set_drive(mask, amp)
+    return s
+
+
+def _sorted_spikes(d):
+    order = np.lexsort((d["neuron"], d["step"], d["trial"]))
+    return np.stack([d["trial"][order], d["step"][order], d["neuron"][order]], 1), d["t"][order]
+
+
+def _compare_forward(net, mask, amp, B, T, precision, refractory=0, backward=True):
+    eng = _engine(net, mask, amp, B, T, precision, refractory=refractory)
+    out = eng.forward()
+    F = eng.frac_bits
+    s = _oracle(net, mask, amp, B, T, precision, F, refractory=refractory)
+    ref = s.forward()
+    assert s.horizon == eng.horizon
+    got = eng.spikes()
+    r_g, t_g = _sorted_spikes(got)
+    r_o, t_o = _sorted_spikes(ref)
+    assert r_g.shape == r_o.shape and np.array_equal(r_g, r_o), "raster differs"
+    assert np.array_equal(t_g.astype(np.float64), t_o)
+    assert np.array_equal(out["v"].double().cpu().numpy(), ref["v"])
+    assert np.array_equal(out["i"].double().cpu().numpy(), ref["i"])
+    assert np.array_equal(eng.counters(), ref["counters"])
+    assert np.array_equal(eng.pending(), ref["pending"])
+    if backward:
+        vbar = 2.0 * (out["v"].double() - 0.25)
+        vbar_t = vbar.to(out["v"].dtype)
+        gw, gd, ga = eng.backward(vbar_t)
+        ow, od, oa = s.backward(vbar_t.double().cpu().numpy())
+        gw, gd, ga = (x.cpu().numpy() for x in (gw, gd, ga))
+        if B == 1:
+            assert np.array_equal(gw, ow) and np.array_equal(gd, od)
+        else:
+            np.testing.assert_allclose(gw, ow, rtol=1e-12, atol=1e-300)
+            np.testing.assert_allclose(gd, od, rtol=1e-12, atol=1e-300)
+        assert np.array_equal(ga, oa)
+    return eng, out
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_n40", "dense_ring_refr3_n10", "sparse_ring_n100"])
+def test_golden_inputs_bitwise_vs_oracle(name, precision):
+    case = BY_NAME[name]
+    net, mask, amp = case.inputs()
+    _compare_forward(net, mask, amp, 1, case.t_steps, precision, refractory=case.refractory)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_multi_trial_bitwise_vs_oracle(precision):
+    net = wl.random_network(300, 30, 11, delay_steps=(1, 20), w_mean=0.02, w_std=0.01)
+    B, T = 3, 400
+    mask = wl.drive_masks(300, B, T, 1e-3, seed0=77)
+    _compare_forward(net, mask, np.full(300, 12.0), B, T, precision)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_c1_full_size_bitwise_vs_oracle(precision):
+    wk = wl.make_workload("C1", n_trials=2)
+    _compare_forward(wk.net, wk.mask, wk.amp, wk.n_trials, wk.t_steps, precision)
+
+
+@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_n40", "dense_ring_refr3_n10", "sparse_ring_n100",
+                                  "c1_ring"])
+def test_fp64_gpu_vs_reference_fixture(name):
+    """Python reference outputs (fixtures) vs the GPU in fp64."""
+    case = BY_NAME[name]
+    path = os.path.join(GOLDEN, name + ".npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture missing")
+    g = np.load(path)
+    net, mask, amp = case.inputs()
+    eng = _engine(net, mask, amp, 1, case.t_steps, 64, refractory=case.refractory)
+    out = eng.forward()
+    sp = eng.spikes()
+    raster = np.stack([sp["step"], sp["neuron"]], 1)
+    order = np.lexsort((raster[:, 1], raster[:, 0]))
+    assert np.array_equal(raster[order], g["raster"])
+    np.testing.assert_allclose(out["v"][0].cpu().numpy(), g["v_final_primal"], rtol=1e-9, atol=1e-12)
+    # reverse mode vs the reference's forward-mode JVP along the stored directions
+    if len(g["jvp"]):
+        vbar = 2.0 * (out["v"] - 0.25)
+        gw, gd, ga = (x.cpu().numpy() for x in eng.backward(vbar))
+        for (p, i, j), jvp in zip(g["directions"].tolist(), g["jvp"].tolist()):
+            got = ga[i] if p == 2 else (gw if p == 0 else gd)[edge_index(net, i, j)]
+            assert got == pytest.approx(jvp, rel=1e-7, abs=1e-10), (p, i, j)
+
+
+def test_trace_matches_oracle():
+    case = BY_NAME["dense_ring_n8"]
+    net, mask, amp = case.inputs()
+    eng = _engine(net, mask, amp, 1, case.t_steps, 64)
+    out = eng.forward(record_v=True)
+    s = OracleSession(n=net.n, n_trials=1, t_steps=case.t_steps, mode="device", precision=64,
+                      frac_bits=eng.frac_bits, record_v=True)
+    s.set_network(net.rowptr, net.col, net.weight, net.delay)
+    s.set_drive(mask, amp)
+    ref = s.forward()
+    assert np.array_equal(out["v_trace"][:, 0].cpu().numpy(), ref["v_trace"][0])
+
+
+def test_stepwise_run_equals_forward():
+    """eq_run in pieces (network_step granularity) == one eq_forward."""
+    import torch
+    case = BY_NAME["sparse_ring_n100"]
+    net, mask, amp = case.inputs()
+    eng = _engine(net, mask, amp, 1, case.t_steps, 32)
+    full = eng.forward()["v"].clone()
+    eng.reset()
+    for chunk in (1, 7, 92, 400, 500):
+        eng.run(chunk)
+    torch.cuda.synchronize()
+    v = torch.empty_like(full)
+    # the handle's V is exposed through a zero-step forward copy: re-run to compare raster instead
+    sp_pieces = eng.spikes()
+    eng.forward()
+    sp_full = eng.spikes()
+    for k in ("trial", "step", "neuron", "t"):
+        assert np.array_equal(sp_pieces[k], sp_full[k])
+    del v
+
+
+def test_donothing_counts_every_event_as_dropped():
+    case = BY_NAME["dense_donothing_n8"]
+    net, mask, amp = case.inputs()
+    g = np.load(os.path.join(GOLDEN, case.name + ".npz"))
+    eng = _engine(net, mask, amp, 1, case.t_steps, 64, kind="donothing")
+    eng.forward()
+    spikes, events, drops = eng.counters()[0].tolist()
+    assert spikes == int(g["spike_count"]) and drops == int(g["drop_count"]) == events
+
+
+def test_configuration_errors_name_the_edge():
+    from paper_2512_05906_b200.errors import ConfigurationError
+    net = wl.random_network(20, 5, 3, delay_steps=(1, 8))
+    net.delay[7] = 0.5e-3
+    src = np.repeat(np.arange(net.n), np.diff(net.rowptr))
+    mask = wl.drive_masks(20, 1, 50, 1e-3)
+    with pytest.raises(ConfigurationError, match=rf"edge \({src[7]},{net.col[7]}\).*below one step"):
+        _engine(net, mask, np.full(20, 12.0), 1, 50, 32)
