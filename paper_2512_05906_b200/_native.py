@@ -61,6 +61,7 @@ def lib() -> ctypes.CDLL:
         "eq_frac_bits": (ctypes.c_int, [H]),
         "eq_geometry": (ctypes.c_int, [H, vp, vp]),
         "eq_launch_count": (i64, [H]),
+        "eq_debug_timeline": (ctypes.c_int, [H, ctypes.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -73,7 +74,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive",
             "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_counters", "eq_spike_count",
             "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",
-            "eq_launch_count")
+            "eq_launch_count", "eq_debug_timeline")
 
 
 def check(handle, code: int) -> None:

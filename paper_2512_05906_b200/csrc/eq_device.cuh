@@ -55,8 +55,12 @@ __device__ __forceinline__ void unpack2(long long p, long long& qs, long long& q
 
 // ---------------------------------------------------------------- memory
 
-__device__ __forceinline__ long long ld_cg(const long long* p) { return __ldcg(p); }
-__device__ __forceinline__ void st_cg(long long* p, long long v) { __stcg(p, v); }
+// Slot rows are written by other CTAs' red.add (at L2) in earlier phases; every
+// phase starts after grid_sync's acquire fence, which invalidates L1, so plain
+// (weak) accesses observe them.  __ldcg/__stcg compile to STRONG.GPU accesses on
+// sm_100a and were 5x slower in the pop loop.
+__device__ __forceinline__ long long ld_slot(const long long* p) { return *p; }
+__device__ __forceinline__ void st_slot(long long* p, long long v) { *p = v; }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -86,35 +90,56 @@ __device__ __forceinline__ void raise_error(int* err, int code, int step, int tr
   }
 }
 
-// Grid-wide barrier for a cooperative (co-resident) launch: sense by generation
-// counter, release/acquire at gpu scope, 20 s watchdog so a bug can never wedge
-// the GPU (the kernel then exits with EQ_ERR_CUDA).
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Grid-wide barrier for a cooperative (co-resident) launch.  bar[0] = arrival
+// count, bar[32] = generation (separate 128-byte lines so spinning readers do
+// not queue behind arrivals).  Arrival is an acq_rel atomic (cumulative over
+// the CTA's writes ordered before it by bar.sync); waiters spin with relaxed
+// loads (no L1 invalidation per poll) and take one acquire fence on exit.  No
+// seq_cst fences: MEMBAR.SC.GPU on 296 CTAs per step cost ~100 us here.  A 20 s
+// watchdog turns a wedged barrier into EQ_ERR_CUDA instead of a hung GPU.
 __device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* err) {
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
     s_ok = 1;
     unsigned* count = bar;
-    unsigned* gen = bar + 1;
-    unsigned g = ld_acquire(gen);
-    __threadfence();
-    unsigned prev = atomicAdd(count, 1u);
+    unsigned* gen = bar + 32;
+    unsigned g = ld_relaxed(gen);
+    unsigned prev = atom_add_acq_rel(count, 1u);
     if (prev == nblocks - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
+      st_relaxed(count, 0u);
       st_release(gen, g + 1);
     } else {
-      unsigned long long t0 = globaltimer();
-      while (ld_acquire(gen) == g) {
-        __nanosleep(40);
-        if (globaltimer() - t0 > 20000000000ULL) {
-          atomicCAS(err, 0, EQ_ERR_CUDA);
-          s_ok = 0;
-          break;
+      unsigned long long t0 = 0;
+      int spins = 0;
+      while (ld_relaxed(gen) == g) {
+        if (++spins > 64) {
+          __nanosleep(64);
+          if (t0 == 0) t0 = globaltimer();
+          else if (globaltimer() - t0 > 20000000000ULL) {
+            atomicCAS(err, 0, EQ_ERR_CUDA);
+            s_ok = 0;
+            break;
+          }
         }
       }
     }
-    __threadfence();
+    fence_acq_rel_gpu();
   }
   __syncthreads();
   return s_ok;

@@ -60,6 +60,7 @@ struct FwdArgs {
   int* chunk_cnt;        // [m][G]
   long long* counters;   // [B][3]
   T* v_trace;            // [m1-m0][B][N] or null
+  unsigned long long* tl;  // debug timeline [m][G][4] (globaltimer ns) or null
   int* err;
   unsigned* bar;
 };
@@ -69,6 +70,10 @@ struct FwdShared {
   static constexpr int kCap = 1024;   // spikes staged in smem per step per CTA
   static constexpr int kTrials = 8;   // per-CTA trial counters kept in smem
 };
+
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int m, int G, int cta, int k) {
+  if (tl && threadIdx.x == 0) tl[((size_t)m * G + cta) * 4 + k] = globaltimer();
+}
 
 template <typename T>
 __device__ __forceinline__ bool drive_bit(const NetView<T>& net, int b, int m, int j) {
@@ -101,6 +106,7 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
   for (int m = A.m0; m < A.m1; ++m) {
     if (tid == 0) s_n = 0;
     __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 0);
     // ---------------- neuron update: pop, synapse, membrane, crossing
     for (long long base = begin; base < end; base += (long long)NT * U) {
       long long slot_v[U][2];
@@ -109,21 +115,18 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
       bool on[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        long long idx = base + (long long)u * NT + tid;
+        const int idx = (int)base + u * NT + tid;
         slot_v[u][0] = slot_v[u][1] = 0;
         if (idx < end) {
-          int b = (int)(idx / A.N);
-          int j = (int)(idx - (long long)b * A.N);
+          const int b = idx / A.N;
+          const int j = idx - b * A.N;
           size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
           if (A.kind == EQ_KIND_RING) {
             if (P::kSlotWords == 1) {
-              slot_v[u][0] = ld_cg(A.ring + so);
-              st_cg(A.ring + so, 0);
+              slot_v[u][0] = ld_slot(A.ring + so);
             } else {
-              slot_v[u][0] = ld_cg(A.ring + 2 * so);
-              slot_v[u][1] = ld_cg(A.ring + 2 * so + 1);
-              st_cg(A.ring + 2 * so, 0);
-              st_cg(A.ring + 2 * so + 1, 0);
+              slot_v[u][0] = ld_slot(A.ring + 2 * so);
+              slot_v[u][1] = ld_slot(A.ring + 2 * so + 1);
             }
           }
           Iv[u] = A.I[idx];
@@ -134,10 +137,10 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        long long idx = base + (long long)u * NT + tid;
+        const int idx = (int)base + u * NT + tid;
         if (idx >= end) continue;
-        int b = (int)(idx / A.N);
-        int j = (int)(idx - (long long)b * A.N);
+        const int b = idx / A.N;
+        const int j = idx - b * A.N;
         T ps, pm;
         if (P::kSlotWords == 1) {
           long long qs, qm;
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
             rf[u] = A.refractory;
             int pos = atomicAdd(&s_n, 1);
             SpikeRec<T> rec;
-            rec.idx = (int)idx;
+            rec.idx = idx;
             rec.t = t_spk;
             rec.a = a;
             rec.vh = v;
@@ -184,6 +187,24 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
       }
     }
     __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 1);
+    // Clear the popped slot row (RingQueue._pop_raw zeroes it, queues.py:114-117).
+    // Done here, not next to the load: a store to the line a pending load is
+    // filling stalled the pop loop ~8x.  Row m mod R receives no red.add in
+    // this phase (fan-out targets rows m+2 .. m+horizon, R = horizon + 1).
+    if (A.kind == EQ_KIND_RING) {
+      const int row = m % A.R;
+      for (int idx = (int)begin + tid; idx < end; idx += NT) {
+        const int b = idx / A.N;
+        const size_t so = ((size_t)b * A.R + row) * A.N + (idx - b * A.N);
+        if (P::kSlotWords == 1) {
+          st_slot(A.ring + so, 0);
+        } else {
+          st_slot(A.ring + 2 * so, 0);
+          st_slot(A.ring + 2 * so + 1, 0);
+        }
+      }
+    }
     const int nspk = s_n;
     // ---------------- fan-out (network.py:583-611): one warp per spike
     for (int k = warp; k < nspk; k += NT / kWarp) {
@@ -246,7 +267,10 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
     if (s_off + nspk <= A.log_cap) {
       for (int k = tid; k < nspk; k += NT) A.log[s_off + k] = k < kCap ? s_spk[k] : spill[k - kCap];
     }
+    __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err)) break;
+    tl_mark(A.tl, m, A.G, cta, 3);
     if (ld_volatile(A.err) != 0) break;
   }
   __syncthreads();
@@ -279,6 +303,7 @@ struct BwdArgs {
   T* lt_log;                   // dL/dt_spk per log record
   const long long* chunk_off;
   const int* chunk_cnt;
+  unsigned long long* tl;  // debug timeline [m][G][4] or null
   int* err;
   unsigned* bar;
 };
@@ -298,6 +323,7 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
   __syncthreads();
 
   for (int m = A.m_run - 1; m >= 0; --m) {
+    tl_mark(A.tl, m, A.G, cta, 0);
     const long long off = A.chunk_off[(size_t)m * A.G + cta];
     const int cnt = A.chunk_cnt[(size_t)m * A.G + cta];
     // ---------------- R-fanout(m): own spikes, one warp per spike
@@ -318,7 +344,7 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
         T phi = (T)st * c.dt - t_post;
         T es = eq_exp_t(-phi / c.tau_s);
         T em = eq_exp_t(-phi / c.tau_m);
-        T2 L = __ldcg(lam_b + (size_t)(st % A.R) * A.N + j);
+        T2 L = lam_b[(size_t)(st % A.R) * A.N + j];   // weak load: see ld_slot
         T g_w = es * L.x + em * L.y;
         T g_tp = w * (es * L.x / c.tau_s + em * L.y / c.tau_m);
         atomicAdd(A.gw + x, (double)g_w);
@@ -333,20 +359,21 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
       }
     }
     __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 1);
     // ---------------- R-neuron(m)
     for (long long base = begin; base < end; base += (long long)NT * U) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        long long idx = base + (long long)u * NT + tid;
+        const int idx = (int)base + u * NT + tid;
         if (idx >= end) continue;
-        int b = (int)(idx / A.N);
-        int j = (int)(idx - (long long)b * A.N);
+        const int b = idx / A.N;
+        const int j = idx - b * A.N;
         T lv = A.lamV[idx];
         T la, lvh;
-        long long loc = idx - begin;
+        const int loc = idx - (int)begin;
         if ((s_bits[loc >> 5] >> (loc & 31)) & 1u) {
           int k = 0;
-          while (k < cnt && A.log[off + k].idx != (int)idx) ++k;
+          while (k < cnt && A.log[off + k].idx != idx) ++k;
           SpikeRec<T> rec = A.log[off + k];
           T lt0 = A.lt_log[off + k];
           T t = rec.t, a = rec.a, vh = rec.vh;
@@ -378,7 +405,10 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
       long long loc = (long long)A.log[off + k].idx - begin;
       s_bits[loc >> 5] = 0u;
     }
+    __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err)) break;
+    tl_mark(A.tl, m, A.G, cta, 3);
     if (ld_volatile(A.err) != 0) break;
   }
 }

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -78,6 +79,9 @@ struct eq_handle {
   void* lam = nullptr;
   void* lt_log = nullptr;
   double* gamp_bt = nullptr;
+  unsigned long long* tl_f = nullptr;   // debug timelines (EQ_TIMELINE=1)
+  unsigned long long* tl_b = nullptr;
+  int tl_steps = 0;
   int steps_done = 0;
   long long launches = 0;
   std::vector<void*> owned;
@@ -306,6 +310,7 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
   A.chunk_cnt = h->chunk_cnt;
   A.counters = h->counters;
   A.v_trace = (T*)v_trace;
+  A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
   void* args[] = {&A};
@@ -330,7 +335,7 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   EQ_CUDA(h, cudaMemsetAsync(gw, 0, h->E * sizeof(double), s));
   EQ_CUDA(h, cudaMemsetAsync(gd, 0, h->E * sizeof(double), s));
   if (gamp) EQ_CUDA(h, cudaMemsetAsync(h->gamp_bt, 0, total * sizeof(double), s));
-  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 64 * sizeof(unsigned), s));
   BwdArgs<T> A;
   A.N = N;
   A.B = B;
@@ -352,6 +357,7 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   A.lt_log = (T*)h->lt_log;
   A.chunk_off = h->chunk_off;
   A.chunk_cnt = h->chunk_cnt;
+  A.tl = (h->tl_b && A.m_run <= h->tl_steps) ? h->tl_b : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
   size_t smem = (size_t)((h->per + 31) / 32) * sizeof(unsigned);
@@ -395,7 +401,9 @@ int setup_geometry(eq_handle* h) {
   h->G = h->n_sm * occ;
   // never more CTAs than there are neuron-trials to own
   if ((long long)h->G > h->total) h->G = (int)h->total;
-  h->per = (h->total + h->G - 1) / h->G;
+  // ranges in whole warps so a warp's 32 neurons share one drive-mask word
+  h->per = ((h->total + h->G - 1) / h->G + 31) / 32 * 32;
+  h->G = (int)((h->total + h->per - 1) / h->per);
   return EQ_OK;
 }
 
@@ -477,7 +485,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   EQ_CUDA(h, alloc(h, (void**)&h->gamp_bt, h->total * sizeof(double)));
   EQ_CUDA(h, alloc(h, (void**)&h->counters, (size_t)c.n_trials * 3 * sizeof(long long)));
   EQ_CUDA(h, alloc(h, (void**)&h->err_dev, 4 * sizeof(int)));
-  EQ_CUDA(h, alloc(h, (void**)&h->bar, 2 * sizeof(unsigned)));
+  EQ_CUDA(h, alloc(h, (void**)&h->bar, 64 * sizeof(unsigned)));
   EQ_CUDA(h, alloc(h, (void**)&h->log_count, sizeof(unsigned long long)));
   const size_t rec = c.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
   EQ_CUDA(h, alloc(h, &h->scratch, (size_t)h->G * h->per * rec));
@@ -488,6 +496,15 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   EQ_CUDA(h, alloc(h, &h->lt_log, (size_t)cap * T));
   rc = ensure_chunks(h, c.t_steps);
   if (rc) return rc;
+  const char* tl = getenv("EQ_TIMELINE");
+  if (tl && tl[0] == '1') {
+    h->tl_steps = c.t_steps;
+    size_t nb = (size_t)c.t_steps * h->G * 4 * sizeof(unsigned long long);
+    EQ_CUDA(h, alloc(h, (void**)&h->tl_f, nb));
+    EQ_CUDA(h, alloc(h, (void**)&h->tl_b, nb));
+    EQ_CUDA(h, cudaMemset(h->tl_f, 0, nb));
+    EQ_CUDA(h, cudaMemset(h->tl_b, 0, nb));
+  }
   return EQ_OK;
 }
 
@@ -622,7 +639,7 @@ int eq_reset(eq_handle* h, void* stream) {
   EQ_CUDA(h, cudaMemsetAsync(h->refr, 0, h->total * sizeof(int32_t), s));
   EQ_CUDA(h, cudaMemsetAsync(h->counters, 0, (size_t)h->cfg.n_trials * 3 * sizeof(long long), s));
   EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, 4 * sizeof(int), s));
-  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 64 * sizeof(unsigned), s));
   EQ_CUDA(h, cudaMemsetAsync(h->log_count, 0, sizeof(unsigned long long), s));
   h->steps_done = 0;
   return EQ_OK;
@@ -636,7 +653,7 @@ int eq_run(eq_handle* h, int32_t n_steps, void* v_trace, void* stream) {
   int rc = ensure_chunks(h, h->steps_done + n_steps);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 64 * sizeof(unsigned), s));
   if (h->cfg.precision == 32) return launch_forward<float>(h, n_steps, v_trace, s);
   return launch_forward<double>(h, n_steps, v_trace, s);
 }
@@ -736,5 +753,17 @@ int eq_geometry(const eq_handle* h, int32_t* ctas, int32_t* threads) {
   return EQ_OK;
 }
 int64_t eq_launch_count(const eq_handle* h) { return h ? h->launches : -1; }
+
+/* Debug: per-step, per-CTA phase timestamps (ns) of the last forward (which=0)
+ * or reverse (which=1) run, [t_steps][ctas][4]; needs EQ_TIMELINE=1 at create. */
+int eq_debug_timeline(eq_handle* h, int which, uint64_t* host_out) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  unsigned long long* src = which ? h->tl_b : h->tl_f;
+  if (!src) return fail(h, EQ_ERR_CONFIGURATION, "timeline disabled (set EQ_TIMELINE=1 before eq_create)");
+  DeviceGuard g(h->device);
+  EQ_CUDA(h, cudaDeviceSynchronize());
+  EQ_CUDA(h, cudaMemcpy(host_out, src, (size_t)h->tl_steps * h->G * 4 * 8, cudaMemcpyDeviceToHost));
+  return EQ_OK;
+}
 
 }  // extern "C"
