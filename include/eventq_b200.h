@@ -129,8 +129,9 @@ int eq_geometry(const eq_handle* h, int32_t* ctas, int32_t* threads);
 /* Number of kernels this handle has launched (for launch accounting). */
 int64_t eq_launch_count(const eq_handle* h);
 /* Debug: per-step, per-CTA phase timestamps (ns, %globaltimer) of the last
- * forward (which=0) or reverse (which=1) launch, uint64[t_steps][ctas][4]:
- * step start, after neuron/R-fanout phase, before the grid barrier, after it.
+ * forward (which=0) or reverse (which=1) launch, uint64[t_steps][ctas][8]:
+ * [0] step start, [1] after the neuron (fwd) / R-fanout (rev) phase, [2] before
+ * the grid barrier, [3] after it, [4..7] kernel-specific sub-phase marks (0 = unset).
  * Only when the environment had EQ_TIMELINE=1 at eq_create. */
 int eq_debug_timeline(eq_handle* h, int which, uint64_t* host_out);
 

@@ -389,8 +389,8 @@ int run_forward(Session& s) {
  *     Lambda_s, Lambda_m at its events' delivery steps s (zero for s >= T) and
  *     produces dL/dw_e, dL/dd_e and dL/dt_spk.
  *   R-neuron(m): per neuron, the adjoint of F1..F6 of PrimalRSNN.step.
- * dL/dt_spk of one spike is reduced over its row with the same 32-lane
- * partial + xor-butterfly order the GPU warp uses, so lambda_t matches bitwise.
+ * dL/dt_spk of one spike is the sequential sum over its row in CSR order (the
+ * order the kernel's per-spike reduction uses), so lambda_t matches bitwise.
  * Gradients accumulate in double.
  */
 template <typename T, bool DEV>
@@ -445,17 +445,17 @@ int run_backward(Session& s, const double* vbar, const double* ibar, double* gw,
           const Spike& sp = s.spikes[k];
           int i = sp.neuron;
           T t = (T)sp.t;
-          T part[32];
-          for (int l = 0; l < 32; ++l) part[l] = (T)0;
+          // dL/dt_spk: sequential sum over the row in CSR order, zeros for
+          // events delivered at or after T (the kernel's reduction order)
+          T lt_sum = (T)0;
           int64_t r0 = s.rowptr[i], r1 = s.rowptr[i + 1];
           for (int64_t x = r0; x < r1; ++x) {
-            int lane = (int)((x - r0) & 31);
             int j = s.col[x];
             T w = (T)s.w[x];
             T dd = (T)s.d[x];
             T t_post = t + dd;
             int32_t st = delivery<T, DEV>(t_post, dd, dt, m);
-            if (st >= TT) continue;
+            if (st >= TT) { lt_sum = lt_sum + (T)0; continue; }
             T phi = (T)st * dt - t_post;
             T es = xexp<T, DEV>(-phi / tau_s);
             T em = xexp<T, DEV>(-phi / tau_m);
@@ -465,11 +465,9 @@ int run_backward(Session& s, const double* vbar, const double* ibar, double* gw,
             T g_tp = w * (es * as / tau_s + em * am / tau_m);
             lw[x] += (double)g_w;
             ld[x] += (double)g_tp;
-            part[lane] = part[lane] + g_tp;
+            lt_sum = lt_sum + g_tp;
           }
-          for (int off = 16; off >= 1; off >>= 1)
-            for (int l = 0; l < off; ++l) part[l] = part[l] + part[l + off];
-          spk_lt[i] = part[0];
+          spk_lt[i] = lt_sum;
           spk_of[i] = k;
         }
         // R-neuron(m)

@@ -72,7 +72,39 @@ struct FwdShared {
 };
 
 __device__ __forceinline__ void tl_mark(unsigned long long* tl, int m, int G, int cta, int k) {
-  if (tl && threadIdx.x == 0) tl[((size_t)m * G + cta) * 4 + k] = globaltimer();
+  if (tl && threadIdx.x == 0) tl[((size_t)m * G + cta) * 8 + k] = globaltimer();
+}
+
+// Exclusive prefix over a staged spike batch's row lengths, by warp 0.
+// On entry pre[k+1] = len[k] (k < n); on exit pre[0..n] is the exclusive scan.
+__device__ __forceinline__ void warp0_scan(int* pre, int n) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int carry = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int k = base + lane;
+      int v = k < n ? pre[k + 1] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      if (k < n) pre[k + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) pre[0] = 0;
+  }
+}
+
+// Row of flat event f: the largest k < n with pre[k] <= f.
+__device__ __forceinline__ int find_row(const int* pre, int n, int f) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (pre[mid] <= f) lo = mid;
+    else hi = mid;
+  }
+  return lo;
 }
 
 template <typename T>
@@ -88,12 +120,13 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
   constexpr int kCap = FwdShared<NT>::kCap;
   constexpr int kTr = FwdShared<NT>::kTrials;
   __shared__ SpikeRec<T> s_spk[kCap];
+  __shared__ long long s_r0[kCap];
+  __shared__ int s_pre[kCap + 1];
   __shared__ int s_n;
   __shared__ long long s_off;
   __shared__ unsigned long long s_ctr[kTr][2];
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
   const int cta = blockIdx.x;
   const long long begin = (long long)cta * A.per;
   const long long end = begin + A.per < A.total ? begin + A.per : A.total;
@@ -205,53 +238,9 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
         }
       }
     }
+    __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 4);
     const int nspk = s_n;
-    // ---------------- fan-out (network.py:583-611): one warp per spike
-    for (int k = warp; k < nspk; k += NT / kWarp) {
-      SpikeRec<T> rec = k < kCap ? s_spk[k] : spill[k - kCap];
-      int b = rec.idx / A.N;
-      int i = rec.idx - b * A.N;
-      long long r0 = __ldg(A.net.rowptr + i), r1 = __ldg(A.net.rowptr + i + 1);
-      if (lane == 0) {
-        int tb = b - b_first;
-        unsigned long long ev = (unsigned long long)(r1 - r0);
-        if (tb < kTr) {
-          atomicAdd(&s_ctr[tb][0], 1ULL);
-          atomicAdd(&s_ctr[tb][1], ev);
-        } else {
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), ev);
-        }
-        if (A.kind == EQ_KIND_DONOTHING)
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), ev);
-      }
-      if (A.kind != EQ_KIND_RING) continue;
-      long long* ring_b = A.ring + (size_t)b * A.R * A.N * P::kSlotWords;
-      for (long long x = r0 + lane; x < r1; x += kWarp) {
-        int j = __ldg(A.net.col + x);
-        T w = __ldg(A.net.w + x);
-        T d = __ldg(A.net.d + x);
-        T t_post = rec.t + d;                              // :588
-        int ds = delivery_step(t_post, d, c.dt, m);        // jumps.py:96
-        T ws, wm;
-        if (A.exact) {
-          T phi = (T)ds * c.dt - t_post;                   // :599
-          ws = w * eq_exp_t(-phi / c.tau_s);               // :601
-          wm = w * eq_exp_t(-phi / c.tau_m);               // :606
-        } else {
-          ws = w;
-          wm = (T)0;
-        }
-        size_t so = (size_t)(ds % A.R) * A.N + j;
-        long long qs = P::q(ws, c.scale), qm = P::q(wm, c.scale);
-        if (P::kSlotWords == 1) {
-          red_add(ring_b + so, pack2(qs, qm));
-        } else {
-          red_add(ring_b + 2 * so, qs);
-          if (A.exact) red_add(ring_b + 2 * so + 1, qm);
-        }
-      }
-    }
     // ---------------- spike log for the reverse pass: one chunk per (step, CTA)
     if (tid == 0) {
       unsigned long long off = nspk ? atomicAdd(A.log_count, (unsigned long long)nspk) : 0ULL;
@@ -266,6 +255,87 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
     __syncthreads();
     if (s_off + nspk <= A.log_cap) {
       for (int k = tid; k < nspk; k += NT) A.log[s_off + k] = k < kCap ? s_spk[k] : spill[k - kCap];
+    }
+    __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 5);
+    // ---------------- fan-out (network.py:583-611), flattened over (spike, edge)
+    // so every lane carries an event: batch of <= kCap spikes, prefix of their
+    // row lengths, then flat events f -> (spike, x) with EV events per thread in
+    // flight.  Slot sums are fixed-point, so the order of the red.adds is free.
+    for (int k0 = 0; k0 < nspk; k0 += kCap) {
+      const int nb = nspk - k0 < kCap ? nspk - k0 : kCap;
+      __syncthreads();
+      if (k0 > 0)
+        for (int k = tid; k < nb; k += NT) s_spk[k] = spill[k0 - kCap + k];
+      __syncthreads();
+      for (int k = tid; k < nb; k += NT) {
+        const int b = s_spk[k].idx / A.N;
+        const int i = s_spk[k].idx - b * A.N;
+        const long long r0 = __ldg(A.net.rowptr + i);
+        const int len = (int)(__ldg(A.net.rowptr + i + 1) - r0);
+        s_r0[k] = r0;
+        s_pre[k + 1] = len;
+        const int tb = b - b_first;
+        if (tb < kTr) {
+          atomicAdd(&s_ctr[tb][0], 1ULL);
+          atomicAdd(&s_ctr[tb][1], (unsigned long long)len);
+        } else {
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), (unsigned long long)len);
+        }
+        if (A.kind == EQ_KIND_DONOTHING)
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), (unsigned long long)len);
+      }
+      __syncthreads();
+      warp0_scan(s_pre, nb);
+      __syncthreads();
+      if (k0 == 0) tl_mark(A.tl, m, A.G, cta, 6);
+      if (A.kind != EQ_KIND_RING) continue;
+      const int total = s_pre[nb];
+      constexpr int EV = 4;
+      for (int f0 = tid; f0 < total; f0 += EV * NT) {
+        int jj[EV], kk[EV];
+        T ww[EV], dd[EV];
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          const int f = f0 + e * NT;
+          kk[e] = -1;
+          if (f < total) {
+            const int k = find_row(s_pre, nb, f);
+            const long long x = s_r0[k] + (f - s_pre[k]);
+            kk[e] = k;
+            jj[e] = __ldg(A.net.col + x);
+            ww[e] = __ldg(A.net.w + x);
+            dd[e] = __ldg(A.net.d + x);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          if (kk[e] < 0) continue;
+          const SpikeRec<T> rec = s_spk[kk[e]];
+          const int b = rec.idx / A.N;
+          const T w = ww[e], d = dd[e];
+          const T t_post = rec.t + d;                        // :588
+          const int ds = delivery_step(t_post, d, c.dt, m);  // jumps.py:96
+          T ws, wm;
+          if (A.exact) {
+            const T phi = (T)ds * c.dt - t_post;             // :599
+            ws = w * eq_exp_t(-phi / c.tau_s);               // :601
+            wm = w * eq_exp_t(-phi / c.tau_m);               // :606
+          } else {
+            ws = w;
+            wm = (T)0;
+          }
+          const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
+          const long long qs = P::q(ws, c.scale), qm = P::q(wm, c.scale);
+          if (P::kSlotWords == 1) {
+            red_add(A.ring + so, pack2(qs, qm));
+          } else {
+            red_add(A.ring + 2 * so, qs);
+            if (A.exact) red_add(A.ring + 2 * so + 1, qm);
+          }
+        }
+      }
     }
     __syncthreads();
     tl_mark(A.tl, m, A.G, cta, 2);
@@ -311,9 +381,15 @@ struct BwdArgs {
 template <typename T, int NT, int U>
 __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
   typedef typename Prec<T>::T2 T2;
+  constexpr int kCapB = sizeof(T) == 4 ? 512 : 256;   // spikes per batch
+  constexpr int kEv = sizeof(T) == 4 ? 4096 : 2048;    // events per reduction window
+  __shared__ SpikeRec<T> s_rec[kCapB];
+  __shared__ long long s_r0[kCapB];
+  __shared__ int s_pre[kCapB + 1];
+  __shared__ T s_lt[kCapB];
+  __shared__ T s_gtp[kEv];
   extern __shared__ unsigned int s_bits[];   // one bit per owned neuron-trial
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
   const int cta = blockIdx.x;
   const long long begin = (long long)cta * A.per;
   const long long end = begin + A.per < A.total ? begin + A.per : A.total;
@@ -326,35 +402,86 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
     tl_mark(A.tl, m, A.G, cta, 0);
     const long long off = A.chunk_off[(size_t)m * A.G + cta];
     const int cnt = A.chunk_cnt[(size_t)m * A.G + cta];
-    // ---------------- R-fanout(m): own spikes, one warp per spike
-    for (int k = warp; k < cnt; k += NT / kWarp) {
-      SpikeRec<T> rec = A.log[off + k];
-      int b = rec.idx / A.N;
-      int i = rec.idx - b * A.N;
-      long long r0 = __ldg(A.net.rowptr + i), r1 = __ldg(A.net.rowptr + i + 1);
-      const T2* lam_b = A.lam + (size_t)b * A.R * A.N;
-      T part = (T)0;
-      for (long long x = r0 + lane; x < r1; x += kWarp) {
-        int j = __ldg(A.net.col + x);
-        T w = __ldg(A.net.w + x);
-        T d = __ldg(A.net.d + x);
-        T t_post = rec.t + d;
-        int st = delivery_step(t_post, d, c.dt, m);
-        if (st >= A.m_run) continue;                       // never popped: no effect
-        T phi = (T)st * c.dt - t_post;
-        T es = eq_exp_t(-phi / c.tau_s);
-        T em = eq_exp_t(-phi / c.tau_m);
-        T2 L = lam_b[(size_t)(st % A.R) * A.N + j];   // weak load: see ld_slot
-        T g_w = es * L.x + em * L.y;
-        T g_tp = w * (es * L.x / c.tau_s + em * L.y / c.tau_m);
-        atomicAdd(A.gw + x, (double)g_w);
-        atomicAdd(A.gd + x, (double)g_tp);
-        part = part + g_tp;
+    // ---------------- R-fanout(m): own spikes of step m, flattened over
+    // (spike, edge).  dL/dt_spk of a spike is the SEQUENTIAL sum of its edges'
+    // g_tp in row order (zeros for events never popped), staged through s_gtp
+    // in windows of kEv events; the oracle sums in the same order.
+    for (int k0 = 0; k0 < cnt; k0 += kCapB) {
+      const int nb = cnt - k0 < kCapB ? cnt - k0 : kCapB;
+      __syncthreads();
+      for (int k = tid; k < nb; k += NT) {
+        const SpikeRec<T> rec = A.log[off + k0 + k];
+        s_rec[k] = rec;
+        const int b = rec.idx / A.N;
+        const int i = rec.idx - b * A.N;
+        const long long r0 = __ldg(A.net.rowptr + i);
+        s_r0[k] = r0;
+        s_pre[k + 1] = (int)(__ldg(A.net.rowptr + i + 1) - r0);
+        s_lt[k] = (T)0;
       }
-      part = warp_sum_butterfly(part);
-      if (lane == 0) {
-        A.lt_log[off + k] = part;
-        long long loc = (long long)rec.idx - begin;
+      __syncthreads();
+      warp0_scan(s_pre, nb);
+      __syncthreads();
+      const int total = s_pre[nb];
+      for (int w0 = 0; w0 < total; w0 += kEv) {
+        const int wend = total - w0 < kEv ? total : w0 + kEv;
+        constexpr int EV = 4;
+        for (int f0 = w0 + tid; f0 < wend; f0 += EV * NT) {
+          int jj[EV], kk[EV];
+          long long xx[EV];
+          T ww[EV], dd[EV];
+#pragma unroll
+          for (int e = 0; e < EV; ++e) {
+            const int f = f0 + e * NT;
+            kk[e] = -1;
+            if (f < wend) {
+              const int k = find_row(s_pre, nb, f);
+              const long long x = s_r0[k] + (f - s_pre[k]);
+              kk[e] = k;
+              xx[e] = x;
+              jj[e] = __ldg(A.net.col + x);
+              ww[e] = __ldg(A.net.w + x);
+              dd[e] = __ldg(A.net.d + x);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < EV; ++e) {
+            if (kk[e] < 0) continue;
+            const int f = f0 + e * NT;
+            const SpikeRec<T> rec = s_rec[kk[e]];
+            const int b = rec.idx / A.N;
+            const T w = ww[e], d = dd[e];
+            const T t_post = rec.t + d;
+            const int st = delivery_step(t_post, d, c.dt, m);
+            T g_tp = (T)0;
+            if (st < A.m_run) {                              // never popped: no effect
+              const T phi = (T)st * c.dt - t_post;
+              const T es = eq_exp_t(-phi / c.tau_s);
+              const T em = eq_exp_t(-phi / c.tau_m);
+              const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
+              const T g_w = es * L.x + em * L.y;
+              g_tp = w * (es * L.x / c.tau_s + em * L.y / c.tau_m);
+              atomicAdd(A.gw + xx[e], (double)g_w);
+              atomicAdd(A.gd + xx[e], (double)g_tp);
+            }
+            s_gtp[f - w0] = g_tp;
+          }
+        }
+        __syncthreads();
+        const int ka = find_row(s_pre, nb, w0);
+        const int kb = find_row(s_pre, nb, wend - 1);
+        for (int k = ka + tid; k <= kb; k += NT) {
+          const int lo = s_pre[k] > w0 ? s_pre[k] : w0;
+          const int hi = s_pre[k + 1] < wend ? s_pre[k + 1] : wend;
+          T acc = s_lt[k];
+          for (int q = lo; q < hi; ++q) acc = acc + s_gtp[q - w0];
+          s_lt[k] = acc;
+        }
+        __syncthreads();
+      }
+      for (int k = tid; k < nb; k += NT) {
+        A.lt_log[off + k0 + k] = s_lt[k];
+        const int loc = s_rec[k].idx - (int)begin;
         atomicOr(&s_bits[loc >> 5], 1u << (loc & 31));
       }
     }

@@ -499,7 +499,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   const char* tl = getenv("EQ_TIMELINE");
   if (tl && tl[0] == '1') {
     h->tl_steps = c.t_steps;
-    size_t nb = (size_t)c.t_steps * h->G * 4 * sizeof(unsigned long long);
+    size_t nb = (size_t)c.t_steps * h->G * 8 * sizeof(unsigned long long);
     EQ_CUDA(h, alloc(h, (void**)&h->tl_f, nb));
     EQ_CUDA(h, alloc(h, (void**)&h->tl_b, nb));
     EQ_CUDA(h, cudaMemset(h->tl_f, 0, nb));
@@ -762,7 +762,7 @@ int eq_debug_timeline(eq_handle* h, int which, uint64_t* host_out) {
   if (!src) return fail(h, EQ_ERR_CONFIGURATION, "timeline disabled (set EQ_TIMELINE=1 before eq_create)");
   DeviceGuard g(h->device);
   EQ_CUDA(h, cudaDeviceSynchronize());
-  EQ_CUDA(h, cudaMemcpy(host_out, src, (size_t)h->tl_steps * h->G * 4 * 8, cudaMemcpyDeviceToHost));
+  EQ_CUDA(h, cudaMemcpy(host_out, src, (size_t)h->tl_steps * h->G * 8 * 8, cudaMemcpyDeviceToHost));
   return EQ_OK;
 }
 

@@ -20,6 +20,7 @@ import bench  # noqa: E402
 
 def report(tl, label):
     t = tl.astype(np.int64)
+    sub = t[:, :, 4:]
     ok = (t[:, :, 0] > 0)
     steps = np.nonzero(ok.all(axis=1))[0]
     t = t[steps]
@@ -32,6 +33,14 @@ def report(tl, label):
     for name, a in (("phase1", ph1), ("phase2", ph2), ("barrier", bar)):
         print(f"   {name:8s} max {np.median(a.max(1))/1e3:8.2f}  mean {np.median(a.mean(1))/1e3:8.2f}")
     print(f"   step     {np.median(step)/1e3:8.2f}   start-skew {np.median(skew)/1e3:8.2f}")
+    sub = sub[steps]
+    prev = t[:, :, 1]
+    for k in range(4):
+        mk = sub[:, :, k]
+        if (mk > 0).all():
+            d = mk - prev
+            print(f"   sub{k}     max {np.median(d.max(1))/1e3:8.2f}  mean {np.median(d.mean(1))/1e3:8.2f}")
+            prev = mk
 
 
 def main():
@@ -52,7 +61,7 @@ def main():
     torch.cuda.synchronize()
     G, _ = eng.geometry
     for which, label in ((0, "forward"), (1, "reverse")):
-        buf = np.zeros((T, G, 4), dtype=np.uint64)
+        buf = np.zeros((T, G, 8), dtype=np.uint64)
         eng.L.eq_debug_timeline(eng.h, which, buf.ctypes.data_as(ctypes.c_void_p))
         report(buf, label)
     c = eng.counters()
