@@ -64,6 +64,7 @@ struct Cfg {
 struct Spike {
   int32_t step, trial, neuron;
   double t, a, vh;       // exact copies of the T values
+  int64_t ev_off;        // offset of this spike's first event in its trial's accept list
 };
 
 template <typename T> struct FixedOf;
@@ -93,6 +94,7 @@ struct Session {
   std::vector<double> v_out, i_out, v_trace;
   std::vector<Spike> spikes;
   std::vector<int64_t> counters;   // [B][3]
+  std::vector<std::vector<uint8_t>> accepted;  // per trial, per event in fan-out order
   std::vector<int64_t> pending;    // [B][N][horizon][2] fixed (device mode)
   std::vector<double> pending_ref; // [B][N][horizon][2] (reference mode)
   std::string err;
@@ -158,6 +160,7 @@ struct Trial {
   std::vector<std::vector<Ev>> pool;
   std::vector<int32_t> tail_key;
   int64_t n_spk = 0, n_enq = 0, n_drop = 0;
+  std::vector<uint8_t> acc;        // accepted flag per event, fan-out order
   Error e;
 
   Trial(const Session& s, int trial) : S(s), c(s.cfg), b(trial) {
@@ -301,10 +304,12 @@ struct Trial {
       if (vtrace) for (int j = 0; j < N; ++j) vtrace[(size_t)m * N + j] = (double)V[j];
       // fan-out in ascending source order, CSR row order (network.py:583-611)
       const int now = m + 1;  // queues were popped for step m
+      const size_t first = out.size() - crossing.size();
       for (size_t k = 0; k < crossing.size() && e.code == OK; ++k) {
         int i = crossing[k];
         T t_spk = cross_t[k];
         n_spk += 1;
+        out[first + k].ev_off = (int64_t)acc.size();
         for (int64_t x = S.rowptr[i]; x < S.rowptr[i + 1]; ++x) {
           int j = S.col[x];
           T d = (T)S.d[x];
@@ -323,6 +328,7 @@ struct Trial {
           bool ok = enqueue(j, now, dstep, ws, wm);
           if (e.code != OK) return;
           if (!ok) n_drop += 1;
+          acc.push_back(ok || c.kind == K_RING ? 1 : 0);
         }
       }
     }
@@ -342,11 +348,13 @@ int run_forward(Session& s) {
   s.pending_ref.assign(DEV ? 0 : (size_t)B * N * s.horizon * 2, 0.0);
   std::vector<std::vector<Spike>> per_trial(B);
   std::vector<Error> errs(B);
+  s.accepted.assign(B, std::vector<uint8_t>());
 #pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < B; ++b) {
     Trial<T, DEV> tr(s, b);
     tr.run(per_trial[b], c.record_v ? s.v_trace.data() + (size_t)b * c.t_steps * N : nullptr);
     errs[b] = tr.e;
+    s.accepted[b].swap(tr.acc);
     for (int j = 0; j < N; ++j) {
       s.v_out[(size_t)b * N + j] = (double)tr.V[j];
       s.i_out[(size_t)b * N + j] = (double)tr.I[j];
@@ -396,7 +404,7 @@ int run_forward(Session& s) {
 template <typename T, bool DEV>
 int run_backward(Session& s, const double* vbar, const double* ibar, double* gw, double* gd, double* gamp) {
   const Cfg& c = s.cfg;
-  if (c.kind != K_RING) { s.err = "backward is implemented for the ring kind"; return E_CONFIG; }
+  if (c.kind == K_DONOTHING) { /* every event dropped: only the neuron recurrences remain */ }
   if (!c.exact_delivery) { s.err = "backward requires exact_delivery"; return E_CONFIG; }
   int B = c.n_trials, N = c.n, TT = c.t_steps;
   size_t E = s.col.size();
@@ -449,13 +457,14 @@ int run_backward(Session& s, const double* vbar, const double* ibar, double* gw,
           // events delivered at or after T (the kernel's reduction order)
           T lt_sum = (T)0;
           int64_t r0 = s.rowptr[i], r1 = s.rowptr[i + 1];
+          const uint8_t* okv = s.accepted[b].data() + sp.ev_off;
           for (int64_t x = r0; x < r1; ++x) {
             int j = s.col[x];
             T w = (T)s.w[x];
             T dd = (T)s.d[x];
             T t_post = t + dd;
             int32_t st = delivery<T, DEV>(t_post, dd, dt, m);
-            if (st >= TT) { lt_sum = lt_sum + (T)0; continue; }
+            if (st >= TT || !okv[x - r0]) { lt_sum = lt_sum + (T)0; continue; }
             T phi = (T)st * dt - t_post;
             T es = xexp<T, DEV>(-phi / tau_s);
             T em = xexp<T, DEV>(-phi / tau_m);

@@ -1,0 +1,401 @@
+// eq_bounded.cuh — persistent fused forward kernel for the bounded queue kinds:
+// FIFORing (queues.py:184-260), BinaryHeap (queues.py:481-571) and SortedArray
+// (queues.py:308-403).
+//
+// All three drop the INCOMING event when the queue holds `capacity` events and
+// pop every event due now, so their accepted sets are identical (SURVEY App.
+// A.6); only the data structure — and so the cost profile — differs.  The
+// accept decision depends on arrival order, which the reference fixes as
+// (emit step, source ascending, CSR row order) = ascending CSR edge index.
+// Parallel fan-out cannot produce that order, so an arrival is not inserted by
+// its producer.  Instead:
+//
+//   phase m, producer (the CTA that detected the crossing): for each event of
+//     edge x -> target j write a staging record at the edge's in-edge slot
+//     csc_off[j] + in_pos[x] and set bit in_pos[x] of j's arrival bitmap
+//     (plus j's bit in a dense per-target "has arrivals" word);
+//   phase m+1, owner of j, before pop(m+1): walk j's arrival bits in ascending
+//     order (= ascending x) and insert in exactly the reference order — FIFO
+//     tail-key check (CapabilityError), drop when full, structure insert.
+//
+// Staging and bitmaps are double-buffered by step parity (phase m+1 producers
+// write step m+1 while owners read step m).  The final step's arrivals are
+// inserted after a last barrier so the queue contents after a run equal the
+// reference's.  Pops and sums are fixed point (order-free), as for the ring.
+#pragma once
+
+#include "eq_ring.cuh"
+
+namespace eq {
+
+// staging / queue entry.  `tag` = log position of the source spike (staging)
+// or insertion sequence number (heap).  due_off = due - emit step (<= horizon);
+// row_off = edge offset within the source's CSR row (drop bookkeeping).
+template <typename T> struct QEv;
+template <> struct alignas(16) QEv<float> {
+  int tag;
+  int due;
+  long long p;        // packed fixed-point pair (qm << 32) + qs
+  __device__ __forceinline__ void add_to(long long& s, long long& m) const {
+    long long a, b;
+    unpack2(p, a, b);
+    s += a;
+    m += b;
+  }
+};
+template <> struct alignas(16) QEv<double> {
+  int tag;
+  int due;
+  long long ps, pm;
+  long long pad;
+  __device__ __forceinline__ void add_to(long long& s, long long& m) const {
+    s += ps;
+    m += pm;
+  }
+};
+
+template <typename T>
+struct BndArgs {
+  FwdArgs<T> f;
+  int cap;                    // events per queue
+  const int* in_pos;          // [E] rank of edge x among its target's in-edges
+  const long long* csc_off;   // [N+1] in-edge slot offsets
+  const long long* word_off;  // [N+1] arrival-bitmap word offsets
+  long long E, W;             // edges, bitmap words per trial
+  QEv<T>* stage;              // [2][B][E]
+  unsigned short* stage_row;  // [2][B][E] row offsets of staged events
+  unsigned* arr;              // [2][B][W]
+  unsigned* flags;            // [2][B][words]
+  QEv<T>* q;                  // [B*N][cap]
+  int4* meta;                 // [B*N] {count, head|seq, tail_key, next_due}
+  long long* ev_base;         // [log_cap] flat event id of each logged spike's first edge
+  unsigned long long* ev_count;  // run-wide event id counter
+  unsigned* drop_bits;        // [drop_cap/32]
+  long long drop_cap;
+  int insert_first;           // first step whose arrivals this launch inserts
+};
+
+__device__ __forceinline__ bool key_less(int da, int sa, int db, int sb) {
+  return da < db || (da == db && sa < sb);
+}
+
+// Insert one event (reference order) into the owner's queue; false = dropped.
+template <typename T>
+__device__ __forceinline__ int queue_insert(int kind, int cap, QEv<T>* q, int4& mt, QEv<T> ev) {
+  // returns 0 accepted, 1 dropped, 2 capability error
+  if (kind == EQ_KIND_FIFORING && ev.due < mt.z) return 2;      // queues.py:220-224
+  if (mt.x == cap) return 1;                                     // :225-226, :514-515, :344-345
+  if (kind == EQ_KIND_FIFORING) {
+    int slot = mt.y + mt.x;
+    if (slot >= cap) slot -= cap;
+    q[slot] = ev;
+    mt.x += 1;
+    mt.z = ev.due;
+    if (mt.x == 1) mt.w = ev.due;
+  } else if (kind == EQ_KIND_BINARYHEAP) {
+    ev.tag = mt.y++;                                             // insertion seq, :517-518
+    int i = mt.x++;
+    while (i > 0) {                                              // sift up, :522-528
+      const int parent = (i - 1) >> 1;
+      const QEv<T> pv = q[parent];
+      if (!key_less(ev.due, ev.tag, pv.due, pv.tag)) break;
+      q[i] = pv;
+      i = parent;
+    }
+    q[i] = ev;
+    mt.w = q[0].due;
+  } else {  // sorted array, circular with head mt.y; stable for equal due (:351-366)
+    int k = mt.x;
+    while (k > 0) {
+      int pi = mt.y + k - 1;
+      if (pi >= cap) pi -= cap;
+      const QEv<T> pv = q[pi];
+      if (pv.due <= ev.due) break;
+      int di = pi + 1;
+      if (di >= cap) di -= cap;
+      q[di] = pv;
+      --k;
+    }
+    int di = mt.y + k;
+    if (di >= cap) di -= cap;
+    q[di] = ev;
+    mt.x += 1;
+    int h = mt.y;
+    mt.w = q[h].due;
+  }
+  return 0;
+}
+
+// Pop every event due at step `now` (the minimum), summing fixed-point payloads.
+template <typename T>
+__device__ __forceinline__ void queue_pop(int kind, int cap, QEv<T>* q, int4& mt, int now, long long& s,
+                                          long long& mm) {
+  if (mt.x == 0 || mt.w != now) return;
+  if (kind == EQ_KIND_BINARYHEAP) {
+    while (mt.x > 0 && q[0].due == now) {                        // :555-568
+      q[0].add_to(s, mm);
+      const int last = --mt.x;
+      const QEv<T> item = q[last];
+      if (last > 0) {
+        int i = 0;
+        const int half = last >> 1;
+        while (i < half) {                                       // sift down, :541-551
+          int child = 2 * i + 1;
+          const int right = child + 1;
+          QEv<T> cv = q[child];
+          if (right < last) {
+            const QEv<T> rv = q[right];
+            if (key_less(rv.due, rv.tag, cv.due, cv.tag)) {
+              child = right;
+              cv = rv;
+            }
+          }
+          if (!key_less(cv.due, cv.tag, item.due, item.tag)) break;
+          q[i] = cv;
+          i = child;
+        }
+        q[i] = item;
+      }
+    }
+    mt.w = mt.x ? q[0].due : 0x7fffffff;
+  } else {  // FIFO and sorted: due run at the head (:245-254, :378-386)
+    while (mt.x > 0 && q[mt.y].due == now) {
+      q[mt.y].add_to(s, mm);
+      mt.y += 1;
+      if (mt.y == cap) mt.y = 0;
+      mt.x -= 1;
+    }
+    mt.w = mt.x ? q[mt.y].due : 0x7fffffff;
+  }
+}
+
+// Owner-side insertion of one target's arrivals of step `ms` (parity ms & 1).
+template <typename T>
+__device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int j, int idx, int ms, int4& mt,
+                                                unsigned long long& drops) {
+  const int par = ms & 1;
+  const long long w0 = A.word_off[j], w1 = A.word_off[j + 1];
+  unsigned* arr = A.arr + ((size_t)par * A.f.B + b) * A.W;
+  const QEv<T>* stg = A.stage + ((size_t)par * A.f.B + b) * A.E + A.csc_off[j];
+  const unsigned short* srow = A.stage_row + ((size_t)par * A.f.B + b) * A.E + A.csc_off[j];
+  QEv<T>* q = A.q + (size_t)idx * A.cap;
+  for (long long w = w0; w < w1; ++w) {
+    unsigned bits = arr[w];
+    if (!bits) continue;
+    arr[w] = 0u;
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int pos = (int)((w - w0) * 32 + bit);
+      QEv<T> ev = stg[pos];
+      const int log_pos = ev.tag;
+      const int rc = queue_insert<T>(A.f.kind, A.cap, q, mt, ev);
+      if (rc == 2) {
+        raise_error(A.f.err, EQ_ERR_CAPABILITY, ms + 1, b, j);
+      } else if (rc == 1) {
+        drops += 1;
+        const long long id = A.ev_base[log_pos] + srow[pos];
+        if (id < A.drop_cap) atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
+        else raise_error(A.f.err, EQ_ERR_CAPACITY, ms, b, j);
+      }
+    }
+  }
+}
+
+template <typename T, int NT, int U>
+__global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
+  typedef Prec<T> P;
+  constexpr int kCap = FwdShared<NT>::kCap;
+  constexpr int kTr = FwdShared<NT>::kTrials;
+  __shared__ SpikeRec<T> s_spk[kCap];
+  __shared__ long long s_r0[kCap];
+  __shared__ int s_pre[kCap + 1];
+  __shared__ int s_n;
+  __shared__ long long s_off;
+  __shared__ long long s_evoff;
+  __shared__ unsigned long long s_ctr[kTr][3];
+  FwdArgs<T>& F = A.f;
+
+  const int tid = threadIdx.x;
+  const int cta = blockIdx.x;
+  const long long begin = (long long)cta * F.per;
+  const long long end = begin + F.per < F.total ? begin + F.per : F.total;
+  const int b_first = (int)(begin / F.N);
+  const StepConsts<T> c = F.c;
+  SpikeRec<T>* spill = F.scratch + (size_t)cta * F.per;
+  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
+  const int fwords = (F.N + 31) / 32;
+
+  for (int m = F.m0; m <= F.m1; ++m) {
+    const bool last = (m == F.m1);   // extra pass: insert the final step's arrivals only
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    if (!last) tl_mark(F.tl, m, F.G, cta, 0);
+    // ---------------- owner phase: insert arrivals(m-1), pop(m), neuron update
+    for (long long base = begin; base < end; base += NT) {
+      const int idx = (int)base + tid;
+      if (idx >= end) continue;
+      const int b = idx / F.N;
+      const int j = idx - b * F.N;
+      int4 mt = A.meta[idx];
+      bool dirty = false;
+      if (m - 1 >= A.insert_first && m >= 1) {
+        unsigned* fl = A.flags + ((size_t)((m - 1) & 1) * F.B + b) * fwords;
+        const unsigned bit = 1u << (j & 31);
+        if (fl[j >> 5] & bit) {
+          // a flag word can straddle two CTAs' ranges when N % 32 != 0: clear our bit only
+          atomicAnd(fl + (j >> 5), ~bit);
+          unsigned long long d = 0;
+          insert_arrivals<T>(A, b, j, idx, m - 1, mt, d);
+          const int tb = b - b_first;
+          if (d) {
+            if (tb < kTr) atomicAdd(&s_ctr[tb][2], d);
+            else atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 2), d);
+          }
+          dirty = true;
+        }
+      }
+      if (last) {
+        if (dirty) A.meta[idx] = mt;
+        continue;
+      }
+      long long qs = 0, qm = 0;
+      if (mt.x > 0 && mt.w == m) {
+        queue_pop<T>(F.kind, A.cap, A.q + (size_t)idx * A.cap, mt, m, qs, qm);
+        dirty = true;
+      }
+      if (dirty) A.meta[idx] = mt;
+      T ps = P::deq(qs, c.inv_scale), pm = P::deq(qm, c.inv_scale);
+      if (!F.exact) pm = (T)0;
+      int rf = F.refractory ? F.refr[idx] : 0;
+      const T drive = drive_bit(F.net, b, m, j) ? __ldg(F.net.amp + j) : (T)0;
+      T i, v_new, a, v, t_spk;
+      if (lif_step(c, F.exact != 0, F.refractory, m, ps, pm, F.I[idx], F.V[idx], drive, rf, i, v_new, a, v, t_spk)) {
+        if (t_spk != t_spk) {
+          raise_error(F.err, EQ_ERR_GRAZING, m + 1, b, j);
+        } else {
+          int pos = atomicAdd(&s_n, 1);
+          SpikeRec<T> rec;
+          rec.idx = idx;
+          rec.t = t_spk;
+          rec.a = a;
+          rec.vh = v;
+          if (pos < kCap) s_spk[pos] = rec;
+          else spill[pos - kCap] = rec;
+        }
+      }
+      F.I[idx] = i;
+      F.V[idx] = v_new;
+      if (F.refractory) F.refr[idx] = rf;
+      if (F.v_trace) F.v_trace[(size_t)(m - F.m0) * F.total + idx] = v_new;
+    }
+    __syncthreads();
+    if (last) break;
+    tl_mark(F.tl, m, F.G, cta, 1);
+    const int nspk = s_n;
+    // ---------------- spike log + event-id range for this (step, CTA)
+    if (tid == 0) {
+      unsigned long long off = nspk ? atomicAdd(F.log_count, (unsigned long long)nspk) : 0ULL;
+      if (nspk && (long long)(off + nspk) > F.log_cap) {
+        raise_error(F.err, EQ_ERR_CAPACITY, m, -1, -1);
+        off = 0;
+      }
+      s_off = (long long)off;
+      F.chunk_off[(size_t)m * F.G + cta] = (long long)off;
+      F.chunk_cnt[(size_t)m * F.G + cta] = nspk;
+    }
+    __syncthreads();
+    const bool log_ok = s_off + nspk <= F.log_cap;
+    if (log_ok)
+      for (int k = tid; k < nspk; k += NT) F.log[s_off + k] = k < kCap ? s_spk[k] : spill[k - kCap];
+    // ---------------- fan-out: stage each event at its in-edge slot
+    for (int k0 = 0; k0 < nspk; k0 += kCap) {
+      const int nb = nspk - k0 < kCap ? nspk - k0 : kCap;
+      __syncthreads();
+      if (k0 > 0)
+        for (int k = tid; k < nb; k += NT) s_spk[k] = spill[k0 - kCap + k];
+      __syncthreads();
+      for (int k = tid; k < nb; k += NT) {
+        const int b = s_spk[k].idx / F.N;
+        const int i = s_spk[k].idx - b * F.N;
+        const long long r0 = __ldg(F.net.rowptr + i);
+        const int len = (int)(__ldg(F.net.rowptr + i + 1) - r0);
+        s_r0[k] = r0;
+        s_pre[k + 1] = len;
+        const int tb = b - b_first;
+        if (tb < kTr) {
+          atomicAdd(&s_ctr[tb][0], 1ULL);
+          atomicAdd(&s_ctr[tb][1], (unsigned long long)len);
+        } else {
+          atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b), 1ULL);
+          atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 1), (unsigned long long)len);
+        }
+      }
+      __syncthreads();
+      warp0_scan(s_pre, nb);
+      __syncthreads();
+      const int total = s_pre[nb];
+      if (tid == 0) s_evoff = (long long)atomicAdd(A.ev_count, (unsigned long long)total);
+      __syncthreads();
+      if (log_ok)
+        for (int k = tid; k < nb; k += NT) A.ev_base[s_off + k0 + k] = s_evoff + s_pre[k];
+      const int par = m & 1;
+      for (int f = tid; f < total; f += NT) {
+        const int k = find_row(s_pre, nb, f);
+        const int ro = f - s_pre[k];
+        const long long x = s_r0[k] + ro;
+        const SpikeRec<T> rec = s_spk[k];
+        const int b = rec.idx / F.N;
+        const int jt = __ldg(F.net.col + x);
+        const T w = __ldg(F.net.w + x);
+        const T d = __ldg(F.net.d + x);
+        const T t_post = rec.t + d;
+        const int ds = delivery_step(t_post, d, c.dt, m);
+        T ws, wm;
+        if (F.exact) {
+          const T phi = (T)ds * c.dt - t_post;
+          ws = w * eq_exp_t(-phi / c.tau_s);
+          wm = w * eq_exp_t(-phi / c.tau_m);
+        } else {
+          ws = w;
+          wm = (T)0;
+        }
+        const int pos = __ldg(A.in_pos + x);
+        QEv<T> ev;
+        ev.tag = (int)(s_off + k0 + k);
+        ev.due = ds;
+        const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
+        if constexpr (sizeof(T) == 4) {
+          ev.p = pack2(q1, q2);
+        } else {
+          ev.ps = q1;
+          ev.pm = q2;
+          ev.pad = 0;
+        }
+        const size_t so = ((size_t)par * F.B + b) * A.E + A.csc_off[jt] + pos;
+        A.stage[so] = ev;
+        A.stage_row[so] = (unsigned short)ro;
+        unsigned* arr = A.arr + ((size_t)par * F.B + b) * A.W + A.word_off[jt];
+        atomicOr(arr + (pos >> 5), 1u << (pos & 31));
+        unsigned* fl = A.flags + ((size_t)par * F.B + b) * fwords;
+        atomicOr(fl + (jt >> 5), 1u << (jt & 31));
+      }
+    }
+    __syncthreads();
+    tl_mark(F.tl, m, F.G, cta, 2);
+    if (!grid_sync(F.bar, F.G, F.err)) break;
+    tl_mark(F.tl, m, F.G, cta, 3);
+    if (ld_volatile(F.err) != 0) break;
+  }
+  // per-trial counters
+  __syncthreads();
+  if (tid < kTr) {
+    int b = b_first + tid;
+    if (b < F.B && (long long)b * F.N < end) {
+      for (int q = 0; q < 3; ++q)
+        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + q), s_ctr[tid][q]);
+    }
+  }
+}
+
+}  // namespace eq

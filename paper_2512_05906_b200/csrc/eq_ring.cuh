@@ -107,6 +107,42 @@ __device__ __forceinline__ int find_row(const int* pre, int n, int f) {
   return lo;
 }
 
+// One neuron-step of PrimalRSNN.step (network.py:559-580) after the pop.
+// Returns true on a threshold crossing; t_spk is NaN for a grazing crossing
+// (slope below 1e-9, neuro.py:194-199), which the caller turns into an error.
+template <typename T>
+__device__ __forceinline__ bool lif_step(const StepConsts<T>& c, bool exact, int refractory, int m, T ps, T pm,
+                                         T I, T V, T drive, int& rf, T& i_out, T& v_out, T& a_out, T& vh_out,
+                                         T& t_out) {
+  const T i = (I + ps) * c.k_s;                       // :559
+  const T a = i + drive;                              // :561
+  T v = V;
+  if (exact) v = v + c.cc * (pm - ps);                // :564
+  T v_new = a + (v - a) * c.k_m;                      // :565
+  bool spike = false;
+  if (rf > 0) {                                       // :566-567
+    rf -= 1;
+  } else if (v < c.v_th && c.v_th <= v_new) {         // :568
+    const T v_dot = (a - c.v_th) / c.tau_m;           // :569
+    if (v_dot < (T)1e-9) {
+      t_out = (T)NAN;
+    } else {
+      const T r = (c.v_th - a) / (v - a);             // :574
+      const T t_spk = (T)m * c.dt - c.tau_m * eq_log_t(r);  // :575
+      const T uu = (T)(m + 1) * c.dt - t_spk;         // :576
+      v_new = a + (c.v_reset - a) * eq_exp_t(-uu / c.tau_m);  // :577
+      rf = refractory;                                // :578
+      t_out = t_spk;
+    }
+    spike = true;
+  }
+  i_out = i;
+  v_out = v_new;
+  a_out = a;
+  vh_out = v;
+  return spike;
+}
+
 template <typename T>
 __device__ __forceinline__ bool drive_bit(const NetView<T>& net, int b, int m, int j) {
   int mm = m < net.t_mask ? m : net.t_mask - 1;   // network.py:155 rows[-1]
@@ -185,24 +221,12 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
           pm = P::deq(slot_v[u][1], c.inv_scale);
         }
         if (!A.exact) pm = (T)0;
-        T i = (Iv[u] + ps) * c.k_s;                       // network.py:559
-        T drive = on[u] ? __ldg(A.net.amp + j) : (T)0;
-        T a = i + drive;                                   // :561
-        T v = Vv[u];
-        if (A.exact) v = v + c.cc * (pm - ps);             // :564
-        T v_new = a + (v - a) * c.k_m;                     // :565
-        if (rf[u] > 0) {                                   // :566-567
-          rf[u] -= 1;
-        } else if (v < c.v_th && c.v_th <= v_new) {        // :568
-          T v_dot = (a - c.v_th) / c.tau_m;
-          if (v_dot < (T)1e-9) {
+        const T drive = on[u] ? __ldg(A.net.amp + j) : (T)0;
+        T i, v_new, a, v, t_spk;
+        if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, Iv[u], Vv[u], drive, rf[u], i, v_new, a, v, t_spk)) {
+          if (t_spk != t_spk) {
             raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, j);
           } else {
-            T r = (c.v_th - a) / (v - a);                  // :574
-            T t_spk = (T)m * c.dt - c.tau_m * eq_log_t(r); // :575
-            T uu = (T)(m + 1) * c.dt - t_spk;              // :576
-            v_new = a + (c.v_reset - a) * eq_exp_t(-uu / c.tau_m);
-            rf[u] = A.refractory;
             int pos = atomicAdd(&s_n, 1);
             SpikeRec<T> rec;
             rec.idx = idx;
@@ -373,6 +397,9 @@ struct BwdArgs {
   T* lt_log;                   // dL/dt_spk per log record
   const long long* chunk_off;
   const int* chunk_cnt;
+  const long long* ev_base;     // bounded kinds: flat event id of each log record's first edge
+  const unsigned* drop_bits;    // bounded kinds: dropped events (contribute nothing); null for ring
+  int no_events;                // donothing: every event was dropped
   unsigned long long* tl;  // debug timeline [m][G][4] or null
   int* err;
   unsigned* bar;
@@ -454,7 +481,12 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
             const T t_post = rec.t + d;
             const int st = delivery_step(t_post, d, c.dt, m);
             T g_tp = (T)0;
-            if (st < A.m_run) {                              // never popped: no effect
+            bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
+            if (live && A.drop_bits) {                       // dropped by a bounded queue
+              const long long id = A.ev_base[off + k0 + kk[e]] + (f - s_pre[kk[e]]);
+              live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
+            }
+            if (live) {
               const T phi = (T)st * c.dt - t_post;
               const T es = eq_exp_t(-phi / c.tau_s);
               const T em = eq_exp_t(-phi / c.tau_m);

@@ -3,7 +3,6 @@
 // Host code only orchestrates: validation of the network on the device
 // (reference checks of build_rsnn, network.py:213-268), buffer ownership, and
 // one cooperative launch of a persistent kernel per eq_run / eq_backward.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,6 +15,9 @@
 
 #include "eq_device.cuh"
 #include "eq_ring.cuh"
+#include "eq_bounded.cuh"
+
+#include <cub/cub.cuh>
 
 using namespace eq;
 
@@ -79,6 +81,24 @@ struct eq_handle {
   void* lam = nullptr;
   void* lt_log = nullptr;
   double* gamp_bt = nullptr;
+  // bounded kinds (fifo / heap / sorted)
+  bool bounded = false;
+  int cap = 0;                 // physical events per queue
+  long long cap_ref = 0;       // the reference's capacity (acceptance rule)
+  int* in_pos = nullptr;
+  long long* csc_off = nullptr;
+  long long* word_off = nullptr;
+  long long W = 0;
+  void* stage = nullptr;
+  unsigned short* stage_row = nullptr;
+  unsigned* arr = nullptr;
+  unsigned* flags = nullptr;
+  void* q = nullptr;
+  int4* meta = nullptr;
+  long long* ev_base = nullptr;
+  unsigned long long* ev_count = nullptr;
+  unsigned* drop_bits = nullptr;
+  long long drop_cap = 0;
   unsigned long long* tl_f = nullptr;   // debug timelines (EQ_TIMELINE=1)
   unsigned long long* tl_b = nullptr;
   int tl_steps = 0;
@@ -159,7 +179,8 @@ NetView<T> netview(const eq_handle* h) {
 // sum of |w| per target (2^-40 units; deterministic integer adds).
 template <typename T>
 __global__ void k_net_stats(int N, const int64_t* rowptr, const int32_t* col, const T* w, const T* d,
-                            T dt, int homogeneous_only, long long* insum, long long* stats) {
+                            T dt, int homogeneous_only, long long* insum, long long* stats, long long* inocc,
+                            int* indeg) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   long long r0 = rowptr[i], r1 = rowptr[i + 1];
@@ -181,6 +202,8 @@ __global__ void k_net_stats(int N, const int64_t* rowptr, const int32_t* col, co
     prev = j;
     int q = (int)ceil(d[x] / dt);
     hmax = q > hmax ? q : hmax;
+    atomicAdd(reinterpret_cast<unsigned long long*>(inocc + j), (unsigned long long)(q + 1));
+    atomicAdd(indeg + j, 1);
     atomicAdd(reinterpret_cast<unsigned long long*>(insum + j),
               (unsigned long long)__double2ll_rn(fabs((double)w[x]) * 1099511627776.0));
   }
@@ -256,6 +279,55 @@ __global__ void k_pending(const long long* ring, int B, int R, int N, int H, int
   }
 }
 
+__global__ void k_iota(int* v, long long n) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    v[k] = (int)k;
+}
+
+// in_pos[x] = rank of edge x among its target's in-edges (sorted stably by x)
+__global__ void k_in_pos(const int* sorted_col, const int* sorted_x, const long long* csc_off, long long E,
+                         int* in_pos) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < E; k += (long long)gridDim.x * blockDim.x)
+    in_pos[sorted_x[k]] = (int)(k - csc_off[sorted_col[k]]);
+}
+
+__global__ void k_words_of(const int* indeg, int N, long long* words) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < N) words[j] = (indeg[j] + 31) / 32;
+}
+
+__global__ void k_meta_init(int4* meta, long long n) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    meta[k] = make_int4(0, 0, -1, 0x7fffffff);
+}
+
+template <typename T>
+__global__ void k_pending_bounded(const QEv<T>* q, const int4* meta, int kind, int cap, long long total, int H,
+                                  int now, long long* out) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long* o = out + idx * H * 2;
+    for (int k = 0; k < 2 * H; ++k) o[k] = 0;
+    const int4 mt = meta[idx];
+    const QEv<T>* qq = q + idx * cap;
+    for (int k = 0; k < mt.x; ++k) {
+      int pos = k;
+      if (kind != EQ_KIND_BINARYHEAP) {
+        pos = mt.y + k;
+        if (pos >= cap) pos -= cap;
+      }
+      const QEv<T> ev = qq[pos];
+      const int h = ev.due - now;
+      if (h >= 0 && h < H) {
+        long long a = 0, b = 0;
+        ev.add_to(a, b);
+        o[2 * h] += a;
+        o[2 * h + 1] += b;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ launches
 
 int check_err(eq_handle* h, cudaStream_t s) {
@@ -313,9 +385,34 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
   A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
-  void* args[] = {&A};
-  EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_forward<T, kNT, kU>, dim3(h->G), dim3(kNT), args,
-                                         0, s));
+  if (h->bounded) {
+    BndArgs<T> Bk;
+    Bk.f = A;
+    Bk.cap = h->cap;
+    Bk.in_pos = h->in_pos;
+    Bk.csc_off = h->csc_off;
+    Bk.word_off = h->word_off;
+    Bk.E = h->E;
+    Bk.W = h->W;
+    Bk.stage = (QEv<T>*)h->stage;
+    Bk.stage_row = h->stage_row;
+    Bk.arr = h->arr;
+    Bk.flags = h->flags;
+    Bk.q = (QEv<T>*)h->q;
+    Bk.meta = h->meta;
+    Bk.ev_base = h->ev_base;
+    Bk.ev_count = h->ev_count;
+    Bk.drop_bits = h->drop_bits;
+    Bk.drop_cap = h->drop_cap;
+    Bk.insert_first = h->steps_done;
+    void* bargs[] = {&Bk};
+    EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_forward_bounded<T, kNT, kU>, dim3(h->G), dim3(kNT),
+                                           bargs, 0, s));
+  } else {
+    void* args[] = {&A};
+    EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_forward<T, kNT, kU>, dim3(h->G), dim3(kNT), args,
+                                           0, s));
+  }
   h->launches += 1;
   int rc = check_err(h, s);
   if (rc == EQ_OK || rc == EQ_ERR_GRAZING) h->steps_done += n_steps;
@@ -357,6 +454,9 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   A.lt_log = (T*)h->lt_log;
   A.chunk_off = h->chunk_off;
   A.chunk_cnt = h->chunk_cnt;
+  A.ev_base = h->bounded ? h->ev_base : nullptr;
+  A.drop_bits = h->bounded ? h->drop_bits : nullptr;
+  A.no_events = h->cfg.kind == EQ_KIND_DONOTHING;
   A.tl = (h->tl_b && A.m_run <= h->tl_steps) ? h->tl_b : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
@@ -386,6 +486,13 @@ int setup_geometry(eq_handle* h) {
     kb = (const void*)k_backward<double, kNT, kU>;
   }
   EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf, kNT, 0));
+  {
+    int occ_q = 0;
+    const void* kq = h->cfg.precision == 32 ? (const void*)k_forward_bounded<float, kNT, kU>
+                                            : (const void*)k_forward_bounded<double, kNT, kU>;
+    EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, kq, kNT, 0));
+    occ_f = std::min(occ_f, occ_q);
+  }
   int occ = std::max(1, occ_f);
   for (; occ >= 1; --occ) {
     long long G = (long long)h->n_sm * occ;
@@ -425,6 +532,91 @@ int ensure_chunks(eq_handle* h, int steps_needed) {
   return EQ_OK;
 }
 
+// Bounded kinds: in-edge ranks (stable CSC order via CUB radix sort), bitmap
+// layout, queue storage.  Capacity: the reference's (`queue_capacity or
+// horizon*(n-1)+1`, network.py:327); the physical array is min(that, the
+// lossless bound max_j sum_{e->j}(ceil(d_e/dt)+1)), which cannot change any
+// accept decision because occupancy never exceeds the bound.
+int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStream_t s) {
+  const eq_config& c = h->cfg;
+  const int N = c.n_neurons, B = c.n_trials;
+  const long long E = h->E;
+  h->cap_ref = c.capacity > 0 ? c.capacity : (long long)h->horizon * (N - 1) + 1;
+  long long cap = std::min<long long>(h->cap_ref, std::max<long long>(occ_bound, 1));
+  if (cap > (1 << 20)) return fail(h, EQ_ERR_CONFIGURATION, "queue capacity too large; set eq_config.capacity");
+  h->cap = (int)cap;
+  if (E >= (1LL << 31)) return fail(h, EQ_ERR_CONFIGURATION, "bounded kinds support < 2^31 edges");
+  size_t qbytes = (size_t)B * N * h->cap * (c.precision == 32 ? sizeof(QEv<float>) : sizeof(QEv<double>));
+  if (qbytes > ((size_t)96 << 30))
+    return fail(h, EQ_ERR_CONFIGURATION, "queue storage " + std::to_string(qbytes >> 20) +
+                                             " MiB exceeds 96 GiB; set eq_config.capacity");
+  for (void** p : {(void**)&h->in_pos, (void**)&h->csc_off, (void**)&h->word_off, &h->stage,
+                   (void**)&h->stage_row, (void**)&h->arr, (void**)&h->flags, &h->q, (void**)&h->meta,
+                   (void**)&h->ev_base, (void**)&h->ev_count, (void**)&h->drop_bits}) {
+    release(h, *p);
+    *p = nullptr;
+  }
+  // stable sort of (target, edge) pairs -> csc order
+  void *keys_out = nullptr, *vals_in = nullptr, *vals_out = nullptr, *tmp = nullptr;
+  EQ_CUDA(h, alloc(h, &keys_out, E * sizeof(int)));
+  EQ_CUDA(h, alloc(h, &vals_in, E * sizeof(int)));
+  EQ_CUDA(h, alloc(h, &vals_out, E * sizeof(int)));
+  k_iota<<<592, 256, 0, s>>>((int*)vals_in, E);
+  size_t tmp_bytes = 0;
+  int end_bit = 1;
+  while ((1LL << end_bit) < N) ++end_bit;
+  EQ_CUDA(h, cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, h->col, (int*)keys_out, (const int*)vals_in,
+                                             (int*)vals_out, (int)E, 0, end_bit, s));
+  EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
+  EQ_CUDA(h, cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, h->col, (int*)keys_out, (const int*)vals_in,
+                                             (int*)vals_out, (int)E, 0, end_bit, s));
+  release(h, tmp);
+  // csc_off = exclusive scan of in-degree; word_off = exclusive scan of ceil(indeg/32)
+  EQ_CUDA(h, alloc(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, (void**)&h->word_off, (size_t)(N + 1) * sizeof(long long)));
+  void *deg64 = nullptr, *words = nullptr;
+  EQ_CUDA(h, alloc(h, &deg64, (size_t)(N + 1) * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, &words, (size_t)(N + 1) * sizeof(long long)));
+  EQ_CUDA(h, cudaMemsetAsync(deg64, 0, (size_t)(N + 1) * sizeof(long long), s));
+  EQ_CUDA(h, cudaMemsetAsync(words, 0, (size_t)(N + 1) * sizeof(long long), s));
+  k_words_of<<<(N + 255) / 256, 256, 0, s>>>(indeg, N, (long long*)words);
+  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const long long*)words, h->word_off, N + 1, s));
+  EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
+  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, (const long long*)words, h->word_off, N + 1, s));
+  release(h, tmp);
+  tmp_bytes = 0;
+  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, indeg, h->csc_off, N + 1, s));
+  EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
+  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, indeg, h->csc_off, N + 1, s));
+  release(h, tmp);
+  release(h, deg64);
+  EQ_CUDA(h, alloc(h, (void**)&h->in_pos, E * sizeof(int)));
+  k_in_pos<<<592, 256, 0, s>>>((const int*)keys_out, (const int*)vals_out, h->csc_off, E, h->in_pos);
+  h->launches += 4;
+  long long wtot = 0;
+  EQ_CUDA(h, cudaMemcpyAsync(&wtot, h->word_off + N, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  release(h, words);
+  release(h, keys_out);
+  release(h, vals_in);
+  release(h, vals_out);
+  h->W = wtot;
+  const size_t qe = c.precision == 32 ? sizeof(QEv<float>) : sizeof(QEv<double>);
+  const int fwords = (N + 31) / 32;
+  EQ_CUDA(h, alloc(h, &h->stage, (size_t)2 * B * E * qe));
+  EQ_CUDA(h, alloc(h, (void**)&h->stage_row, (size_t)2 * B * E * sizeof(unsigned short)));
+  EQ_CUDA(h, alloc(h, (void**)&h->arr, (size_t)2 * B * h->W * sizeof(unsigned)));
+  EQ_CUDA(h, alloc(h, (void**)&h->flags, (size_t)2 * B * fwords * sizeof(unsigned)));
+  EQ_CUDA(h, alloc(h, &h->q, qbytes));
+  EQ_CUDA(h, alloc(h, (void**)&h->meta, (size_t)B * N * sizeof(int4)));
+  EQ_CUDA(h, alloc(h, (void**)&h->ev_base, (size_t)h->log_cap * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, (void**)&h->ev_count, sizeof(unsigned long long)));
+  // one bit per event of the run: spike-log capacity x mean out-degree x 2
+  h->drop_cap = ((long long)h->log_cap * std::max<long long>(1, 2 * E / N) + 31) / 32 * 32;
+  EQ_CUDA(h, alloc(h, (void**)&h->drop_bits, (size_t)h->drop_cap / 8));
+  return EQ_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -453,8 +645,11 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   if (!(c.tau_m > 0.0)) return bad("tau_m must be positive, got " + std::to_string(c.tau_m));
   if (!(c.tau_syn > 0.0)) return bad("tau_syn must be positive, got " + std::to_string(c.tau_syn));
   if (!(c.v_th > c.v_reset)) return bad("threshold must sit above reset");
-  if (c.kind != EQ_KIND_RING && c.kind != EQ_KIND_DONOTHING)
-    return bad("queue kind " + std::to_string(c.kind) + " is not available in this build");
+  if (c.kind != EQ_KIND_RING && c.kind != EQ_KIND_DONOTHING && c.kind != EQ_KIND_FIFORING &&
+      c.kind != EQ_KIND_BINARYHEAP && c.kind != EQ_KIND_SORTEDARRAY)
+    return bad("unknown queue kind " + std::to_string(c.kind));
+  if (c.capacity < 0) return bad("capacity must be >= 1, got " + std::to_string(c.capacity));
+  h->bounded = c.kind == EQ_KIND_FIFORING || c.kind == EQ_KIND_BINARYHEAP || c.kind == EQ_KIND_SORTEDARRAY;
   if (c.exact_delivery && std::fabs(c.tau_m - c.tau_syn) < 1e-3 * c.tau_m)
     return bad("exact delivery splits the membrane/synapse eigenmodes and needs tau_m != tau_syn");
   h->total = (long long)c.n_neurons * c.n_trials;
@@ -526,28 +721,36 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   const eq_config& c = h->cfg;
   const int N = c.n_neurons;
   if (n_edges < 1) return fail(h, EQ_ERR_CONFIGURATION, "network has no edges");
-  void *insum = nullptr, *stats = nullptr;
+  void *insum = nullptr, *stats = nullptr, *inocc = nullptr, *indeg = nullptr;
   EQ_CUDA(h, alloc(h, &insum, (size_t)N * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, &inocc, (size_t)N * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, &indeg, (size_t)(N + 1) * sizeof(int)));   // +1: exclusive scan reads n+1
   EQ_CUDA(h, alloc(h, &stats, 4 * sizeof(long long)));
   long long init[4] = {1, -1LL, 0, 0};
   init[1] = (long long)~0ULL;
   EQ_CUDA(h, cudaMemsetAsync(insum, 0, (size_t)N * sizeof(long long), s));
+  EQ_CUDA(h, cudaMemsetAsync(inocc, 0, (size_t)N * sizeof(long long), s));
+  EQ_CUDA(h, cudaMemsetAsync(indeg, 0, (size_t)(N + 1) * sizeof(int), s));
   EQ_CUDA(h, cudaMemcpyAsync(stats, init, sizeof init, cudaMemcpyHostToDevice, s));
   int homog = c.kind == EQ_KIND_FIFORING;
   if (c.precision == 32)
     k_net_stats<float><<<(N + 127) / 128, 128, 0, s>>>(N, rowptr, col, (const float*)weight, (const float*)delay,
-                                                        (float)c.dt, homog, (long long*)insum, (long long*)stats);
+                                                        (float)c.dt, homog, (long long*)insum, (long long*)stats,
+                                                        (long long*)inocc, (int*)indeg);
   else
     k_net_stats<double><<<(N + 127) / 128, 128, 0, s>>>(N, rowptr, col, (const double*)weight,
                                                          (const double*)delay, c.dt, homog, (long long*)insum,
-                                                         (long long*)stats);
+                                                         (long long*)stats, (long long*)inocc, (int*)indeg);
   k_max_ll<<<256, 256, 0, s>>>((const long long*)insum, N, (long long*)stats + 2);
-  h->launches += 2;
+  k_max_ll<<<256, 256, 0, s>>>((const long long*)inocc, N, (long long*)stats + 3);
+  h->launches += 3;
   long long st[4];
   EQ_CUDA(h, cudaMemcpyAsync(st, stats, sizeof st, cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));
   release(h, insum);
+  release(h, inocc);
   release(h, stats);
+  struct Free { eq_handle* h; void* p; ~Free() { release(h, p); } } free_indeg{h, indeg};
   if ((unsigned long long)st[1] != ~0ULL) {
     unsigned long long key = (unsigned long long)st[1];
     long long x = (long long)(key >> 2);
@@ -610,6 +813,10 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   h->ring_words = words;
   EQ_CUDA(h, alloc(h, (void**)&h->ring, words * sizeof(long long)));
   EQ_CUDA(h, alloc(h, &h->lam, (size_t)c.n_trials * h->R * N * 2 * h->tsize));
+  if (h->bounded) {
+    int rc = setup_bounded(h, (const int*)indeg, st[3], s);
+    if (rc) return rc;
+  }
   h->net_set = true;
   return eq_reset(h, stream);
 }
@@ -641,6 +848,15 @@ int eq_reset(eq_handle* h, void* stream) {
   EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, 4 * sizeof(int), s));
   EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 64 * sizeof(unsigned), s));
   EQ_CUDA(h, cudaMemsetAsync(h->log_count, 0, sizeof(unsigned long long), s));
+  if (h->bounded) {
+    const int B = h->cfg.n_trials, N = h->cfg.n_neurons;
+    EQ_CUDA(h, cudaMemsetAsync(h->arr, 0, (size_t)2 * B * h->W * sizeof(unsigned), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->flags, 0, (size_t)2 * B * ((N + 31) / 32) * sizeof(unsigned), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->ev_count, 0, sizeof(unsigned long long), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
+    k_meta_init<<<592, 256, 0, s>>>(h->meta, (long long)B * N);
+    h->launches += 1;
+  }
   h->steps_done = 0;
   return EQ_OK;
 }
@@ -674,8 +890,6 @@ int eq_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* grad
                 double* grad_amp, void* stream) {
   if (!h) return EQ_ERR_CONFIGURATION;
   if (h->steps_done < 1) return fail(h, EQ_ERR_CONFIGURATION, "backward needs a forward run first");
-  if (h->cfg.kind != EQ_KIND_RING && h->cfg.kind != EQ_KIND_DONOTHING)
-    return fail(h, EQ_ERR_CONFIGURATION, "reverse mode not available for this queue kind");
   if (!h->cfg.exact_delivery) return fail(h, EQ_ERR_CONFIGURATION, "reverse mode requires exact_delivery");
   if (!v_bar || !grad_w || !grad_d) return fail(h, EQ_ERR_CONFIGURATION, "v_bar, grad_w, grad_d are required");
   DeviceGuard g(h->device);
@@ -726,17 +940,25 @@ int eq_get_spikes(eq_handle* h, int32_t* step, int32_t* trial, int32_t* neuron, 
 
 int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream) {
   if (!h) return EQ_ERR_CONFIGURATION;
-  if (h->cfg.kind != EQ_KIND_RING) return fail(h, EQ_ERR_CONFIGURATION, "pending contents: ring kind only");
+  if (h->cfg.kind == EQ_KIND_DONOTHING) return fail(h, EQ_ERR_CONFIGURATION, "donothing holds no events");
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int N = h->cfg.n_neurons, B = h->cfg.n_trials, H = h->horizon;
   size_t n = (size_t)B * N * H * 2;
   void* buf = nullptr;
   EQ_CUDA(h, alloc(h, &buf, n * sizeof(long long)));
-  if (h->cfg.precision == 32)
+  if (h->bounded) {
+    if (h->cfg.precision == 32)
+      k_pending_bounded<float><<<592, 256, 0, s>>>((const QEv<float>*)h->q, h->meta, h->cfg.kind, h->cap,
+                                                    (long long)B * N, H, h->steps_done, (long long*)buf);
+    else
+      k_pending_bounded<double><<<592, 256, 0, s>>>((const QEv<double>*)h->q, h->meta, h->cfg.kind, h->cap,
+                                                     (long long)B * N, H, h->steps_done, (long long*)buf);
+  } else if (h->cfg.precision == 32) {
     k_pending<float><<<592, 256, 0, s>>>(h->ring, B, h->R, N, H, h->steps_done, (long long*)buf);
-  else
+  } else {
     k_pending<double><<<592, 256, 0, s>>>(h->ring, B, h->R, N, H, h->steps_done, (long long*)buf);
+  }
   h->launches += 1;
   EQ_CUDA(h, cudaMemcpyAsync(host_out, buf, n * sizeof(long long), cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));

@@ -178,3 +178,123 @@ def test_configuration_errors_name_the_edge():
     mask = wl.drive_masks(20, 1, 50, 1e-3)
     with pytest.raises(ConfigurationError, match=rf"edge \({src[7]},{net.col[7]}\).*below one step"):
         _engine(net, mask, np.full(20, 12.0), 1, 50, 32)
+
+
+# ---------------------------------------------------------------- bounded kinds
+
+BOUNDED = ["dense_heap_n8", "dense_sorted_n8", "dense_fifo_n8", "dense_heap_cap3_n12", "dense_sorted_cap3_n12",
+           "dense_fifo_cap2_n12"]
+
+
+def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=True):
+    from paper_2512_05906_b200.engine import Engine
+    eng = Engine(net.n, B, T, kind=kind, precision=precision, capacity=capacity or 0)
+    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+    eng.set_drive(mask, amp)
+    out = eng.forward()
+    s = OracleSession(n=net.n, n_trials=B, t_steps=T, kind=kind, mode="device", precision=precision,
+                      frac_bits=eng.frac_bits, capacity=capacity or 0)
+    s.set_network(net.rowptr, net.col, net.weight, net.delay)
+    s.set_drive(mask, amp)
+    ref = s.forward()
+    r_g, t_g = _sorted_spikes(eng.spikes())
+    r_o, t_o = _sorted_spikes(ref)
+    assert np.array_equal(r_g, r_o), "raster differs"
+    assert np.array_equal(t_g.astype(np.float64), t_o)
+    assert np.array_equal(out["v"].double().cpu().numpy(), ref["v"])
+    assert np.array_equal(out["i"].double().cpu().numpy(), ref["i"])
+    assert np.array_equal(eng.counters(), ref["counters"])      # incl. drops
+    assert np.array_equal(eng.pending(), ref["pending"])        # queue contents after the run
+    return eng, out, ref
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("name", BOUNDED)
+def test_bounded_kinds_bitwise_vs_oracle(name, precision):
+    case = BY_NAME[name]
+    net, mask, amp = case.inputs()
+    _compare_bounded(net, mask, amp, 1, case.t_steps, precision, case.kind, case.capacity)
+
+
+@pytest.mark.parametrize("name", BOUNDED)
+def test_bounded_fp64_vs_reference_fixture(name):
+    case = BY_NAME[name]
+    g = np.load(os.path.join(GOLDEN, name + ".npz"))
+    net, mask, amp = case.inputs()
+    from paper_2512_05906_b200.engine import Engine
+    eng = Engine(net.n, 1, case.t_steps, kind=case.kind, precision=64, capacity=case.capacity or 0)
+    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+    eng.set_drive(mask, amp)
+    out = eng.forward()
+    sp = eng.spikes()
+    raster = np.stack([sp["step"], sp["neuron"]], 1)
+    raster = raster[np.lexsort((raster[:, 1], raster[:, 0]))]
+    assert np.array_equal(raster, g["raster"])
+    np.testing.assert_allclose(out["v"][0].cpu().numpy(), g["v_final_primal"], rtol=1e-9, atol=1e-12)
+    spikes, events, drops = eng.counters()[0].tolist()
+    assert spikes == int(g["spike_count"]) and drops == int(g["drop_count"])
+
+
+@pytest.mark.parametrize("kind", ["binaryheap", "sortedarray"])
+def test_bounded_multi_trial_with_drops_and_reverse(kind):
+    """Sparse net, 3 trials, capacity small enough to drop: forward bitwise vs
+    the oracle; the reverse pass must skip dropped events exactly (its
+    gradients equal the oracle's pool-semantics reverse)."""
+    net = wl.random_network(200, 20, 13, delay_steps=(1, 12), w_mean=0.05, w_std=0.02)
+    B, T = 3, 400
+    mask = wl.drive_masks(200, B, T, 1e-3, seed0=91)
+    amp = np.full(200, 12.0)
+    eng, out, ref = _compare_bounded(net, mask, amp, B, T, 32, kind, 4)
+    assert eng.counters()[:, 2].sum() > 0, "capacity 4 should drop"
+    vbar = (2.0 * (out["v"] - 0.25)).float()
+    gw, gd, ga = (x.cpu().numpy() for x in eng.backward(vbar))
+    s = OracleSession(n=200, n_trials=B, t_steps=T, kind=kind, mode="device", precision=32,
+                      frac_bits=eng.frac_bits, capacity=4)
+    s.set_network(net.rowptr, net.col, net.weight, net.delay)
+    s.set_drive(mask, amp)
+    s.forward()
+    ow, od, oa = s.backward(vbar.double().cpu().numpy())
+    np.testing.assert_allclose(gw, ow, rtol=1e-12, atol=1e-12 * np.abs(ow).max())
+    np.testing.assert_allclose(gd, od, rtol=1e-12, atol=1e-12 * np.abs(od).max())
+    assert np.array_equal(ga, oa)
+
+
+@pytest.mark.parametrize("kind", ["binaryheap", "fiforing", "donothing"])
+def test_bounded_single_trial_reverse_bitwise(kind):
+    case = BY_NAME["dense_fifo_cap2_n12" if kind == "fiforing" else "dense_heap_cap3_n12"]
+    net, mask, amp = case.inputs()
+    cap = case.capacity if kind != "donothing" else 0
+    from paper_2512_05906_b200.engine import Engine
+    eng = Engine(net.n, 1, case.t_steps, kind=kind, precision=64, capacity=cap)
+    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+    eng.set_drive(mask, amp)
+    out = eng.forward()
+    vbar = 2.0 * (out["v"] - 0.25)
+    gw, gd, ga = (x.cpu().numpy() for x in eng.backward(vbar))
+    s = OracleSession(n=net.n, n_trials=1, t_steps=case.t_steps, kind=kind, mode="device", precision=64,
+                      frac_bits=eng.frac_bits, capacity=cap)
+    s.set_network(net.rowptr, net.col, net.weight, net.delay)
+    s.set_drive(mask, amp)
+    s.forward()
+    ow, od, oa = s.backward(vbar.cpu().numpy())
+    assert np.array_equal(gw, ow) and np.array_equal(gd, od) and np.array_equal(ga, oa)
+
+
+def test_lossless_bounded_equals_ring_bitwise():
+    """Without drops every kind delivers the same sums."""
+    net = wl.random_network(150, 15, 17, delay_steps=(1, 10), w_mean=0.03, w_std=0.01)
+    B, T = 2, 300
+    mask = wl.drive_masks(150, B, T, 1e-3, seed0=5)
+    amp = np.full(150, 12.0)
+    outs = {}
+    from paper_2512_05906_b200.engine import Engine
+    for kind in ("ring", "binaryheap", "sortedarray"):
+        eng = Engine(150, B, T, kind=kind, precision=32)
+        eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+        eng.set_drive(mask, amp)
+        o = eng.forward()
+        outs[kind] = (o["v"].cpu().numpy(), eng.spikes()["t"], eng.pending())
+    for kind in ("binaryheap", "sortedarray"):
+        assert np.array_equal(outs[kind][0], outs["ring"][0])
+        assert np.array_equal(outs[kind][1], outs["ring"][1])
+        assert np.array_equal(outs[kind][2], outs["ring"][2])
