@@ -48,6 +48,7 @@ enum {
   EQ_KIND_FIFORING = 1,    /* FIFORingQueue   queues.py:184-260 */
   EQ_KIND_BINARYHEAP = 2,  /* BinaryHeapQueue queues.py:481-571 */
   EQ_KIND_SORTEDARRAY = 3, /* SortedArrayQueue queues.py:308-403 */
+  EQ_KIND_LOSSYRING = 4,   /* LossyRingQueue  queues.py:126-181 (queue API only) */
   EQ_KIND_DONOTHING = 5    /* DoNothingQueue  queues.py:26-52   */
 };
 
@@ -134,6 +135,37 @@ int64_t eq_launch_count(const eq_handle* h);
  * the grid barrier, [3] after it, [4..7] kernel-specific sub-phase marks (0 = unset).
  * Only when the environment had EQ_TIMELINE=1 at eq_create. */
 int eq_debug_timeline(eq_handle* h, int which, uint64_t* host_out);
+
+/* ------------------------------------------------------------------------
+ * Queue operator API: a batch of Q independent queues of one kind that step
+ * together.  Replaces make_queue (queues.py:636-692) and the EventQueue
+ * protocol (events.py:99-141): enqueue -> bool accepted, pop_due -> merged
+ * (weight, weight_tangent, weighted_time_tangent) per queue, occupancy, now.
+ * Payload arrays are float (precision 32) or double (64); merges happen in
+ * insertion order in that precision, exactly as the Python classes do.
+ * ------------------------------------------------------------------------ */
+typedef struct eq_queues eq_queues;
+
+int eq_queues_create(int kind, int precision, int n_queues, int capacity, int max_delay_steps, int device,
+                     eq_queues** out);
+int eq_queues_destroy(eq_queues* h);
+const char* eq_queues_last_error(const eq_queues* h);
+int eq_queues_capacity(const eq_queues* h);
+int eq_queues_now(const eq_queues* h);
+/* n events in CALL order (device arrays): target queue, deliver_step, weight,
+ * weight tangent, time tangent; accepted[k] = 0 when the kind's drop policy
+ * rejected event k.  The first offending event (CausalityError /
+ * CapabilityError) aborts the batch: events before it in call order are
+ * applied, none after. */
+int eq_queues_enqueue(eq_queues* h, const int32_t* queue, const int32_t* deliver_step, const void* weight,
+                      const void* weight_tangent, const void* time_tangent, int64_t n, uint8_t* accepted,
+                      void* stream);
+/* pop_due for every queue (advances now by one): out arrays of length Q;
+ * has[q] = 0 where _pop_raw would return None. */
+int eq_queues_pop(eq_queues* h, void* out_w, void* out_dw, void* out_wtt, uint8_t* out_has, void* stream);
+int eq_queues_occupancy(eq_queues* h, int32_t* out, void* stream);
+/* LossyRingQueue.aliased / .merged per queue (device int64 arrays). */
+int eq_queues_lossy_counts(eq_queues* h, int64_t* aliased, int64_t* merged, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ from .errors import STATUS_TO_ERROR, EventQError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libeventq_b200.so")
 
-KIND_IDS = {"ring": 0, "fiforing": 1, "binaryheap": 2, "sortedarray": 3, "donothing": 5}
+KIND_IDS = {"ring": 0, "fiforing": 1, "binaryheap": 2, "sortedarray": 3, "lossyring": 4, "donothing": 5}
 
 
 class Config(ctypes.Structure):
@@ -62,6 +62,15 @@ def lib() -> ctypes.CDLL:
         "eq_geometry": (ctypes.c_int, [H, vp, vp]),
         "eq_launch_count": (i64, [H]),
         "eq_debug_timeline": (ctypes.c_int, [H, ctypes.c_int, vp]),
+        "eq_queues_create": (ctypes.c_int, [ctypes.c_int] * 6 + [ctypes.POINTER(H)]),
+        "eq_queues_destroy": (ctypes.c_int, [H]),
+        "eq_queues_last_error": (ctypes.c_char_p, [H]),
+        "eq_queues_capacity": (ctypes.c_int, [H]),
+        "eq_queues_now": (ctypes.c_int, [H]),
+        "eq_queues_enqueue": (ctypes.c_int, [H, vp, vp, vp, vp, vp, i64, vp, vp]),
+        "eq_queues_pop": (ctypes.c_int, [H, vp, vp, vp, vp, vp]),
+        "eq_queues_occupancy": (ctypes.c_int, [H, vp, vp]),
+        "eq_queues_lossy_counts": (ctypes.c_int, [H, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -74,12 +83,14 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive",
             "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_counters", "eq_spike_count",
             "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",
-            "eq_launch_count", "eq_debug_timeline")
+            "eq_launch_count", "eq_debug_timeline", "eq_queues_create", "eq_queues_destroy",
+            "eq_queues_last_error", "eq_queues_capacity", "eq_queues_now", "eq_queues_enqueue", "eq_queues_pop",
+            "eq_queues_occupancy", "eq_queues_lossy_counts")
 
 
-def check(handle, code: int) -> None:
+def check(handle, code: int, queues: bool = False) -> None:
     if code == 0:
         return
-    msg = lib().eq_last_error(handle)
+    msg = (lib().eq_queues_last_error if queues else lib().eq_last_error)(handle)
     msg = msg.decode() if msg else ""
     raise STATUS_TO_ERROR.get(code, EventQError)(msg)

@@ -18,8 +18,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libeventq_b200.so")
-SOURCES = ["eventq.cu"]
-HEADERS = ["eq_device.cuh", "eq_ring.cuh"]
+SOURCES = ["eventq.cu", "eq_queues.cu"]
+HEADERS = ["eq_device.cuh", "eq_ring.cuh", "eq_bounded.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
