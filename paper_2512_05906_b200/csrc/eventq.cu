@@ -105,6 +105,7 @@ struct eq_handle {
   int steps_done = 0;
   long long launches = 0;
   std::vector<void*> owned;
+  std::vector<std::pair<void*, size_t>> sizes;   // reusable buffers
 };
 
 namespace {
@@ -136,6 +137,23 @@ void release(eq_handle* h, void* p) {
   if (!p) return;
   cudaFree(p);
   h->owned.erase(std::remove(h->owned.begin(), h->owned.end(), p), h->owned.end());
+  h->sizes.erase(std::remove_if(h->sizes.begin(), h->sizes.end(),
+                                [p](const std::pair<void*, size_t>& e) { return e.first == p; }),
+                 h->sizes.end());
+}
+
+// Keep *p if it already holds >= bytes (set_network is called every training
+// step by the autograd shell; cudaMalloc/free per call would dominate).
+cudaError_t ensure(eq_handle* h, void** p, size_t bytes) {
+  if (*p) {
+    for (auto& e : h->sizes)
+      if (e.first == *p && e.second >= bytes) return cudaSuccess;
+    release(h, *p);
+    *p = nullptr;
+  }
+  cudaError_t e = alloc(h, p, bytes);
+  if (e == cudaSuccess) h->sizes.push_back({*p, bytes});
+  return e;
 }
 
 template <typename T>
@@ -550,12 +568,6 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   if (qbytes > ((size_t)96 << 30))
     return fail(h, EQ_ERR_CONFIGURATION, "queue storage " + std::to_string(qbytes >> 20) +
                                              " MiB exceeds 96 GiB; set eq_config.capacity");
-  for (void** p : {(void**)&h->in_pos, (void**)&h->csc_off, (void**)&h->word_off, &h->stage,
-                   (void**)&h->stage_row, (void**)&h->arr, (void**)&h->flags, &h->q, (void**)&h->meta,
-                   (void**)&h->ev_base, (void**)&h->ev_count, (void**)&h->drop_bits}) {
-    release(h, *p);
-    *p = nullptr;
-  }
   // stable sort of (target, edge) pairs -> csc order
   void *keys_out = nullptr, *vals_in = nullptr, *vals_out = nullptr, *tmp = nullptr;
   EQ_CUDA(h, alloc(h, &keys_out, E * sizeof(int)));
@@ -572,8 +584,8 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
                                              (int*)vals_out, (int)E, 0, end_bit, s));
   release(h, tmp);
   // csc_off = exclusive scan of in-degree; word_off = exclusive scan of ceil(indeg/32)
-  EQ_CUDA(h, alloc(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
-  EQ_CUDA(h, alloc(h, (void**)&h->word_off, (size_t)(N + 1) * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, (void**)&h->word_off, (size_t)(N + 1) * sizeof(long long)));
   void *deg64 = nullptr, *words = nullptr;
   EQ_CUDA(h, alloc(h, &deg64, (size_t)(N + 1) * sizeof(long long)));
   EQ_CUDA(h, alloc(h, &words, (size_t)(N + 1) * sizeof(long long)));
@@ -590,7 +602,7 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, indeg, h->csc_off, N + 1, s));
   release(h, tmp);
   release(h, deg64);
-  EQ_CUDA(h, alloc(h, (void**)&h->in_pos, E * sizeof(int)));
+  EQ_CUDA(h, ensure(h, (void**)&h->in_pos, E * sizeof(int)));
   k_in_pos<<<592, 256, 0, s>>>((const int*)keys_out, (const int*)vals_out, h->csc_off, E, h->in_pos);
   h->launches += 4;
   long long wtot = 0;
@@ -603,17 +615,17 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   h->W = wtot;
   const size_t qe = c.precision == 32 ? sizeof(QEv<float>) : sizeof(QEv<double>);
   const int fwords = (N + 31) / 32;
-  EQ_CUDA(h, alloc(h, &h->stage, (size_t)2 * B * E * qe));
-  EQ_CUDA(h, alloc(h, (void**)&h->stage_row, (size_t)2 * B * E * sizeof(unsigned short)));
-  EQ_CUDA(h, alloc(h, (void**)&h->arr, (size_t)2 * B * h->W * sizeof(unsigned)));
-  EQ_CUDA(h, alloc(h, (void**)&h->flags, (size_t)2 * B * fwords * sizeof(unsigned)));
-  EQ_CUDA(h, alloc(h, &h->q, qbytes));
-  EQ_CUDA(h, alloc(h, (void**)&h->meta, (size_t)B * N * sizeof(int4)));
-  EQ_CUDA(h, alloc(h, (void**)&h->ev_base, (size_t)h->log_cap * sizeof(long long)));
-  EQ_CUDA(h, alloc(h, (void**)&h->ev_count, sizeof(unsigned long long)));
+  EQ_CUDA(h, ensure(h, &h->stage, (size_t)2 * B * E * qe));
+  EQ_CUDA(h, ensure(h, (void**)&h->stage_row, (size_t)2 * B * E * sizeof(unsigned short)));
+  EQ_CUDA(h, ensure(h, (void**)&h->arr, (size_t)2 * B * h->W * sizeof(unsigned)));
+  EQ_CUDA(h, ensure(h, (void**)&h->flags, (size_t)2 * B * fwords * sizeof(unsigned)));
+  EQ_CUDA(h, ensure(h, &h->q, qbytes));
+  EQ_CUDA(h, ensure(h, (void**)&h->meta, (size_t)B * N * sizeof(int4)));
+  EQ_CUDA(h, ensure(h, (void**)&h->ev_base, (size_t)h->log_cap * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, (void**)&h->ev_count, sizeof(unsigned long long)));
   // one bit per event of the run: spike-log capacity x mean out-degree x 2
   h->drop_cap = ((long long)h->log_cap * std::max<long long>(1, 2 * E / N) + 31) / 32 * 32;
-  EQ_CUDA(h, alloc(h, (void**)&h->drop_bits, (size_t)h->drop_cap / 8));
+  EQ_CUDA(h, ensure(h, (void**)&h->drop_bits, (size_t)h->drop_cap / 8));
   return EQ_OK;
 }
 
@@ -805,14 +817,10 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   h->d = delay;
   h->E = n_edges;
   // queue storage
-  release(h, h->ring);
-  release(h, h->lam);
-  h->ring = nullptr;
-  h->lam = nullptr;
   size_t words = c.kind == EQ_KIND_RING ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
   h->ring_words = words;
-  EQ_CUDA(h, alloc(h, (void**)&h->ring, words * sizeof(long long)));
-  EQ_CUDA(h, alloc(h, &h->lam, (size_t)c.n_trials * h->R * N * 2 * h->tsize));
+  EQ_CUDA(h, ensure(h, (void**)&h->ring, words * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, &h->lam, (size_t)c.n_trials * h->R * N * 2 * h->tsize));
   if (h->bounded) {
     int rc = setup_bounded(h, (const int*)indeg, st[3], s);
     if (rc) return rc;
