@@ -114,10 +114,10 @@ def dist_env():
     return rank, world, local
 
 
-def make_inputs(cfg, trials, rank, seed=0):
+def make_inputs(cfg, trials, rank, seed=0, delay_steps=None):
     from paper_2512_05906_b200 import workload as wl
     n, k, drange, _, T = wl.CONFIGS[cfg]
-    net = wl.random_network(n, k, seed, delay_steps=drange)
+    net = wl.random_network(n, k, seed, delay_steps=delay_steps or drange)
     # trial b of rank r has drive seed 1000 + r*trials + b
     from concurrent.futures import ProcessPoolExecutor
     seeds = [1000 + rank * trials + b for b in range(trials)]
@@ -136,7 +136,7 @@ def _one_mask(args):
 
 # ---------------------------------------------------------------- reference arm (CPU)
 
-def cpu_reference_sample(net, mask, amp, T, max_trials=None, steps=None):
+def cpu_reference_sample(net, mask, amp, T, max_trials=None, steps=None, kind="ring", capacity=0):
     """The oracle (C++ port of the reference path) on host cores: forward +
     reverse over `trials` trials of the same network; returns (events/s, info)."""
     from oracle import oracle as orc
@@ -144,7 +144,8 @@ def cpu_reference_sample(net, mask, amp, T, max_trials=None, steps=None):
     B = max_trials or min(threads, 16)
     B = min(B, mask.shape[0])
     steps = steps or T
-    s = orc.OracleSession(n=net.n, n_trials=B, t_steps=steps, mode="device", precision=32,
+    s = orc.OracleSession(n=net.n, n_trials=B, t_steps=steps, mode="device", precision=32, kind=kind,
+                          capacity=capacity,
                           frac_bits=orc.frac_bits(float(np.bincount(net.col, weights=np.abs(net.weight),
                                                                      minlength=net.n).max()), 32))
     s.set_network(net.rowptr, net.col, net.weight, net.delay)
@@ -154,7 +155,7 @@ def cpu_reference_sample(net, mask, amp, T, max_trials=None, steps=None):
     s.backward(2.0 * (out["v"] - 0.25))
     dt = time.perf_counter() - t0
     events = int(out["counters"][:, 1].sum())
-    return events / dt, dict(cores=threads, trials=B, steps=steps, seconds=dt, events=events,
+    return events / dt, dict(cores=min(threads, B), trials=B, steps=steps, seconds=dt, events=events,
                              neuron_steps=B * steps * net.n)
 
 
@@ -164,11 +165,12 @@ def run_reference(args):
         return
     from oracle import oracle as orc
     trials = args.cpu_trials or min(orc.threads(), 16)
-    net, mask, amp, T = make_inputs(args.config, trials, 0)
+    net, mask, amp, T = make_inputs(args.config, trials, 0, delay_steps=args.delays)
     vals = []
     info = None
     for it in range(args.warmup + args.steps):
-        v, info = cpu_reference_sample(net, mask, amp, T, max_trials=args.cpu_trials, steps=args.cpu_steps)
+        v, info = cpu_reference_sample(net, mask, amp, T, max_trials=args.cpu_trials, steps=args.cpu_steps,
+                                       kind=args.kind, capacity=args.capacity)
         if it >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -176,7 +178,7 @@ def run_reference(args):
         "impl": "reference", "metric": "synaptic events/sec (fwd+bwd)", "value": value,
         "unit": "events/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": f"{args.config} ring fwd+bwd (sample)", **info},
+        "data": "synthetic", "config": {"workload": f"{args.config} {args.kind} fwd+bwd (sample)", **info},
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": info["cores"], "kind": "port",
                          "sample": f"{info['trials']} trials x {info['steps']} steps of {args.config}"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -198,12 +200,12 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    net, mask, amp, T = make_inputs(args.config, args.trials, rank)
+    net, mask, amp, T = make_inputs(args.config, args.trials, rank, delay_steps=args.delays)
     B = args.trials
     if args.steps_per_pass:
         T = args.steps_per_pass
         mask = np.ascontiguousarray(mask[:, :T])
-    eng = Engine(net.n, B, T, precision=args.precision, device=local)
+    eng = Engine(net.n, B, T, kind=args.kind, capacity=args.capacity, precision=args.precision, device=local)
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     mask_dev = torch.from_numpy(mask.view(np.int32)).to(dev)
     amp_dev = torch.from_numpy(amp).to(dev, eng.dtype)
@@ -316,7 +318,8 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
-            v, info = cpu_reference_sample(net, mask, amp, T, max_trials=args.cpu_trials, steps=args.cpu_steps)
+            v, info = cpu_reference_sample(net, mask, amp, T, max_trials=args.cpu_trials, steps=args.cpu_steps,
+                                           kind=args.kind, capacity=args.capacity)
             cpu = {"value": v, "unit": "events/s", "cores": info["cores"], "kind": "port",
                    "sample": f"{info['trials']} trials x {info['steps']} steps of {args.config}, "
                              f"fwd+bwd, OpenMP over trials ({info['seconds']:.1f} s)"}
@@ -336,11 +339,15 @@ def run_ours(args):
         "dtype": "f32" if args.precision == 32 else "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {net.n} LIF neurons, {net.n_edges // net.n} syn/neuron, "
-                               f"delay<=64 steps, ring, fwd+bwd T={T}",
+                               f"delay {int(round(net.delay.min() / 1e-3))}..{int(round(net.delay.max() / 1e-3))} "
+                               f"steps, {args.kind}" + (f"[{args.capacity}]" if args.capacity else "") +
+                               f", fwd+bwd T={T}",
+                   "queue_kind": args.kind, "capacity": args.capacity or None,
+                   "drops_per_gpu": int(counters[:, 2].sum()),
                    "trials_per_gpu": B, "global_trials": B * world, "neurons": net.n, "steps_per_pass": T,
                    "spikes_per_gpu": spikes, "events_per_gpu": events,
                    "neuron_steps_per_sec": neuron_steps * world / (ms_per_step / 1e3),
-                   "l2": "inputs larger than L2 (ring %.2f GB/GPU)" % (B * (eng.horizon + 1) * net.n * 8 / 1e9),
+                   "l2": "inputs larger than L2 (queue storage %.2f GB/GPU)" % (B * (eng.horizon + 1) * net.n * 8 / 1e9),
                    "parallelism": f"trial-dp{world}"},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
@@ -370,6 +377,10 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--steps-per-pass", type=int, default=0, help="override T (debug)")
+    ap.add_argument("--kind", default="ring", choices=["ring", "fiforing", "binaryheap", "sortedarray", "donothing"])
+    ap.add_argument("--capacity", type=int, default=0, help="bounded kinds: events per queue")
+    ap.add_argument("--delays", type=lambda s: tuple(int(x) for x in s.split(",")), default=None,
+                    help="delay range in steps lo,hi (FIFO needs lo == hi)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
