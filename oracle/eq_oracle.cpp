@@ -117,17 +117,27 @@ template <typename T, bool DEV> inline T xlog(T x) {
 
 /*
  * delivery_step (jumps.py:90-96) for a spike emitted in loop step m:
- * max(ceil(t_post/dt), m+2).  In exact arithmetic ceil(t_post/dt) <= m+1+ceil(d/dt)
- * because t_spk <= (m+1)dt; device mode clamps to that bound so that a rounding
- * overshoot of t_post/dt (frequent in fp32 near the end of a step) cannot move
- * an event one step past its edge's horizon.  Reference mode is literal.
+ * max(ceil(t_post/dt), m+2).  For t_spk in (m dt, (m+1) dt] exact arithmetic
+ * bounds ceil(t_post/dt) to [m+1+floor(d/dt), m+1+ceil(d/dt)] — one value when
+ * d is grid-aligned (|d/dt - k| <= tol*k, tol 1e-5 fp32 / 1e-12 fp64).  Device
+ * mode clamps to those bounds so rounding of t_post/dt (frequent in fp32 near
+ * a step edge) cannot move an event by a step; reference mode is literal.
  */
 template <typename T, bool DEV>
 inline int32_t delivery(T t_post, T d, T dt, int m) {
   int32_t q = (int32_t)std::ceil(t_post / dt);
   if (DEV) {
-    int32_t hi = m + 1 + (int32_t)std::ceil(d / dt);
-    q = std::min(q, hi);
+    const T tol = sizeof(T) == 4 ? (T)1e-5 : (T)1e-12;
+    const T kd = d / dt;
+    const T kr = std::rint(kd);
+    int32_t lo, hi;
+    if (std::fabs(kd - kr) <= tol * (kr > (T)1 ? kr : (T)1)) {
+      lo = hi = m + 1 + (int32_t)kr;
+    } else {
+      lo = m + 1 + (int32_t)std::floor(kd);
+      hi = m + 1 + (int32_t)std::ceil(kd);
+    }
+    q = std::min(std::max(q, lo), hi);
   }
   return std::max(q, (int32_t)(m + 2));
 }

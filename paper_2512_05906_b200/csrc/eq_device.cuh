@@ -157,11 +157,26 @@ __device__ __forceinline__ T warp_sum_butterfly(T v) {
 // Mirrors network.py:547-611 (PrimalRSNN.step) with the device-mode delivery
 // clamp of oracle/eq_oracle.cpp::delivery.
 
+// Exact-arithmetic bounds of ceil((t_spk + d)/dt) for t_spk in (m dt, (m+1) dt]:
+// [m+1+floor(d/dt), m+1+ceil(d/dt)], a single value when d is grid-aligned
+// (|d/dt - k| <= tol*k; tol 1e-5 in fp32, 1e-12 in fp64).  Clamping to them
+// removes rounding artefacts of t_post/dt (fp32 near a step edge) that would
+// otherwise move an event one step (spurious CapabilityError on the ring
+// horizon, spurious FIFO order violations for homogeneous delays).
 template <typename T>
 __device__ __forceinline__ int delivery_step(T t_post, T d, T dt, int m) {
+  const T tol = sizeof(T) == 4 ? (T)1e-5 : (T)1e-12;
+  const T kd = d / dt;
+  const T kr = rint(kd);
+  int lo, hi;
+  if (fabs(kd - kr) <= tol * (kr > (T)1 ? kr : (T)1)) {
+    lo = hi = m + 1 + (int)kr;
+  } else {
+    lo = m + 1 + (int)floor(kd);
+    hi = m + 1 + (int)ceil(kd);
+  }
   int q = (int)ceil(t_post / dt);
-  int hi = m + 1 + (int)ceil(d / dt);
-  q = q < hi ? q : hi;
+  q = q < lo ? lo : (q > hi ? hi : q);
   return q > m + 2 ? q : m + 2;
 }
 

@@ -1,0 +1,15 @@
+#!/bin/bash
+# Queue-variant sweep (BASELINE configs C2/C3/C4): one bench line per (config, kind).
+# Usage: bash scripts/variant_sweep.sh OUT.jsonl [steps] [warmup]
+OUT=${1:-gpurun_out/variants.jsonl}
+K=${2:-3}
+W=${3:-3}
+: > "$OUT"
+run() { python bench.py --steps $K --warmup $W --no-cpu "$@" 2>>"${OUT%.jsonl}.err" | tail -1 >> "$OUT"; }
+run --config C2 --trials 32 --kind ring
+run --config C2 --trials 32 --kind binaryheap --capacity 64
+run --config C2 --trials 32 --kind sortedarray --capacity 64
+run --config C2 --trials 32 --kind fiforing --capacity 64 --delays 32,32
+run --config C2 --trials 32 --kind ring --delays 32,32
+run --config C3 --trials 16 --kind binaryheap --capacity 64
+run --config C3 --trials 16 --kind sortedarray --capacity 64
