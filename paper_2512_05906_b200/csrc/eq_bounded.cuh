@@ -205,7 +205,7 @@ __device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int 
 template <typename T, int NT, int U>
 __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
   typedef Prec<T> P;
-  constexpr int kCap = FwdShared<NT>::kCap;
+  constexpr int kCap = FwdShared<NT, T>::kCap;
   constexpr int kTr = FwdShared<NT>::kTrials;
   __shared__ SpikeRec<T> s_spk[kCap];
   __shared__ long long s_r0[kCap];
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
     for (long long base = begin; base < end; base += NT) {
       const int idx = (int)base + tid;
       if (idx >= end) continue;
-      const int b = idx / F.N;
+      const int b = c.divN.div(idx);
       const int j = idx - b * F.N;
       int4 mt = A.meta[idx];
       bool dirty = false;
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
         for (int k = tid; k < nb; k += NT) s_spk[k] = spill[k0 - kCap + k];
       __syncthreads();
       for (int k = tid; k < nb; k += NT) {
-        const int b = s_spk[k].idx / F.N;
+        const int b = c.divN.div(s_spk[k].idx);
         const int i = s_spk[k].idx - b * F.N;
         const long long r0 = __ldg(F.net.rowptr + i);
         const int len = (int)(__ldg(F.net.rowptr + i + 1) - r0);
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
         const int ro = f - s_pre[k];
         const long long x = s_r0[k] + ro;
         const SpikeRec<T> rec = s_spk[k];
-        const int b = rec.idx / F.N;
+        const int b = c.divN.div(rec.idx);
         const int jt = __ldg(F.net.col + x);
         const T w = __ldg(F.net.w + x);
         const T d = __ldg(F.net.d + x);
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
     }
     __syncthreads();
     tl_mark(F.tl, m, F.G, cta, 2);
-    if (!grid_sync(F.bar, F.G, F.err)) break;
+    if (!grid_sync(F.bar, F.G, F.err, F.step_start + m + 1, F.log_count)) break;
     tl_mark(F.tl, m, F.G, cta, 3);
     if (ld_volatile(F.err) != 0) break;
   }

@@ -20,15 +20,18 @@ constexpr int kWarp = 32;
 
 template <typename T> struct Prec;
 
-// fp32: slot = one int64 holding two int32 fixed-point sums (membrane << 32 | synapse)
+// fp32: slot = one int64 holding two int32 fixed-point sums (membrane << 32 | synapse).
+// q = rint(v * 2^F) and v = q * 2^-F are evaluated in float: scaling by a power
+// of two is exact and |q| < 2^31, so they round exactly like the oracle's
+// double-precision ldexp/llrint (no FP64 in the fp32 hot loops).
 template <> struct Prec<float> {
   typedef float2 T2;
   static constexpr int kSlotWords = 1;
-  __device__ __forceinline__ static long long q(float v, double scale) {
-    return (long long)__double2int_rn((double)v * scale);
+  __device__ __forceinline__ static long long q(float v, float scale) {
+    return (long long)__float2int_rn(v * scale);
   }
-  __device__ __forceinline__ static float deq(long long q, double inv) {
-    return __double2float_rn((double)q * inv);
+  __device__ __forceinline__ static float deq(long long q, float inv) {
+    return __int2float_rn((int)q) * inv;
   }
 };
 template <> struct Prec<double> {
@@ -39,6 +42,22 @@ template <> struct Prec<double> {
   }
   __device__ __forceinline__ static double deq(long long q, double inv) {
     return __ll2double_rn(q) * inv;
+  }
+};
+
+// n / d for 0 <= n < 2^31 without an integer divide: M = ceil(2^(31+L)/d),
+// L = ceil(log2 d), q = (n*M) >> (31+L) (Granlund-Montgomery, exact here).
+struct FastDiv {
+  unsigned d, M, S;
+  __host__ __device__ FastDiv() : d(1), M(1u << 31), S(31) {}
+  __host__ explicit FastDiv(unsigned dd) : d(dd) {
+    unsigned L = 0;
+    while ((1ull << L) < dd) ++L;
+    S = 31 + L;
+    M = (unsigned)(((1ull << S) + dd - 1) / dd);
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return (int)(((unsigned long long)(unsigned)n * M) >> S);
   }
 };
 
@@ -112,7 +131,15 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 // loads (no L1 invalidation per poll) and take one acquire fence on exit.  No
 // seq_cst fences: MEMBAR.SC.GPU on 296 CTAs per step cost ~100 us here.  A 20 s
 // watchdog turns a wedged barrier into EQ_ERR_CUDA instead of a hung GPU.
-__device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* err) {
+// publish_dst/src (optional): the last arriver copies *src to *dst before the
+// release, so every CTA sees a value that no CTA can change until the next
+// phase (used to publish the spike-log end of the finished step).
+// zero_u64 / zero_i32 (optional): reset by the last arriver (state consumed
+// by every CTA in the finished phase).
+__device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* err,
+                                          long long* publish_dst = nullptr,
+                                          const unsigned long long* publish_src = nullptr,
+                                          unsigned long long* zero_u64 = nullptr, int* zero_i32 = nullptr) {
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -122,6 +149,9 @@ __device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* 
     unsigned g = ld_relaxed(gen);
     unsigned prev = atom_add_acq_rel(count, 1u);
     if (prev == nblocks - 1) {
+      if (publish_dst) *publish_dst = (long long)*(volatile const unsigned long long*)publish_src;
+      if (zero_u64) *(volatile unsigned long long*)zero_u64 = 0ULL;
+      if (zero_i32) *(volatile int*)zero_i32 = 0;
       st_relaxed(count, 0u);
       st_release(gen, g + 1);
     } else {

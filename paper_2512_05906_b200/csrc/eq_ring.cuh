@@ -26,7 +26,8 @@ namespace eq {
 template <typename T>
 struct StepConsts {
   T dt, tau_m, tau_s, v_th, v_reset, k_m, k_s, cc;
-  double scale, inv_scale;  // 2^F, 2^-F
+  T scale, inv_scale;       // 2^F, 2^-F (exact powers of two)
+  FastDiv divN;             // idx -> trial
 };
 
 template <typename T>
@@ -58,17 +59,28 @@ struct FwdArgs {
   unsigned long long* log_count;
   long long* chunk_off;  // [m][G]
   int* chunk_cnt;        // [m][G]
+  long long* step_start; // [m] first log record of step m (published at each barrier)
   long long* counters;   // [B][3]
   T* v_trace;            // [m1-m0][B][N] or null
   unsigned long long* tl;  // debug timeline [m][G][4] (globaltimer ns) or null
   int* err;
   unsigned* bar;
+  // calendar (ring kind): events due at step s wait in bucket s % NB until phase
+  // s-1 delivers them into the L2-resident accumulator acc[s & 1]
+  long long* acc;        // [2][total] x words
+  int* bk_tgt;           // [G][NB][cap_b] flat target index (per-CTA private buckets)
+  long long* bk_pay;     // [G][NB][cap_b] x words
+  int* bk_cnt;           // [G][NB] fill (kept in smem inside a launch)
+  long long cap_b;
+  int NB;
+  int* ring_dirty;       // [R] a bucket overflowed into ring row r
 };
 
-template <int NT>
+template <int NT, typename T = float>
 struct FwdShared {
-  static constexpr int kCap = 1024;   // spikes staged in smem per step per CTA
+  static constexpr int kCap = sizeof(T) == 4 ? 1024 : 512;   // spikes staged in smem per batch
   static constexpr int kTrials = 8;   // per-CTA trial counters kept in smem
+  static constexpr int kBins = 512;   // calendar buckets (horizon + 1 <= kBins)
 };
 
 __device__ __forceinline__ void tl_mark(unsigned long long* tl, int m, int G, int cta, int k) {
@@ -150,17 +162,38 @@ __device__ __forceinline__ bool drive_bit(const NetView<T>& net, int b, int m, i
   return (__ldg(row + (j >> 5)) >> (j & 31)) & 1u;
 }
 
+// Stage log records [k0, k0+nb) in smem with their CSR row starts and the
+// exclusive prefix of their row lengths (s_pre[nb] = events in the batch).
+template <typename T, int NT>
+__device__ __forceinline__ void stage_spikes(const SpikeRec<T>* log, long long k0, int nb, int N, FastDiv divN,
+                                             const int64_t* rowptr, SpikeRec<T>* s_rec, long long* s_r0,
+                                             int* s_pre) {
+  __syncthreads();
+  for (int k = threadIdx.x; k < nb; k += NT) {
+    const SpikeRec<T> rec = log[k0 + k];
+    s_rec[k] = rec;
+    const int i = rec.idx - divN.div(rec.idx) * N;
+    const long long r0 = __ldg(rowptr + i);
+    s_r0[k] = r0;
+    s_pre[k + 1] = (int)(__ldg(rowptr + i + 1) - r0);
+  }
+  __syncthreads();
+  warp0_scan(s_pre, nb);
+  __syncthreads();
+}
+
 template <typename T, int NT, int U>
-__global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
+__global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   typedef Prec<T> P;
-  constexpr int kCap = FwdShared<NT>::kCap;
+  constexpr int kCap = FwdShared<NT, T>::kCap;
   constexpr int kTr = FwdShared<NT>::kTrials;
   __shared__ SpikeRec<T> s_spk[kCap];
   __shared__ long long s_r0[kCap];
   __shared__ int s_pre[kCap + 1];
   __shared__ int s_n;
   __shared__ long long s_off;
-  __shared__ unsigned long long s_ctr[kTr][2];
+  __shared__ unsigned long long s_ctr[kTr][3];
+  __shared__ int s_bin[FwdShared<NT>::kBins];   // this CTA's bucket fill levels
 
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;
@@ -170,13 +203,155 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
   const StepConsts<T> c = A.c;
   SpikeRec<T>* spill = A.scratch + (size_t)cta * A.per;
 
-  if (tid < kTr * 2) (&s_ctr[0][0])[tid] = 0ULL;
+  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
+  if (A.kind == EQ_KIND_RING)
+    for (int k = tid; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
 
-  for (int m = A.m0; m < A.m1; ++m) {
+  // Phase m: (a) fan out the crossings of step m-1 — the whole grid shares them
+  // evenly (they are in the log, contiguous per step); (b) pop + update step m
+  // for the owned neurons and log their crossings.  Events of step m-1 land at
+  // steps >= m+1, never in row m, and the row of m+1 is popped only after the
+  // barrier.  A last pass m = m1 fans out the final step so the queue contents
+  // after the run are complete.
+  for (int m = A.m0; m <= A.m1; ++m) {
     if (tid == 0) s_n = 0;
     __syncthreads();
-    tl_mark(A.tl, m, A.G, cta, 0);
-    // ---------------- neuron update: pop, synapse, membrane, crossing
+    tl_mark(A.tl, m < A.m1 ? m : A.m1 - 1, A.G, cta, m < A.m1 ? 0 : 7);
+    // ---------------- (a1) deliver this CTA's bucket m+1 into acc[(m+1)&1]
+    // (L2-resident): the events due at m+1 it appended in earlier phases.
+    // Buckets are private per CTA, so appends need no global atomics; the
+    // delivery load is balanced because the fan-out shares are.
+    if (m > A.m0 && A.kind == EQ_KIND_RING) {
+      const int bin = (m + 1) % A.NB;
+      int n = s_bin[bin];
+      n = n < A.cap_b ? n : (int)A.cap_b;
+      const size_t base = ((size_t)cta * A.NB + bin) * A.cap_b;
+      const int* bt = A.bk_tgt + base;
+      const long long* bp = A.bk_pay + base * P::kSlotWords;
+      long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
+      constexpr int DV = 4;
+      for (int q = tid; q < n; q += DV * NT) {
+        int tg[DV];
+        long long pv[DV][2];
+#pragma unroll
+        for (int e = 0; e < DV; ++e) {
+          const int k = q + e * NT;
+          tg[e] = -1;
+          if (k < n) {
+            tg[e] = bt[k];
+            pv[e][0] = bp[(size_t)k * P::kSlotWords];
+            pv[e][1] = P::kSlotWords == 2 ? bp[(size_t)k * P::kSlotWords + 1] : 0;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < DV; ++e) {
+          if (tg[e] < 0) continue;
+          if (P::kSlotWords == 1) {
+            red_add(accn + tg[e], pv[e][0]);
+          } else {
+            red_add(accn + 2 * (size_t)tg[e], pv[e][0]);
+            red_add(accn + 2 * (size_t)tg[e] + 1, pv[e][1]);
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s_bin[bin] = 0;
+    }
+    if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 5);
+    // ---------------- (a2) fan-out of step m-1 (network.py:583-611): the grid
+    // shares the step's crossings evenly (contiguous in the log).  An event due
+    // at m+1 goes straight into acc[(m+1)&1]; a later one is appended to this
+    // CTA's bucket of its delivery step (rank from a shared-memory counter).
+    // No read-modify-write touches DRAM; a full bucket spills into the DRAM
+    // ring row (flagged) and never loses an event.
+    if (m > A.m0 && A.kind == EQ_KIND_RING) {
+      const int me = m - 1;                          // emitting step
+      const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
+      const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
+      long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
+      int* bt_cta = A.bk_tgt + (size_t)cta * A.NB * A.cap_b;
+      long long* bp_cta = A.bk_pay + (size_t)cta * A.NB * A.cap_b * P::kSlotWords;
+      for (long long k0 = s0; k0 < s1; k0 += kCap) {
+        const int nb = (int)(s1 - k0 < kCap ? s1 - k0 : kCap);
+        stage_spikes<T, NT>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_spk, s_r0, s_pre);
+        if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 6);
+        const int total = s_pre[nb];
+        constexpr int EV = 4;
+        for (int f0 = tid; f0 < total; f0 += EV * NT) {
+          int jj[EV], kk[EV];
+          T ww[EV], dd[EV];
+#pragma unroll
+          for (int e = 0; e < EV; ++e) {
+            const int f = f0 + e * NT;
+            kk[e] = -1;
+            if (f < total) {
+              const int k = find_row(s_pre, nb, f);
+              const long long x = s_r0[k] + (f - s_pre[k]);
+              kk[e] = k;
+              jj[e] = __ldg(A.net.col + x);
+              ww[e] = __ldg(A.net.w + x);
+              dd[e] = __ldg(A.net.d + x);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < EV; ++e) {
+            if (kk[e] < 0) continue;
+            const SpikeRec<T> rec = s_spk[kk[e]];
+            const int b = c.divN.div(rec.idx);
+            const T w = ww[e], d = dd[e];
+            const T t_post = rec.t + d;                         // :588
+            const int ds = delivery_step(t_post, d, c.dt, me);  // jumps.py:96
+            T ws, wm;
+            if (A.exact) {
+              const T phi = (T)ds * c.dt - t_post;              // :599
+              ws = w * eq_exp_t(-phi / c.tau_s);                // :601
+              wm = w * eq_exp_t(-phi / c.tau_m);                // :606
+            } else {
+              ws = w;
+              wm = (T)0;
+            }
+            const int tgt = b * A.N + jj[e];                    // flat target
+            const long long q1 = P::q(ws, c.scale);
+            const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
+            if (ds == m + 1) {
+              if (P::kSlotWords == 1) {
+                red_add(accn + tgt, pack2(q1, q2));
+              } else {
+                red_add(accn + 2 * (size_t)tgt, q1);
+                red_add(accn + 2 * (size_t)tgt + 1, q2);
+              }
+              continue;
+            }
+            const int bn = ds % A.NB;
+            const int pos = atomicAdd(&s_bin[bn], 1);
+            if (pos < A.cap_b) {
+              const size_t o = (size_t)bn * A.cap_b + pos;
+              bt_cta[o] = tgt;
+              if (P::kSlotWords == 1) {
+                bp_cta[o] = pack2(q1, q2);
+              } else {
+                bp_cta[2 * o] = q1;
+                bp_cta[2 * o + 1] = q2;
+              }
+            } else {                                            // bucket full: DRAM ring row
+              const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
+              if (P::kSlotWords == 1) {
+                red_add(A.ring + so, pack2(q1, q2));
+              } else {
+                red_add(A.ring + 2 * so, q1);
+                red_add(A.ring + 2 * so + 1, q2);
+              }
+              if (A.ring_dirty[ds % A.R] == 0) atomicExch(A.ring_dirty + ds % A.R, 1);
+            }
+          }
+        }
+      }
+    }
+    if (m == A.m1) break;
+    __syncthreads();
+    tl_mark(A.tl, m, A.G, cta, 1);
+    // ---------------- (b) neuron update: pop, synapse, membrane, crossing
+    const bool dirty = A.kind == EQ_KIND_RING && ld_volatile(A.ring_dirty + m % A.R) != 0;
     for (long long base = begin; base < end; base += (long long)NT * U) {
       long long slot_v[U][2];
       T Iv[U], Vv[U];
@@ -187,15 +362,24 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
         const int idx = (int)base + u * NT + tid;
         slot_v[u][0] = slot_v[u][1] = 0;
         if (idx < end) {
-          const int b = idx / A.N;
+          const int b = c.divN.div(idx);
           const int j = idx - b * A.N;
-          size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
           if (A.kind == EQ_KIND_RING) {
+            const long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
             if (P::kSlotWords == 1) {
-              slot_v[u][0] = ld_slot(A.ring + so);
+              slot_v[u][0] = ld_slot(accm + idx);
             } else {
-              slot_v[u][0] = ld_slot(A.ring + 2 * so);
-              slot_v[u][1] = ld_slot(A.ring + 2 * so + 1);
+              slot_v[u][0] = ld_slot(accm + 2 * (size_t)idx);
+              slot_v[u][1] = ld_slot(accm + 2 * (size_t)idx + 1);
+            }
+            if (dirty) {                       // a bucket overflowed into the DRAM row
+              size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
+              if (P::kSlotWords == 1) {
+                slot_v[u][0] += ld_slot(A.ring + so);
+              } else {
+                slot_v[u][0] += ld_slot(A.ring + 2 * so);
+                slot_v[u][1] += ld_slot(A.ring + 2 * so + 1);
+              }
             }
           }
           Iv[u] = A.I[idx];
@@ -208,7 +392,7 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
       for (int u = 0; u < U; ++u) {
         const int idx = (int)base + u * NT + tid;
         if (idx >= end) continue;
-        const int b = idx / A.N;
+        const int b = c.divN.div(idx);
         const int j = idx - b * A.N;
         T ps, pm;
         if (P::kSlotWords == 1) {
@@ -244,28 +428,40 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
       }
     }
     __syncthreads();
-    tl_mark(A.tl, m, A.G, cta, 1);
+    tl_mark(A.tl, m, A.G, cta, 4);
     // Clear the popped slot row (RingQueue._pop_raw zeroes it, queues.py:114-117).
     // Done here, not next to the load: a store to the line a pending load is
     // filling stalled the pop loop ~8x.  Row m mod R receives no red.add in
-    // this phase (fan-out targets rows m+2 .. m+horizon, R = horizon + 1).
+    // this phase (fan-out of step m-1 targets rows m+1 .. m-1+horizon, R = horizon + 1).
     if (A.kind == EQ_KIND_RING) {
-      const int row = m % A.R;
+      long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
       for (int idx = (int)begin + tid; idx < end; idx += NT) {
-        const int b = idx / A.N;
-        const size_t so = ((size_t)b * A.R + row) * A.N + (idx - b * A.N);
         if (P::kSlotWords == 1) {
-          st_slot(A.ring + so, 0);
+          st_slot(accm + idx, 0);
         } else {
-          st_slot(A.ring + 2 * so, 0);
-          st_slot(A.ring + 2 * so + 1, 0);
+          st_slot(accm + 2 * (size_t)idx, 0);
+          st_slot(accm + 2 * (size_t)idx + 1, 0);
+        }
+      }
+      if (dirty) {
+        const int row = m % A.R;
+        for (int idx = (int)begin + tid; idx < end; idx += NT) {
+          const int b = c.divN.div(idx);
+          const size_t so = ((size_t)b * A.R + row) * A.N + (idx - b * A.N);
+          if (P::kSlotWords == 1) {
+            st_slot(A.ring + so, 0);
+          } else {
+            st_slot(A.ring + 2 * so, 0);
+            st_slot(A.ring + 2 * so + 1, 0);
+          }
         }
       }
     }
-    __syncthreads();
-    tl_mark(A.tl, m, A.G, cta, 4);
     const int nspk = s_n;
-    // ---------------- spike log for the reverse pass: one chunk per (step, CTA)
+    // ---------------- spike log: one chunk per (step, CTA); the chunks of a
+    // step are contiguous because every reservation of step m happens between
+    // the two barriers around phase m.  Counters per trial (spikes, events;
+    // donothing drops every event, queues.py:42-45).
     if (tid == 0) {
       unsigned long long off = nspk ? atomicAdd(A.log_count, (unsigned long long)nspk) : 0ULL;
       if (nspk && (long long)(off + nspk) > A.log_cap) {
@@ -277,102 +473,41 @@ __global__ void __launch_bounds__(NT) k_forward(FwdArgs<T> A) {
       A.chunk_cnt[(size_t)m * A.G + cta] = nspk;
     }
     __syncthreads();
-    if (s_off + nspk <= A.log_cap) {
-      for (int k = tid; k < nspk; k += NT) A.log[s_off + k] = k < kCap ? s_spk[k] : spill[k - kCap];
-    }
-    __syncthreads();
-    tl_mark(A.tl, m, A.G, cta, 5);
-    // ---------------- fan-out (network.py:583-611), flattened over (spike, edge)
-    // so every lane carries an event: batch of <= kCap spikes, prefix of their
-    // row lengths, then flat events f -> (spike, x) with EV events per thread in
-    // flight.  Slot sums are fixed-point, so the order of the red.adds is free.
-    for (int k0 = 0; k0 < nspk; k0 += kCap) {
-      const int nb = nspk - k0 < kCap ? nspk - k0 : kCap;
-      __syncthreads();
-      if (k0 > 0)
-        for (int k = tid; k < nb; k += NT) s_spk[k] = spill[k0 - kCap + k];
-      __syncthreads();
-      for (int k = tid; k < nb; k += NT) {
-        const int b = s_spk[k].idx / A.N;
-        const int i = s_spk[k].idx - b * A.N;
-        const long long r0 = __ldg(A.net.rowptr + i);
-        const int len = (int)(__ldg(A.net.rowptr + i + 1) - r0);
-        s_r0[k] = r0;
-        s_pre[k + 1] = len;
-        const int tb = b - b_first;
-        if (tb < kTr) {
-          atomicAdd(&s_ctr[tb][0], 1ULL);
-          atomicAdd(&s_ctr[tb][1], (unsigned long long)len);
-        } else {
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), (unsigned long long)len);
-        }
+    const bool log_ok = s_off + nspk <= A.log_cap;
+    for (int k = tid; k < nspk; k += NT) {
+      const SpikeRec<T> rec = k < kCap ? s_spk[k] : spill[k - kCap];
+      if (log_ok) A.log[s_off + k] = rec;
+      const int b = c.divN.div(rec.idx);
+      const int i = rec.idx - b * A.N;
+      const unsigned long long len = (unsigned long long)(__ldg(A.net.rowptr + i + 1) - __ldg(A.net.rowptr + i));
+      const int tb = b - b_first;
+      if (tb < kTr) {
+        atomicAdd(&s_ctr[tb][0], 1ULL);
+        atomicAdd(&s_ctr[tb][1], len);
+        if (A.kind == EQ_KIND_DONOTHING) atomicAdd(&s_ctr[tb][2], len);
+      } else {
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), len);
         if (A.kind == EQ_KIND_DONOTHING)
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), (unsigned long long)len);
-      }
-      __syncthreads();
-      warp0_scan(s_pre, nb);
-      __syncthreads();
-      if (k0 == 0) tl_mark(A.tl, m, A.G, cta, 6);
-      if (A.kind != EQ_KIND_RING) continue;
-      const int total = s_pre[nb];
-      constexpr int EV = 4;
-      for (int f0 = tid; f0 < total; f0 += EV * NT) {
-        int jj[EV], kk[EV];
-        T ww[EV], dd[EV];
-#pragma unroll
-        for (int e = 0; e < EV; ++e) {
-          const int f = f0 + e * NT;
-          kk[e] = -1;
-          if (f < total) {
-            const int k = find_row(s_pre, nb, f);
-            const long long x = s_r0[k] + (f - s_pre[k]);
-            kk[e] = k;
-            jj[e] = __ldg(A.net.col + x);
-            ww[e] = __ldg(A.net.w + x);
-            dd[e] = __ldg(A.net.d + x);
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < EV; ++e) {
-          if (kk[e] < 0) continue;
-          const SpikeRec<T> rec = s_spk[kk[e]];
-          const int b = rec.idx / A.N;
-          const T w = ww[e], d = dd[e];
-          const T t_post = rec.t + d;                        // :588
-          const int ds = delivery_step(t_post, d, c.dt, m);  // jumps.py:96
-          T ws, wm;
-          if (A.exact) {
-            const T phi = (T)ds * c.dt - t_post;             // :599
-            ws = w * eq_exp_t(-phi / c.tau_s);               // :601
-            wm = w * eq_exp_t(-phi / c.tau_m);               // :606
-          } else {
-            ws = w;
-            wm = (T)0;
-          }
-          const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
-          const long long qs = P::q(ws, c.scale), qm = P::q(wm, c.scale);
-          if (P::kSlotWords == 1) {
-            red_add(A.ring + so, pack2(qs, qm));
-          } else {
-            red_add(A.ring + 2 * so, qs);
-            if (A.exact) red_add(A.ring + 2 * so + 1, qm);
-          }
-        }
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), len);
       }
     }
     __syncthreads();
     tl_mark(A.tl, m, A.G, cta, 2);
-    if (!grid_sync(A.bar, A.G, A.err)) break;
+    if (!grid_sync(A.bar, A.G, A.err, A.step_start + m + 1, A.log_count, nullptr,
+                   A.kind == EQ_KIND_RING ? A.ring_dirty + m % A.R : nullptr))
+      break;
     tl_mark(A.tl, m, A.G, cta, 3);
     if (ld_volatile(A.err) != 0) break;
   }
   __syncthreads();
+  if (A.kind == EQ_KIND_RING)
+    for (int k = tid; k < A.NB; k += NT) A.bk_cnt[(size_t)cta * A.NB + k] = s_bin[k];
   if (tid < kTr) {
     int b = b_first + tid;
     if (b < A.B && (long long)b * A.N < end) {
-      if (s_ctr[tid][0]) atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), s_ctr[tid][0]);
-      if (s_ctr[tid][1]) atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), s_ctr[tid][1]);
+      for (int q = 0; q < 3; ++q)
+        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + q), s_ctr[tid][q]);
     }
   }
 }
@@ -397,6 +532,7 @@ struct BwdArgs {
   T* lt_log;                   // dL/dt_spk per log record
   const long long* chunk_off;
   const int* chunk_cnt;
+  const long long* step_start;  // [m] first log record of step m
   const long long* ev_base;     // bounded kinds: flat event id of each log record's first edge
   const unsigned* drop_bits;    // bounded kinds: dropped events (contribute nothing); null for ring
   int no_events;                // donothing: every event was dropped
@@ -429,93 +565,91 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
     tl_mark(A.tl, m, A.G, cta, 0);
     const long long off = A.chunk_off[(size_t)m * A.G + cta];
     const int cnt = A.chunk_cnt[(size_t)m * A.G + cta];
-    // ---------------- R-fanout(m): own spikes of step m, flattened over
-    // (spike, edge).  dL/dt_spk of a spike is the SEQUENTIAL sum of its edges'
-    // g_tp in row order (zeros for events never popped), staged through s_gtp
-    // in windows of kEv events; the oracle sums in the same order.
-    for (int k0 = 0; k0 < cnt; k0 += kCapB) {
-      const int nb = cnt - k0 < kCapB ? cnt - k0 : kCapB;
-      __syncthreads();
-      for (int k = tid; k < nb; k += NT) {
-        const SpikeRec<T> rec = A.log[off + k0 + k];
-        s_rec[k] = rec;
-        const int b = rec.idx / A.N;
-        const int i = rec.idx - b * A.N;
-        const long long r0 = __ldg(A.net.rowptr + i);
-        s_r0[k] = r0;
-        s_pre[k + 1] = (int)(__ldg(A.net.rowptr + i + 1) - r0);
-        s_lt[k] = (T)0;
-      }
-      __syncthreads();
-      warp0_scan(s_pre, nb);
-      __syncthreads();
-      const int total = s_pre[nb];
-      for (int w0 = 0; w0 < total; w0 += kEv) {
-        const int wend = total - w0 < kEv ? total : w0 + kEv;
-        constexpr int EV = 4;
-        for (int f0 = w0 + tid; f0 < wend; f0 += EV * NT) {
-          int jj[EV], kk[EV];
-          long long xx[EV];
-          T ww[EV], dd[EV];
+    // ---------------- R-fanout(m-1): the crossings of step m-1, shared evenly
+    // by the whole grid (whole spikes per CTA).  They read reverse slots of
+    // steps >= m+1, all final; R-neuron(m) below writes only slot m.  dL/dt_spk
+    // of a spike is the SEQUENTIAL sum of its edges' g_tp in row order (zeros
+    // for events never popped or dropped), staged through s_gtp in windows of
+    // kEv events; the oracle sums in the same order.  R-neuron(m-1) in the
+    // next phase reads it from lt_log.
+    if (m >= 1) {
+      const int me = m - 1;
+      const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
+      const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
+      for (long long k0 = s0; k0 < s1; k0 += kCapB) {
+        const int nb = (int)(s1 - k0 < kCapB ? s1 - k0 : kCapB);
+        stage_spikes<T, NT>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_rec, s_r0, s_pre);
+        for (int k = tid; k < nb; k += NT) s_lt[k] = (T)0;
+        __syncthreads();
+        const int total = s_pre[nb];
+        for (int w0 = 0; w0 < total; w0 += kEv) {
+          const int wend = total - w0 < kEv ? total : w0 + kEv;
+          constexpr int EV = 4;
+          for (int f0 = w0 + tid; f0 < wend; f0 += EV * NT) {
+            int jj[EV], kk[EV];
+            long long xx[EV];
+            T ww[EV], dd[EV];
 #pragma unroll
-          for (int e = 0; e < EV; ++e) {
-            const int f = f0 + e * NT;
-            kk[e] = -1;
-            if (f < wend) {
-              const int k = find_row(s_pre, nb, f);
-              const long long x = s_r0[k] + (f - s_pre[k]);
-              kk[e] = k;
-              xx[e] = x;
-              jj[e] = __ldg(A.net.col + x);
-              ww[e] = __ldg(A.net.w + x);
-              dd[e] = __ldg(A.net.d + x);
+            for (int e = 0; e < EV; ++e) {
+              const int f = f0 + e * NT;
+              kk[e] = -1;
+              if (f < wend) {
+                const int k = find_row(s_pre, nb, f);
+                const long long x = s_r0[k] + (f - s_pre[k]);
+                kk[e] = k;
+                xx[e] = x;
+                jj[e] = __ldg(A.net.col + x);
+                ww[e] = __ldg(A.net.w + x);
+                dd[e] = __ldg(A.net.d + x);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < EV; ++e) {
+              if (kk[e] < 0) continue;
+              const int f = f0 + e * NT;
+              const SpikeRec<T> rec = s_rec[kk[e]];
+              const int b = c.divN.div(rec.idx);
+              const T w = ww[e], d = dd[e];
+              const T t_post = rec.t + d;
+              const int st = delivery_step(t_post, d, c.dt, me);
+              T g_tp = (T)0;
+              bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
+              if (live && A.drop_bits) {                       // dropped by a bounded queue
+                const long long id = A.ev_base[k0 + kk[e]] + (f - s_pre[kk[e]]);
+                live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
+              }
+              if (live) {
+                const T phi = (T)st * c.dt - t_post;
+                const T es = eq_exp_t(-phi / c.tau_s);
+                const T em = eq_exp_t(-phi / c.tau_m);
+                const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
+                const T g_w = es * L.x + em * L.y;
+                g_tp = w * (es * L.x / c.tau_s + em * L.y / c.tau_m);
+                atomicAdd(A.gw + xx[e], (double)g_w);
+                atomicAdd(A.gd + xx[e], (double)g_tp);
+              }
+              s_gtp[f - w0] = g_tp;
             }
           }
-#pragma unroll
-          for (int e = 0; e < EV; ++e) {
-            if (kk[e] < 0) continue;
-            const int f = f0 + e * NT;
-            const SpikeRec<T> rec = s_rec[kk[e]];
-            const int b = rec.idx / A.N;
-            const T w = ww[e], d = dd[e];
-            const T t_post = rec.t + d;
-            const int st = delivery_step(t_post, d, c.dt, m);
-            T g_tp = (T)0;
-            bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
-            if (live && A.drop_bits) {                       // dropped by a bounded queue
-              const long long id = A.ev_base[off + k0 + kk[e]] + (f - s_pre[kk[e]]);
-              live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
-            }
-            if (live) {
-              const T phi = (T)st * c.dt - t_post;
-              const T es = eq_exp_t(-phi / c.tau_s);
-              const T em = eq_exp_t(-phi / c.tau_m);
-              const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
-              const T g_w = es * L.x + em * L.y;
-              g_tp = w * (es * L.x / c.tau_s + em * L.y / c.tau_m);
-              atomicAdd(A.gw + xx[e], (double)g_w);
-              atomicAdd(A.gd + xx[e], (double)g_tp);
-            }
-            s_gtp[f - w0] = g_tp;
+          __syncthreads();
+          const int ka = find_row(s_pre, nb, w0);
+          const int kb = find_row(s_pre, nb, wend - 1);
+          for (int k = ka + tid; k <= kb; k += NT) {
+            const int lo = s_pre[k] > w0 ? s_pre[k] : w0;
+            const int hi = s_pre[k + 1] < wend ? s_pre[k + 1] : wend;
+            T acc = s_lt[k];
+            for (int q = lo; q < hi; ++q) acc = acc + s_gtp[q - w0];
+            s_lt[k] = acc;
           }
+          __syncthreads();
         }
-        __syncthreads();
-        const int ka = find_row(s_pre, nb, w0);
-        const int kb = find_row(s_pre, nb, wend - 1);
-        for (int k = ka + tid; k <= kb; k += NT) {
-          const int lo = s_pre[k] > w0 ? s_pre[k] : w0;
-          const int hi = s_pre[k + 1] < wend ? s_pre[k + 1] : wend;
-          T acc = s_lt[k];
-          for (int q = lo; q < hi; ++q) acc = acc + s_gtp[q - w0];
-          s_lt[k] = acc;
-        }
-        __syncthreads();
+        for (int k = tid; k < nb; k += NT) A.lt_log[k0 + k] = s_lt[k];
       }
-      for (int k = tid; k < nb; k += NT) {
-        A.lt_log[off + k0 + k] = s_lt[k];
-        const int loc = s_rec[k].idx - (int)begin;
-        atomicOr(&s_bits[loc >> 5], 1u << (loc & 31));
-      }
+    }
+    // own spikers of step m -> bitmap (R-neuron looks them up in the own chunk)
+    for (int k = tid; k < cnt; k += NT) {
+      const int loc = A.log[off + k].idx - (int)begin;
+      atomicOr(&s_bits[loc >> 5], 1u << (loc & 31));
     }
     __syncthreads();
     tl_mark(A.tl, m, A.G, cta, 1);
@@ -525,7 +659,7 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
       for (int u = 0; u < U; ++u) {
         const int idx = (int)base + u * NT + tid;
         if (idx >= end) continue;
-        const int b = idx / A.N;
+        const int b = c.divN.div(idx);
         const int j = idx - b * A.N;
         T lv = A.lamV[idx];
         T la, lvh;
@@ -534,7 +668,7 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
           int k = 0;
           while (k < cnt && A.log[off + k].idx != idx) ++k;
           SpikeRec<T> rec = A.log[off + k];
-          T lt0 = A.lt_log[off + k];
+          const T lt0 = m + 1 < A.m_run ? A.lt_log[off + k] : (T)0;
           T t = rec.t, a = rec.a, vh = rec.vh;
           T uu = (T)(m + 1) * c.dt - t;
           T ku = eq_exp_t(-uu / c.tau_m);

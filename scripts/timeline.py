@@ -18,29 +18,29 @@ from paper_2512_05906_b200.engine import Engine  # noqa: E402
 import bench  # noqa: E402
 
 
+ORDER = {"forward": [(0, "start"), (5, "deliver"), (6, "stage"), (1, "fan-out"), (4, "update"), (2, "clear+log"),
+                     (3, "barrier")],
+         "reverse": [(0, "start"), (1, "R-fanout"), (2, "R-neuron"), (3, "barrier")]}
+
+
 def report(tl, label):
+    """Per step: each mark minus the previous present mark (median over steps of
+    the max and the mean over CTAs), in time order."""
     t = tl.astype(np.int64)
-    sub = t[:, :, 4:]
-    ok = (t[:, :, 0] > 0)
+    ok = (t[:, :, 0] > 0) & (t[:, :, 3] > 0)
     steps = np.nonzero(ok.all(axis=1))[0]
     t = t[steps]
-    ph1 = t[:, :, 1] - t[:, :, 0]
-    ph2 = t[:, :, 2] - t[:, :, 1]
-    bar = t[:, :, 3] - t[:, :, 2]
-    step = t[:, :, 3].max(axis=1)[1:] - t[:, :, 3].max(axis=1)[:-1]
+    step = np.abs(np.diff(t[:, :, 3].max(axis=1)))
     skew = t[:, :, 0].max(axis=1) - t[:, :, 0].min(axis=1)
-    print(f"[{label}] steps={len(steps)}  (us: median over steps of max over CTAs / of mean)")
-    for name, a in (("phase1", ph1), ("phase2", ph2), ("barrier", bar)):
-        print(f"   {name:8s} max {np.median(a.max(1))/1e3:8.2f}  mean {np.median(a.mean(1))/1e3:8.2f}")
-    print(f"   step     {np.median(step)/1e3:8.2f}   start-skew {np.median(skew)/1e3:8.2f}")
-    sub = sub[steps]
-    prev = t[:, :, 1]
-    for k in range(4):
-        mk = sub[:, :, k]
-        if (mk > 0).all():
-            d = mk - prev
-            print(f"   sub{k}     max {np.median(d.max(1))/1e3:8.2f}  mean {np.median(d.mean(1))/1e3:8.2f}")
-            prev = mk
+    print(f"[{label}] steps={len(steps)}  step {np.median(step)/1e3:.2f} us  start-skew {np.median(skew)/1e3:.2f} us")
+    prev = t[:, :, 0]
+    for k, name in ORDER[label][1:]:
+        mk = t[:, :, k]
+        if not (mk > 0).all():
+            continue
+        d = mk - prev
+        print(f"   {name:10s} max {np.median(d.max(1))/1e3:8.2f}  mean {np.median(d.mean(1))/1e3:8.2f}")
+        prev = mk
 
 
 def main():
