@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
         stage_spikes<T, NT>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_rec, s_r0, s_pre);
         for (int k = tid; k < nb; k += NT) s_lt[k] = (T)0;
         __syncthreads();
+        if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 4);
         const int total = s_pre[nb];
         for (int w0 = 0; w0 < total; w0 += kEv) {
           const int wend = total - w0 < kEv ? total : w0 + kEv;
@@ -632,6 +633,7 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
             }
           }
           __syncthreads();
+          if (k0 == s0 && w0 == 0) tl_mark(A.tl, m, A.G, cta, 5);
           const int ka = find_row(s_pre, nb, w0);
           const int kb = find_row(s_pre, nb, wend - 1);
           for (int k = ka + tid; k <= kb; k += NT) {
@@ -642,6 +644,7 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
             s_lt[k] = acc;
           }
           __syncthreads();
+          if (k0 == s0 && w0 == 0) tl_mark(A.tl, m, A.G, cta, 6);
         }
         for (int k = tid; k < nb; k += NT) A.lt_log[k0 + k] = s_lt[k];
       }
