@@ -273,6 +273,7 @@ struct Trial {
     const T k_s = (T)std::exp(-c.dt / c.tau_syn);
     const T cc = c.exact_delivery ? (T)(c.tau_syn / (c.tau_m - c.tau_syn)) : (T)0;
     const bool exact = c.exact_delivery != 0;
+    const T inv_s = (T)(1.0 / c.tau_syn), inv_m = (T)(1.0 / c.tau_m);
     std::vector<int> crossing;
     std::vector<T> cross_t;
     for (int m = 0; m < c.t_steps && e.code == OK; ++m) {
@@ -330,8 +331,9 @@ struct Trial {
           T ws, wm;
           if (exact) {
             T phi = (T)dstep * dt - t_post;                     // :599
-            ws = w * xexp<T, DEV>(-phi / tau_s);                // :601
-            wm = w * xexp<T, DEV>(-phi / tau_m);                // :606
+            // device mode multiplies by (T)(1/tau) per event
+            ws = w * xexp<T, DEV>(DEV ? -phi * inv_s : -phi / tau_s);  // :601
+            wm = w * xexp<T, DEV>(DEV ? -phi * inv_m : -phi / tau_m);  // :606
           } else {
             ws = w; wm = (T)0;
           }
@@ -423,6 +425,7 @@ int run_backward(Session& s, const double* vbar, const double* ibar, double* gw,
   const T k_m = (T)std::exp(-c.dt / c.tau_m);
   const T k_s = (T)std::exp(-c.dt / c.tau_syn);
   const T cc = (T)(c.tau_syn / (c.tau_m - c.tau_syn));
+  const T inv_s = (T)(1.0 / c.tau_syn), inv_m = (T)(1.0 / c.tau_m);
   const int R = s.horizon + 1;
   std::fill(gw, gw + E, 0.0);
   std::fill(gd, gd + E, 0.0);
@@ -476,12 +479,12 @@ int run_backward(Session& s, const double* vbar, const double* ibar, double* gw,
             int32_t st = delivery<T, DEV>(t_post, dd, dt, m);
             if (st >= TT || !okv[x - r0]) { lt_sum = lt_sum + (T)0; continue; }
             T phi = (T)st * dt - t_post;
-            T es = xexp<T, DEV>(-phi / tau_s);
-            T em = xexp<T, DEV>(-phi / tau_m);
+            T es = xexp<T, DEV>(DEV ? -phi * inv_s : -phi / tau_s);
+            T em = xexp<T, DEV>(DEV ? -phi * inv_m : -phi / tau_m);
             size_t o = (size_t)(st % R) * N + j;
             T as = Ls[o], am = Lm[o];
             T g_w = es * as + em * am;
-            T g_tp = w * (es * as / tau_s + em * am / tau_m);
+            T g_tp = DEV ? w * (es * as * inv_s + em * am * inv_m) : w * (es * as / tau_s + em * am / tau_m);
             lw[x] += (double)g_w;
             ld[x] += (double)g_tp;
             lt_sum = lt_sum + g_tp;

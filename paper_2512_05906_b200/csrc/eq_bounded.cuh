@@ -354,8 +354,8 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
         T ws, wm;
         if (F.exact) {
           const T phi = (T)ds * c.dt - t_post;
-          ws = w * eq_exp_t(-phi / c.tau_s);
-          wm = w * eq_exp_t(-phi / c.tau_m);
+          ws = w * eq_exp_t(-phi * c.inv_tau_s);
+          wm = w * eq_exp_t(-phi * c.inv_tau_m);
         } else {
           ws = w;
           wm = (T)0;

@@ -96,8 +96,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Fire-and-forget reductions (no return value travels back to the SM).
 __device__ __forceinline__ void red_add(long long* p, long long v) {
-  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 // error word: [0] code, [1] step, [2] trial, [3] neuron
@@ -207,6 +211,30 @@ __device__ __forceinline__ int delivery_step(T t_post, T d, T dt, int m) {
   }
   int q = (int)ceil(t_post / dt);
   q = q < lo ? lo : (q > hi ? hi : q);
+  return q > m + 2 ? q : m + 2;
+}
+
+// Per-edge delivery offset, precomputed once per network (eq_set_network):
+// bit 15 set = delay not grid-aligned; bits 0..14 = m+1+floor(d/dt) - m (or
+// the rounded value when aligned), i.e. the exact-arithmetic lower bound of
+// dstep - m.  For an aligned delay dstep = m + max(lo, 2) with no division.
+template <typename T>
+__device__ __forceinline__ unsigned short delivery_code(T d, T dt) {
+  const T tol = sizeof(T) == 4 ? (T)1e-5 : (T)1e-12;
+  const T kd = d / dt;
+  const T kr = rint(kd);
+  if (fabs(kd - kr) <= tol * (kr > (T)1 ? kr : (T)1)) return (unsigned short)(1 + (int)kr);
+  return (unsigned short)(0x8000 | (1 + (int)floor(kd)));
+}
+
+template <typename T>
+__device__ __forceinline__ int delivery_step_coded(T t_post, unsigned short code, T dt, int m) {
+  const int lo = m + (code & 0x7fff);
+  int q = lo;
+  if (code & 0x8000) {                   // not grid-aligned: ceil within [lo, lo + 1]
+    q = (int)ceil(t_post / dt);
+    q = q < lo ? lo : (q > lo + 1 ? lo + 1 : q);
+  }
   return q > m + 2 ? q : m + 2;
 }
 

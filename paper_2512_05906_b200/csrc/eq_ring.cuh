@@ -26,6 +26,7 @@ namespace eq {
 template <typename T>
 struct StepConsts {
   T dt, tau_m, tau_s, v_th, v_reset, k_m, k_s, cc;
+  T inv_tau_m, inv_tau_s;   // (T)(1/tau) for the per-event exponents (device-mode contract)
   T scale, inv_scale;       // 2^F, 2^-F (exact powers of two)
   FastDiv divN;             // idx -> trial
 };
@@ -36,6 +37,7 @@ struct NetView {
   const int32_t* col;
   const T* w;
   const T* d;
+  const unsigned short* dcode;  // [E] delivery_code(d, dt)
   const uint32_t* mask;  // [B][t_mask][words]
   const T* amp;          // [N]
   int words, t_mask;
@@ -85,6 +87,10 @@ struct FwdShared {
 
 __device__ __forceinline__ void tl_mark(unsigned long long* tl, int m, int G, int cta, int k) {
   if (tl && threadIdx.x == 0) tl[((size_t)m * G + cta) * 8 + k] = globaltimer();
+}
+// same, from whichever thread calls it (warp-group leaders)
+__device__ __forceinline__ void tl_mark_any(unsigned long long* tl, int m, int G, int cta, int k) {
+  if (tl) tl[((size_t)m * G + cta) * 8 + k] = globaltimer();
 }
 
 // Exclusive prefix over a staged spike batch's row lengths, by warp 0.
@@ -162,14 +168,41 @@ __device__ __forceinline__ bool drive_bit(const NetView<T>& net, int b, int m, i
   return (__ldg(row + (j >> 5)) >> (j & 31)) & 1u;
 }
 
+// Named barrier for a warp group (ids 1..15; 0 is __syncthreads).
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Exclusive prefix over a staged batch's row lengths by the group's first warp.
+// On entry pre[k+1] = len[k] (k < n); on exit pre[0..n] is the exclusive scan.
+__device__ __forceinline__ void group_scan(int* pre, int n, int gtid) {
+  if (gtid < 32) {
+    const int lane = gtid;
+    int carry = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int k = base + lane;
+      int v = k < n ? pre[k + 1] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      if (k < n) pre[k + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) pre[0] = 0;
+  }
+}
+
 // Stage log records [k0, k0+nb) in smem with their CSR row starts and the
 // exclusive prefix of their row lengths (s_pre[nb] = events in the batch).
-template <typename T, int NT>
+// Executed by one warp group (gtid in [0, gsize), named barrier bar_id).
+template <typename T>
 __device__ __forceinline__ void stage_spikes(const SpikeRec<T>* log, long long k0, int nb, int N, FastDiv divN,
                                              const int64_t* rowptr, SpikeRec<T>* s_rec, long long* s_r0,
-                                             int* s_pre) {
-  __syncthreads();
-  for (int k = threadIdx.x; k < nb; k += NT) {
+                                             int* s_pre, int gtid, int gsize, int bar_id) {
+  group_sync(bar_id, gsize);
+  for (int k = gtid; k < nb; k += gsize) {
     const SpikeRec<T> rec = log[k0 + k];
     s_rec[k] = rec;
     const int i = rec.idx - divN.div(rec.idx) * N;
@@ -177,23 +210,40 @@ __device__ __forceinline__ void stage_spikes(const SpikeRec<T>* log, long long k
     s_r0[k] = r0;
     s_pre[k + 1] = (int)(__ldg(rowptr + i + 1) - r0);
   }
-  __syncthreads();
-  warp0_scan(s_pre, nb);
-  __syncthreads();
+  group_sync(bar_id, gsize);
+  group_scan(s_pre, nb, gtid);
+  group_sync(bar_id, gsize);
 }
 
-template <typename T, int NT, int U>
+// Warp specialisation of the persistent kernels: in every phase the first NF
+// threads run the event side (delivery + fan-out of step m-1, or R-fanout of
+// step m-1), the other NT-NF threads the neuron side (update / R-neuron of
+// step m).  The two sides touch disjoint data within a phase, so they overlap
+// their memory latencies instead of running back to back.
+template <int NT, int NF_ = NT / 2>
+struct Roles {
+  static constexpr int NF = NF_;
+  static constexpr int NN = NT - NF_;
+  static constexpr int kBarF = 1, kBarN = 2;
+};
+
+template <typename T, int NT, int U, int NF = NT / 2>
 __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   typedef Prec<T> P;
+  typedef Roles<NT, NF> Ro;
   constexpr int kCap = FwdShared<NT, T>::kCap;
+  constexpr int kCapN = kCap / 2;
   constexpr int kTr = FwdShared<NT>::kTrials;
+  // event side
   __shared__ SpikeRec<T> s_spk[kCap];
   __shared__ long long s_r0[kCap];
   __shared__ int s_pre[kCap + 1];
+  __shared__ int s_bin[FwdShared<NT>::kBins];   // this CTA's bucket fill levels
+  // neuron side
+  __shared__ SpikeRec<T> s_own[kCapN];
   __shared__ int s_n;
   __shared__ long long s_off;
   __shared__ unsigned long long s_ctr[kTr][3];
-  __shared__ int s_bin[FwdShared<NT>::kBins];   // this CTA's bucket fill levels
 
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;
@@ -206,293 +256,379 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
   if (A.kind == EQ_KIND_RING)
     for (int k = tid; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
+  if (tid == 0) s_n = 0;
+  __syncthreads();
 
-  // Phase m: (a) fan out the crossings of step m-1 — the whole grid shares them
-  // evenly (they are in the log, contiguous per step); (b) pop + update step m
-  // for the owned neurons and log their crossings.  Events of step m-1 land at
-  // steps >= m+1, never in row m, and the row of m+1 is popped only after the
-  // barrier.  A last pass m = m1 fans out the final step so the queue contents
-  // after the run are complete.
+  // Phase m: (a) [event side] deliver this CTA's bucket m+1 and fan out its
+  // share of the crossings of step m-1 — the whole grid shares them evenly
+  // (they are in the log, contiguous per step); (b) [neuron side] pop + update
+  // step m for the owned neurons and log their crossings.  Events of step m-1
+  // land at steps >= m+1, never in acc[m&1], and acc[(m+1)&1] is popped only
+  // after the barrier.  A last pass m = m1 fans out the final step so the
+  // queue contents after the run are complete.
   for (int m = A.m0; m <= A.m1; ++m) {
-    if (tid == 0) s_n = 0;
-    __syncthreads();
     tl_mark(A.tl, m < A.m1 ? m : A.m1 - 1, A.G, cta, m < A.m1 ? 0 : 7);
-    // ---------------- (a1) deliver this CTA's bucket m+1 into acc[(m+1)&1]
-    // (L2-resident): the events due at m+1 it appended in earlier phases.
-    // Buckets are private per CTA, so appends need no global atomics; the
-    // delivery load is balanced because the fan-out shares are.
-    if (m > A.m0 && A.kind == EQ_KIND_RING) {
-      const int bin = (m + 1) % A.NB;
-      int n = s_bin[bin];
-      n = n < A.cap_b ? n : (int)A.cap_b;
-      const size_t base = ((size_t)cta * A.NB + bin) * A.cap_b;
-      const int* bt = A.bk_tgt + base;
-      const long long* bp = A.bk_pay + base * P::kSlotWords;
-      long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
-      constexpr int DV = 4;
-      for (int q = tid; q < n; q += DV * NT) {
-        int tg[DV];
-        long long pv[DV][2];
+    if (tid < Ro::NF) {
+      // ======================== event side
+      const int gtid = tid;
+      // ---------------- (a1) deliver this CTA's bucket m+1 into acc[(m+1)&1]
+      // (L2-resident): the events due at m+1 it appended in earlier phases.
+      // Buckets are private per CTA, so appends need no global atomics; the
+      // delivery load is balanced because the fan-out shares are.
+      if (m > A.m0 && A.kind == EQ_KIND_RING) {
+        const int bin = (m + 1) % A.NB;
+        int n = s_bin[bin];
+        n = n < A.cap_b ? n : (int)A.cap_b;
+        const size_t base = ((size_t)cta * A.NB + bin) * A.cap_b;
+        const int* bt = A.bk_tgt + base;
+        const long long* bp = A.bk_pay + base * P::kSlotWords;
+        long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
+        constexpr int DV = 4;
+        for (int q = gtid; q < n; q += DV * Ro::NF) {
+          int tg[DV];
+          long long pv[DV][2];
 #pragma unroll
-        for (int e = 0; e < DV; ++e) {
-          const int k = q + e * NT;
-          tg[e] = -1;
-          if (k < n) {
-            tg[e] = bt[k];
-            pv[e][0] = bp[(size_t)k * P::kSlotWords];
-            pv[e][1] = P::kSlotWords == 2 ? bp[(size_t)k * P::kSlotWords + 1] : 0;
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < DV; ++e) {
-          if (tg[e] < 0) continue;
-          if (P::kSlotWords == 1) {
-            red_add(accn + tg[e], pv[e][0]);
-          } else {
-            red_add(accn + 2 * (size_t)tg[e], pv[e][0]);
-            red_add(accn + 2 * (size_t)tg[e] + 1, pv[e][1]);
-          }
-        }
-      }
-      __syncthreads();
-      if (tid == 0) s_bin[bin] = 0;
-    }
-    if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 5);
-    // ---------------- (a2) fan-out of step m-1 (network.py:583-611): the grid
-    // shares the step's crossings evenly (contiguous in the log).  An event due
-    // at m+1 goes straight into acc[(m+1)&1]; a later one is appended to this
-    // CTA's bucket of its delivery step (rank from a shared-memory counter).
-    // No read-modify-write touches DRAM; a full bucket spills into the DRAM
-    // ring row (flagged) and never loses an event.
-    if (m > A.m0 && A.kind == EQ_KIND_RING) {
-      const int me = m - 1;                          // emitting step
-      const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
-      const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
-      long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
-      int* bt_cta = A.bk_tgt + (size_t)cta * A.NB * A.cap_b;
-      long long* bp_cta = A.bk_pay + (size_t)cta * A.NB * A.cap_b * P::kSlotWords;
-      for (long long k0 = s0; k0 < s1; k0 += kCap) {
-        const int nb = (int)(s1 - k0 < kCap ? s1 - k0 : kCap);
-        stage_spikes<T, NT>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_spk, s_r0, s_pre);
-        if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 6);
-        const int total = s_pre[nb];
-        constexpr int EV = 4;
-        for (int f0 = tid; f0 < total; f0 += EV * NT) {
-          int jj[EV], kk[EV];
-          T ww[EV], dd[EV];
-#pragma unroll
-          for (int e = 0; e < EV; ++e) {
-            const int f = f0 + e * NT;
-            kk[e] = -1;
-            if (f < total) {
-              const int k = find_row(s_pre, nb, f);
-              const long long x = s_r0[k] + (f - s_pre[k]);
-              kk[e] = k;
-              jj[e] = __ldg(A.net.col + x);
-              ww[e] = __ldg(A.net.w + x);
-              dd[e] = __ldg(A.net.d + x);
+          for (int e = 0; e < DV; ++e) {
+            const int k = q + e * Ro::NF;
+            tg[e] = -1;
+            if (k < n) {
+              tg[e] = __ldcs(bt + k);
+              pv[e][0] = __ldcs(bp + (size_t)k * P::kSlotWords);
+              pv[e][1] = P::kSlotWords == 2 ? __ldcs(bp + (size_t)k * P::kSlotWords + 1) : 0;
             }
           }
 #pragma unroll
-          for (int e = 0; e < EV; ++e) {
-            if (kk[e] < 0) continue;
-            const SpikeRec<T> rec = s_spk[kk[e]];
-            const int b = c.divN.div(rec.idx);
-            const T w = ww[e], d = dd[e];
-            const T t_post = rec.t + d;                         // :588
-            const int ds = delivery_step(t_post, d, c.dt, me);  // jumps.py:96
-            T ws, wm;
-            if (A.exact) {
-              const T phi = (T)ds * c.dt - t_post;              // :599
-              ws = w * eq_exp_t(-phi / c.tau_s);                // :601
-              wm = w * eq_exp_t(-phi / c.tau_m);                // :606
-            } else {
-              ws = w;
-              wm = (T)0;
-            }
-            const int tgt = b * A.N + jj[e];                    // flat target
-            const long long q1 = P::q(ws, c.scale);
-            const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
-            if (ds == m + 1) {
-              if (P::kSlotWords == 1) {
-                red_add(accn + tgt, pack2(q1, q2));
-              } else {
-                red_add(accn + 2 * (size_t)tgt, q1);
-                red_add(accn + 2 * (size_t)tgt + 1, q2);
-              }
-              continue;
-            }
-            const int bn = ds % A.NB;
-            const int pos = atomicAdd(&s_bin[bn], 1);
-            if (pos < A.cap_b) {
-              const size_t o = (size_t)bn * A.cap_b + pos;
-              bt_cta[o] = tgt;
-              if (P::kSlotWords == 1) {
-                bp_cta[o] = pack2(q1, q2);
-              } else {
-                bp_cta[2 * o] = q1;
-                bp_cta[2 * o + 1] = q2;
-              }
-            } else {                                            // bucket full: DRAM ring row
-              const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
-              if (P::kSlotWords == 1) {
-                red_add(A.ring + so, pack2(q1, q2));
-              } else {
-                red_add(A.ring + 2 * so, q1);
-                red_add(A.ring + 2 * so + 1, q2);
-              }
-              if (A.ring_dirty[ds % A.R] == 0) atomicExch(A.ring_dirty + ds % A.R, 1);
-            }
-          }
-        }
-      }
-    }
-    if (m == A.m1) break;
-    __syncthreads();
-    tl_mark(A.tl, m, A.G, cta, 1);
-    // ---------------- (b) neuron update: pop, synapse, membrane, crossing
-    const bool dirty = A.kind == EQ_KIND_RING && ld_volatile(A.ring_dirty + m % A.R) != 0;
-    for (long long base = begin; base < end; base += (long long)NT * U) {
-      long long slot_v[U][2];
-      T Iv[U], Vv[U];
-      int rf[U];
-      bool on[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = (int)base + u * NT + tid;
-        slot_v[u][0] = slot_v[u][1] = 0;
-        if (idx < end) {
-          const int b = c.divN.div(idx);
-          const int j = idx - b * A.N;
-          if (A.kind == EQ_KIND_RING) {
-            const long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
+          for (int e = 0; e < DV; ++e) {
+            if (tg[e] < 0) continue;
             if (P::kSlotWords == 1) {
-              slot_v[u][0] = ld_slot(accm + idx);
+              red_add(accn + tg[e], pv[e][0]);
             } else {
-              slot_v[u][0] = ld_slot(accm + 2 * (size_t)idx);
-              slot_v[u][1] = ld_slot(accm + 2 * (size_t)idx + 1);
+              red_add(accn + 2 * (size_t)tg[e], pv[e][0]);
+              red_add(accn + 2 * (size_t)tg[e] + 1, pv[e][1]);
             }
-            if (dirty) {                       // a bucket overflowed into the DRAM row
-              size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
-              if (P::kSlotWords == 1) {
-                slot_v[u][0] += ld_slot(A.ring + so);
+          }
+        }
+        group_sync(Ro::kBarF, Ro::NF);
+        if (gtid == 0) s_bin[bin] = 0;
+      }
+      if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 5);
+      // ---------------- (a2) fan-out of step m-1 (network.py:583-611).  An
+      // event due at m+1 goes straight into acc[(m+1)&1]; a later one is
+      // appended to this CTA's bucket of its delivery step (rank from a
+      // shared-memory counter).  No read-modify-write touches DRAM; a full
+      // bucket spills into the DRAM ring row (flagged), never losing events.
+      if (m > A.m0 && A.kind == EQ_KIND_RING) {
+        const int me = m - 1;                          // emitting step
+        const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
+        const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
+        long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
+        int* bt_cta = A.bk_tgt + (size_t)cta * A.NB * A.cap_b;
+        long long* bp_cta = A.bk_pay + (size_t)cta * A.NB * A.cap_b * P::kSlotWords;
+        for (long long k0 = s0; k0 < s1; k0 += kCap) {
+          const int nb = (int)(s1 - k0 < kCap ? s1 - k0 : kCap);
+          stage_spikes<T>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_spk, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
+          const int total = s_pre[nb];
+          constexpr int EV = 4;
+          const int me_bin = me % A.NB;
+          for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
+            int jj[EV], kk[EV];
+            T ww[EV], dd[EV];
+            unsigned short cc[EV];
+#pragma unroll
+            for (int e = 0; e < EV; ++e) {
+              const int f = f0 + e * Ro::NF;
+              kk[e] = -1;
+              if (f < total) {
+                const int k = find_row(s_pre, nb, f);
+                const long long x = s_r0[k] + (f - s_pre[k]);
+                kk[e] = k;
+                jj[e] = __ldcs(A.net.col + x);      // streamed once per event: evict-first
+                ww[e] = __ldcs(A.net.w + x);
+                dd[e] = __ldcs(A.net.d + x);
+                cc[e] = __ldcs(A.net.dcode + x);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < EV; ++e) {
+              if (kk[e] < 0) continue;
+              const SpikeRec<T> rec = s_spk[kk[e]];
+              const int b = c.divN.div(rec.idx);
+              const T w = ww[e], d = dd[e];
+              const T t_post = rec.t + d;                              // :588
+              const int ds = delivery_step_coded(t_post, cc[e], c.dt, me);  // jumps.py:96
+              T ws, wm;
+              if (A.exact) {
+                const T phi = (T)ds * c.dt - t_post;              // :599
+                ws = w * eq_exp_t(-phi * c.inv_tau_s);            // :601 (x 1/tau)
+                wm = w * eq_exp_t(-phi * c.inv_tau_m);            // :606
               } else {
-                slot_v[u][0] += ld_slot(A.ring + 2 * so);
-                slot_v[u][1] += ld_slot(A.ring + 2 * so + 1);
+                ws = w;
+                wm = (T)0;
+              }
+              const int tgt = b * A.N + jj[e];                    // flat target
+              const long long q1 = P::q(ws, c.scale);
+              const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
+              if (ds == m + 1) {
+                if (P::kSlotWords == 1) {
+                  red_add(accn + tgt, pack2(q1, q2));
+                } else {
+                  red_add(accn + 2 * (size_t)tgt, q1);
+                  red_add(accn + 2 * (size_t)tgt + 1, q2);
+                }
+                continue;
+              }
+              int bn = me_bin + (ds - me);                        // ds % NB, ds - me in [2, H]
+              if (bn >= A.NB) bn -= A.NB;
+              const int pos = atomicAdd(&s_bin[bn], 1);
+              if (pos < A.cap_b) {
+                const size_t o = (size_t)bn * A.cap_b + pos;
+                __stcs(bt_cta + o, tgt);                          // read once, ~H/2 steps later
+                if (P::kSlotWords == 1) {
+                  __stcs(bp_cta + o, pack2(q1, q2));
+                } else {
+                  __stcs(bp_cta + 2 * o, q1);
+                  __stcs(bp_cta + 2 * o + 1, q2);
+                }
+              } else {                                            // bucket full: DRAM ring row
+                const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
+                if (P::kSlotWords == 1) {
+                  red_add(A.ring + so, pack2(q1, q2));
+                } else {
+                  red_add(A.ring + 2 * so, q1);
+                  red_add(A.ring + 2 * so + 1, q2);
+                }
+                if (A.ring_dirty[ds % A.R] == 0) atomicExch(A.ring_dirty + ds % A.R, 1);
               }
             }
           }
-          Iv[u] = A.I[idx];
-          Vv[u] = A.V[idx];
-          rf[u] = A.refractory ? A.refr[idx] : 0;
-          on[u] = drive_bit(A.net, b, m, j);
         }
       }
+      if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 1);
+    } else if (m < A.m1) {
+      // ======================== neuron side
+      const int gtid = tid - Ro::NF;
+      const bool dirty = A.kind == EQ_KIND_RING && ld_volatile(A.ring_dirty + m % A.R) != 0;
+      // ---------------- (b) neuron update: pop, synapse, membrane, crossing.
+      // Walked per trial segment of the owned range so the row pointers are
+      // computed once per segment, not per neuron.
+      const int mm = m < A.net.t_mask ? m : A.net.t_mask - 1;   // network.py:155 rows[-1]
+      const long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
+      const int b_last = (int)((end - 1) / A.N);
+      for (int b = b_first; b <= b_last; ++b) {
+        const int tb0 = b * A.N;
+        const int j0 = (int)(begin > tb0 ? begin - tb0 : 0);
+        const int j1 = (int)(end < (long long)tb0 + A.N ? end - tb0 : A.N);
+        const uint32_t* mrow = A.net.mask + ((size_t)b * A.net.t_mask + mm) * A.net.words;
+        if (P::kSlotWords == 1 && (A.N & 3) == 0 && !dirty) {
+          // fp32 fast path: four neurons per thread with 16-byte accesses
+          // (segment bounds are multiples of 4 when N % 4 == 0: ranges are
+          // warp-aligned).  Same per-neuron arithmetic as the scalar path.
+          for (int jq = j0 + 4 * gtid; jq < j1; jq += 4 * Ro::NN) {
+            const int idx = tb0 + jq;
+            const longlong2 a01 = *reinterpret_cast<const longlong2*>(accm + idx);
+            const longlong2 a23 = *reinterpret_cast<const longlong2*>(accm + idx + 2);
+            const float4 I4 = *reinterpret_cast<const float4*>(A.I + idx);
+            const float4 V4 = *reinterpret_cast<const float4*>(A.V + idx);
+            const float4 M4 = __ldg(reinterpret_cast<const float4*>(A.net.amp + jq));
+            const unsigned mw = __ldg(mrow + (jq >> 5)) >> (jq & 31);
+            int4 R4 = make_int4(0, 0, 0, 0);
+            if (A.refractory) R4 = *reinterpret_cast<const int4*>(A.refr + idx);
+            const long long av[4] = {a01.x, a01.y, a23.x, a23.y};
+            const float Iv4[4] = {I4.x, I4.y, I4.z, I4.w};
+            const float Vv4[4] = {V4.x, V4.y, V4.z, V4.w};
+            const float Av4[4] = {M4.x, M4.y, M4.z, M4.w};
+            int rf4[4] = {R4.x, R4.y, R4.z, R4.w};
+            float In[4], Vn[4];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = (int)base + u * NT + tid;
-        if (idx >= end) continue;
-        const int b = c.divN.div(idx);
-        const int j = idx - b * A.N;
-        T ps, pm;
-        if (P::kSlotWords == 1) {
-          long long qs, qm;
-          unpack2(slot_v[u][0], qs, qm);
-          ps = P::deq(qs, c.inv_scale);
-          pm = P::deq(qm, c.inv_scale);
-        } else {
-          ps = P::deq(slot_v[u][0], c.inv_scale);
-          pm = P::deq(slot_v[u][1], c.inv_scale);
+            for (int q = 0; q < 4; ++q) {
+              long long qs, qm;
+              unpack2(av[q], qs, qm);
+              const T ps = P::deq(qs, c.inv_scale);
+              const T pm = A.exact ? P::deq(qm, c.inv_scale) : (T)0;
+              const T drive = ((mw >> q) & 1u) ? (T)Av4[q] : (T)0;
+              T i, v_new, a, v, t_spk;
+              if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, (T)Iv4[q], (T)Vv4[q], drive, rf4[q], i, v_new,
+                           a, v, t_spk)) {
+                if (t_spk != t_spk) {
+                  raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, jq + q);
+                } else {
+                  int pos = atomicAdd(&s_n, 1);
+                  SpikeRec<T> rec;
+                  rec.idx = idx + q;
+                  rec.t = t_spk;
+                  rec.a = a;
+                  rec.vh = v;
+                  if (pos < kCapN) s_own[pos] = rec;
+                  else spill[pos - kCapN] = rec;
+                }
+              }
+              In[q] = (float)i;
+              Vn[q] = (float)v_new;
+            }
+            *reinterpret_cast<float4*>(A.I + idx) = make_float4(In[0], In[1], In[2], In[3]);
+            *reinterpret_cast<float4*>(A.V + idx) = make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
+            if (A.refractory)
+              *reinterpret_cast<int4*>(A.refr + idx) = make_int4(rf4[0], rf4[1], rf4[2], rf4[3]);
+            if (A.v_trace)
+              *reinterpret_cast<float4*>(A.v_trace + (size_t)(m - A.m0) * A.total + idx) =
+                  make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
+          }
+          continue;
         }
-        if (!A.exact) pm = (T)0;
-        const T drive = on[u] ? __ldg(A.net.amp + j) : (T)0;
-        T i, v_new, a, v, t_spk;
-        if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, Iv[u], Vv[u], drive, rf[u], i, v_new, a, v, t_spk)) {
-          if (t_spk != t_spk) {
-            raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, j);
-          } else {
-            int pos = atomicAdd(&s_n, 1);
-            SpikeRec<T> rec;
-            rec.idx = idx;
-            rec.t = t_spk;
-            rec.a = a;
-            rec.vh = v;
-            if (pos < kCap) s_spk[pos] = rec;
-            else spill[pos - kCap] = rec;
+        for (int jb = j0; jb < j1; jb += Ro::NN * U) {
+          long long slot_v[U][2];
+          T Iv[U], Vv[U], Am[U];
+          int rf[U];
+          unsigned mw[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = jb + u * Ro::NN + gtid;
+            slot_v[u][0] = slot_v[u][1] = 0;
+            if (j < j1) {
+              const int idx = tb0 + j;
+              if (A.kind == EQ_KIND_RING) {
+                if (P::kSlotWords == 1) {
+                  slot_v[u][0] = ld_slot(accm + idx);
+                } else {
+                  slot_v[u][0] = ld_slot(accm + 2 * (size_t)idx);
+                  slot_v[u][1] = ld_slot(accm + 2 * (size_t)idx + 1);
+                }
+                if (dirty) {                       // a bucket overflowed into the DRAM row
+                  size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
+                  if (P::kSlotWords == 1) {
+                    slot_v[u][0] += ld_slot(A.ring + so);
+                  } else {
+                    slot_v[u][0] += ld_slot(A.ring + 2 * so);
+                    slot_v[u][1] += ld_slot(A.ring + 2 * so + 1);
+                  }
+                }
+              }
+              Iv[u] = A.I[idx];
+              Vv[u] = A.V[idx];
+              rf[u] = A.refractory ? A.refr[idx] : 0;
+              mw[u] = __ldg(mrow + (j >> 5));
+              Am[u] = __ldg(A.net.amp + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = jb + u * Ro::NN + gtid;
+            if (j >= j1) continue;
+            const int idx = tb0 + j;
+            T ps, pm;
+            if (P::kSlotWords == 1) {
+              long long qs, qm;
+              unpack2(slot_v[u][0], qs, qm);
+              ps = P::deq(qs, c.inv_scale);
+              pm = P::deq(qm, c.inv_scale);
+            } else {
+              ps = P::deq(slot_v[u][0], c.inv_scale);
+              pm = P::deq(slot_v[u][1], c.inv_scale);
+            }
+            if (!A.exact) pm = (T)0;
+            const T drive = ((mw[u] >> (j & 31)) & 1u) ? Am[u] : (T)0;
+            T i, v_new, a, v, t_spk;
+            if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, Iv[u], Vv[u], drive, rf[u], i, v_new, a, v,
+                         t_spk)) {
+              if (t_spk != t_spk) {
+                raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, j);
+              } else {
+                int pos = atomicAdd(&s_n, 1);
+                SpikeRec<T> rec;
+                rec.idx = idx;
+                rec.t = t_spk;
+                rec.a = a;
+                rec.vh = v;
+                if (pos < kCapN) s_own[pos] = rec;
+                else spill[pos - kCapN] = rec;
+              }
+            }
+            A.I[idx] = i;
+            A.V[idx] = v_new;
+            if (A.refractory) A.refr[idx] = rf[u];
+            if (A.v_trace) A.v_trace[(size_t)(m - A.m0) * A.total + idx] = v_new;
           }
         }
-        A.I[idx] = i;
-        A.V[idx] = v_new;
-        if (A.refractory) A.refr[idx] = rf[u];
-        if (A.v_trace) A.v_trace[(size_t)(m - A.m0) * A.total + idx] = v_new;
       }
-    }
-    __syncthreads();
-    tl_mark(A.tl, m, A.G, cta, 4);
-    // Clear the popped slot row (RingQueue._pop_raw zeroes it, queues.py:114-117).
-    // Done here, not next to the load: a store to the line a pending load is
-    // filling stalled the pop loop ~8x.  Row m mod R receives no red.add in
-    // this phase (fan-out of step m-1 targets rows m+1 .. m-1+horizon, R = horizon + 1).
-    if (A.kind == EQ_KIND_RING) {
-      long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
-      for (int idx = (int)begin + tid; idx < end; idx += NT) {
-        if (P::kSlotWords == 1) {
-          st_slot(accm + idx, 0);
+      group_sync(Ro::kBarN, Ro::NN);
+      if (gtid == 0) tl_mark_any(A.tl, m, A.G, cta, 4);
+      // Clear the popped accumulator (RingQueue._pop_raw zeroes the slot,
+      // queues.py:114-117), in a separate pass: a store next to the pending
+      // load of the same line stalled the pop loop ~8x.  acc[m&1] receives no
+      // red.add in this phase (the event side writes acc[(m+1)&1]).
+      if (A.kind == EQ_KIND_RING) {
+        long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
+        if (P::kSlotWords == 1 && ((begin | end) & 1) == 0) {
+          for (long long idx = begin + 2 * gtid; idx < end; idx += 2 * Ro::NN)
+            *reinterpret_cast<longlong2*>(accm + idx) = make_longlong2(0, 0);
         } else {
-          st_slot(accm + 2 * (size_t)idx, 0);
-          st_slot(accm + 2 * (size_t)idx + 1, 0);
+          for (int idx = (int)begin + gtid; idx < end; idx += Ro::NN) {
+            if (P::kSlotWords == 1) {
+              st_slot(accm + idx, 0);
+            } else {
+              st_slot(accm + 2 * (size_t)idx, 0);
+              st_slot(accm + 2 * (size_t)idx + 1, 0);
+            }
+          }
         }
-      }
-      if (dirty) {
-        const int row = m % A.R;
-        for (int idx = (int)begin + tid; idx < end; idx += NT) {
-          const int b = c.divN.div(idx);
-          const size_t so = ((size_t)b * A.R + row) * A.N + (idx - b * A.N);
-          if (P::kSlotWords == 1) {
-            st_slot(A.ring + so, 0);
-          } else {
-            st_slot(A.ring + 2 * so, 0);
-            st_slot(A.ring + 2 * so + 1, 0);
+        if (dirty) {
+          const int row = m % A.R;
+          for (int idx = (int)begin + gtid; idx < end; idx += Ro::NN) {
+            const int b = c.divN.div(idx);   // rare path (bucket overflow)
+            const size_t so = ((size_t)b * A.R + row) * A.N + (idx - b * A.N);
+            if (P::kSlotWords == 1) {
+              st_slot(A.ring + so, 0);
+            } else {
+              st_slot(A.ring + 2 * so, 0);
+              st_slot(A.ring + 2 * so + 1, 0);
+            }
           }
         }
       }
-    }
-    const int nspk = s_n;
-    // ---------------- spike log: one chunk per (step, CTA); the chunks of a
-    // step are contiguous because every reservation of step m happens between
-    // the two barriers around phase m.  Counters per trial (spikes, events;
-    // donothing drops every event, queues.py:42-45).
-    if (tid == 0) {
-      unsigned long long off = nspk ? atomicAdd(A.log_count, (unsigned long long)nspk) : 0ULL;
-      if (nspk && (long long)(off + nspk) > A.log_cap) {
-        raise_error(A.err, EQ_ERR_CAPACITY, m, -1, -1);
-        off = 0;
+      const int nspk = s_n;
+      // ---------------- spike log: one chunk per (step, CTA); the chunks of a
+      // step are contiguous because every reservation of step m happens between
+      // the two barriers around phase m.  Counters per trial (spikes, events;
+      // donothing drops every event, queues.py:42-45).
+      if (gtid == 0) {
+        unsigned long long off = nspk ? atomicAdd(A.log_count, (unsigned long long)nspk) : 0ULL;
+        if (nspk && (long long)(off + nspk) > A.log_cap) {
+          raise_error(A.err, EQ_ERR_CAPACITY, m, -1, -1);
+          off = 0;
+        }
+        s_off = (long long)off;
+        A.chunk_off[(size_t)m * A.G + cta] = (long long)off;
+        A.chunk_cnt[(size_t)m * A.G + cta] = nspk;
       }
-      s_off = (long long)off;
-      A.chunk_off[(size_t)m * A.G + cta] = (long long)off;
-      A.chunk_cnt[(size_t)m * A.G + cta] = nspk;
+      group_sync(Ro::kBarN, Ro::NN);
+      const bool log_ok = s_off + nspk <= A.log_cap;
+      for (int k = gtid; k < nspk; k += Ro::NN) {
+        const SpikeRec<T> rec = k < kCapN ? s_own[k] : spill[k - kCapN];
+        if (log_ok) A.log[s_off + k] = rec;
+        const int b = c.divN.div(rec.idx);
+        const int i = rec.idx - b * A.N;
+        const unsigned long long len =
+            (unsigned long long)(__ldg(A.net.rowptr + i + 1) - __ldg(A.net.rowptr + i));
+        const int tb = b - b_first;
+        if (tb < kTr) {
+          atomicAdd(&s_ctr[tb][0], 1ULL);
+          atomicAdd(&s_ctr[tb][1], len);
+          if (A.kind == EQ_KIND_DONOTHING) atomicAdd(&s_ctr[tb][2], len);
+        } else {
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), len);
+          if (A.kind == EQ_KIND_DONOTHING)
+            atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), len);
+        }
+      }
+      group_sync(Ro::kBarN, Ro::NN);
+      if (gtid == 0) {
+        s_n = 0;
+        tl_mark_any(A.tl, m, A.G, cta, 6);
+      }
     }
     __syncthreads();
-    const bool log_ok = s_off + nspk <= A.log_cap;
-    for (int k = tid; k < nspk; k += NT) {
-      const SpikeRec<T> rec = k < kCap ? s_spk[k] : spill[k - kCap];
-      if (log_ok) A.log[s_off + k] = rec;
-      const int b = c.divN.div(rec.idx);
-      const int i = rec.idx - b * A.N;
-      const unsigned long long len = (unsigned long long)(__ldg(A.net.rowptr + i + 1) - __ldg(A.net.rowptr + i));
-      const int tb = b - b_first;
-      if (tb < kTr) {
-        atomicAdd(&s_ctr[tb][0], 1ULL);
-        atomicAdd(&s_ctr[tb][1], len);
-        if (A.kind == EQ_KIND_DONOTHING) atomicAdd(&s_ctr[tb][2], len);
-      } else {
-        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
-        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), len);
-        if (A.kind == EQ_KIND_DONOTHING)
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), len);
-      }
-    }
-    __syncthreads();
+    if (m == A.m1) break;
     tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err, A.step_start + m + 1, A.log_count, nullptr,
                    A.kind == EQ_KIND_RING ? A.ring_dirty + m % A.R : nullptr))
@@ -541,9 +677,10 @@ struct BwdArgs {
   unsigned* bar;
 };
 
-template <typename T, int NT, int U>
-__global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
+template <typename T, int NT, int U, int NF = NT / 2>
+__global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
   typedef typename Prec<T>::T2 T2;
+  typedef Roles<NT, NF> Ro;
   constexpr int kCapB = sizeof(T) == 4 ? 512 : 256;   // spikes per batch
   constexpr int kEv = sizeof(T) == 4 ? 4096 : 2048;    // events per reduction window
   __shared__ SpikeRec<T> s_rec[kCapB];
@@ -551,155 +688,241 @@ __global__ void __launch_bounds__(NT) k_backward(BwdArgs<T> A) {
   __shared__ int s_pre[kCapB + 1];
   __shared__ T s_lt[kCapB];
   __shared__ T s_gtp[kEv];
-  extern __shared__ unsigned int s_bits[];   // one bit per owned neuron-trial
+  extern __shared__ unsigned int s_bits[];   // one bit per owned neuron-trial, then uint16 chunk positions
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;
   const long long begin = (long long)cta * A.per;
   const long long end = begin + A.per < A.total ? begin + A.per : A.total;
   const int nwords = (int)((A.per + 31) / 32);
+  unsigned short* s_pos = reinterpret_cast<unsigned short*>(s_bits + nwords);
   const StepConsts<T> c = A.c;
   for (int k = tid; k < nwords; k += NT) s_bits[k] = 0u;
   __syncthreads();
 
+  // Phase m (m = m_run-1 .. 0): [event side] R-fanout of step m-1 (its events
+  // read reverse slots of steps >= m+1, all final); [neuron side] R-neuron(m),
+  // which writes reverse slot m only and reads dL/dt_spk of its own spikes of
+  // step m, produced by the event side of phase m+1.
   for (int m = A.m_run - 1; m >= 0; --m) {
     tl_mark(A.tl, m, A.G, cta, 0);
-    const long long off = A.chunk_off[(size_t)m * A.G + cta];
-    const int cnt = A.chunk_cnt[(size_t)m * A.G + cta];
-    // ---------------- R-fanout(m-1): the crossings of step m-1, shared evenly
-    // by the whole grid (whole spikes per CTA).  They read reverse slots of
-    // steps >= m+1, all final; R-neuron(m) below writes only slot m.  dL/dt_spk
-    // of a spike is the SEQUENTIAL sum of its edges' g_tp in row order (zeros
-    // for events never popped or dropped), staged through s_gtp in windows of
-    // kEv events; the oracle sums in the same order.  R-neuron(m-1) in the
-    // next phase reads it from lt_log.
-    if (m >= 1) {
-      const int me = m - 1;
-      const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
-      const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
-      for (long long k0 = s0; k0 < s1; k0 += kCapB) {
-        const int nb = (int)(s1 - k0 < kCapB ? s1 - k0 : kCapB);
-        stage_spikes<T, NT>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_rec, s_r0, s_pre);
-        for (int k = tid; k < nb; k += NT) s_lt[k] = (T)0;
-        __syncthreads();
-        if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 4);
-        const int total = s_pre[nb];
-        for (int w0 = 0; w0 < total; w0 += kEv) {
-          const int wend = total - w0 < kEv ? total : w0 + kEv;
-          constexpr int EV = 4;
-          for (int f0 = w0 + tid; f0 < wend; f0 += EV * NT) {
-            int jj[EV], kk[EV];
-            long long xx[EV];
-            T ww[EV], dd[EV];
+    if (tid < Ro::NF) {
+      // ======================== event side: R-fanout(m-1), shared evenly by
+      // the whole grid (whole spikes per CTA).  dL/dt_spk of a spike is the
+      // SEQUENTIAL sum of its edges' g_tp in row order (zeros for events never
+      // popped or dropped), staged through s_gtp in windows of kEv events; the
+      // oracle sums in the same order.
+      const int gtid = tid;
+      if (m >= 1) {
+        const int me = m - 1;
+        const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
+        const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
+        for (long long k0 = s0; k0 < s1; k0 += kCapB) {
+          const int nb = (int)(s1 - k0 < kCapB ? s1 - k0 : kCapB);
+          stage_spikes<T>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_rec, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
+          for (int k = gtid; k < nb; k += Ro::NF) s_lt[k] = (T)0;
+          group_sync(Ro::kBarF, Ro::NF);
+          if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 4);
+          const int total = s_pre[nb];
+          for (int w0 = 0; w0 < total; w0 += kEv) {
+            const int wend = total - w0 < kEv ? total : w0 + kEv;
+            constexpr int EV = 4;
+            for (int f0 = w0 + gtid; f0 < wend; f0 += EV * Ro::NF) {
+              int jj[EV], kk[EV];
+              long long xx[EV];
+              T ww[EV], dd[EV];
+              unsigned short cc[EV];
 #pragma unroll
-            for (int e = 0; e < EV; ++e) {
-              const int f = f0 + e * NT;
-              kk[e] = -1;
-              if (f < wend) {
-                const int k = find_row(s_pre, nb, f);
-                const long long x = s_r0[k] + (f - s_pre[k]);
-                kk[e] = k;
-                xx[e] = x;
-                jj[e] = __ldg(A.net.col + x);
-                ww[e] = __ldg(A.net.w + x);
-                dd[e] = __ldg(A.net.d + x);
+              for (int e = 0; e < EV; ++e) {
+                const int f = f0 + e * Ro::NF;
+                kk[e] = -1;
+                if (f < wend) {
+                  const int k = find_row(s_pre, nb, f);
+                  const long long x = s_r0[k] + (f - s_pre[k]);
+                  kk[e] = k;
+                  xx[e] = x;
+                  jj[e] = __ldcs(A.net.col + x);
+                  ww[e] = __ldcs(A.net.w + x);
+                  dd[e] = __ldcs(A.net.d + x);
+                  cc[e] = __ldcs(A.net.dcode + x);
+                }
+              }
+#pragma unroll
+              for (int e = 0; e < EV; ++e) {
+                if (kk[e] < 0) continue;
+                const int f = f0 + e * Ro::NF;
+                const SpikeRec<T> rec = s_rec[kk[e]];
+                const int b = c.divN.div(rec.idx);
+                const T w = ww[e], d = dd[e];
+                const T t_post = rec.t + d;
+                const int st = delivery_step_coded(t_post, cc[e], c.dt, me);
+                T g_tp = (T)0;
+                bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
+                if (live && A.drop_bits) {                       // dropped by a bounded queue
+                  const long long id = A.ev_base[k0 + kk[e]] + (f - s_pre[kk[e]]);
+                  live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
+                }
+                if (live) {
+                  const T phi = (T)st * c.dt - t_post;
+                  const T es = eq_exp_t(-phi * c.inv_tau_s);
+                  const T em = eq_exp_t(-phi * c.inv_tau_m);
+                  const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
+                  const T g_w = es * L.x + em * L.y;
+                  g_tp = w * (es * L.x * c.inv_tau_s + em * L.y * c.inv_tau_m);
+                  red_add_f64(A.gw + xx[e], (double)g_w);
+                  red_add_f64(A.gd + xx[e], (double)g_tp);
+                }
+                s_gtp[f - w0] = g_tp;
               }
             }
+            group_sync(Ro::kBarF, Ro::NF);
+            if (k0 == s0 && w0 == 0) tl_mark(A.tl, m, A.G, cta, 5);
+            const int ka = find_row(s_pre, nb, w0);
+            const int kb = find_row(s_pre, nb, wend - 1);
+            for (int k = ka + gtid; k <= kb; k += Ro::NF) {
+              const int lo = s_pre[k] > w0 ? s_pre[k] : w0;
+              const int hi = s_pre[k + 1] < wend ? s_pre[k + 1] : wend;
+              T acc = s_lt[k];
+              for (int q = lo; q < hi; ++q) acc = acc + s_gtp[q - w0];
+              s_lt[k] = acc;
+            }
+            group_sync(Ro::kBarF, Ro::NF);
+          }
+          for (int k = gtid; k < nb; k += Ro::NF) A.lt_log[k0 + k] = s_lt[k];
+        }
+      }
+      tl_mark(A.tl, m, A.G, cta, 1);
+    } else {
+      // ======================== neuron side: R-neuron(m)
+      const int gtid = tid - Ro::NF;
+      const long long off = A.chunk_off[(size_t)m * A.G + cta];
+      const int cnt = A.chunk_cnt[(size_t)m * A.G + cta];
+      // own spikers of step m -> bitmap (looked up in the own log chunk)
+      for (int k = gtid; k < cnt; k += Ro::NN) {
+        const int loc = A.log[off + k].idx - (int)begin;
+        atomicOr(&s_bits[loc >> 5], 1u << (loc & 31));
+        s_pos[loc] = (unsigned short)(k < 0xffff ? k : 0xffff);
+      }
+      group_sync(Ro::kBarN, Ro::NN);
+      const int mm = m < A.net.t_mask ? m : A.net.t_mask - 1;
+      const int b_first = (int)(begin / A.N);
+      const int b_last = (int)((end - 1) / A.N);
+      for (int b = b_first; b <= b_last; ++b) {
+        const int tb0 = b * A.N;
+        const int j0 = (int)(begin > tb0 ? begin - tb0 : 0);
+        const int j1 = (int)(end < (long long)tb0 + A.N ? end - tb0 : A.N);
+        const uint32_t* mrow = A.net.mask + ((size_t)b * A.net.t_mask + mm) * A.net.words;
+        T2* lam_row = A.lam + ((size_t)b * A.R + (size_t)(m % A.R)) * A.N;
+        if (sizeof(T) == 4 && (A.N & 3) == 0 && ((j0 | j1) & 3) == 0) {
+          // fp32 fast path: four neurons per thread, 16-byte accesses
+          for (int jq = j0 + 4 * gtid; jq < j1; jq += 4 * Ro::NN) {
+            const int idx = tb0 + jq;
+            const float4 LV4 = *reinterpret_cast<const float4*>(A.lamV + idx);
+            const float4 LI4 = *reinterpret_cast<const float4*>(A.lamI + idx);
+            const float lvv[4] = {LV4.x, LV4.y, LV4.z, LV4.w};
+            const float liv[4] = {LI4.x, LI4.y, LI4.z, LI4.w};
+            float nv[4], ni[4], ls[4], lm[4];
+            unsigned mw = 0;
+            if (A.gamp_bt) mw = __ldg(mrow + (jq >> 5)) >> (jq & 31);
+            const int loc0 = idx - (int)begin;
+            const unsigned sb = (s_bits[loc0 >> 5] >> (loc0 & 31)) & 0xfu;
 #pragma unroll
-            for (int e = 0; e < EV; ++e) {
-              if (kk[e] < 0) continue;
-              const int f = f0 + e * NT;
-              const SpikeRec<T> rec = s_rec[kk[e]];
-              const int b = c.divN.div(rec.idx);
-              const T w = ww[e], d = dd[e];
-              const T t_post = rec.t + d;
-              const int st = delivery_step(t_post, d, c.dt, me);
-              T g_tp = (T)0;
-              bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
-              if (live && A.drop_bits) {                       // dropped by a bounded queue
-                const long long id = A.ev_base[k0 + kk[e]] + (f - s_pre[kk[e]]);
-                live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
+            for (int q = 0; q < 4; ++q) {
+              const T lv = (T)lvv[q];
+              T la, lvh;
+              if ((sb >> q) & 1u) {
+                int k = s_pos[loc0 + q];
+                if (k == 0xffff) {
+                  k = 0;
+                  while (k < cnt && A.log[off + k].idx != idx + q) ++k;
+                }
+                SpikeRec<T> rec = A.log[off + k];
+                const T lt0 = m + 1 < A.m_run ? A.lt_log[off + k] : (T)0;
+                T t = rec.t, a = rec.a, vh = rec.vh;
+                T uu = (T)(m + 1) * c.dt - t;
+                T ku = eq_exp_t(-uu / c.tau_m);
+                T r = (c.v_th - a) / (vh - a);
+                T lt = lt0 + lv * (c.v_reset - a) * ku / c.tau_m;
+                T lr = -c.tau_m * lt / r;
+                T den = vh - a;
+                T den2 = den * den;
+                la = lv * ((T)1 - ku) + lr * (c.v_th - vh) / den2;
+                lvh = -lr * (c.v_th - a) / den2;
+              } else {
+                la = lv * ((T)1 - c.k_m);
+                lvh = lv * c.k_m;
               }
-              if (live) {
-                const T phi = (T)st * c.dt - t_post;
-                const T es = eq_exp_t(-phi / c.tau_s);
-                const T em = eq_exp_t(-phi / c.tau_m);
-                const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
-                const T g_w = es * L.x + em * L.y;
-                g_tp = w * (es * L.x / c.tau_s + em * L.y / c.tau_m);
-                atomicAdd(A.gw + xx[e], (double)g_w);
-                atomicAdd(A.gd + xx[e], (double)g_tp);
-              }
-              s_gtp[f - w0] = g_tp;
+              const T lip = (T)liv[q] + la;
+              if (A.gamp_bt && ((mw >> q) & 1u)) A.gamp_bt[idx + q] += (double)la;
+              ls[q] = (float)(c.k_s * lip - c.cc * lvh);
+              lm[q] = (float)(c.cc * lvh);
+              ni[q] = (float)(c.k_s * lip);
+              nv[q] = (float)lvh;
+            }
+            float4* lr4 = reinterpret_cast<float4*>(lam_row + jq);
+            lr4[0] = make_float4(ls[0], lm[0], ls[1], lm[1]);
+            lr4[1] = make_float4(ls[2], lm[2], ls[3], lm[3]);
+            *reinterpret_cast<float4*>(A.lamI + idx) = make_float4(ni[0], ni[1], ni[2], ni[3]);
+            *reinterpret_cast<float4*>(A.lamV + idx) = make_float4(nv[0], nv[1], nv[2], nv[3]);
+          }
+          continue;
+        }
+        for (int jb = j0; jb < j1; jb += Ro::NN * U) {
+          T LV[U], LI[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = jb + u * Ro::NN + gtid;
+            if (j < j1) {
+              LV[u] = A.lamV[tb0 + j];
+              LI[u] = A.lamI[tb0 + j];
             }
           }
-          __syncthreads();
-          if (k0 == s0 && w0 == 0) tl_mark(A.tl, m, A.G, cta, 5);
-          const int ka = find_row(s_pre, nb, w0);
-          const int kb = find_row(s_pre, nb, wend - 1);
-          for (int k = ka + tid; k <= kb; k += NT) {
-            const int lo = s_pre[k] > w0 ? s_pre[k] : w0;
-            const int hi = s_pre[k + 1] < wend ? s_pre[k + 1] : wend;
-            T acc = s_lt[k];
-            for (int q = lo; q < hi; ++q) acc = acc + s_gtp[q - w0];
-            s_lt[k] = acc;
-          }
-          __syncthreads();
-          if (k0 == s0 && w0 == 0) tl_mark(A.tl, m, A.G, cta, 6);
-        }
-        for (int k = tid; k < nb; k += NT) A.lt_log[k0 + k] = s_lt[k];
-      }
-    }
-    // own spikers of step m -> bitmap (R-neuron looks them up in the own chunk)
-    for (int k = tid; k < cnt; k += NT) {
-      const int loc = A.log[off + k].idx - (int)begin;
-      atomicOr(&s_bits[loc >> 5], 1u << (loc & 31));
-    }
-    __syncthreads();
-    tl_mark(A.tl, m, A.G, cta, 1);
-    // ---------------- R-neuron(m)
-    for (long long base = begin; base < end; base += (long long)NT * U) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = (int)base + u * NT + tid;
-        if (idx >= end) continue;
-        const int b = c.divN.div(idx);
-        const int j = idx - b * A.N;
-        T lv = A.lamV[idx];
-        T la, lvh;
-        const int loc = idx - (int)begin;
-        if ((s_bits[loc >> 5] >> (loc & 31)) & 1u) {
-          int k = 0;
-          while (k < cnt && A.log[off + k].idx != idx) ++k;
-          SpikeRec<T> rec = A.log[off + k];
-          const T lt0 = m + 1 < A.m_run ? A.lt_log[off + k] : (T)0;
-          T t = rec.t, a = rec.a, vh = rec.vh;
-          T uu = (T)(m + 1) * c.dt - t;
-          T ku = eq_exp_t(-uu / c.tau_m);
-          T r = (c.v_th - a) / (vh - a);
-          T lt = lt0 + lv * (c.v_reset - a) * ku / c.tau_m;
-          T lr = -c.tau_m * lt / r;
-          T den = vh - a;
-          T den2 = den * den;
-          la = lv * ((T)1 - ku) + lr * (c.v_th - vh) / den2;
-          lvh = -lr * (c.v_th - a) / den2;
-        } else {
-          la = lv * ((T)1 - c.k_m);
-          lvh = lv * c.k_m;
+          for (int u = 0; u < U; ++u) {
+            const int j = jb + u * Ro::NN + gtid;
+            if (j >= j1) continue;
+            const int idx = tb0 + j;
+            const T lv = LV[u];
+            T la, lvh;
+            const int loc = idx - (int)begin;
+            if ((s_bits[loc >> 5] >> (loc & 31)) & 1u) {
+              int k = s_pos[loc];
+              if (k == 0xffff) {
+                k = 0;
+                while (k < cnt && A.log[off + k].idx != idx) ++k;
+              }
+              SpikeRec<T> rec = A.log[off + k];
+              const T lt0 = m + 1 < A.m_run ? A.lt_log[off + k] : (T)0;
+              T t = rec.t, a = rec.a, vh = rec.vh;
+              T uu = (T)(m + 1) * c.dt - t;
+              T ku = eq_exp_t(-uu / c.tau_m);
+              T r = (c.v_th - a) / (vh - a);
+              T lt = lt0 + lv * (c.v_reset - a) * ku / c.tau_m;
+              T lr = -c.tau_m * lt / r;
+              T den = vh - a;
+              T den2 = den * den;
+              la = lv * ((T)1 - ku) + lr * (c.v_th - vh) / den2;
+              lvh = -lr * (c.v_th - a) / den2;
+            } else {
+              la = lv * ((T)1 - c.k_m);
+              lvh = lv * c.k_m;
+            }
+            T lip = LI[u] + la;
+            if (A.gamp_bt && ((__ldg(mrow + (j >> 5)) >> (j & 31)) & 1u)) A.gamp_bt[idx] += (double)la;
+            T2 L;
+            L.x = c.k_s * lip - c.cc * lvh;
+            L.y = c.cc * lvh;
+            lam_row[j] = L;
+            A.lamI[idx] = c.k_s * lip;
+            A.lamV[idx] = lvh;
+          }
         }
-        T lip = A.lamI[idx] + la;
-        if (A.gamp_bt && drive_bit(A.net, b, m, j)) A.gamp_bt[idx] += (double)la;
-        T2 L;
-        L.x = c.k_s * lip - c.cc * lvh;
-        L.y = c.cc * lvh;
-        A.lam[((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j] = L;
-        A.lamI[idx] = c.k_s * lip;
-        A.lamV[idx] = lvh;
       }
-    }
-    __syncthreads();
-    for (int k = tid; k < cnt; k += NT) {
-      long long loc = (long long)A.log[off + k].idx - begin;
-      s_bits[loc >> 5] = 0u;
+      group_sync(Ro::kBarN, Ro::NN);
+      for (int k = gtid; k < cnt; k += Ro::NN) {
+        const int loc = A.log[off + k].idx - (int)begin;
+        s_bits[loc >> 5] = 0u;
+      }
+      if (gtid == 0) tl_mark_any(A.tl, m, A.G, cta, 6);
     }
     __syncthreads();
     tl_mark(A.tl, m, A.G, cta, 2);

@@ -25,6 +25,8 @@ namespace {
 
 constexpr int kNT = 512;   // threads per CTA of the persistent kernels
 constexpr int kU = 4;      // neurons per thread in flight per round
+constexpr int kSplitF = 384;  // forward event-side threads per CTA
+constexpr int kSplitB = 256;  // reverse event-side threads per CTA
 
 struct DeviceGuard {
   int prev = -1;
@@ -57,7 +59,9 @@ struct eq_handle {
   const void* d = nullptr;
   const uint32_t* mask = nullptr;
   const void* amp = nullptr;
+  unsigned short* dcode = nullptr;   // per-edge delivery codes
   bool net_set = false, drive_set = false;
+  bool l2_set = false;
   size_t tsize = 4;
   // forward state
   void* I = nullptr;
@@ -166,6 +170,9 @@ cudaError_t ensure(eq_handle* h, void** p, size_t bytes) {
 }
 
 template <typename T>
+constexpr int P_words() { return Prec<T>::kSlotWords; }
+
+template <typename T>
 StepConsts<T> consts(const eq_handle* h) {
   const eq_config& c = h->cfg;
   StepConsts<T> k;
@@ -179,6 +186,8 @@ StepConsts<T> consts(const eq_handle* h) {
   k.k_m = (T)std::exp(-c.dt / c.tau_m);
   k.k_s = (T)std::exp(-c.dt / c.tau_syn);
   k.cc = c.exact_delivery ? (T)(c.tau_syn / (c.tau_m - c.tau_syn)) : (T)0;
+  k.inv_tau_m = (T)(1.0 / c.tau_m);
+  k.inv_tau_s = (T)(1.0 / c.tau_syn);
   k.scale = (T)std::ldexp(1.0, h->frac_bits);
   k.inv_scale = (T)std::ldexp(1.0, -h->frac_bits);
   k.divN = FastDiv((unsigned)h->cfg.n_neurons);
@@ -192,6 +201,7 @@ NetView<T> netview(const eq_handle* h) {
   n.col = h->col;
   n.w = (const T*)h->w;
   n.d = (const T*)h->d;
+  n.dcode = h->dcode;
   n.mask = h->mask;
   n.amp = (const T*)h->amp;
   n.words = (h->cfg.n_neurons + 31) / 32;
@@ -236,6 +246,12 @@ __global__ void k_net_stats(int N, const int64_t* rowptr, const int32_t* col, co
               (unsigned long long)__double2ll_rn(fabs((double)w[x]) * 1099511627776.0));
   }
   atomicMax(stats, (long long)hmax);
+}
+
+template <typename T>
+__global__ void k_dcode(const T* d, long long E, T dt, unsigned short* out) {
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < E; x += (long long)gridDim.x * blockDim.x)
+    out[x] = delivery_code(d[x], dt);
 }
 
 __global__ void k_max_ll(const long long* a, long long n, long long* out) {
@@ -413,6 +429,11 @@ __global__ void k_pending_bounded(const QEv<T>* q, const int4* meta, int kind, i
 
 // ------------------------------------------------------------ launches
 
+// reverse kernel dynamic smem: spiker bitmap + uint16 chunk position per owned neuron
+size_t bwd_smem(long long per) {
+  return (size_t)((per + 31) / 32) * sizeof(unsigned) + (size_t)((per + 1) / 2) * sizeof(unsigned);
+}
+
 int check_err(eq_handle* h, cudaStream_t s) {
   int e[4];
   EQ_CUDA(h, cudaMemcpyAsync(e, h->err_dev, sizeof e, cudaMemcpyDeviceToHost, s));
@@ -501,8 +522,28 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
                                            bargs, 0, s));
   } else {
     void* args[] = {&A};
-    EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_forward<T, kNT, kU>, dim3(h->G), dim3(kNT), args,
-                                           0, s));
+    if (h->cfg.kind == EQ_KIND_RING && !h->l2_set && getenv("EQ_L2_PERSIST")) {
+      // keep the two accumulator rows L2-resident (every event's red.add lands there)
+      int maxp = 0;
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+      size_t bytes = (size_t)2 * h->total * P_words<T>() * sizeof(long long);
+      size_t win = std::min<size_t>(bytes, (size_t)maxp);
+      if (win > 0) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, win);
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = h->acc;
+        v.accessPolicyWindow.num_bytes = win;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+        h->l2_set = true;
+      }
+    }
+    // warp split (event side / neuron side) measured at C3 x 16 trials:
+    // 384/128 balances the forward's sides (timeline, profiles/)
+    const void* kf = (const void*)k_forward<T, kNT, kU, kSplitF>;
+    EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, 0, s));
   }
   h->launches += 1;
   int rc = check_err(h, s);
@@ -552,10 +593,11 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   A.tl = (h->tl_b && A.m_run <= h->tl_steps) ? h->tl_b : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
-  size_t smem = (size_t)((h->per + 31) / 32) * sizeof(unsigned);
+  size_t smem = bwd_smem(h->per);
   void* args[] = {&A};
-  EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_backward<T, kNT, kU>, dim3(h->G), dim3(kNT), args,
-                                         smem, s));
+  const void* kb = (const void*)k_backward<T, kNT, kU, kSplitB>;
+  if (smem > 48 * 1024) EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  EQ_CUDA(h, cudaLaunchCooperativeKernel(kb, dim3(h->G), dim3(kNT), args, smem, s));
   h->launches += 1;
   if (gamp) {
     k_sum_trials<T><<<(N + 255) / 256, 256, 0, s>>>(h->gamp_bt, B, N, gamp);
@@ -571,11 +613,11 @@ int setup_geometry(eq_handle* h) {
   const void* kf;
   const void* kb;
   if (h->cfg.precision == 32) {
-    kf = (const void*)k_forward<float, kNT, kU>;
-    kb = (const void*)k_backward<float, kNT, kU>;
+    kf = (const void*)k_forward<float, kNT, kU, kSplitF>;
+    kb = (const void*)k_backward<float, kNT, kU, kSplitB>;
   } else {
-    kf = (const void*)k_forward<double, kNT, kU>;
-    kb = (const void*)k_backward<double, kNT, kU>;
+    kf = (const void*)k_forward<double, kNT, kU, kSplitF>;
+    kb = (const void*)k_backward<double, kNT, kU, kSplitB>;
   }
   EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf, kNT, 0));
   {
@@ -589,8 +631,8 @@ int setup_geometry(eq_handle* h) {
   for (; occ >= 1; --occ) {
     long long G = (long long)h->n_sm * occ;
     long long per = (h->total + G - 1) / G;
-    size_t smem = (size_t)((per + 31) / 32) * sizeof(unsigned);
-    if (smem > 200 * 1024) continue;
+    size_t smem = bwd_smem(per);
+    if (smem > 160 * 1024) continue;
     if (smem > 48 * 1024)
       EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, kb, kNT, smem));
@@ -895,6 +937,13 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   h->w = weight;
   h->d = delay;
   h->E = n_edges;
+  if (h->horizon > 0x7ffe) return fail(h, EQ_ERR_CONFIGURATION, "delay horizon beyond 32766 steps");
+  EQ_CUDA(h, ensure(h, (void**)&h->dcode, (size_t)n_edges * sizeof(unsigned short)));
+  if (c.precision == 32)
+    k_dcode<float><<<1184, 256, 0, s>>>((const float*)delay, n_edges, (float)c.dt, h->dcode);
+  else
+    k_dcode<double><<<1184, 256, 0, s>>>((const double*)delay, n_edges, c.dt, h->dcode);
+  h->launches += 1;
   // queue storage
   size_t words = c.kind == EQ_KIND_RING ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
   h->ring_words = words;

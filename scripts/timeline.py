@@ -18,15 +18,15 @@ from paper_2512_05906_b200.engine import Engine  # noqa: E402
 import bench  # noqa: E402
 
 
-ORDER = {"forward": [(0, "start"), (5, "deliver"), (6, "stage"), (1, "fan-out"), (4, "update"), (2, "clear+log"),
-                     (3, "barrier")],
-         "reverse": [(0, "start"), (4, "stage"), (5, "events"), (6, "reduce"), (1, "R-fanout"), (2, "R-neuron"),
-                     (3, "barrier")]}
+ORDER = {"forward": [(5, "deliver done"), (1, "fan-out done"), (4, "update done"), (6, "clear+log done"),
+                     (2, "both sides done"), (3, "barrier done")],
+         "reverse": [(4, "stage done"), (5, "events done"), (1, "R-fanout done"), (6, "R-neuron done"),
+                     (2, "both sides done"), (3, "barrier done")]}
 
 
 def report(tl, label):
-    """Per step: each mark minus the previous present mark (median over steps of
-    the max and the mean over CTAs), in time order."""
+    """Per step: each mark's offset from the step start (median over steps of
+    the max and the mean over CTAs)."""
     t = tl.astype(np.int64)
     ok = (t[:, :, 0] > 0) & (t[:, :, 3] > 0)
     steps = np.nonzero(ok.all(axis=1))[0]
@@ -34,17 +34,14 @@ def report(tl, label):
     step = np.abs(np.diff(t[:, :, 3].max(axis=1)))
     skew = t[:, :, 0].max(axis=1) - t[:, :, 0].min(axis=1)
     print(f"[{label}] steps={len(steps)}  step {np.median(step)/1e3:.2f} us  start-skew {np.median(skew)/1e3:.2f} us")
-    prev = t[:, :, 0]
-    for k, name in ORDER[label][1:]:
+    t0 = t[:, :, 0]
+    for k, name in ORDER[label]:
         mk = t[:, :, k]
-        if not (mk > 0).all():
-            good = (mk > 0).all(axis=1)
-            if good.sum() < 0.5 * len(good):
-                continue
-            mk = np.where(mk > 0, mk, prev)
-        d = mk - prev
-        print(f"   {name:10s} max {np.median(d.max(1))/1e3:8.2f}  mean {np.median(d.mean(1))/1e3:8.2f}")
-        prev = mk
+        good = mk > 0
+        if good.mean() < 0.5:
+            continue
+        d = np.where(good, mk - t0, 0)
+        print(f"   {name:16s} max {np.median(d.max(1))/1e3:8.2f}  mean {np.median(d.sum(1) / np.maximum(good.sum(1), 1))/1e3:8.2f}")
 
 
 def main():
