@@ -322,6 +322,10 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
         const int len = (int)(__ldg(F.net.rowptr + i + 1) - r0);
         s_r0[k] = r0;
         s_pre[k + 1] = len;
+        if (log_ok) {
+          F.log_r0[s_off + k0 + k] = r0;
+          F.log_len[s_off + k0 + k] = len;
+        }
         const int tb = b - b_first;
         if (tb < kTr) {
           atomicAdd(&s_ctr[tb][0], 1ULL);

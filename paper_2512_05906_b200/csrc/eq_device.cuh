@@ -135,11 +135,22 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 // loads (no L1 invalidation per poll) and take one acquire fence on exit.  No
 // seq_cst fences: MEMBAR.SC.GPU on 296 CTAs per step cost ~100 us here.  A 20 s
 // watchdog turns a wedged barrier into EQ_ERR_CUDA instead of a hung GPU.
-// publish_dst/src (optional): the last arriver copies *src to *dst before the
+// Two-level grid barrier for a cooperative (co-resident) launch: CTAs arrive
+// on a per-group counter (16 CTAs per group, own 128-byte line), the last of
+// each group arrives on the top counter, the last group releases a new
+// generation.  Arrivals are acq_rel atomics (cumulative over the CTA's writes
+// ordered before them by bar.sync); waiters spin with relaxed loads (no L1
+// invalidation per poll) and take one acquire fence on exit.  No seq_cst
+// fences (MEMBAR.SC.GPU on 296 CTAs per step cost ~100 us here).  A 20 s
+// watchdog turns a wedged barrier into EQ_ERR_CUDA instead of a hung GPU.
+// Layout of `bar`: [0] top count, [32] generation, [64 + 32*g] group counts.
+// publish_dst/src (optional): the final arriver copies *src to *dst before the
 // release, so every CTA sees a value that no CTA can change until the next
-// phase (used to publish the spike-log end of the finished step).
-// zero_u64 / zero_i32 (optional): reset by the last arriver (state consumed
-// by every CTA in the finished phase).
+// phase (used to publish the spike-log end of the finished step);
+// zero_u64 / zero_i32 (optional): reset by the final arriver.
+constexpr unsigned kBarGroup = 16;
+constexpr unsigned kBarWords = 64 + 32 * 256;   // up to 4096 CTAs
+
 __device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* err,
                                           long long* publish_dst = nullptr,
                                           const unsigned long long* publish_src = nullptr,
@@ -148,17 +159,26 @@ __device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* 
   __syncthreads();
   if (threadIdx.x == 0) {
     s_ok = 1;
-    unsigned* count = bar;
+    unsigned* top = bar;
     unsigned* gen = bar + 32;
+    const unsigned grp = blockIdx.x / kBarGroup;
+    const unsigned ngroups = (nblocks + kBarGroup - 1) / kBarGroup;
+    const unsigned members = min(kBarGroup, nblocks - grp * kBarGroup);
+    unsigned* gcount = bar + 64 + 32 * grp;
     unsigned g = ld_relaxed(gen);
-    unsigned prev = atom_add_acq_rel(count, 1u);
-    if (prev == nblocks - 1) {
-      if (publish_dst) *publish_dst = (long long)*(volatile const unsigned long long*)publish_src;
-      if (zero_u64) *(volatile unsigned long long*)zero_u64 = 0ULL;
-      if (zero_i32) *(volatile int*)zero_i32 = 0;
-      st_relaxed(count, 0u);
-      st_release(gen, g + 1);
-    } else {
+    bool released = false;
+    if (atom_add_acq_rel(gcount, 1u) == members - 1) {
+      st_relaxed(gcount, 0u);
+      if (atom_add_acq_rel(top, 1u) == ngroups - 1) {
+        if (publish_dst) *publish_dst = (long long)*(volatile const unsigned long long*)publish_src;
+        if (zero_u64) *(volatile unsigned long long*)zero_u64 = 0ULL;
+        if (zero_i32) *(volatile int*)zero_i32 = 0;
+        st_relaxed(top, 0u);
+        st_release(gen, g + 1);
+        released = true;
+      }
+    }
+    if (!released) {
       unsigned long long t0 = 0;
       int spins = 0;
       while (ld_relaxed(gen) == g) {

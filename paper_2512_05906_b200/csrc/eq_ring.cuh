@@ -57,6 +57,8 @@ struct FwdArgs {
   long long* ring;    // fp32: [B][R][N]; fp64: [B][R][N][2]
   SpikeRec<T>* scratch;  // [G][per] per-CTA spill area for the step's spikes
   SpikeRec<T>* log;
+  long long* log_r0;     // CSR row start of each logged spike's source (written by its owner)
+  int* log_len;          // its row length
   long long log_cap;
   unsigned long long* log_count;
   long long* chunk_off;  // [m][G]
@@ -198,17 +200,14 @@ __device__ __forceinline__ void group_scan(int* pre, int n, int gtid) {
 // exclusive prefix of their row lengths (s_pre[nb] = events in the batch).
 // Executed by one warp group (gtid in [0, gsize), named barrier bar_id).
 template <typename T>
-__device__ __forceinline__ void stage_spikes(const SpikeRec<T>* log, long long k0, int nb, int N, FastDiv divN,
-                                             const int64_t* rowptr, SpikeRec<T>* s_rec, long long* s_r0,
-                                             int* s_pre, int gtid, int gsize, int bar_id) {
+__device__ __forceinline__ void stage_spikes(const SpikeRec<T>* log, const long long* log_r0, const int* log_len,
+                                             long long k0, int nb, SpikeRec<T>* s_rec, long long* s_r0, int* s_pre,
+                                             int gtid, int gsize, int bar_id) {
   group_sync(bar_id, gsize);
   for (int k = gtid; k < nb; k += gsize) {
-    const SpikeRec<T> rec = log[k0 + k];
-    s_rec[k] = rec;
-    const int i = rec.idx - divN.div(rec.idx) * N;
-    const long long r0 = __ldg(rowptr + i);
-    s_r0[k] = r0;
-    s_pre[k + 1] = (int)(__ldg(rowptr + i + 1) - r0);
+    s_rec[k] = log[k0 + k];
+    s_r0[k] = log_r0[k0 + k];        // row start/length stored by the owner: no dependent rowptr load
+    s_pre[k + 1] = log_len[k0 + k];
   }
   group_sync(bar_id, gsize);
   group_scan(s_pre, nb, gtid);
@@ -326,7 +325,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         long long* bp_cta = A.bk_pay + (size_t)cta * A.NB * A.cap_b * P::kSlotWords;
         for (long long k0 = s0; k0 < s1; k0 += kCap) {
           const int nb = (int)(s1 - k0 < kCap ? s1 - k0 : kCap);
-          stage_spikes<T>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_spk, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
+          stage_spikes<T>(A.log, A.log_r0, A.log_len, k0, nb, s_spk, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
           const int total = s_pre[nb];
           constexpr int EV = 4;
           const int me_bin = me % A.NB;
@@ -604,11 +603,15 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
       const bool log_ok = s_off + nspk <= A.log_cap;
       for (int k = gtid; k < nspk; k += Ro::NN) {
         const SpikeRec<T> rec = k < kCapN ? s_own[k] : spill[k - kCapN];
-        if (log_ok) A.log[s_off + k] = rec;
         const int b = c.divN.div(rec.idx);
         const int i = rec.idx - b * A.N;
-        const unsigned long long len =
-            (unsigned long long)(__ldg(A.net.rowptr + i + 1) - __ldg(A.net.rowptr + i));
+        const long long r0 = __ldg(A.net.rowptr + i);
+        const unsigned long long len = (unsigned long long)(__ldg(A.net.rowptr + i + 1) - r0);
+        if (log_ok) {
+          A.log[s_off + k] = rec;
+          A.log_r0[s_off + k] = r0;
+          A.log_len[s_off + k] = (int)len;
+        }
         const int tb = b - b_first;
         if (tb < kTr) {
           atomicAdd(&s_ctr[tb][0], 1ULL);
@@ -665,6 +668,8 @@ struct BwdArgs {
   double* gd;
   double* gamp_bt;             // [B][N] or null
   const SpikeRec<T>* log;
+  const long long* log_r0;
+  const int* log_len;
   T* lt_log;                   // dL/dt_spk per log record
   const long long* chunk_off;
   const int* chunk_cnt;
@@ -718,7 +723,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
         const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
         for (long long k0 = s0; k0 < s1; k0 += kCapB) {
           const int nb = (int)(s1 - k0 < kCapB ? s1 - k0 : kCapB);
-          stage_spikes<T>(A.log, k0, nb, A.N, c.divN, A.net.rowptr, s_rec, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
+          stage_spikes<T>(A.log, A.log_r0, A.log_len, k0, nb, s_rec, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
           for (int k = gtid; k < nb; k += Ro::NF) s_lt[k] = (T)0;
           group_sync(Ro::kBarF, Ro::NF);
           if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 4);

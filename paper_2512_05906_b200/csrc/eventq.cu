@@ -79,6 +79,8 @@ struct eq_handle {
   int* ring_dirty = nullptr;
   void* scratch = nullptr;
   void* log = nullptr;
+  long long* log_r0 = nullptr;
+  int* log_len = nullptr;
   long long log_cap = 0;
   unsigned long long* log_count = nullptr;
   long long* chunk_off = nullptr;
@@ -487,6 +489,8 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
   A.ring_dirty = h->ring_dirty;
   A.scratch = (SpikeRec<T>*)h->scratch;
   A.log = (SpikeRec<T>*)h->log;
+  A.log_r0 = h->log_r0;
+  A.log_len = h->log_len;
   A.log_cap = h->log_cap;
   A.log_count = h->log_count;
   A.chunk_off = h->chunk_off;
@@ -564,7 +568,7 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   EQ_CUDA(h, cudaMemsetAsync(gw, 0, h->E * sizeof(double), s));
   EQ_CUDA(h, cudaMemsetAsync(gd, 0, h->E * sizeof(double), s));
   if (gamp) EQ_CUDA(h, cudaMemsetAsync(h->gamp_bt, 0, total * sizeof(double), s));
-  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 64 * sizeof(unsigned), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
   BwdArgs<T> A;
   A.N = N;
   A.B = B;
@@ -583,6 +587,8 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   A.gd = gd;
   A.gamp_bt = gamp ? h->gamp_bt : nullptr;
   A.log = (const SpikeRec<T>*)h->log;
+  A.log_r0 = h->log_r0;
+  A.log_len = h->log_len;
   A.lt_log = (T*)h->lt_log;
   A.chunk_off = h->chunk_off;
   A.chunk_cnt = h->chunk_cnt;
@@ -813,7 +819,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   EQ_CUDA(h, alloc(h, (void**)&h->gamp_bt, h->total * sizeof(double)));
   EQ_CUDA(h, alloc(h, (void**)&h->counters, (size_t)c.n_trials * 3 * sizeof(long long)));
   EQ_CUDA(h, alloc(h, (void**)&h->err_dev, 4 * sizeof(int)));
-  EQ_CUDA(h, alloc(h, (void**)&h->bar, 64 * sizeof(unsigned)));
+  EQ_CUDA(h, alloc(h, (void**)&h->bar, kBarWords * sizeof(unsigned)));
   EQ_CUDA(h, alloc(h, (void**)&h->log_count, sizeof(unsigned long long)));
   const size_t rec = c.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
   EQ_CUDA(h, alloc(h, &h->scratch, (size_t)h->G * h->per * rec));
@@ -821,6 +827,8 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
                                    : std::max<long long>(1LL << 20, h->total * (long long)c.t_steps / 32);
   h->log_cap = cap;
   EQ_CUDA(h, alloc(h, &h->log, (size_t)cap * rec));
+  EQ_CUDA(h, alloc(h, (void**)&h->log_r0, (size_t)cap * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, (void**)&h->log_len, (size_t)cap * sizeof(int)));
   EQ_CUDA(h, alloc(h, &h->lt_log, (size_t)cap * T));
   rc = ensure_chunks(h, c.t_steps);
   if (rc) return rc;
@@ -1006,7 +1014,7 @@ int eq_reset(eq_handle* h, void* stream) {
   EQ_CUDA(h, cudaMemsetAsync(h->refr, 0, h->total * sizeof(int32_t), s));
   EQ_CUDA(h, cudaMemsetAsync(h->counters, 0, (size_t)h->cfg.n_trials * 3 * sizeof(long long), s));
   EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, 4 * sizeof(int), s));
-  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 64 * sizeof(unsigned), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
   EQ_CUDA(h, cudaMemsetAsync(h->log_count, 0, sizeof(unsigned long long), s));
   EQ_CUDA(h, cudaMemsetAsync(h->step_start, 0, sizeof(long long), s));
   if (h->bounded) {
@@ -1030,7 +1038,7 @@ int eq_run(eq_handle* h, int32_t n_steps, void* v_trace, void* stream) {
   int rc = ensure_chunks(h, h->steps_done + n_steps);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, 64 * sizeof(unsigned), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
   if (h->cfg.precision == 32) return launch_forward<float>(h, n_steps, v_trace, s);
   return launch_forward<double>(h, n_steps, v_trace, s);
 }
