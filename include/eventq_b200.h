@@ -98,11 +98,16 @@ int eq_set_drive(eq_handle* h, const uint32_t* mask, const void* amplitude, void
 int eq_reset(eq_handle* h, void* stream);
 
 /* Advance n_steps steps from the current step.  v_trace (optional, device,
- * float|double[n_steps][n_trials][n]) receives the membrane after each step. */
+ * float|double[n_steps][n_trials][n]) receives the membrane after each step.
+ * n_steps = 0 only delivers spikes imported at this step into the queues
+ * (partitioned networks, after the last window). */
 int eq_run(eq_handle* h, int32_t n_steps, void* v_trace, void* stream);
 
 /* eq_reset + eq_run(t_steps) + copy final state: v_out/i_out float|double[n_trials][n]. */
 int eq_forward(eq_handle* h, void* v_out, void* i_out, void* v_trace, void* stream);
+
+/* Copy the current membrane / synaptic current, float|double[n_trials][n] (device; either may be NULL). */
+int eq_get_state(eq_handle* h, void* v_out, void* i_out, void* stream);
 
 /* Reverse mode over the steps run since the last reset.  v_bar/i_bar: cotangents of
  * the final membrane / synaptic current, float|double[n_trials][n] (i_bar may be
@@ -110,6 +115,48 @@ int eq_forward(eq_handle* h, void* v_out, void* i_out, void* v_trace, void* stre
  * grad_amp[n] summed over trials. */
 int eq_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* grad_w, double* grad_d,
                 double* grad_amp, void* stream);
+
+/* The same reverse pass in windows, for partitioned networks: eq_backward_begin
+ * sets the cotangents and outputs, then each eq_backward_window(m_lo) runs the
+ * reverse phases from the current cursor (initially the run length) down to
+ * m_lo.  eq_backward == begin + window(0). */
+int eq_backward_begin(eq_handle* h, const void* v_bar, const void* i_bar, double* grad_w, double* grad_d,
+                      double* grad_amp, void* stream);
+int eq_backward_window(eq_handle* h, int32_t m_lo, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Partitioned single network (BASELINE config 5; no reference
+ * counterpart — the reference has no sharding).  Each handle owns the
+ * contiguous neuron range [src_offset, src_offset + n_neurons) of an
+ * n_global-neuron network: its CSR (eq_set_network) has n_global rows (every
+ * source) whose columns are LOCAL target indices (only edges into the owned
+ * range).  Steps run in exchange windows of W <= D_min steps (D_min = the
+ * smallest floor(d/dt) over all edges): after eq_run(W) a partition
+ * exports its window's spikes, every partition imports the others' (in any
+ * fixed order) before its next eq_run, which fans them out in its first
+ * phase.  An event emitted at step m is due no earlier than m + 1 + D_min
+ * (jumps.py:90-96), so the window never delivers late (checked on device:
+ * CausalityError).  Results equal the unpartitioned network's bitwise when all
+ * partitions use the same fraction bits (eq_set_frac_bits with the minimum). */
+typedef struct eq_spike_f32 { int32_t src, trial, step; float t; } eq_spike_f32;
+typedef struct eq_spike_f64 { int32_t src, trial, step, pad; double t; } eq_spike_f64;
+/* Ring kind only; call before eq_set_network. */
+int eq_set_partition(eq_handle* h, int32_t n_global, int32_t src_offset);
+/* Lower the fixed-point fraction bits to a common value (<= eq_frac_bits). */
+int eq_set_frac_bits(eq_handle* h, int32_t frac_bits);
+/* Own spikes of steps [step_lo, step_hi) as eq_spike_f32|f64 (device `out`, may
+ * be NULL to query *n_out, which is written on the host). */
+int eq_export_spikes(eq_handle* h, int32_t step_lo, int32_t step_hi, void* out, int64_t* n_out, void* stream);
+/* Other partitions' spikes for the next eq_run (device records). */
+int eq_import_spikes(eq_handle* h, const void* recs, int64_t n, void* stream);
+/* Reverse: after eq_backward_window(m_lo), the partial dL/dt_spk over this
+ * partition's edges of each spike imported before the forward launch that
+ * started at m_lo (same order as imported; float|double, device). */
+int eq_get_import_adjoints(eq_handle* h, int32_t start_step, void* out, void* stream);
+/* Add other partitions' partial dL/dt_spk to this partition's spikes of the
+ * export window starting at step_lo (same order as exported), before the
+ * reverse window that contains those steps. */
+int eq_add_spike_adjoints(eq_handle* h, int32_t step_lo, const void* vals, int64_t n, void* stream);
 
 /* Host-side queries (synchronise the stream). */
 int eq_counters(eq_handle* h, int64_t* out /* [n_trials][3] spikes, events, drops */, void* stream);

@@ -53,6 +53,15 @@ def lib() -> ctypes.CDLL:
         "eq_run": (ctypes.c_int, [H, i32, vp, vp]),
         "eq_forward": (ctypes.c_int, [H, vp, vp, vp, vp]),
         "eq_backward": (ctypes.c_int, [H, vp, vp, vp, vp, vp, vp]),
+        "eq_get_state": (ctypes.c_int, [H, vp, vp, vp]),
+        "eq_backward_begin": (ctypes.c_int, [H, vp, vp, vp, vp, vp, vp]),
+        "eq_backward_window": (ctypes.c_int, [H, i32, vp]),
+        "eq_set_partition": (ctypes.c_int, [H, i32, i32]),
+        "eq_set_frac_bits": (ctypes.c_int, [H, i32]),
+        "eq_export_spikes": (ctypes.c_int, [H, i32, i32, vp, ctypes.POINTER(i64), vp]),
+        "eq_import_spikes": (ctypes.c_int, [H, vp, i64, vp]),
+        "eq_get_import_adjoints": (ctypes.c_int, [H, i32, vp, vp]),
+        "eq_add_spike_adjoints": (ctypes.c_int, [H, i32, vp, i64, vp]),
         "eq_counters": (ctypes.c_int, [H, vp, vp]),
         "eq_spike_count": (i64, [H, vp]),
         "eq_get_spikes": (ctypes.c_int, [H, vp, vp, vp, vp, vp]),
@@ -81,7 +90,9 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive",
-            "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_counters", "eq_spike_count",
+            "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_get_state", "eq_backward_begin", "eq_backward_window",
+            "eq_set_partition", "eq_set_frac_bits", "eq_export_spikes", "eq_import_spikes",
+            "eq_get_import_adjoints", "eq_add_spike_adjoints", "eq_counters", "eq_spike_count",
             "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",
             "eq_launch_count", "eq_debug_timeline", "eq_queues_create", "eq_queues_destroy",
             "eq_queues_last_error", "eq_queues_capacity", "eq_queues_now", "eq_queues_enqueue", "eq_queues_pop",

@@ -78,6 +78,14 @@ struct FwdArgs {
   long long cap_b;
   int NB;
   int* ring_dirty;       // [R] a bucket overflowed into ring row r
+  // partitioned network (eq_set_partition): owned neuron j is CSR row
+  // src_off + j; spikes imported from other partitions (emitted in the
+  // previous exchange window) are fanned out in the launch's first phase
+  int src_off;
+  const SpikeRec<T>* imp;    // idx = trial*N (flat base of the trial), a = (T)emit step
+  const long long* imp_r0;
+  const int* imp_len;
+  long long imp_n;
 };
 
 template <int NT, typename T = float>
@@ -226,6 +234,147 @@ struct Roles {
   static constexpr int kBarF = 1, kBarN = 2;
 };
 
+// Fan-out (network.py:583-611) of log records [s0, s1): the CTA's share of
+// step m-1's own spikes (kImp = false) or, in a launch's first phase, of the
+// spikes imported from other partitions (kImp = true: per-spike emit steps in
+// rec.a, flat trial base in rec.idx).  An event due at m+1 goes straight into
+// acc[(m+1)&1]; a later one is appended to this CTA's bucket of its delivery
+// step (rank from a shared-memory counter).  No read-modify-write touches
+// DRAM; a full bucket spills into the DRAM ring row (flagged), never losing
+// events.  Executed by the event-side warp group.
+template <typename T, int NT, int NF, bool kImp>
+__device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, const int cta, const int gtid,
+                                           const long long s0, const long long s1, SpikeRec<T>* s_spk,
+                                           long long* s_r0, int* s_pre, int* s_bin) {
+  typedef Prec<T> P;
+  typedef Roles<NT, NF> Ro;
+  constexpr int kCap = FwdShared<NT, T>::kCap;
+  const StepConsts<T>& c = A.c;
+  const SpikeRec<T>* lg = kImp ? A.imp : A.log;
+  const long long* lr0 = kImp ? A.imp_r0 : A.log_r0;
+  const int* llen = kImp ? A.imp_len : A.log_len;
+  const int me_fixed = m - 1;
+  long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
+  int* bt_cta = A.bk_tgt + (size_t)cta * A.NB * A.cap_b;
+  long long* bp_cta = A.bk_pay + (size_t)cta * A.NB * A.cap_b * P::kSlotWords;
+  const int me_bin = kImp ? 0 : me_fixed % A.NB;
+  for (long long k0 = s0; k0 < s1; k0 += kCap) {
+    const int nb = (int)(s1 - k0 < kCap ? s1 - k0 : kCap);
+    stage_spikes<T>(lg, lr0, llen, k0, nb, s_spk, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
+    const int total = s_pre[nb];
+    if (kImp) {                                           // imported: count their events here
+      for (int k = gtid; k < nb; k += Ro::NF) {
+        const int b = c.divN.div(s_spk[k].idx);
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1),
+                  (unsigned long long)(s_pre[k + 1] - s_pre[k]));
+      }
+    }
+    constexpr int EV = 4;
+    for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
+      int jj[EV], kk[EV];
+      T ww[EV], dd[EV];
+      unsigned short cc[EV];
+#pragma unroll
+      for (int e = 0; e < EV; ++e) {
+        const int f = f0 + e * Ro::NF;
+        kk[e] = -1;
+        if (f < total) {
+          const int k = find_row(s_pre, nb, f);
+          const long long x = s_r0[k] + (f - s_pre[k]);
+          kk[e] = k;
+          jj[e] = __ldcs(A.net.col + x);      // streamed once per event: evict-first
+          ww[e] = __ldcs(A.net.w + x);
+          dd[e] = __ldcs(A.net.d + x);
+          cc[e] = __ldcs(A.net.dcode + x);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < EV; ++e) {
+        if (kk[e] < 0) continue;
+        const SpikeRec<T> rec = s_spk[kk[e]];
+        const int b = c.divN.div(rec.idx);
+        const int me = kImp ? (int)rec.a : me_fixed;
+        const T w = ww[e], d = dd[e];
+        const T t_post = rec.t + d;                              // :588
+        const int ds = delivery_step_coded(t_post, cc[e], c.dt, me);  // jumps.py:96
+        T ws, wm;
+        if (A.exact) {
+          const T phi = (T)ds * c.dt - t_post;              // :599
+          ws = w * eq_exp_t(-phi * c.inv_tau_s);            // :601 (x 1/tau)
+          wm = w * eq_exp_t(-phi * c.inv_tau_m);            // :606
+        } else {
+          ws = w;
+          wm = (T)0;
+        }
+        const int tgt = b * A.N + jj[e];                    // flat target
+        const long long q1 = P::q(ws, c.scale);
+        const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
+        if (ds == m + 1) {
+          if (P::kSlotWords == 1) {
+            red_add(accn + tgt, pack2(q1, q2));
+          } else {
+            red_add(accn + 2 * (size_t)tgt, q1);
+            red_add(accn + 2 * (size_t)tgt + 1, q2);
+          }
+          continue;
+        }
+        int bn;
+        if (!kImp) {
+          bn = me_bin + (ds - me);                          // ds % NB, ds - me in [2, H]
+          if (bn >= A.NB) bn -= A.NB;
+        } else {
+          if (ds <= m) {                                    // exchange window longer than D_min
+            raise_error(A.err, EQ_ERR_CAUSALITY, m, b, jj[e]);
+            continue;
+          }
+          bn = ds % A.NB;
+        }
+        const int pos = atomicAdd(&s_bin[bn], 1);
+        if (pos < A.cap_b) {
+          const size_t o = (size_t)bn * A.cap_b + pos;
+          __stcs(bt_cta + o, tgt);                          // read once, ~H/2 steps later
+          if (P::kSlotWords == 1) {
+            __stcs(bp_cta + o, pack2(q1, q2));
+          } else {
+            __stcs(bp_cta + 2 * o, q1);
+            __stcs(bp_cta + 2 * o + 1, q2);
+          }
+        } else {                                            // bucket full: DRAM ring row
+          const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
+          if (P::kSlotWords == 1) {
+            red_add(A.ring + so, pack2(q1, q2));
+          } else {
+            red_add(A.ring + 2 * so, q1);
+            red_add(A.ring + 2 * so + 1, q2);
+          }
+          if (A.ring_dirty[ds % A.R] == 0) atomicExch(A.ring_dirty + ds % A.R, 1);
+        }
+      }
+    }
+  }
+}
+
+// Spikes imported from other partitions, fanned out by a plain launch just
+// before the persistent kernel's first phase m0 (stream-ordered): the same
+// per-CTA buckets (fill levels round-trip through bk_cnt) and acc[(m0+1)&1]
+// for events due at m0+1.  Kept out of the persistent kernel so its register
+// allocation is that of the own-spike path alone.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) k_import_fanout(FwdArgs<T> A) {
+  constexpr int kCap = FwdShared<NT, T>::kCap;
+  __shared__ SpikeRec<T> s_spk[kCap];
+  __shared__ long long s_r0[kCap];
+  __shared__ int s_pre[kCap + 1];
+  __shared__ int s_bin[FwdShared<NT>::kBins];
+  const int cta = blockIdx.x;
+  for (int k = threadIdx.x; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
+  __syncthreads();
+  fwd_fanout<T, NT, NT, true>(A, A.m0, cta, threadIdx.x, A.imp_n * cta / A.G, A.imp_n * (cta + 1) / A.G, s_spk,
+                              s_r0, s_pre, s_bin);
+  __syncthreads();
+  for (int k = threadIdx.x; k < A.NB; k += NT) A.bk_cnt[(size_t)cta * A.NB + k] = s_bin[k];
+}
+
 template <typename T, int NT, int U, int NF = NT / 2>
 __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   typedef Prec<T> P;
@@ -311,96 +460,12 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         if (gtid == 0) s_bin[bin] = 0;
       }
       if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 5);
-      // ---------------- (a2) fan-out of step m-1 (network.py:583-611).  An
-      // event due at m+1 goes straight into acc[(m+1)&1]; a later one is
-      // appended to this CTA's bucket of its delivery step (rank from a
-      // shared-memory counter).  No read-modify-write touches DRAM; a full
-      // bucket spills into the DRAM ring row (flagged), never losing events.
-      if (m > A.m0 && A.kind == EQ_KIND_RING) {
+      // ---------------- (a2) fan-out of step m-1 (and imported spikes): fwd_fanout
+      if (A.kind == EQ_KIND_RING && m > A.m0) {
         const int me = m - 1;                          // emitting step
         const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
-        const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
-        long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
-        int* bt_cta = A.bk_tgt + (size_t)cta * A.NB * A.cap_b;
-        long long* bp_cta = A.bk_pay + (size_t)cta * A.NB * A.cap_b * P::kSlotWords;
-        for (long long k0 = s0; k0 < s1; k0 += kCap) {
-          const int nb = (int)(s1 - k0 < kCap ? s1 - k0 : kCap);
-          stage_spikes<T>(A.log, A.log_r0, A.log_len, k0, nb, s_spk, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
-          const int total = s_pre[nb];
-          constexpr int EV = 4;
-          const int me_bin = me % A.NB;
-          for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
-            int jj[EV], kk[EV];
-            T ww[EV], dd[EV];
-            unsigned short cc[EV];
-#pragma unroll
-            for (int e = 0; e < EV; ++e) {
-              const int f = f0 + e * Ro::NF;
-              kk[e] = -1;
-              if (f < total) {
-                const int k = find_row(s_pre, nb, f);
-                const long long x = s_r0[k] + (f - s_pre[k]);
-                kk[e] = k;
-                jj[e] = __ldcs(A.net.col + x);      // streamed once per event: evict-first
-                ww[e] = __ldcs(A.net.w + x);
-                dd[e] = __ldcs(A.net.d + x);
-                cc[e] = __ldcs(A.net.dcode + x);
-              }
-            }
-#pragma unroll
-            for (int e = 0; e < EV; ++e) {
-              if (kk[e] < 0) continue;
-              const SpikeRec<T> rec = s_spk[kk[e]];
-              const int b = c.divN.div(rec.idx);
-              const T w = ww[e], d = dd[e];
-              const T t_post = rec.t + d;                              // :588
-              const int ds = delivery_step_coded(t_post, cc[e], c.dt, me);  // jumps.py:96
-              T ws, wm;
-              if (A.exact) {
-                const T phi = (T)ds * c.dt - t_post;              // :599
-                ws = w * eq_exp_t(-phi * c.inv_tau_s);            // :601 (x 1/tau)
-                wm = w * eq_exp_t(-phi * c.inv_tau_m);            // :606
-              } else {
-                ws = w;
-                wm = (T)0;
-              }
-              const int tgt = b * A.N + jj[e];                    // flat target
-              const long long q1 = P::q(ws, c.scale);
-              const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
-              if (ds == m + 1) {
-                if (P::kSlotWords == 1) {
-                  red_add(accn + tgt, pack2(q1, q2));
-                } else {
-                  red_add(accn + 2 * (size_t)tgt, q1);
-                  red_add(accn + 2 * (size_t)tgt + 1, q2);
-                }
-                continue;
-              }
-              int bn = me_bin + (ds - me);                        // ds % NB, ds - me in [2, H]
-              if (bn >= A.NB) bn -= A.NB;
-              const int pos = atomicAdd(&s_bin[bn], 1);
-              if (pos < A.cap_b) {
-                const size_t o = (size_t)bn * A.cap_b + pos;
-                __stcs(bt_cta + o, tgt);                          // read once, ~H/2 steps later
-                if (P::kSlotWords == 1) {
-                  __stcs(bp_cta + o, pack2(q1, q2));
-                } else {
-                  __stcs(bp_cta + 2 * o, q1);
-                  __stcs(bp_cta + 2 * o + 1, q2);
-                }
-              } else {                                            // bucket full: DRAM ring row
-                const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
-                if (P::kSlotWords == 1) {
-                  red_add(A.ring + so, pack2(q1, q2));
-                } else {
-                  red_add(A.ring + 2 * so, q1);
-                  red_add(A.ring + 2 * so + 1, q2);
-                }
-                if (A.ring_dirty[ds % A.R] == 0) atomicExch(A.ring_dirty + ds % A.R, 1);
-              }
-            }
-          }
-        }
+        fwd_fanout<T, NT, NF, false>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G, s_spk, s_r0,
+                                     s_pre, s_bin);
       }
       if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 1);
     } else if (m < A.m1) {
@@ -605,8 +670,8 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         const SpikeRec<T> rec = k < kCapN ? s_own[k] : spill[k - kCapN];
         const int b = c.divN.div(rec.idx);
         const int i = rec.idx - b * A.N;
-        const long long r0 = __ldg(A.net.rowptr + i);
-        const unsigned long long len = (unsigned long long)(__ldg(A.net.rowptr + i + 1) - r0);
+        const long long r0 = __ldg(A.net.rowptr + A.src_off + i);
+        const unsigned long long len = (unsigned long long)(__ldg(A.net.rowptr + A.src_off + i + 1) - r0);
         if (log_ok) {
           A.log[s_off + k] = rec;
           A.log_r0[s_off + k] = r0;
@@ -657,7 +722,8 @@ template <typename T>
 struct BwdArgs {
   int N, B, G;
   long long total, per;
-  int m_run;          // steps simulated since reset (reverse walks m_run-1 .. 0)
+  int m_run;          // steps simulated since reset (the reverse pass walks m_run-1 .. 0)
+  int m_hi, m_lo;     // this launch's phases: m_hi-1 .. m_lo (one exchange window, or all)
   int R, refractory;
   StepConsts<T> c;
   NetView<T> net;
@@ -677,17 +743,128 @@ struct BwdArgs {
   const long long* ev_base;     // bounded kinds: flat event id of each log record's first edge
   const unsigned* drop_bits;    // bounded kinds: dropped events (contribute nothing); null for ring
   int no_events;                // donothing: every event was dropped
+  // partitioned network: dL/dt_spk contributions of the other partitions'
+  // edges to this partition's spikes (added at R-neuron), and the imported
+  // spikes whose partial dL/dt_spk over this partition's edges the last phase
+  // computes (R-fanout of the import block of forward launch m_lo)
+  const T* lt_rem;              // [log] or null
+  const SpikeRec<T>* imp;
+  const long long* imp_r0;
+  const int* imp_len;
+  long long imp_n;
+  T* imp_lt;
   unsigned long long* tl;  // debug timeline [m][G][4] or null
   int* err;
   unsigned* bar;
 };
 
+template <typename T>
+struct BwdShared {
+  static constexpr int kCapB = sizeof(T) == 4 ? 512 : 256;   // spikes per batch
+  static constexpr int kEv = sizeof(T) == 4 ? 4096 : 2048;    // events per reduction window
+};
+
+// R-fanout of log records [s0, s1): the CTA's share of step
+// m-1's own spikes (kImp = false, dL/dt_spk into lt_log) or of the spikes
+// imported before forward launch m_lo (kImp = true, partial dL/dt_spk over
+// this partition's edges into imp_lt).  dL/dt_spk of a spike is the SEQUENTIAL
+// sum of its edges' g_tp in row order (zeros for events never popped or
+// dropped), staged through s_gtp in windows of kEv events; the oracle sums in
+// the same order.  Executed by the event-side warp group.
+template <typename T, int NT, int NF, bool kImp, int kCapB, int kEv>
+__device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, const int cta, const int gtid,
+                                            const long long s0, const long long s1, SpikeRec<T>* s_rec,
+                                            long long* s_r0, int* s_pre, T* s_lt, T* s_gtp) {
+  typedef typename Prec<T>::T2 T2;
+  typedef Roles<NT, NF> Ro;
+  const StepConsts<T>& c = A.c;
+  const SpikeRec<T>* lg = kImp ? A.imp : A.log;
+  const long long* lr0 = kImp ? A.imp_r0 : A.log_r0;
+  const int* llen = kImp ? A.imp_len : A.log_len;
+  T* lt_out = kImp ? A.imp_lt : A.lt_log;
+  const int me_fixed = m - 1;
+  for (long long k0 = s0; k0 < s1; k0 += kCapB) {
+    const int nb = (int)(s1 - k0 < kCapB ? s1 - k0 : kCapB);
+    stage_spikes<T>(lg, lr0, llen, k0, nb, s_rec, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
+    for (int k = gtid; k < nb; k += Ro::NF) s_lt[k] = (T)0;
+    group_sync(Ro::kBarF, Ro::NF);
+    if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 4);
+    const int total = s_pre[nb];
+    for (int w0 = 0; w0 < total; w0 += kEv) {
+      const int wend = total - w0 < kEv ? total : w0 + kEv;
+      constexpr int EV = 4;
+      for (int f0 = w0 + gtid; f0 < wend; f0 += EV * Ro::NF) {
+        int jj[EV], kk[EV];
+        long long xx[EV];
+        T ww[EV], dd[EV];
+        unsigned short cc[EV];
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          const int f = f0 + e * Ro::NF;
+          kk[e] = -1;
+          if (f < wend) {
+            const int k = find_row(s_pre, nb, f);
+            const long long x = s_r0[k] + (f - s_pre[k]);
+            kk[e] = k;
+            xx[e] = x;
+            jj[e] = __ldcs(A.net.col + x);
+            ww[e] = __ldcs(A.net.w + x);
+            dd[e] = __ldcs(A.net.d + x);
+            cc[e] = __ldcs(A.net.dcode + x);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          if (kk[e] < 0) continue;
+          const int f = f0 + e * Ro::NF;
+          const SpikeRec<T> rec = s_rec[kk[e]];
+          const int b = c.divN.div(rec.idx);
+          const int me = kImp ? (int)rec.a : me_fixed;
+          const T w = ww[e], d = dd[e];
+          const T t_post = rec.t + d;
+          const int st = delivery_step_coded(t_post, cc[e], c.dt, me);
+          T g_tp = (T)0;
+          bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
+          if (live && A.drop_bits) {                       // dropped by a bounded queue
+            const long long id = A.ev_base[k0 + kk[e]] + (f - s_pre[kk[e]]);
+            live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
+          }
+          if (live) {
+            const T phi = (T)st * c.dt - t_post;
+            const T es = eq_exp_t(-phi * c.inv_tau_s);
+            const T em = eq_exp_t(-phi * c.inv_tau_m);
+            const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
+            const T g_w = es * L.x + em * L.y;
+            g_tp = w * (es * L.x * c.inv_tau_s + em * L.y * c.inv_tau_m);
+            red_add_f64(A.gw + xx[e], (double)g_w);
+            red_add_f64(A.gd + xx[e], (double)g_tp);
+          }
+          s_gtp[f - w0] = g_tp;
+        }
+      }
+      group_sync(Ro::kBarF, Ro::NF);
+      if (k0 == s0 && w0 == 0) tl_mark(A.tl, m, A.G, cta, 5);
+      const int ka = find_row(s_pre, nb, w0);
+      const int kb = find_row(s_pre, nb, wend - 1);
+      for (int k = ka + gtid; k <= kb; k += Ro::NF) {
+        const int lo = s_pre[k] > w0 ? s_pre[k] : w0;
+        const int hi = s_pre[k + 1] < wend ? s_pre[k + 1] : wend;
+        T acc = s_lt[k];
+        for (int q = lo; q < hi; ++q) acc = acc + s_gtp[q - w0];
+        s_lt[k] = acc;
+      }
+      group_sync(Ro::kBarF, Ro::NF);
+    }
+    for (int k = gtid; k < nb; k += Ro::NF) lt_out[k0 + k] = s_lt[k];
+  }
+}
+
 template <typename T, int NT, int U, int NF = NT / 2>
 __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
   typedef typename Prec<T>::T2 T2;
   typedef Roles<NT, NF> Ro;
-  constexpr int kCapB = sizeof(T) == 4 ? 512 : 256;   // spikes per batch
-  constexpr int kEv = sizeof(T) == 4 ? 4096 : 2048;    // events per reduction window
+  constexpr int kCapB = BwdShared<T>::kCapB;
+  constexpr int kEv = BwdShared<T>::kEv;
   __shared__ SpikeRec<T> s_rec[kCapB];
   __shared__ long long s_r0[kCapB];
   __shared__ int s_pre[kCapB + 1];
@@ -708,92 +885,17 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
   // read reverse slots of steps >= m+1, all final); [neuron side] R-neuron(m),
   // which writes reverse slot m only and reads dL/dt_spk of its own spikes of
   // step m, produced by the event side of phase m+1.
-  for (int m = A.m_run - 1; m >= 0; --m) {
+  for (int m = A.m_hi - 1; m >= A.m_lo; --m) {
     tl_mark(A.tl, m, A.G, cta, 0);
     if (tid < Ro::NF) {
       // ======================== event side: R-fanout(m-1), shared evenly by
-      // the whole grid (whole spikes per CTA).  dL/dt_spk of a spike is the
-      // SEQUENTIAL sum of its edges' g_tp in row order (zeros for events never
-      // popped or dropped), staged through s_gtp in windows of kEv events; the
-      // oracle sums in the same order.
+      // the whole grid (whole spikes per CTA): bwd_rfanout
       const int gtid = tid;
       if (m >= 1) {
         const int me = m - 1;
         const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
-        const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
-        for (long long k0 = s0; k0 < s1; k0 += kCapB) {
-          const int nb = (int)(s1 - k0 < kCapB ? s1 - k0 : kCapB);
-          stage_spikes<T>(A.log, A.log_r0, A.log_len, k0, nb, s_rec, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
-          for (int k = gtid; k < nb; k += Ro::NF) s_lt[k] = (T)0;
-          group_sync(Ro::kBarF, Ro::NF);
-          if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 4);
-          const int total = s_pre[nb];
-          for (int w0 = 0; w0 < total; w0 += kEv) {
-            const int wend = total - w0 < kEv ? total : w0 + kEv;
-            constexpr int EV = 4;
-            for (int f0 = w0 + gtid; f0 < wend; f0 += EV * Ro::NF) {
-              int jj[EV], kk[EV];
-              long long xx[EV];
-              T ww[EV], dd[EV];
-              unsigned short cc[EV];
-#pragma unroll
-              for (int e = 0; e < EV; ++e) {
-                const int f = f0 + e * Ro::NF;
-                kk[e] = -1;
-                if (f < wend) {
-                  const int k = find_row(s_pre, nb, f);
-                  const long long x = s_r0[k] + (f - s_pre[k]);
-                  kk[e] = k;
-                  xx[e] = x;
-                  jj[e] = __ldcs(A.net.col + x);
-                  ww[e] = __ldcs(A.net.w + x);
-                  dd[e] = __ldcs(A.net.d + x);
-                  cc[e] = __ldcs(A.net.dcode + x);
-                }
-              }
-#pragma unroll
-              for (int e = 0; e < EV; ++e) {
-                if (kk[e] < 0) continue;
-                const int f = f0 + e * Ro::NF;
-                const SpikeRec<T> rec = s_rec[kk[e]];
-                const int b = c.divN.div(rec.idx);
-                const T w = ww[e], d = dd[e];
-                const T t_post = rec.t + d;
-                const int st = delivery_step_coded(t_post, cc[e], c.dt, me);
-                T g_tp = (T)0;
-                bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
-                if (live && A.drop_bits) {                       // dropped by a bounded queue
-                  const long long id = A.ev_base[k0 + kk[e]] + (f - s_pre[kk[e]]);
-                  live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
-                }
-                if (live) {
-                  const T phi = (T)st * c.dt - t_post;
-                  const T es = eq_exp_t(-phi * c.inv_tau_s);
-                  const T em = eq_exp_t(-phi * c.inv_tau_m);
-                  const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
-                  const T g_w = es * L.x + em * L.y;
-                  g_tp = w * (es * L.x * c.inv_tau_s + em * L.y * c.inv_tau_m);
-                  red_add_f64(A.gw + xx[e], (double)g_w);
-                  red_add_f64(A.gd + xx[e], (double)g_tp);
-                }
-                s_gtp[f - w0] = g_tp;
-              }
-            }
-            group_sync(Ro::kBarF, Ro::NF);
-            if (k0 == s0 && w0 == 0) tl_mark(A.tl, m, A.G, cta, 5);
-            const int ka = find_row(s_pre, nb, w0);
-            const int kb = find_row(s_pre, nb, wend - 1);
-            for (int k = ka + gtid; k <= kb; k += Ro::NF) {
-              const int lo = s_pre[k] > w0 ? s_pre[k] : w0;
-              const int hi = s_pre[k + 1] < wend ? s_pre[k + 1] : wend;
-              T acc = s_lt[k];
-              for (int q = lo; q < hi; ++q) acc = acc + s_gtp[q - w0];
-              s_lt[k] = acc;
-            }
-            group_sync(Ro::kBarF, Ro::NF);
-          }
-          for (int k = gtid; k < nb; k += Ro::NF) A.lt_log[k0 + k] = s_lt[k];
-        }
+        bwd_rfanout<T, NT, NF, false, kCapB, kEv>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G,
+                                                  s_rec, s_r0, s_pre, s_lt, s_gtp);
       }
       tl_mark(A.tl, m, A.G, cta, 1);
     } else {
@@ -841,7 +943,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
                   while (k < cnt && A.log[off + k].idx != idx + q) ++k;
                 }
                 SpikeRec<T> rec = A.log[off + k];
-                const T lt0 = m + 1 < A.m_run ? A.lt_log[off + k] : (T)0;
+                const T lt0 = (m + 1 < A.m_run ? A.lt_log[off + k] : (T)0) + (A.lt_rem ? A.lt_rem[off + k] : (T)0);
                 T t = rec.t, a = rec.a, vh = rec.vh;
                 T uu = (T)(m + 1) * c.dt - t;
                 T ku = eq_exp_t(-uu / c.tau_m);
@@ -896,7 +998,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
                 while (k < cnt && A.log[off + k].idx != idx) ++k;
               }
               SpikeRec<T> rec = A.log[off + k];
-              const T lt0 = m + 1 < A.m_run ? A.lt_log[off + k] : (T)0;
+              const T lt0 = (m + 1 < A.m_run ? A.lt_log[off + k] : (T)0) + (A.lt_rem ? A.lt_rem[off + k] : (T)0);
               T t = rec.t, a = rec.a, vh = rec.vh;
               T uu = (T)(m + 1) * c.dt - t;
               T ku = eq_exp_t(-uu / c.tau_m);
@@ -935,6 +1037,24 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
     tl_mark(A.tl, m, A.G, cta, 3);
     if (ld_volatile(A.err) != 0) break;
   }
+}
+
+// Reverse of k_import_fanout: after a reverse window's launch (phases down to
+// m_lo, so reverse slots >= m_lo are final), the partial dL/dt_spk over this
+// partition's edges of the spikes imported before forward launch m_lo — their
+// events are due >= m_lo + 1 because the exchange window is <= D_min.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) k_import_rfanout(BwdArgs<T> A) {
+  constexpr int kCapB = BwdShared<T>::kCapB;
+  constexpr int kEv = BwdShared<T>::kEv;
+  __shared__ SpikeRec<T> s_rec[kCapB];
+  __shared__ long long s_r0[kCapB];
+  __shared__ int s_pre[kCapB + 1];
+  __shared__ T s_lt[kCapB];
+  __shared__ T s_gtp[kEv];
+  const int cta = blockIdx.x;
+  bwd_rfanout<T, NT, NT, true, kCapB, kEv>(A, A.m_lo, cta, threadIdx.x, A.imp_n * cta / A.G,
+                                           A.imp_n * (cta + 1) / A.G, s_rec, s_r0, s_pre, s_lt, s_gtp);
 }
 
 }  // namespace eq

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -119,6 +120,23 @@ struct eq_handle {
   int tl_steps = 0;
   int steps_done = 0;
   long long launches = 0;
+  // partitioned network (eq_set_partition): CSR rows are all n_src sources,
+  // columns the n_neurons owned targets; owned neuron j is source src_off + j
+  int n_src = 0, src_off = 0;
+  bool partitioned = false;
+  int frac_safe = 0;                  // largest overflow-free fraction bits of this network
+  void* imp = nullptr;                // imported spikes of all windows (SpikeRec)
+  long long* imp_r0 = nullptr;
+  int* imp_len = nullptr;
+  void* imp_lt = nullptr;             // partial dL/dt_spk of each imported spike (reverse)
+  long long imp_cap = 0, imp_n = 0;
+  std::vector<std::array<long long, 4>> imp_blocks;   // {forward launch start step, first, count, fanned out}
+  void* lt_rem = nullptr;             // [log_cap] other partitions' dL/dt_spk of own spikes
+  // reverse pass in windows (eq_backward_begin / eq_backward_window)
+  int bwd_cursor = -1;
+  double* bw_gw = nullptr;
+  double* bw_gd = nullptr;
+  double* bw_gamp = nullptr;
   std::vector<void*> owned;
   std::vector<std::pair<void*, size_t>> sizes;   // reusable buffers
 };
@@ -218,11 +236,11 @@ NetView<T> netview(const eq_handle* h) {
 // ConfigurationError, stats[2] = code of that error; insum = fixed-point
 // sum of |w| per target (2^-40 units; deterministic integer adds).
 template <typename T>
-__global__ void k_net_stats(int N, const int64_t* rowptr, const int32_t* col, const T* w, const T* d,
-                            T dt, int homogeneous_only, long long* insum, long long* stats, long long* inocc,
-                            int* indeg) {
+__global__ void k_net_stats(int n_rows, int N, int src_off, const int64_t* rowptr, const int32_t* col, const T* w,
+                            const T* d, T dt, int homogeneous_only, long long* insum, long long* stats,
+                            long long* inocc, int* indeg) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
+  if (i >= n_rows) return;
   long long r0 = rowptr[i], r1 = rowptr[i + 1];
   int hmax = 1;
   T d0 = d[0];
@@ -230,7 +248,7 @@ __global__ void k_net_stats(int N, const int64_t* rowptr, const int32_t* col, co
   for (long long x = r0; x < r1; ++x) {
     int j = col[x];
     int code = 0;
-    if (j < 0 || j >= N || j == i || j <= prev) code = 1;
+    if (j < 0 || j >= N || j + src_off == i || j <= prev) code = 1;
     else if (!(d[x] >= dt)) code = 2;
     else if (homogeneous_only && d[x] != d0) code = 3;
     if (code) {
@@ -429,6 +447,78 @@ __global__ void k_pending_bounded(const QEv<T>* q, const int4* meta, int kind, i
   }
 }
 
+// ------------------------------------------------------------ spike exchange (partitioned networks)
+
+// Wire record of one spike (eq_spike_f32 / eq_spike_f64 in the header).
+template <typename T>
+struct ExRec {
+  int src, trial, step;
+  T t;
+};
+static_assert(sizeof(ExRec<float>) == 16 && sizeof(ExRec<double>) == 24, "wire layout");
+
+// Log records of steps [lo, hi) -> wire records with global source ids.
+template <typename T>
+__global__ void k_export(const SpikeRec<T>* log, const long long* step_start, int lo, int hi, int N, int src_off,
+                         ExRec<T>* out) {
+  const long long k0 = step_start[lo], n = step_start[hi] - k0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long pos = k0 + k;
+    int a = lo, b = hi;                    // largest m in [lo, hi) with step_start[m] <= pos
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (step_start[mid] <= pos) a = mid;
+      else b = mid;
+    }
+    const SpikeRec<T> r = log[pos];
+    ExRec<T> e;
+    e.trial = r.idx / N;
+    e.src = src_off + (r.idx - e.trial * N);
+    e.step = a;
+    e.t = r.t;
+    out[k] = e;
+  }
+}
+
+// Wire records -> fan-out records of this partition: idx = trial base, a = emit
+// step, CSR row of the (remote) source.
+template <typename T>
+__global__ void k_import(const ExRec<T>* in, long long n, const int64_t* rowptr, int n_src, int src_off, int n_own,
+                         int B, int N, int now, SpikeRec<T>* imp, long long* r0, int* len, int* err) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const ExRec<T> e = in[k];
+    const bool bad = e.src < 0 || e.src >= n_src || (e.src >= src_off && e.src < src_off + n_own) || e.trial < 0 ||
+                     e.trial >= B || e.step < 0 || e.step >= now;
+    if (bad) {
+      raise_error(err, EQ_ERR_CONFIGURATION, e.step, e.trial, e.src);
+      len[k] = 0;
+      r0[k] = 0;
+      SpikeRec<T> z{};
+      imp[k] = z;
+      continue;
+    }
+    SpikeRec<T> r{};
+    r.idx = e.trial * N;
+    r.t = e.t;
+    r.a = (T)e.step;      // exact: steps < 2^24
+    r.vh = (T)0;
+    imp[k] = r;
+    const long long a = rowptr[e.src];
+    r0[k] = a;
+    len[k] = (int)(rowptr[e.src + 1] - a);
+  }
+}
+
+template <typename T>
+__global__ void k_add_lt(T* lt_rem, const long long* step_start, int lo, const T* vals, long long n) {
+  const long long k0 = step_start[lo];
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    lt_rem[k0 + k] += vals[k];
+}
+
 // ------------------------------------------------------------ launches
 
 // reverse kernel dynamic smem: spiker bitmap + uint16 chunk position per owned neuron
@@ -458,6 +548,12 @@ int check_err(eq_handle* h, cudaStream_t s) {
       snprintf(buf, sizeof buf, "device error %d at step %d (trial %d, neuron %d)", e[0], e[1], e[2], e[3]);
   }
   return fail(h, e[0], buf);
+}
+
+std::array<long long, 4>* find_block(eq_handle* h, int start) {
+  for (auto& b : h->imp_blocks)
+    if (b[0] == start && b[2] > 0) return &b;
+  return nullptr;
 }
 
 template <typename T>
@@ -498,6 +594,19 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
   A.step_start = h->step_start;
   A.counters = h->counters;
   A.v_trace = (T*)v_trace;
+  A.src_off = h->src_off;
+  A.imp = nullptr;
+  A.imp_r0 = nullptr;
+  A.imp_len = nullptr;
+  A.imp_n = 0;
+  std::array<long long, 4>* blk = find_block(h, h->steps_done);
+  if (blk && !(*blk)[3]) {
+    (*blk)[3] = 1;
+    A.imp = (const SpikeRec<T>*)h->imp + (*blk)[1];
+    A.imp_r0 = h->imp_r0 + (*blk)[1];
+    A.imp_len = h->imp_len + (*blk)[1];
+    A.imp_n = (*blk)[2];
+  }
   A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
@@ -546,6 +655,13 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
     }
     // warp split (event side / neuron side) measured at C3 x 16 trials:
     // 384/128 balances the forward's sides (timeline, profiles/)
+    if (A.imp_n > 0) {   // other partitions' spikes of the last window, due >= m0+1
+      FwdArgs<T> Ai = A;
+      Ai.tl = nullptr;
+      k_import_fanout<T, kNT><<<h->G, kNT, 0, s>>>(Ai);
+      h->launches += 1;
+      if (n_steps == 0) return check_err(h, s);   // flush: deliver the imports, no step
+    }
     const void* kf = (const void*)k_forward<T, kNT, kU, kSplitF>;
     EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, 0, s));
   }
@@ -556,8 +672,8 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
 }
 
 template <typename T>
-int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* gw, double* gd, double* gamp,
-                    cudaStream_t s) {
+int backward_begin(eq_handle* h, const void* v_bar, const void* i_bar, double* gw, double* gd, double* gamp,
+                   cudaStream_t s) {
   typedef typename Prec<T>::T2 T2;
   const int N = h->cfg.n_neurons, B = h->cfg.n_trials;
   const long long total = h->total;
@@ -568,14 +684,29 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   EQ_CUDA(h, cudaMemsetAsync(gw, 0, h->E * sizeof(double), s));
   EQ_CUDA(h, cudaMemsetAsync(gd, 0, h->E * sizeof(double), s));
   if (gamp) EQ_CUDA(h, cudaMemsetAsync(h->gamp_bt, 0, total * sizeof(double), s));
+  if (h->partitioned) EQ_CUDA(h, cudaMemsetAsync(h->lt_rem, 0, (size_t)h->log_cap * sizeof(T), s));
+  h->bwd_cursor = h->steps_done;
+  h->bw_gw = gw;
+  h->bw_gd = gd;
+  h->bw_gamp = gamp;
+  return EQ_OK;
+}
+
+// Reverse phases bwd_cursor-1 .. m_lo in one persistent launch.
+template <typename T>
+int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
+  typedef typename Prec<T>::T2 T2;
+  const int N = h->cfg.n_neurons, B = h->cfg.n_trials;
   EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
   BwdArgs<T> A;
   A.N = N;
   A.B = B;
   A.G = h->G;
-  A.total = total;
+  A.total = h->total;
   A.per = h->per;
   A.m_run = h->steps_done;
+  A.m_hi = h->bwd_cursor;
+  A.m_lo = m_lo;
   A.R = h->R;
   A.refractory = h->cfg.refractory_steps;
   A.c = consts<T>(h);
@@ -583,9 +714,9 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   A.lamV = (T*)h->lamV;
   A.lamI = (T*)h->lamI;
   A.lam = (T2*)h->lam;
-  A.gw = gw;
-  A.gd = gd;
-  A.gamp_bt = gamp ? h->gamp_bt : nullptr;
+  A.gw = h->bw_gw;
+  A.gd = h->bw_gd;
+  A.gamp_bt = h->bw_gamp ? h->gamp_bt : nullptr;
   A.log = (const SpikeRec<T>*)h->log;
   A.log_r0 = h->log_r0;
   A.log_len = h->log_len;
@@ -596,6 +727,19 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   A.ev_base = h->bounded ? h->ev_base : nullptr;
   A.drop_bits = h->bounded ? h->drop_bits : nullptr;
   A.no_events = h->cfg.kind == EQ_KIND_DONOTHING;
+  A.lt_rem = h->partitioned ? (const T*)h->lt_rem : nullptr;
+  A.imp = nullptr;
+  A.imp_r0 = nullptr;
+  A.imp_len = nullptr;
+  A.imp_n = 0;
+  A.imp_lt = nullptr;
+  if (std::array<long long, 4>* blk = find_block(h, m_lo)) {
+    A.imp = (const SpikeRec<T>*)h->imp + (*blk)[1];
+    A.imp_r0 = h->imp_r0 + (*blk)[1];
+    A.imp_len = h->imp_len + (*blk)[1];
+    A.imp_n = (*blk)[2];
+    A.imp_lt = (T*)h->imp_lt + (*blk)[1];
+  }
   A.tl = (h->tl_b && A.m_run <= h->tl_steps) ? h->tl_b : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
@@ -605,8 +749,15 @@ int launch_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* 
   if (smem > 48 * 1024) EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   EQ_CUDA(h, cudaLaunchCooperativeKernel(kb, dim3(h->G), dim3(kNT), args, smem, s));
   h->launches += 1;
-  if (gamp) {
-    k_sum_trials<T><<<(N + 255) / 256, 256, 0, s>>>(h->gamp_bt, B, N, gamp);
+  if (A.imp_n > 0) {   // partial dL/dt_spk of the imported spikes (reverse slots >= m_lo final)
+    BwdArgs<T> Ai = A;
+    Ai.tl = nullptr;
+    k_import_rfanout<T, kNT><<<h->G, kNT, 0, s>>>(Ai);
+    h->launches += 1;
+  }
+  h->bwd_cursor = m_lo;
+  if (m_lo == 0 && h->bw_gamp) {
+    k_sum_trials<T><<<(N + 255) / 256, 256, 0, s>>>(h->gamp_bt, B, N, h->bw_gamp);
     h->launches += 1;
   }
   return check_err(h, s);
@@ -807,6 +958,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
                                     std::to_string(prop.major) + std::to_string(prop.minor));
   }
   h->n_sm = prop.multiProcessorCount;
+  h->n_src = c.n_neurons;
   *out = h;
   int rc = setup_geometry(h);
   if (rc) return rc;
@@ -830,6 +982,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   EQ_CUDA(h, alloc(h, (void**)&h->log_r0, (size_t)cap * sizeof(long long)));
   EQ_CUDA(h, alloc(h, (void**)&h->log_len, (size_t)cap * sizeof(int)));
   EQ_CUDA(h, alloc(h, &h->lt_log, (size_t)cap * T));
+  EQ_CUDA(h, alloc(h, &h->lt_rem, (size_t)cap * T));
   rc = ensure_chunks(h, c.t_steps);
   if (rc) return rc;
   const char* tl = getenv("EQ_TIMELINE");
@@ -875,13 +1028,13 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   EQ_CUDA(h, cudaMemcpyAsync(stats, init, sizeof init, cudaMemcpyHostToDevice, s));
   int homog = c.kind == EQ_KIND_FIFORING;
   if (c.precision == 32)
-    k_net_stats<float><<<(N + 127) / 128, 128, 0, s>>>(N, rowptr, col, (const float*)weight, (const float*)delay,
-                                                        (float)c.dt, homog, (long long*)insum, (long long*)stats,
-                                                        (long long*)inocc, (int*)indeg);
+    k_net_stats<float><<<(h->n_src + 127) / 128, 128, 0, s>>>(
+        h->n_src, N, h->src_off, rowptr, col, (const float*)weight, (const float*)delay, (float)c.dt, homog,
+        (long long*)insum, (long long*)stats, (long long*)inocc, (int*)indeg);
   else
-    k_net_stats<double><<<(N + 127) / 128, 128, 0, s>>>(N, rowptr, col, (const double*)weight,
-                                                         (const double*)delay, c.dt, homog, (long long*)insum,
-                                                         (long long*)stats, (long long*)inocc, (int*)indeg);
+    k_net_stats<double><<<(h->n_src + 127) / 128, 128, 0, s>>>(
+        h->n_src, N, h->src_off, rowptr, col, (const double*)weight, (const double*)delay, c.dt, homog,
+        (long long*)insum, (long long*)stats, (long long*)inocc, (int*)indeg);
   k_max_ll<<<256, 256, 0, s>>>((const long long*)insum, N, (long long*)stats + 2);
   k_max_ll<<<256, 256, 0, s>>>((const long long*)inocc, N, (long long*)stats + 3);
   h->launches += 3;
@@ -897,8 +1050,8 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
     long long x = (long long)(key >> 2);
     int code = (int)(key & 3);
     // locate the row of edge x on the host (validation path only)
-    std::vector<int64_t> rp(N + 1);
-    EQ_CUDA(h, cudaMemcpy(rp.data(), rowptr, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    std::vector<int64_t> rp(h->n_src + 1);
+    EQ_CUDA(h, cudaMemcpy(rp.data(), rowptr, (h->n_src + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
     int i = (int)(std::upper_bound(rp.begin(), rp.end(), (int64_t)x) - rp.begin()) - 1;
     int j = -1;
     EQ_CUDA(h, cudaMemcpy(&j, col + x, sizeof(int), cudaMemcpyDeviceToHost));
@@ -938,6 +1091,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
     int ceil_log2 = (m == 0.5) ? e - 1 : e;
     h->frac_bits = (bits - 2) - ceil_log2;
   }
+  h->frac_safe = h->frac_bits;
   h->scale = std::ldexp(1.0, h->frac_bits);
   h->inv_scale = std::ldexp(1.0, -h->frac_bits);
   h->rowptr = rowptr;
@@ -1027,13 +1181,20 @@ int eq_reset(eq_handle* h, void* stream) {
     h->launches += 1;
   }
   h->steps_done = 0;
+  h->imp_n = 0;
+  h->imp_blocks.clear();
+  h->bwd_cursor = -1;
   return EQ_OK;
 }
 
 int eq_run(eq_handle* h, int32_t n_steps, void* v_trace, void* stream) {
   if (!h) return EQ_ERR_CONFIGURATION;
   if (!h->net_set || !h->drive_set) return fail(h, EQ_ERR_CONFIGURATION, "network and drive must be set");
-  if (n_steps < 1) return fail(h, EQ_ERR_CONFIGURATION, "n_steps must be >= 1");
+  if (n_steps < 0) return fail(h, EQ_ERR_CONFIGURATION, "n_steps must be >= 0");
+  if (n_steps == 0) {   // partitioned: only fan out the spikes imported at this step
+    std::array<long long, 4>* blk = find_block(h, h->steps_done);
+    if (!blk || (*blk)[3]) return EQ_OK;
+  }
   DeviceGuard g(h->device);
   int rc = ensure_chunks(h, h->steps_done + n_steps);
   if (rc) return rc;
@@ -1055,16 +1216,192 @@ int eq_forward(eq_handle* h, void* v_out, void* i_out, void* v_trace, void* stre
   return EQ_OK;
 }
 
+int eq_get_state(eq_handle* h, void* v_out, void* i_out, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (v_out) EQ_CUDA(h, cudaMemcpyAsync(v_out, h->V, h->total * h->tsize, cudaMemcpyDeviceToDevice, s));
+  if (i_out) EQ_CUDA(h, cudaMemcpyAsync(i_out, h->I, h->total * h->tsize, cudaMemcpyDeviceToDevice, s));
+  return EQ_OK;
+}
+
 int eq_backward(eq_handle* h, const void* v_bar, const void* i_bar, double* grad_w, double* grad_d,
                 double* grad_amp, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  int rc = eq_backward_begin(h, v_bar, i_bar, grad_w, grad_d, grad_amp, stream);
+  if (rc) return rc;
+  return eq_backward_window(h, 0, stream);
+}
+
+int eq_backward_begin(eq_handle* h, const void* v_bar, const void* i_bar, double* grad_w, double* grad_d,
+                      double* grad_amp, void* stream) {
   if (!h) return EQ_ERR_CONFIGURATION;
   if (h->steps_done < 1) return fail(h, EQ_ERR_CONFIGURATION, "backward needs a forward run first");
   if (!h->cfg.exact_delivery) return fail(h, EQ_ERR_CONFIGURATION, "reverse mode requires exact_delivery");
   if (!v_bar || !grad_w || !grad_d) return fail(h, EQ_ERR_CONFIGURATION, "v_bar, grad_w, grad_d are required");
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (h->cfg.precision == 32) return launch_backward<float>(h, v_bar, i_bar, grad_w, grad_d, grad_amp, s);
-  return launch_backward<double>(h, v_bar, i_bar, grad_w, grad_d, grad_amp, s);
+  if (h->cfg.precision == 32) return backward_begin<float>(h, v_bar, i_bar, grad_w, grad_d, grad_amp, s);
+  return backward_begin<double>(h, v_bar, i_bar, grad_w, grad_d, grad_amp, s);
+}
+
+int eq_backward_window(eq_handle* h, int32_t m_lo, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (h->bwd_cursor < 0) return fail(h, EQ_ERR_CONFIGURATION, "eq_backward_begin must come first");
+  if (m_lo < 0 || m_lo >= h->bwd_cursor)
+    return fail(h, EQ_ERR_CONFIGURATION, "reverse window start " + std::to_string(m_lo) + " outside [0, " +
+                                             std::to_string(h->bwd_cursor) + ")");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (h->cfg.precision == 32) return launch_backward<float>(h, m_lo, s);
+  return launch_backward<double>(h, m_lo, s);
+}
+
+int eq_set_partition(eq_handle* h, int32_t n_global, int32_t src_offset) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (h->cfg.kind != EQ_KIND_RING)
+    return fail(h, EQ_ERR_CONFIGURATION, "partitioned networks support the ring kind (bounded kinds insert in "
+                                         "global source order, which needs the whole step's spikes)");
+  if (src_offset < 0 || (long long)src_offset + h->cfg.n_neurons > n_global)
+    return fail(h, EQ_ERR_CONFIGURATION, "partition [" + std::to_string(src_offset) + ", " +
+                                             std::to_string((long long)src_offset + h->cfg.n_neurons) +
+                                             ") outside the " + std::to_string(n_global) + "-neuron network");
+  h->n_src = n_global;
+  h->src_off = src_offset;
+  h->partitioned = true;
+  h->net_set = false;   // the CSR must be (re)validated with the new row count
+  return EQ_OK;
+}
+
+int eq_set_frac_bits(eq_handle* h, int32_t frac_bits) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (!h->net_set) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_network must come first");
+  if (frac_bits < 0 || frac_bits > h->frac_safe)
+    return fail(h, EQ_ERR_CONFIGURATION, "fraction bits " + std::to_string(frac_bits) + " outside [0, " +
+                                             std::to_string(h->frac_safe) + "] (overflow-free bound)");
+  h->frac_bits = frac_bits;
+  h->scale = std::ldexp(1.0, frac_bits);
+  h->inv_scale = std::ldexp(1.0, -frac_bits);
+  return EQ_OK;
+}
+
+int eq_export_spikes(eq_handle* h, int32_t step_lo, int32_t step_hi, void* out, int64_t* n_out, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (step_lo < 0 || step_hi < step_lo || step_hi > h->steps_done)
+    return fail(h, EQ_ERR_CONFIGURATION, "export window [" + std::to_string(step_lo) + ", " +
+                                             std::to_string(step_hi) + ") outside the run");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  long long ss[2];
+  EQ_CUDA(h, cudaMemcpyAsync(&ss[0], h->step_start + step_lo, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaMemcpyAsync(&ss[1], h->step_start + step_hi, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  const long long n = ss[1] - ss[0];
+  if (n_out) *n_out = n;
+  if (!out || n == 0) return EQ_OK;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4096);
+  if (h->cfg.precision == 32)
+    k_export<float><<<blocks, 256, 0, s>>>((const SpikeRec<float>*)h->log, h->step_start, step_lo, step_hi,
+                                           h->cfg.n_neurons, h->src_off, (ExRec<float>*)out);
+  else
+    k_export<double><<<blocks, 256, 0, s>>>((const SpikeRec<double>*)h->log, h->step_start, step_lo, step_hi,
+                                            h->cfg.n_neurons, h->src_off, (ExRec<double>*)out);
+  h->launches += 1;
+  EQ_CUDA(h, cudaGetLastError());
+  return EQ_OK;
+}
+
+int eq_import_spikes(eq_handle* h, const void* recs, int64_t n, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (!h->partitioned) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_partition must come first");
+  if (!h->net_set) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_network must come first");
+  if (n < 0 || (n > 0 && !recs)) return fail(h, EQ_ERR_CONFIGURATION, "bad import batch");
+  if (find_block(h, h->steps_done))
+    return fail(h, EQ_ERR_CONFIGURATION, "spikes already imported for the launch at step " +
+                                             std::to_string(h->steps_done));
+  if (n == 0) return EQ_OK;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rec = h->cfg.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
+  if (h->imp_n + n > h->imp_cap) {
+    const long long ncap = std::max<long long>(h->imp_n + n, 2 * h->imp_cap);
+    void *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr;
+    EQ_CUDA(h, alloc(h, &a, (size_t)ncap * rec));
+    EQ_CUDA(h, alloc(h, &b, (size_t)ncap * sizeof(long long)));
+    EQ_CUDA(h, alloc(h, &c, (size_t)ncap * sizeof(int)));
+    EQ_CUDA(h, alloc(h, &d, (size_t)ncap * h->tsize));
+    if (h->imp_n) {
+      EQ_CUDA(h, cudaMemcpyAsync(a, h->imp, (size_t)h->imp_n * rec, cudaMemcpyDeviceToDevice, s));
+      EQ_CUDA(h, cudaMemcpyAsync(b, h->imp_r0, (size_t)h->imp_n * sizeof(long long), cudaMemcpyDeviceToDevice, s));
+      EQ_CUDA(h, cudaMemcpyAsync(c, h->imp_len, (size_t)h->imp_n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+      EQ_CUDA(h, cudaStreamSynchronize(s));
+    }
+    release(h, h->imp);
+    release(h, h->imp_r0);
+    release(h, h->imp_len);
+    release(h, h->imp_lt);
+    h->imp = a;
+    h->imp_r0 = (long long*)b;
+    h->imp_len = (int*)c;
+    h->imp_lt = d;
+    h->imp_cap = ncap;
+  }
+  const long long k0 = h->imp_n;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4096);
+  if (h->cfg.precision == 32)
+    k_import<float><<<blocks, 256, 0, s>>>((const ExRec<float>*)recs, n, h->rowptr, h->n_src, h->src_off,
+                                           h->cfg.n_neurons, h->cfg.n_trials, h->cfg.n_neurons, h->steps_done,
+                                           (SpikeRec<float>*)h->imp + k0, h->imp_r0 + k0, h->imp_len + k0,
+                                           h->err_dev);
+  else
+    k_import<double><<<blocks, 256, 0, s>>>((const ExRec<double>*)recs, n, h->rowptr, h->n_src, h->src_off,
+                                            h->cfg.n_neurons, h->cfg.n_trials, h->cfg.n_neurons, h->steps_done,
+                                            (SpikeRec<double>*)h->imp + k0, h->imp_r0 + k0, h->imp_len + k0,
+                                            h->err_dev);
+  h->launches += 1;
+  EQ_CUDA(h, cudaGetLastError());
+  int e[4];
+  EQ_CUDA(h, cudaMemcpyAsync(e, h->err_dev, sizeof e, cudaMemcpyDeviceToHost, s));
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  if (e[0]) {
+    EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, 4 * sizeof(int), s));
+    char buf[200];
+    snprintf(buf, sizeof buf, "imported spike (source %d, trial %d, step %d) is not a remote spike of an "
+                              "earlier step", e[3], e[2], e[1]);
+    return fail(h, EQ_ERR_CONFIGURATION, buf);
+  }
+  h->imp_blocks.push_back({(long long)h->steps_done, k0, (long long)n, 0LL});
+  h->imp_n += n;
+  return EQ_OK;
+}
+
+int eq_get_import_adjoints(eq_handle* h, int32_t start_step, void* out, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  std::array<long long, 4>* blk = find_block(h, start_step);
+  if (!blk) return EQ_OK;
+  if (h->bwd_cursor < 0 || h->bwd_cursor > start_step)
+    return fail(h, EQ_ERR_CONFIGURATION, "the reverse pass has not reached step " + std::to_string(start_step));
+  DeviceGuard g(h->device);
+  EQ_CUDA(h, cudaMemcpyAsync(out, (char*)h->imp_lt + (*blk)[1] * h->tsize, (size_t)(*blk)[2] * h->tsize,
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return EQ_OK;
+}
+
+int eq_add_spike_adjoints(eq_handle* h, int32_t step_lo, const void* vals, int64_t n, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (!h->partitioned) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_partition must come first");
+  if (step_lo < 0 || step_lo > h->steps_done) return fail(h, EQ_ERR_CONFIGURATION, "step outside the run");
+  if (n <= 0) return EQ_OK;
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4096);
+  if (h->cfg.precision == 32)
+    k_add_lt<float><<<blocks, 256, 0, s>>>((float*)h->lt_rem, h->step_start, step_lo, (const float*)vals, n);
+  else
+    k_add_lt<double><<<blocks, 256, 0, s>>>((double*)h->lt_rem, h->step_start, step_lo, (const double*)vals, n);
+  h->launches += 1;
+  EQ_CUDA(h, cudaGetLastError());
+  return EQ_OK;
 }
 
 int eq_counters(eq_handle* h, int64_t* out, void* stream) {

@@ -8,7 +8,7 @@ the sm_100a kernels of ``lib/libeventq_b200.so``.
 from __future__ import annotations
 
 import ctypes
-from typing import Dict, Optional
+from typing import Dict, Optional, Tuple
 
 import numpy as np
 import torch
@@ -31,7 +31,8 @@ class Engine:
 
     def __init__(self, n: int, n_trials: int, t_steps: int, *, kind: str = "ring",
                  precision: int = 32, lif: Optional[LIFConfig] = None, capacity: int = 0,
-                 max_spikes: int = 0, device: Optional[int] = None):
+                 max_spikes: int = 0, device: Optional[int] = None,
+                 partition: Optional[Tuple[int, int]] = None):
         self.L = _native.lib()
         if kind not in _native.KIND_IDS:
             raise ConfigurationError(f"unknown queue kind {kind!r}")
@@ -59,6 +60,11 @@ class Engine:
         _native.check(self.h, code)
         self._net = None
         self._drive = None
+        # partitioned network (paper_2512_05906_b200.partition): this engine owns
+        # neurons [offset, offset + n) of an n_global-neuron network
+        self.n_global, self.offset = (n, 0) if partition is None else (int(partition[0]), int(partition[1]))
+        if partition is not None:
+            _native.check(self.h, self.L.eq_set_partition(self.h, self.n_global, self.offset))
 
     # ------------------------------------------------------------ lifetime
     def close(self):
@@ -87,8 +93,8 @@ class Engine:
         cl = self._dev(col, torch.int32)
         w = self._dev(weight, self.dtype)
         d = self._dev(delay, self.dtype)
-        if rp.numel() != self.n + 1:
-            raise ConfigurationError(f"rowptr must have n+1 = {self.n + 1} entries")
+        if rp.numel() != self.n_global + 1:
+            raise ConfigurationError(f"rowptr must have n+1 = {self.n_global + 1} entries")
         E = cl.numel()
         if w.numel() != E or d.numel() != E:
             raise ConfigurationError("weight/delay must have one entry per edge")
@@ -120,6 +126,13 @@ class Engine:
             out["v_trace"] = tr
         return out
 
+    def state(self) -> Dict[str, torch.Tensor]:
+        """Current membrane and synaptic current, [n_trials, n]."""
+        v = torch.empty(self.B, self.n, dtype=self.dtype, device=self.device)
+        i = torch.empty_like(v)
+        _native.check(self.h, self.L.eq_get_state(self.h, _ptr(v), _ptr(i), self.stream))
+        return {"v": v, "i": i}
+
     def reset(self) -> None:
         _native.check(self.h, self.L.eq_reset(self.h, self.stream))
 
@@ -135,6 +148,60 @@ class Engine:
         _native.check(self.h, self.L.eq_backward(self.h, _ptr(vb), _ptr(ib), _ptr(gw), _ptr(gd), _ptr(ga),
                                                   self.stream))
         return gw, gd, ga
+
+    def backward_begin(self, v_bar: torch.Tensor, i_bar: Optional[torch.Tensor] = None, want_amp: bool = True):
+        """Start a windowed reverse pass; returns the (grad_w, grad_d, grad_amp)
+        buffers the windows accumulate into (final after the window at step 0)."""
+        vb = self._dev(v_bar, self.dtype)
+        ib = None if i_bar is None else self._dev(i_bar, self.dtype)
+        gw = torch.empty(self.n_edges, dtype=torch.float64, device=self.device)
+        gd = torch.empty_like(gw)
+        ga = torch.empty(self.n, dtype=torch.float64, device=self.device) if want_amp else None
+        self._bw = (vb, ib)
+        _native.check(self.h, self.L.eq_backward_begin(self.h, _ptr(vb), _ptr(ib), _ptr(gw), _ptr(gd), _ptr(ga),
+                                                        self.stream))
+        return gw, gd, ga
+
+    def backward_window(self, m_lo: int) -> None:
+        _native.check(self.h, self.L.eq_backward_window(self.h, int(m_lo), self.stream))
+
+    # ------------------------------------------------------------ partitions
+    @property
+    def spike_words(self) -> int:
+        """int32 words per wire spike record (eq_spike_f32 / eq_spike_f64)."""
+        return 4 if self.precision == 32 else 6
+
+    def set_frac_bits(self, frac_bits: int) -> None:
+        _native.check(self.h, self.L.eq_set_frac_bits(self.h, int(frac_bits)))
+
+    def export_spikes(self, step_lo: int, step_hi: int) -> torch.Tensor:
+        """Own spikes of steps [step_lo, step_hi) as wire records, int32 [n, spike_words]."""
+        n = ctypes.c_int64()
+        _native.check(self.h, self.L.eq_export_spikes(self.h, step_lo, step_hi, None, ctypes.byref(n), self.stream))
+        out = torch.empty(n.value, self.spike_words, dtype=torch.int32, device=self.device)
+        if n.value:
+            _native.check(self.h, self.L.eq_export_spikes(self.h, step_lo, step_hi, _ptr(out), ctypes.byref(n),
+                                                           self.stream))
+        return out
+
+    def import_spikes(self, recs: torch.Tensor) -> None:
+        recs = recs.to(device=self.device, dtype=torch.int32).contiguous()
+        if recs.numel() and (recs.dim() != 2 or recs.shape[1] != self.spike_words):
+            raise ConfigurationError(f"spike records must be int32 [n, {self.spike_words}]")
+        self._imp_keep = recs
+        _native.check(self.h, self.L.eq_import_spikes(self.h, _ptr(recs), recs.shape[0] if recs.numel() else 0,
+                                                       self.stream))
+
+    def import_adjoints(self, start_step: int, n: int) -> torch.Tensor:
+        out = torch.zeros(n, dtype=self.dtype, device=self.device)
+        if n:
+            _native.check(self.h, self.L.eq_get_import_adjoints(self.h, int(start_step), _ptr(out), self.stream))
+        return out
+
+    def add_spike_adjoints(self, step_lo: int, vals: torch.Tensor) -> None:
+        v = self._dev(vals, self.dtype)
+        self._adj_keep = v
+        _native.check(self.h, self.L.eq_add_spike_adjoints(self.h, int(step_lo), _ptr(v), v.numel(), self.stream))
 
     # ------------------------------------------------------------ queries
     def counters(self) -> np.ndarray:
