@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -60,51 +59,69 @@ def alg_bytes(neuron_steps, spikes, events, which):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled in-process through NVML (no
+    nvidia-smi child: its start-up stalled a timed step).  Start it before the
+    warm-up; only samples inside mark_start()..mark_end() are summarised."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("sw_power_cap", 0x4))
 
-    def __init__(self, index=0):
-        self.index = index
+    def __init__(self, index=0, period=0.1):
+        self.index, self.period = index, period
         self.rows = []
-        self.proc = None
+        self.t0 = self.t1 = None
+        self.stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
+        if os.environ.get("EQ_NO_CLOCKS"):
+            return self
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.dev = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.dev, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
+            self.ok = True
         except Exception:
-            self.proc = None
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.dev, nv.NVML_CLOCK_SM)
+                get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                rs = get(self.dev)
+                self.rows.append((time.perf_counter(), sm, rs))
+            except Exception:
+                pass
+            self.stop.wait(self.period)
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.ok:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        rows = [r for r in self.rows if (self.t0 is None or r[0] >= self.t0) and (self.t1 is None or r[0] <= self.t1)]
+        if not rows:   # timed region shorter than one period: nearest samples
+            rows = self.rows[-2:]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        reasons = sorted({name for _, _, rs in rows for name, bit in self.REASONS if rs & bit})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(rows), "source": "nvml"}
 
 
 def dist_env():
@@ -222,6 +239,7 @@ def run_ours(args):
         return out
 
     # ---- device-resident timing, with per-kernel events
+    clocks = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -235,7 +253,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    clocks.mark_start()
+    if True:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
@@ -256,10 +275,15 @@ def run_ours(args):
             bwd_ms.append((e1, e2))
         t_end.record(stream)
         torch.cuda.synchronize()
+    clocks.mark_end()
+    clocks.__exit__(None, None, None)
     launches = eng.launch_count - launches0
     total_ms = t_start.elapsed_time(t_end)
     fwd = [a.elapsed_time(b) for a, b in fwd_ms]
     bwd = [a.elapsed_time(b) for a, b in bwd_ms]
+    if os.environ.get("EQ_BENCH_VERBOSE"):
+        print("fwd ms", " ".join(f"{x:.1f}" for x in fwd), "| bwd ms", " ".join(f"{x:.1f}" for x in bwd),
+              file=sys.stderr, flush=True)
     t = torch.tensor([total_ms], device=dev)
     ev = torch.tensor([float(events)], device=dev, dtype=torch.float64)
     if world > 1:

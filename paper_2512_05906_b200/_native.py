@@ -13,7 +13,7 @@ import os
 from .errors import STATUS_TO_ERROR, EventQError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libeventq_b200.so")
+LIB_PATH = os.environ.get("EQ_LIB_PATH") or os.path.join(HERE, "lib", "libeventq_b200.so")   # override: A/B runs
 
 KIND_IDS = {"ring": 0, "fiforing": 1, "binaryheap": 2, "sortedarray": 3, "lossyring": 4, "donothing": 5}
 

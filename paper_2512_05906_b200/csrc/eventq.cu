@@ -29,6 +29,7 @@ constexpr int kU = 4;      // neurons per thread in flight per round
 constexpr int kSplitF = 384;  // forward event-side threads per CTA
 constexpr int kSplitB = 256;  // reverse event-side threads per CTA
 
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -746,7 +747,8 @@ int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
   size_t smem = bwd_smem(h->per);
   void* args[] = {&A};
   const void* kb = (const void*)k_backward<T, kNT, kU, kSplitB>;
-  if (smem > 48 * 1024) EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // static + dynamic smem beyond 48 KB needs the opt-in (the static part alone is ~41 KB)
+  EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   EQ_CUDA(h, cudaLaunchCooperativeKernel(kb, dim3(h->G), dim3(kNT), args, smem, s));
   h->launches += 1;
   if (A.imp_n > 0) {   // partial dL/dt_spk of the imported spikes (reverse slots >= m_lo final)
@@ -790,8 +792,7 @@ int setup_geometry(eq_handle* h) {
     long long per = (h->total + G - 1) / G;
     size_t smem = bwd_smem(per);
     if (smem > 160 * 1024) continue;
-    if (smem > 48 * 1024)
-      EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, kb, kNT, smem));
     if (occ_b >= occ) break;
   }
@@ -959,6 +960,8 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   }
   h->n_sm = prop.multiProcessorCount;
   h->n_src = c.n_neurons;
+  if (const char* g = getenv("EQ_L2_FETCH"))   // experiment knob: L2 fetch granularity hint (bytes)
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(g));
   *out = h;
   int rc = setup_geometry(h);
   if (rc) return rc;
