@@ -13,3 +13,11 @@ run --config C2 --trials 32 --kind fiforing --capacity 64 --delays 32,32
 run --config C2 --trials 32 --kind ring --delays 32,32
 run --config C3 --trials 16 --kind binaryheap --capacity 64
 run --config C3 --trials 16 --kind sortedarray --capacity 64
+# C4: memory-pressure regime, 1M neurons, delay <= 256, bounded queues drop
+if [ -n "$C4" ]; then
+  run --config C4 --trials 4 --kind ring
+  run --config C4 --trials 4 --kind binaryheap --capacity 16
+  run --config C4 --trials 4 --kind binaryheap --capacity 32
+  run --config C4 --trials 4 --kind sortedarray --capacity 16
+  run --config C4 --trials 4 --kind sortedarray --capacity 32
+fi
