@@ -148,9 +148,15 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 // release, so every CTA sees a value that no CTA can change until the next
 // phase (used to publish the spike-log end of the finished step);
 // zero_u64 / zero_i32 (optional): reset by the final arriver.
-constexpr unsigned kBarGroup = 16;
-constexpr unsigned kBarWords = 64 + 32 * 256;   // up to 4096 CTAs
+constexpr unsigned kBarWords = 64;
 
+// Grid barrier: one arrival atomic per CTA on a single word whose top bit
+// flips when the last CTA arrives (CTA 0 adds 2^31 - (G-1), the others 1), a
+// relaxed spin on that bit, one acquire fence.  1.2 us per barrier at 296 CTAs
+// on B200 (scripts/micro/barrier.cu; a two-level tree with a separate release
+// word took 3.2 us).  The CTA whose arrival flips the bit publishes
+// *publish_src to *publish_dst AFTER the release, so readers of the published
+// value spin on its sentinel (-1, see ld_published); the zero hooks run there too.
 __device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* err,
                                           long long* publish_dst = nullptr,
                                           const unsigned long long* publish_src = nullptr,
@@ -159,33 +165,20 @@ __device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* 
   __syncthreads();
   if (threadIdx.x == 0) {
     s_ok = 1;
-    unsigned* top = bar;
-    unsigned* gen = bar + 32;
-    const unsigned grp = blockIdx.x / kBarGroup;
-    const unsigned ngroups = (nblocks + kBarGroup - 1) / kBarGroup;
-    const unsigned members = min(kBarGroup, nblocks - grp * kBarGroup);
-    unsigned* gcount = bar + 64 + 32 * grp;
-    unsigned g = ld_relaxed(gen);
-    bool released = false;
-    if (atom_add_acq_rel(gcount, 1u) == members - 1) {
-      st_relaxed(gcount, 0u);
-      if (atom_add_acq_rel(top, 1u) == ngroups - 1) {
-        if (publish_dst) *publish_dst = (long long)*(volatile const unsigned long long*)publish_src;
-        if (zero_u64) *(volatile unsigned long long*)zero_u64 = 0ULL;
-        if (zero_i32) *(volatile int*)zero_i32 = 0;
-        st_relaxed(top, 0u);
-        st_release(gen, g + 1);
-        released = true;
-      }
-    }
-    if (!released) {
+    const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (nblocks - 1) : 1u;
+    const unsigned old = atom_add_acq_rel(bar, inc);
+    if (((old ^ (old + inc)) & 0x80000000u) != 0) {        // this arrival completed the barrier
+      if (publish_dst) *(volatile long long*)publish_dst = (long long)*(volatile const unsigned long long*)publish_src;
+      if (zero_u64) *(volatile unsigned long long*)zero_u64 = 0ULL;
+      if (zero_i32) *(volatile int*)zero_i32 = 0;
+    } else {
       unsigned long long t0 = 0;
       int spins = 0;
-      while (ld_relaxed(gen) == g) {
-        if (++spins > 64) {
-          __nanosleep(64);
+      while (((ld_relaxed(bar) ^ old) & 0x80000000u) == 0) {
+        if (++spins > 1024) {
+          spins = 0;
           if (t0 == 0) t0 = globaltimer();
-          else if (globaltimer() - t0 > 20000000000ULL) {
+          else if (globaltimer() - t0 > 20000000000ULL) {   // 20 s watchdog
             atomicCAS(err, 0, EQ_ERR_CUDA);
             s_ok = 0;
             break;
@@ -197,6 +190,14 @@ __device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned nblocks, int* 
   }
   __syncthreads();
   return s_ok;
+}
+
+// A value published by grid_sync's last arriver (sentinel -1 until then).
+__device__ __forceinline__ long long ld_published(const long long* p) {
+  long long v;
+  while ((v = *(volatile const long long*)p) == -1LL) {
+  }
+  return v;
 }
 
 template <typename T>

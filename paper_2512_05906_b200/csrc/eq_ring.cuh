@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
       // ---------------- (a2) fan-out of step m-1 (and imported spikes): fwd_fanout
       if (A.kind == EQ_KIND_RING && m > A.m0) {
         const int me = m - 1;                          // emitting step
-        const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
+        const long long L0 = ld_published(A.step_start + me), S = ld_published(A.step_start + me + 1) - L0;
         fwd_fanout<T, NT, NF, false>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G, s_spk, s_r0,
                                      s_pre, s_bin);
       }

@@ -1203,6 +1203,9 @@ int eq_run(eq_handle* h, int32_t n_steps, void* v_trace, void* stream) {
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
+  // step_start[m0+1 .. m1]: sentinel -1 until the barrier after each phase publishes it
+  if (n_steps > 0)
+    EQ_CUDA(h, cudaMemsetAsync(h->step_start + h->steps_done + 1, 0xFF, (size_t)n_steps * sizeof(long long), s));
   if (h->cfg.precision == 32) return launch_forward<float>(h, n_steps, v_trace, s);
   return launch_forward<double>(h, n_steps, v_trace, s);
 }

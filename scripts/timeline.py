@@ -18,7 +18,8 @@ from paper_2512_05906_b200.engine import Engine  # noqa: E402
 import bench  # noqa: E402
 
 
-ORDER = {"forward": [(5, "deliver done"), (1, "fan-out done"), (4, "update done"), (6, "clear+log done"),
+ORDER = {"forward": [(5, "deliver done"), (1, "fan-out done / owner done"), (4, "update done"),
+                     (6, "clear+log done"),
                      (2, "both sides done"), (3, "barrier done")],
          "reverse": [(4, "stage done"), (5, "events done"), (1, "R-fanout done"), (6, "R-neuron done"),
                      (2, "both sides done"), (3, "barrier done")]}
@@ -49,11 +50,13 @@ def main():
     ap.add_argument("--trials", type=int, default=16)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--kind", default="ring")
+    ap.add_argument("--capacity", type=int, default=0)
     args = ap.parse_args()
     net, mask, amp, T = bench.make_inputs(args.config, args.trials, 0)
     T = args.steps
     mask = np.ascontiguousarray(mask[:, :T])
-    eng = Engine(net.n, args.trials, T, precision=32)
+    eng = Engine(net.n, args.trials, T, precision=32, kind=args.kind, capacity=args.capacity)
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     eng.set_drive(mask, amp)
     for _ in range(2):
