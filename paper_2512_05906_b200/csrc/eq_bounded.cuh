@@ -350,11 +350,12 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
         const long long x = s_r0[k] + ro;
         const SpikeRec<T> rec = s_spk[k];
         const int b = c.divN.div(rec.idx);
-        const int jt = __ldg(F.net.col + x);
-        const T w = __ldg(F.net.w + x);
-        const T d = __ldg(F.net.d + x);
+        const EdgeRec<T> ed = ld_edge(F.net.er + x);
+        const int jt = ed.col;
+        const T w = ed.w;
+        const T d = ed.d;
         const T t_post = rec.t + d;
-        const int ds = delivery_step(t_post, d, c.dt, m);
+        const int ds = delivery_step_coded(t_post, (unsigned short)ed.code, c.dt, m);
         T ws, wm;
         if (F.exact) {
           const T phi = (T)ds * c.dt - t_post;

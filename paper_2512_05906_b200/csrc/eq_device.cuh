@@ -259,6 +259,43 @@ __device__ __forceinline__ int delivery_step_coded(T t_post, unsigned short code
   return q > m + 2 ? q : m + 2;
 }
 
+// One packed record per CSR edge (built by eq_set_network): the fan-outs read
+// a whole edge with one vector load instead of four scalar ones, so the loads
+// of several events stay in flight without spilling (the 64-register budget
+// of the 2-CTA/SM persistent kernels).  code = delivery_code(d, dt).
+template <typename T>
+struct EdgeRec;
+template <>
+struct alignas(16) EdgeRec<float> {
+  int col;
+  float w, d;
+  int code;
+};
+template <>
+struct alignas(8) EdgeRec<double> {
+  int col;
+  int code;
+  double w, d;
+};
+__device__ __forceinline__ EdgeRec<float> ld_edge(const EdgeRec<float>* p) {
+  const int4 v = __ldcs(reinterpret_cast<const int4*>(p));   // streamed once per event: evict-first
+  EdgeRec<float> e;
+  e.col = v.x;
+  e.w = __int_as_float(v.y);
+  e.d = __int_as_float(v.z);
+  e.code = v.w;
+  return e;
+}
+__device__ __forceinline__ EdgeRec<double> ld_edge(const EdgeRec<double>* p) {
+  const int2 h = __ldcs(reinterpret_cast<const int2*>(p));
+  EdgeRec<double> e;
+  e.col = h.x;
+  e.code = h.y;
+  e.w = __ldcs(&p->w);
+  e.d = __ldcs(&p->d);
+  return e;
+}
+
 template <typename T>
 struct alignas(16) SpikeRec;
 template <>

@@ -31,6 +31,11 @@ struct StepConsts {
   FastDiv divN;             // idx -> trial
 };
 
+// calendar bucket entry: fp32 {target, packed pair} = one 16-byte access;
+// fp64 {target, qs, qm, pad} = two
+template <typename T>
+__host__ __device__ constexpr int bk_words() { return Prec<T>::kSlotWords == 1 ? 2 : 4; }
+
 template <typename T>
 struct NetView {
   const int64_t* rowptr;
@@ -38,6 +43,7 @@ struct NetView {
   const T* w;
   const T* d;
   const unsigned short* dcode;  // [E] delivery_code(d, dt)
+  const EdgeRec<T>* er;         // [E] packed {col, w, d, code}
   const uint32_t* mask;  // [B][t_mask][words]
   const T* amp;          // [N]
   int words, t_mask;
@@ -72,8 +78,7 @@ struct FwdArgs {
   // calendar (ring kind): events due at step s wait in bucket s % NB until phase
   // s-1 delivers them into the L2-resident accumulator acc[s & 1]
   long long* acc;        // [2][total] x words
-  int* bk_tgt;           // [G][NB][cap_b] flat target index (per-CTA private buckets)
-  long long* bk_pay;     // [G][NB][cap_b] x words
+  long long* bk;         // [G][NB][cap_b] entries {target, payload} (bk_words<T>() int64 each; per-CTA private)
   int* bk_cnt;           // [G][NB] fill (kept in smem inside a launch)
   long long cap_b;
   int NB;
@@ -255,8 +260,7 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
   const int* llen = kImp ? A.imp_len : A.log_len;
   const int me_fixed = m - 1;
   long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
-  int* bt_cta = A.bk_tgt + (size_t)cta * A.NB * A.cap_b;
-  long long* bp_cta = A.bk_pay + (size_t)cta * A.NB * A.cap_b * P::kSlotWords;
+  long long* bk_cta = A.bk + (size_t)cta * A.NB * A.cap_b * bk_words<T>();
   const int me_bin = kImp ? 0 : me_fixed % A.NB;
   for (long long k0 = s0; k0 < s1; k0 += kCap) {
     const int nb = (int)(s1 - k0 < kCap ? s1 - k0 : kCap);
@@ -282,10 +286,11 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
           const int k = find_row(s_pre, nb, f);
           const long long x = s_r0[k] + (f - s_pre[k]);
           kk[e] = k;
-          jj[e] = __ldcs(A.net.col + x);      // streamed once per event: evict-first
-          ww[e] = __ldcs(A.net.w + x);
-          dd[e] = __ldcs(A.net.d + x);
-          cc[e] = __ldcs(A.net.dcode + x);
+          const EdgeRec<T> ed = ld_edge(A.net.er + x);   // one 16-byte streamed load per event
+          jj[e] = ed.col;
+          ww[e] = ed.w;
+          dd[e] = ed.d;
+          cc[e] = (unsigned short)ed.code;
         }
       }
 #pragma unroll
@@ -331,13 +336,12 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
         }
         const int pos = atomicAdd(&s_bin[bn], 1);
         if (pos < A.cap_b) {
-          const size_t o = (size_t)bn * A.cap_b + pos;
-          __stcs(bt_cta + o, tgt);                          // read once, ~H/2 steps later
-          if (P::kSlotWords == 1) {
-            __stcs(bp_cta + o, pack2(q1, q2));
+          longlong2* o = reinterpret_cast<longlong2*>(bk_cta + ((size_t)bn * A.cap_b + pos) * bk_words<T>());
+          if (P::kSlotWords == 1) {                         // read once, ~H/2 steps later: streaming
+            __stcs(o, make_longlong2(tgt, pack2(q1, q2)));
           } else {
-            __stcs(bp_cta + 2 * o, q1);
-            __stcs(bp_cta + 2 * o + 1, q2);
+            __stcs(o, make_longlong2(tgt, q1));
+            __stcs(o + 1, make_longlong2(q2, 0));
           }
         } else {                                            // bucket full: DRAM ring row
           const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
@@ -427,32 +431,33 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         const int bin = (m + 1) % A.NB;
         int n = s_bin[bin];
         n = n < A.cap_b ? n : (int)A.cap_b;
-        const size_t base = ((size_t)cta * A.NB + bin) * A.cap_b;
-        const int* bt = A.bk_tgt + base;
-        const long long* bp = A.bk_pay + base * P::kSlotWords;
+        const longlong2* bk = reinterpret_cast<const longlong2*>(
+            A.bk + ((size_t)cta * A.NB + bin) * A.cap_b * bk_words<T>());
         long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
         constexpr int DV = 4;
         for (int q = gtid; q < n; q += DV * Ro::NF) {
-          int tg[DV];
-          long long pv[DV][2];
+          longlong2 ev[DV], ev2[DV];
 #pragma unroll
           for (int e = 0; e < DV; ++e) {
             const int k = q + e * Ro::NF;
-            tg[e] = -1;
+            ev[e] = make_longlong2(-1, 0);
             if (k < n) {
-              tg[e] = __ldcs(bt + k);
-              pv[e][0] = __ldcs(bp + (size_t)k * P::kSlotWords);
-              pv[e][1] = P::kSlotWords == 2 ? __ldcs(bp + (size_t)k * P::kSlotWords + 1) : 0;
+              if (P::kSlotWords == 1) {
+                ev[e] = __ldcs(bk + k);
+              } else {
+                ev[e] = __ldcs(bk + 2 * (size_t)k);
+                ev2[e] = __ldcs(bk + 2 * (size_t)k + 1);
+              }
             }
           }
 #pragma unroll
           for (int e = 0; e < DV; ++e) {
-            if (tg[e] < 0) continue;
+            if (ev[e].x < 0) continue;
             if (P::kSlotWords == 1) {
-              red_add(accn + tg[e], pv[e][0]);
+              red_add(accn + ev[e].x, ev[e].y);
             } else {
-              red_add(accn + 2 * (size_t)tg[e], pv[e][0]);
-              red_add(accn + 2 * (size_t)tg[e] + 1, pv[e][1]);
+              red_add(accn + 2 * (size_t)ev[e].x, ev[e].y);
+              red_add(accn + 2 * (size_t)ev[e].x + 1, ev2[e].x);
             }
           }
         }
@@ -807,10 +812,11 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
             const long long x = s_r0[k] + (f - s_pre[k]);
             kk[e] = k;
             xx[e] = x;
-            jj[e] = __ldcs(A.net.col + x);
-            ww[e] = __ldcs(A.net.w + x);
-            dd[e] = __ldcs(A.net.d + x);
-            cc[e] = __ldcs(A.net.dcode + x);
+            const EdgeRec<T> ed = ld_edge(A.net.er + x);   // one 16-byte streamed load per event
+            jj[e] = ed.col;
+            ww[e] = ed.w;
+            dd[e] = ed.d;
+            cc[e] = (unsigned short)ed.code;
           }
         }
 #pragma unroll

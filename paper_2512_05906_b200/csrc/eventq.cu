@@ -62,6 +62,7 @@ struct eq_handle {
   const uint32_t* mask = nullptr;
   const void* amp = nullptr;
   unsigned short* dcode = nullptr;   // per-edge delivery codes
+  void* edges = nullptr;             // packed EdgeRec<T>[E] (snapshot of col/w/d at eq_set_network)
   bool net_set = false, drive_set = false;
   bool l2_set = false;
   size_t tsize = 4;
@@ -73,8 +74,7 @@ struct eq_handle {
   size_t ring_words = 0;
   // calendar (ring kind)
   long long* acc = nullptr;
-  int* bk_tgt = nullptr;
-  long long* bk_pay = nullptr;
+  long long* bk = nullptr;
   int* bk_cnt = nullptr;
   long long cap_b = 0;
   int NB = 0;
@@ -223,6 +223,7 @@ NetView<T> netview(const eq_handle* h) {
   n.w = (const T*)h->w;
   n.d = (const T*)h->d;
   n.dcode = h->dcode;
+  n.er = (const EdgeRec<T>*)h->edges;
   n.mask = h->mask;
   n.amp = (const T*)h->amp;
   n.words = (h->cfg.n_neurons + 31) / 32;
@@ -270,9 +271,18 @@ __global__ void k_net_stats(int n_rows, int N, int src_off, const int64_t* rowpt
 }
 
 template <typename T>
-__global__ void k_dcode(const T* d, long long E, T dt, unsigned short* out) {
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < E; x += (long long)gridDim.x * blockDim.x)
-    out[x] = delivery_code(d[x], dt);
+__global__ void k_pack_edges(const int32_t* col, const T* w, const T* d, long long E, T dt, unsigned short* code,
+                             EdgeRec<T>* out) {
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < E; x += (long long)gridDim.x * blockDim.x) {
+    const unsigned short cd = delivery_code(d[x], dt);
+    code[x] = cd;
+    EdgeRec<T> e;
+    e.col = col[x];
+    e.w = w[x];
+    e.d = d[x];
+    e.code = cd;
+    out[x] = e;
+  }
 }
 
 __global__ void k_max_ll(const long long* a, long long n, long long* out) {
@@ -329,7 +339,7 @@ __global__ void k_decode_spikes(const SpikeRec<T>* log, const long long* chunk_o
 // due `now`, acc[(now+1)&1] due now+1, the CTAs' buckets (now+h)%NB due now+h
 // (h >= 2), plus flagged DRAM ring rows (bucket overflow).  out int64 [B*N][H][2].
 template <typename T>
-__global__ void k_pending_calendar(const long long* acc, const int* bk_tgt, const long long* bk_pay,
+__global__ void k_pending_calendar(const long long* acc, const long long* bk,
                                    const int* bk_cnt, long long cap_b, int NB, int G, const long long* ring,
                                    const int* ring_dirty, int B, int R, int N, int H, int now, long long* out) {
   const int W = Prec<T>::kSlotWords;
@@ -365,9 +375,10 @@ __global__ void k_pending_calendar(const long long* acc, const int* bk_tgt, cons
       n = n < cap_b ? n : cap_b;
       const size_t base = ((size_t)cta * NB + bin) * cap_b;
       for (long long k = g0; k < n; k += stride) {
-        const long long tg = bk_tgt[base + k];
+        const long long* ent = bk + (base + k) * bk_words<T>();
+        const long long tg = ent[0];
         long long qs, qm;
-        const long long* pp = bk_pay + (base + k) * W;
+        const long long* pp = ent + 1;
         if (W == 1) unpack2(pp[0], qs, qm);
         else { qs = pp[0]; qm = pp[1]; }
         atomicAdd(reinterpret_cast<unsigned long long*>(out + (tg * H + h) * 2), (unsigned long long)qs);
@@ -578,8 +589,7 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
   A.refr = h->refr;
   A.ring = h->ring;
   A.acc = h->acc;
-  A.bk_tgt = h->bk_tgt;
-  A.bk_pay = h->bk_pay;
+  A.bk = h->bk;
   A.bk_cnt = h->bk_cnt;
   A.cap_b = h->cap_b;
   A.NB = h->NB;
@@ -1104,10 +1114,14 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   h->E = n_edges;
   if (h->horizon > 0x7ffe) return fail(h, EQ_ERR_CONFIGURATION, "delay horizon beyond 32766 steps");
   EQ_CUDA(h, ensure(h, (void**)&h->dcode, (size_t)n_edges * sizeof(unsigned short)));
+  EQ_CUDA(h, ensure(h, &h->edges, (size_t)n_edges * (c.precision == 32 ? sizeof(EdgeRec<float>)
+                                                                         : sizeof(EdgeRec<double>))));
   if (c.precision == 32)
-    k_dcode<float><<<1184, 256, 0, s>>>((const float*)delay, n_edges, (float)c.dt, h->dcode);
+    k_pack_edges<float><<<1184, 256, 0, s>>>(col, (const float*)weight, (const float*)delay, n_edges, (float)c.dt,
+                                             h->dcode, (EdgeRec<float>*)h->edges);
   else
-    k_dcode<double><<<1184, 256, 0, s>>>((const double*)delay, n_edges, c.dt, h->dcode);
+    k_pack_edges<double><<<1184, 256, 0, s>>>(col, (const double*)weight, (const double*)delay, n_edges, c.dt,
+                                              h->dcode, (EdgeRec<double>*)h->edges);
   h->launches += 1;
   // queue storage
   size_t words = c.kind == EQ_KIND_RING ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
@@ -1126,8 +1140,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
     h->cap_b = std::max<long long>(256, (h->total * avg_deg / 64 + h->G - 1) / h->G);
     if (h->cap_b > (1LL << 30)) h->cap_b = 1LL << 30;
     EQ_CUDA(h, ensure(h, (void**)&h->acc, (size_t)2 * h->total * wd * sizeof(long long)));
-    EQ_CUDA(h, ensure(h, (void**)&h->bk_tgt, (size_t)h->G * h->NB * h->cap_b * sizeof(int)));
-    EQ_CUDA(h, ensure(h, (void**)&h->bk_pay, (size_t)h->G * h->NB * h->cap_b * wd * sizeof(long long)));
+    EQ_CUDA(h, ensure(h, (void**)&h->bk, (size_t)h->G * h->NB * h->cap_b * (wd == 1 ? 2 : 4) * sizeof(long long)));
     EQ_CUDA(h, ensure(h, (void**)&h->bk_cnt, (size_t)h->G * h->NB * sizeof(int)));
     EQ_CUDA(h, ensure(h, (void**)&h->ring_dirty, (size_t)h->R * sizeof(int)));
   }
@@ -1469,11 +1482,11 @@ int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream) {
   } else {
     EQ_CUDA(h, cudaMemsetAsync(buf, 0, n * sizeof(long long), s));
     if (h->cfg.precision == 32)
-      k_pending_calendar<float><<<592, 256, 0, s>>>(h->acc, h->bk_tgt, h->bk_pay, h->bk_cnt, h->cap_b, h->NB, h->G,
+      k_pending_calendar<float><<<592, 256, 0, s>>>(h->acc, h->bk, h->bk_cnt, h->cap_b, h->NB, h->G,
                                                      h->ring,
                                                      h->ring_dirty, B, h->R, N, H, h->steps_done, (long long*)buf);
     else
-      k_pending_calendar<double><<<592, 256, 0, s>>>(h->acc, h->bk_tgt, h->bk_pay, h->bk_cnt, h->cap_b, h->NB,
+      k_pending_calendar<double><<<592, 256, 0, s>>>(h->acc, h->bk, h->bk_cnt, h->cap_b, h->NB,
                                                       h->G, h->ring, h->ring_dirty, B, h->R, N, H, h->steps_done,
                                                       (long long*)buf);
   }
