@@ -17,7 +17,7 @@ for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     eng.set_drive(md, torch.from_numpy(amp).cuda().float())
     fw, bw = [], []
-    for it in range(6):
+    for it in range(int(os.environ.get("NOISE_ITERS", "6"))):
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record()
         out = eng.forward()
