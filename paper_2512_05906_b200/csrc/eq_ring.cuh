@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         const int j0 = (int)(begin > tb0 ? begin - tb0 : 0);
         const int j1 = (int)(end < (long long)tb0 + A.N ? end - tb0 : A.N);
         const uint32_t* mrow = A.net.mask + ((size_t)b * A.net.t_mask + mm) * A.net.words;
-        if (P::kSlotWords == 1 && (A.N & 3) == 0 && !dirty) {
+        if (P::kSlotWords == 1 && A.kind == EQ_KIND_RING && (A.N & 3) == 0 && !dirty) {
           // fp32 fast path: four neurons per thread with 16-byte accesses
           // (segment bounds are multiples of 4 when N % 4 == 0: ranges are
           // warp-aligned).  Same per-neuron arithmetic as the scalar path.
@@ -536,6 +536,11 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
             }
             *reinterpret_cast<float4*>(A.I + idx) = make_float4(In[0], In[1], In[2], In[3]);
             *reinterpret_cast<float4*>(A.V + idx) = make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
+            // RingQueue._pop_raw zeroes the slot (queues.py:114-117): the load has been
+            // consumed, so this store does not wait behind it
+            long long* accz = const_cast<long long*>(accm) + idx;
+            *reinterpret_cast<longlong2*>(accz) = make_longlong2(0, 0);
+            *reinterpret_cast<longlong2*>(accz + 2) = make_longlong2(0, 0);
             if (A.refractory)
               *reinterpret_cast<int4*>(A.refr + idx) = make_int4(rf4[0], rf4[1], rf4[2], rf4[3]);
             if (A.v_trace)
@@ -625,7 +630,8 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
       // queues.py:114-117), in a separate pass: a store next to the pending
       // load of the same line stalled the pop loop ~8x.  acc[m&1] receives no
       // red.add in this phase (the event side writes acc[(m+1)&1]).
-      if (A.kind == EQ_KIND_RING) {
+      const bool cleared = P::kSlotWords == 1 && A.kind == EQ_KIND_RING && (A.N & 3) == 0 && !dirty;   // by the vector update
+      if (A.kind == EQ_KIND_RING && !cleared) {
         long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
         if (P::kSlotWords == 1 && ((begin | end) & 1) == 0) {
           for (long long idx = begin + 2 * gtid; idx < end; idx += 2 * Ro::NN)

@@ -26,8 +26,8 @@ namespace {
 
 constexpr int kNT = 512;   // threads per CTA of the persistent kernels
 constexpr int kU = 4;      // neurons per thread in flight per round
-constexpr int kSplitF = 384;  // forward event-side threads per CTA
-constexpr int kSplitB = 256;  // reverse event-side threads per CTA
+constexpr int kSplitF = 288;  // forward event-side threads per CTA (measured: 224..384, profiles/)
+constexpr int kSplitB = 352;  // reverse event-side threads per CTA (measured: 224..448, profiles/)
 
 
 struct DeviceGuard {
