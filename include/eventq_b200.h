@@ -211,6 +211,14 @@ int eq_queues_enqueue(eq_queues* h, const int32_t* queue, const int32_t* deliver
  * has[q] = 0 where _pop_raw would return None. */
 int eq_queues_pop(eq_queues* h, void* out_w, void* out_dw, void* out_wtt, uint8_t* out_has, void* stream);
 int eq_queues_occupancy(eq_queues* h, int32_t* out, void* stream);
+/* The reference's Poisson queue benchmark (bench.py:183-205 _drive_queue) for
+ * all Q queues in one launch: for each step s < t_steps pop, then if bit s of
+ * queue q's stream is set enqueue a unit event due `delay` steps later; then
+ * delay+1 draining pops.  spikes: device uint32 [Q][ceil(t_steps/32)].
+ * Outputs (device): delivered weight (double[Q]) and accepted events
+ * (int64[Q]).  Advances `now` by t_steps + delay + 1. */
+int eq_queues_run_poisson(eq_queues* h, const uint32_t* spikes, int32_t t_steps, int32_t delay, double* delivered,
+                          int64_t* accepted, void* stream);
 /* LossyRingQueue.aliased / .merged per queue (device int64 arrays). */
 int eq_queues_lossy_counts(eq_queues* h, int64_t* aliased, int64_t* merged, void* stream);
 

@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
         "eq_queues_enqueue": (ctypes.c_int, [H, vp, vp, vp, vp, vp, i64, vp, vp]),
         "eq_queues_pop": (ctypes.c_int, [H, vp, vp, vp, vp, vp]),
         "eq_queues_occupancy": (ctypes.c_int, [H, vp, vp]),
+        "eq_queues_run_poisson": (ctypes.c_int, [H, vp, i32, i32, vp, vp, vp]),
         "eq_queues_lossy_counts": (ctypes.c_int, [H, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -96,7 +97,7 @@ EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_ne
             "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",
             "eq_launch_count", "eq_debug_timeline", "eq_queues_create", "eq_queues_destroy",
             "eq_queues_last_error", "eq_queues_capacity", "eq_queues_now", "eq_queues_enqueue", "eq_queues_pop",
-            "eq_queues_occupancy", "eq_queues_lossy_counts")
+            "eq_queues_occupancy", "eq_queues_lossy_counts", "eq_queues_run_poisson")
 
 
 def check(handle, code: int, queues: bool = False) -> None:

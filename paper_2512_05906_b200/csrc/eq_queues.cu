@@ -87,6 +87,69 @@ __global__ void k_validate(QView<T> V, const int* sq, const int* sidx, const int
   }
 }
 
+// Apply one event of queue q at queue time `now` (enqueue, events.py:99-141);
+// returns true if accepted.  Callers have validated causality/capability.
+template <typename T>
+__device__ __forceinline__ bool apply_one(const QView<T>& V, int q, int now, int step, T w, T dw, T tt) {
+  if (V.kind == EQ_KIND_DONOTHING) return false;
+  if (V.kind == EQ_KIND_RING || V.kind == EQ_KIND_LOSSYRING) {
+    if (V.kind == EQ_KIND_LOSSYRING && step - now >= V.cap) V.aliased[q] += 1;   // queues.py:164-165
+    const size_t s = (size_t)q * V.cap + (step % V.cap);
+    if (!V.occ[s]) {
+      V.occ[s] = 1;
+      V.count[q] += 1;
+    } else if (V.kind == EQ_KIND_LOSSYRING) {
+      V.merged[q] += 1;                                                  // :167-168
+    }
+    V.sw[s] = V.sw[s] + w;                                               // :104-106
+    V.sdw[s] = V.sdw[s] + dw;
+    V.swtt[s] = V.swtt[s] + w * tt;
+    return true;
+  }
+  const int cnt = V.count[q];
+  if (cnt == V.cap) return false;                                        // drop incoming
+  Ev<T>* a = V.ev + (size_t)q * V.cap;
+  Ev<T> x;
+  x.due = step;
+  x.seq = 0;
+  x.w = w;
+  x.dw = dw;
+  x.tt = tt;
+  if (V.kind == EQ_KIND_FIFORING) {                                      // :227-231
+    int slot = V.head[q] + cnt;
+    if (slot >= V.cap) slot -= V.cap;
+    a[slot] = x;
+    V.tail_key[q] = step;
+  } else if (V.kind == EQ_KIND_BINARYHEAP) {                             // :516-528
+    x.seq = V.seq[q]++;
+    int i = cnt;
+    while (i > 0) {
+      const int parent = (i - 1) >> 1;
+      if (!kless(x.due, x.seq, a[parent].due, a[parent].seq)) break;
+      a[i] = a[parent];
+      i = parent;
+    }
+    a[i] = x;
+  } else {                                                               // sorted, stable (:348-366)
+    const int h = V.head[q];
+    int kk = cnt;
+    while (kk > 0) {
+      int pi = h + kk - 1;
+      if (pi >= V.cap) pi -= V.cap;
+      if (a[pi].due <= step) break;
+      int di = pi + 1;
+      if (di >= V.cap) di -= V.cap;
+      a[di] = a[pi];
+      --kk;
+    }
+    int di = h + kk;
+    if (di >= V.cap) di -= V.cap;
+    a[di] = x;
+  }
+  V.count[q] = cnt + 1;
+  return true;
+}
+
 template <typename T>
 __global__ void k_apply(QView<T> V, const int* sq, const int* sidx, const int* due, const T* w, const T* dw,
                         const T* tt, long long n, int limit, unsigned char* accepted) {
@@ -96,82 +159,20 @@ __global__ void k_apply(QView<T> V, const int* sq, const int* sidx, const int* d
     for (long long r = k; r < n && sq[r] == q; ++r) {
       const int e = sidx[r];
       if (e >= limit) break;   // at or after the first error in call order
-      const int step = due[e];
-      bool ok = true;
-      if (V.kind == EQ_KIND_DONOTHING) {
-        ok = false;
-      } else if (V.kind == EQ_KIND_RING || V.kind == EQ_KIND_LOSSYRING) {
-        if (V.kind == EQ_KIND_LOSSYRING && step - V.now >= V.cap) V.aliased[q] += 1;   // queues.py:164-165
-        const size_t s = (size_t)q * V.cap + (step % V.cap);
-        if (!V.occ[s]) {
-          V.occ[s] = 1;
-          V.count[q] += 1;
-        } else if (V.kind == EQ_KIND_LOSSYRING) {
-          V.merged[q] += 1;                                                  // :167-168
-        }
-        V.sw[s] = V.sw[s] + w[e];                                            // :104-106
-        V.sdw[s] = V.sdw[s] + dw[e];
-        V.swtt[s] = V.swtt[s] + w[e] * tt[e];
-      } else {
-        int cnt = V.count[q];
-        if (cnt == V.cap) {
-          ok = false;                                                        // drop incoming
-        } else {
-          Ev<T>* a = V.ev + (size_t)q * V.cap;
-          Ev<T> x;
-          x.due = step;
-          x.seq = 0;
-          x.w = w[e];
-          x.dw = dw[e];
-          x.tt = tt[e];
-          if (V.kind == EQ_KIND_FIFORING) {                                 // :227-231
-            int slot = V.head[q] + cnt;
-            if (slot >= V.cap) slot -= V.cap;
-            a[slot] = x;
-            V.tail_key[q] = step;
-          } else if (V.kind == EQ_KIND_BINARYHEAP) {                        // :516-528
-            x.seq = V.seq[q]++;
-            int i = cnt;
-            while (i > 0) {
-              const int parent = (i - 1) >> 1;
-              if (!kless(x.due, x.seq, a[parent].due, a[parent].seq)) break;
-              a[i] = a[parent];
-              i = parent;
-            }
-            a[i] = x;
-          } else {                                                           // sorted, stable (:348-366)
-            const int h = V.head[q];
-            int kk = cnt;
-            while (kk > 0) {
-              int pi = h + kk - 1;
-              if (pi >= V.cap) pi -= V.cap;
-              if (a[pi].due <= step) break;
-              int di = pi + 1;
-              if (di >= V.cap) di -= V.cap;
-              a[di] = a[pi];
-              --kk;
-            }
-            int di = h + kk;
-            if (di >= V.cap) di -= V.cap;
-            a[di] = x;
-          }
-          V.count[q] = cnt + 1;
-        }
-      }
-      accepted[e] = ok ? 1 : 0;
+      accepted[e] = apply_one<T>(V, q, V.now, due[e], w[e], dw[e], tt[e]) ? 1 : 0;
     }
   }
 }
 
-// pop_due for every queue: sums in insertion order; has = a slot/event was due.
+// pop_due of queue q at queue time `now`: sums in insertion order; returns
+// whether a slot/event was due (queues.py:109-120, :245-254, :378-398, :555-568).
 template <typename T>
-__global__ void k_pop(QView<T> V, T* ow, T* odw, T* owtt, unsigned char* has) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= V.Q) return;
-  const int now = V.now;
-  T w = (T)0, dw = (T)0, wtt = (T)0;
+__device__ __forceinline__ bool pop_one(const QView<T>& V, int q, int now, T& w, T& dw, T& wtt) {
+  w = (T)0;
+  dw = (T)0;
+  wtt = (T)0;
   bool got = false;
-  if (V.kind == EQ_KIND_RING || V.kind == EQ_KIND_LOSSYRING) {              // queues.py:109-120
+  if (V.kind == EQ_KIND_RING || V.kind == EQ_KIND_LOSSYRING) {
     const size_t s = (size_t)q * V.cap + (now % V.cap);
     if (V.occ[s]) {
       got = true;
@@ -187,7 +188,7 @@ __global__ void k_pop(QView<T> V, T* ow, T* odw, T* owtt, unsigned char* has) {
   } else if (V.kind != EQ_KIND_DONOTHING) {
     Ev<T>* a = V.ev + (size_t)q * V.cap;
     int cnt = V.count[q];
-    if (V.kind == EQ_KIND_BINARYHEAP) {                                      // :555-568
+    if (V.kind == EQ_KIND_BINARYHEAP) {
       while (cnt > 0 && a[0].due == now) {
         const Ev<T> top = a[0];
         got = true;
@@ -210,7 +211,7 @@ __global__ void k_pop(QView<T> V, T* ow, T* odw, T* owtt, unsigned char* has) {
           a[i] = item;
         }
       }
-    } else {                                                                 // fifo :245-254, sorted :378-398
+    } else {
       int h = V.head[q];
       while (cnt > 0 && a[h].due == now) {
         got = true;
@@ -225,10 +226,58 @@ __global__ void k_pop(QView<T> V, T* ow, T* odw, T* owtt, unsigned char* has) {
     }
     V.count[q] = cnt;
   }
+  return got;
+}
+
+template <typename T>
+__global__ void k_pop(QView<T> V, T* ow, T* odw, T* owtt, unsigned char* has) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= V.Q) return;
+  T w, dw, wtt;
+  const bool got = pop_one<T>(V, q, V.now, w, dw, wtt);
   ow[q] = w;
   odw[q] = dw;
   owtt[q] = wtt;
   has[q] = got ? 1 : 0;
+}
+
+// The reference's single-queue Poisson benchmark (bench.py:183-205
+// _drive_queue) for every queue of the batch in one launch: queues are
+// independent, so each thread steps its own queue through the whole stream —
+// pop, then enqueue a unit event due `delay` steps later if the stream spikes
+// — and drains the in-flight tail with delay+1 more pops.
+template <typename T>
+__global__ void k_poisson(QView<T> V, const uint32_t* spikes, int words, int t_steps, int delay, double* delivered,
+                          long long* accepted, int* err) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= V.Q) return;
+  const uint32_t* row = spikes + (size_t)q * words;
+  int now = V.now;
+  double del = 0.0;
+  long long acc = 0;
+  T w, dw, wtt;
+  for (int s = 0; s < t_steps; ++s) {
+    if (pop_one<T>(V, q, now, w, dw, wtt)) del += (double)w;
+    now += 1;
+    if ((__ldg(row + (s >> 5)) >> (s & 31)) & 1u) {
+      const int step = V.now + s + delay;
+      if (V.kind == EQ_KIND_RING && step - now >= V.cap) {               // queues.py:94-98
+        atomicCAS(err, 0, EQ_ERR_CAPABILITY);
+        break;
+      }
+      if (V.kind == EQ_KIND_FIFORING && V.tail_key[q] > step) {           // queues.py:220-224
+        atomicCAS(err, 0, EQ_ERR_CAPABILITY);
+        break;
+      }
+      if (apply_one<T>(V, q, now, step, (T)1, (T)0, (T)0)) acc += 1;
+    }
+  }
+  for (int k = 0; k <= delay; ++k) {
+    if (pop_one<T>(V, q, now, w, dw, wtt)) del += (double)w;
+    now += 1;
+  }
+  delivered[q] = del;
+  accepted[q] = acc;
 }
 
 }  // namespace
@@ -466,6 +515,36 @@ int eq_queues_pop(eq_queues* h, void* out_w, void* out_dw, void* out_wtt, uint8_
                                          out_has);
   QCUDA(h, cudaGetLastError());
   h->now += 1;
+  return EQ_OK;
+}
+
+int eq_queues_run_poisson(eq_queues* h, const uint32_t* spikes, int32_t t_steps, int32_t delay, double* delivered,
+                          int64_t* accepted, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (t_steps < 1 || delay < 1) return qfail(h, EQ_ERR_CONFIGURATION, "t_steps and delay must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  int zero = 0;
+  QCUDA(h, cudaMemcpyAsync(h->bad, &zero, sizeof zero, cudaMemcpyHostToDevice, s));
+  const int blocks = (h->Q + 127) / 128, words = (t_steps + 31) / 32;
+  if (h->precision == 32)
+    k_poisson<float><<<blocks, 128, 0, s>>>(view<float>(h), spikes, words, t_steps, delay, delivered,
+                                            (long long*)accepted, h->bad);
+  else
+    k_poisson<double><<<blocks, 128, 0, s>>>(view<double>(h), spikes, words, t_steps, delay, delivered,
+                                             (long long*)accepted, h->bad);
+  QCUDA(h, cudaGetLastError());
+  int e = 0;
+  QCUDA(h, cudaMemcpyAsync(&e, h->bad, sizeof e, cudaMemcpyDeviceToHost, s));
+  QCUDA(h, cudaStreamSynchronize(s));
+  h->now += t_steps + delay + 1;
+  if (e) {
+    char buf[160];
+    if (h->kind == EQ_KIND_RING)
+      snprintf(buf, sizeof buf, "ring: delay of %d steps exceeds buffer capacity %d", delay, h->cap);
+    else
+      snprintf(buf, sizeof buf, "fiforing supports homogeneous delays only");
+    return qfail(h, e, buf);
+  }
   return EQ_OK;
 }
 

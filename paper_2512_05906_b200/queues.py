@@ -133,6 +133,24 @@ class QueueBatch:
                                                     self._stream), queues=True)
         return self._w, self._dw, self._wtt, self._has
 
+    def run_poisson(self, spike_bits: torch.Tensor, t_steps: int, delay: int):
+        """The reference's Poisson queue benchmark stream (bench.py:183-205) for
+        every queue in one launch.  spike_bits: uint32/int32 [n_queues,
+        ceil(t_steps/32)] (bit s of queue q = a spike at step s).  Returns
+        (delivered weight float64 [Q], accepted int64 [Q]) on the device."""
+        bits = torch.as_tensor(spike_bits).to(self.device)
+        if bits.dtype != torch.int32:
+            bits = bits.to(torch.int32)
+        bits = bits.contiguous()
+        if tuple(bits.shape) != (self.n, (t_steps + 31) // 32):
+            raise ConfigurationError(f"spike bits must be [{self.n}, {(t_steps + 31) // 32}]")
+        delivered = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        accepted = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        _native.check(self.h, self.L.eq_queues_run_poisson(
+            self.h, ctypes.c_void_p(bits.data_ptr()), int(t_steps), int(delay),
+            ctypes.c_void_p(delivered.data_ptr()), ctypes.c_void_p(accepted.data_ptr()), self._stream), queues=True)
+        return delivered, accepted
+
     def occupancy(self) -> torch.Tensor:
         out = torch.empty(self.n, dtype=torch.int32, device=self.device)
         _native.check(self.h, self.L.eq_queues_occupancy(self.h, ctypes.c_void_p(out.data_ptr()), self._stream),

@@ -227,6 +227,19 @@ def drive_masks(n: int, n_trials: int, t_steps: int, dt: float, seed0: int = 100
     return out
 
 
+def poisson_streams(lambda_steps: float, t_steps: int, n_queues: int, seed: int) -> np.ndarray:
+    """Bernoulli(1/lambda) spike streams of the reference's Poisson queue
+    benchmark (restates eventq.bench.gen_poisson, bench.py:86-96: one
+    SeedSequence child per queue, ``default_rng(child).random(T) < 1/lambda``).
+    Returns packed bits uint32 [n_queues, ceil(T/32)].  numpy's Generator
+    streams are version-dependent: the goldens pin them (tests/golden/p_*)."""
+    p = 1.0 / lambda_steps
+    out = np.empty((n_queues, (t_steps + 31) // 32), dtype=np.uint32)
+    for q, ss in enumerate(np.random.SeedSequence(seed).spawn(n_queues)):
+        out[q] = pack_mask(np.random.default_rng(ss).random(t_steps) < p)
+    return out
+
+
 CONFIGS = {
     # name: (n, k_out, delay steps, trials, steps)
     "C1": (1_000, 100, (1, 16), 1, 1000),
