@@ -53,3 +53,26 @@ def gen(name):
 if __name__ == "__main__":
     for name in CONFIGS:
         gen(name)
+
+
+# measure_drop_rate records (bench.py:408-452): kind, capacity, lambda, pressures, steps, seed
+DROP = [("lossyring", 8, 20.0, (0.2, 0.5, 1.0), 20000, 5), ("fiforing", 2, 20.0, (0.2, 0.5, 1.0), 20000, 6),
+        ("binaryheap", 3, 10.0, (0.5, 1.0, 2.0), 20000, 7), ("sortedarray", 3, 10.0, (0.5, 1.0, 2.0), 20000, 8)]
+
+
+def gen_drop():
+    from eventq.bench import measure_drop_rate
+    rows = []
+    for kind, cap, lam, prs, steps, seed in DROP:
+        for pr in prs:
+            delay = max(1, round(pr * lam))
+            r = measure_drop_rate(kind, lam, delay, steps, seed, capacity=cap)
+            rows.append((kind, cap, lam, delay, steps, seed, r.drop_rate, r.spikes_in, r.spikes_out))
+    import json
+    with open(os.path.join(OUT, "p_droprate.json"), "w") as f:
+        json.dump(rows, f, indent=0)
+    print("droprate rows", len(rows))
+
+
+if __name__ == "__main__":
+    gen_drop()

@@ -51,3 +51,27 @@ def test_poisson_ring_overflow_is_a_capability_error():
     qb = QueueBatch("ring", 4, 8, 8)
     with pytest.raises(CapabilityError, match="exceeds"):
         qb.run_poisson(bits.view(np.int32), 64, 10)
+
+
+@pytest.mark.gpu
+def test_drop_rates_equal_the_reference_records():
+    import json
+    from paper_2512_05906_b200.poisson import measure_drop_rate
+    rows = json.load(open(os.path.join(GOLDEN, "p_droprate.json")))
+    for kind, cap, lam, delay, steps, seed, rate, sin, sout in rows:
+        r = measure_drop_rate(kind, lam, delay, steps, seed, capacity=cap)
+        assert (r.drop_rate, r.spikes_in, r.spikes_out) == (rate, sin, sout), (kind, delay)
+
+
+@pytest.mark.gpu
+def test_sweeps_and_records():
+    from paper_2512_05906_b200.poisson import PoissonWorkload, records_to_csv_text, sweep
+    base = PoissonWorkload(20.0, 10, 64, 2000, 3)
+    recs = sweep("capacity", [2, 4, 8], "binaryheap", base, reps=3, warmup=1)
+    assert [r.capacity for r in recs] == [2, 4, 8]
+    rates = [r.drop_rate for r in recs]
+    assert rates[0] >= rates[1] >= rates[2]
+    txt = records_to_csv_text(recs)
+    assert txt.splitlines()[0].startswith("workload,kind,capacity,max_delay,batch,lambda")
+    recs = sweep("pressure", [0.5, 1.0], "fiforing", base, capacity=2, reps=3, warmup=1)
+    assert [r.delay_steps for r in recs] == [10, 20]
