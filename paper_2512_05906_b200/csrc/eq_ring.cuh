@@ -379,6 +379,252 @@ __global__ void __launch_bounds__(NT) k_import_fanout(FwdArgs<T> A) {
   for (int k = threadIdx.x; k < A.NB; k += NT) A.bk_cnt[(size_t)cta * A.NB + k] = s_bin[k];
 }
 
+// Neuron side of one forward phase m (network.py:547-580): pop (the slot sums
+// waiting in acc[m&1] when acc_pop — ring, and bounded kinds whose queue stage
+// wrote them), synapse + LIF + exact crossing for the CTA's neuron-trials, clear
+// the popped slots, then the spike log (one chunk per (step, CTA)) and the
+// per-trial counters.  Executed by the neuron-side warp group (gtid < NN).
+template <typename T, int NT, int U, int NF>
+__device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, const int cta, const int gtid,
+                                            const long long begin, const long long end, const int b_first,
+                                            const bool acc_pop, SpikeRec<T>* s_own, int& s_n, long long& s_off,
+                                            unsigned long long (*s_ctr)[3], SpikeRec<T>* spill) {
+  typedef Prec<T> P;
+  typedef Roles<NT, NF> Ro;
+  constexpr int kCapN = FwdShared<NT, T>::kCap / 2;
+  constexpr int kTr = FwdShared<NT>::kTrials;
+  const StepConsts<T>& c = A.c;
+  const bool dirty = A.kind == EQ_KIND_RING && ld_volatile(A.ring_dirty + m % A.R) != 0;
+  // ---------------- (b) neuron update: pop, synapse, membrane, crossing.
+  // Walked per trial segment of the owned range so the row pointers are
+  // computed once per segment, not per neuron.
+  const int mm = m < A.net.t_mask ? m : A.net.t_mask - 1;   // network.py:155 rows[-1]
+  const long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
+  const int b_last = (int)((end - 1) / A.N);
+  for (int b = b_first; b <= b_last; ++b) {
+    const int tb0 = b * A.N;
+    const int j0 = (int)(begin > tb0 ? begin - tb0 : 0);
+    const int j1 = (int)(end < (long long)tb0 + A.N ? end - tb0 : A.N);
+    const uint32_t* mrow = A.net.mask + ((size_t)b * A.net.t_mask + mm) * A.net.words;
+    if (P::kSlotWords == 1 && acc_pop && (A.N & 3) == 0 && !dirty) {
+      // fp32 fast path: four neurons per thread with 16-byte accesses
+      // (segment bounds are multiples of 4 when N % 4 == 0: ranges are
+      // warp-aligned).  Same per-neuron arithmetic as the scalar path.
+      for (int jq = j0 + 4 * gtid; jq < j1; jq += 4 * Ro::NN) {
+        const int idx = tb0 + jq;
+        const longlong2 a01 = *reinterpret_cast<const longlong2*>(accm + idx);
+        const longlong2 a23 = *reinterpret_cast<const longlong2*>(accm + idx + 2);
+        const float4 I4 = *reinterpret_cast<const float4*>(A.I + idx);
+        const float4 V4 = *reinterpret_cast<const float4*>(A.V + idx);
+        const float4 M4 = __ldg(reinterpret_cast<const float4*>(A.net.amp + jq));
+        const unsigned mw = __ldg(mrow + (jq >> 5)) >> (jq & 31);
+        int4 R4 = make_int4(0, 0, 0, 0);
+        if (A.refractory) R4 = *reinterpret_cast<const int4*>(A.refr + idx);
+        const long long av[4] = {a01.x, a01.y, a23.x, a23.y};
+        const float Iv4[4] = {I4.x, I4.y, I4.z, I4.w};
+        const float Vv4[4] = {V4.x, V4.y, V4.z, V4.w};
+        const float Av4[4] = {M4.x, M4.y, M4.z, M4.w};
+        int rf4[4] = {R4.x, R4.y, R4.z, R4.w};
+        float In[4], Vn[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          long long qs, qm;
+          unpack2(av[q], qs, qm);
+          const T ps = P::deq(qs, c.inv_scale);
+          const T pm = A.exact ? P::deq(qm, c.inv_scale) : (T)0;
+          const T drive = ((mw >> q) & 1u) ? (T)Av4[q] : (T)0;
+          T i, v_new, a, v, t_spk;
+          if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, (T)Iv4[q], (T)Vv4[q], drive, rf4[q], i, v_new,
+                       a, v, t_spk)) {
+            if (t_spk != t_spk) {
+              raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, jq + q);
+            } else {
+              int pos = atomicAdd(&s_n, 1);
+              SpikeRec<T> rec;
+              rec.idx = idx + q;
+              rec.t = t_spk;
+              rec.a = a;
+              rec.vh = v;
+              if (pos < kCapN) s_own[pos] = rec;
+              else spill[pos - kCapN] = rec;
+            }
+          }
+          In[q] = (float)i;
+          Vn[q] = (float)v_new;
+        }
+        *reinterpret_cast<float4*>(A.I + idx) = make_float4(In[0], In[1], In[2], In[3]);
+        *reinterpret_cast<float4*>(A.V + idx) = make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
+        // RingQueue._pop_raw zeroes the slot (queues.py:114-117): the load has been
+        // consumed, so this store does not wait behind it
+        long long* accz = const_cast<long long*>(accm) + idx;
+        *reinterpret_cast<longlong2*>(accz) = make_longlong2(0, 0);
+        *reinterpret_cast<longlong2*>(accz + 2) = make_longlong2(0, 0);
+        if (A.refractory)
+          *reinterpret_cast<int4*>(A.refr + idx) = make_int4(rf4[0], rf4[1], rf4[2], rf4[3]);
+        if (A.v_trace)
+          *reinterpret_cast<float4*>(A.v_trace + (size_t)(m - A.m0) * A.total + idx) =
+              make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
+      }
+      continue;
+    }
+    for (int jb = j0; jb < j1; jb += Ro::NN * U) {
+      long long slot_v[U][2];
+      T Iv[U], Vv[U], Am[U];
+      int rf[U];
+      unsigned mw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = jb + u * Ro::NN + gtid;
+        slot_v[u][0] = slot_v[u][1] = 0;
+        if (j < j1) {
+          const int idx = tb0 + j;
+          if (acc_pop) {
+            if (P::kSlotWords == 1) {
+              slot_v[u][0] = ld_slot(accm + idx);
+            } else {
+              slot_v[u][0] = ld_slot(accm + 2 * (size_t)idx);
+              slot_v[u][1] = ld_slot(accm + 2 * (size_t)idx + 1);
+            }
+            if (dirty) {                       // a bucket overflowed into the DRAM row
+              size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
+              if (P::kSlotWords == 1) {
+                slot_v[u][0] += ld_slot(A.ring + so);
+              } else {
+                slot_v[u][0] += ld_slot(A.ring + 2 * so);
+                slot_v[u][1] += ld_slot(A.ring + 2 * so + 1);
+              }
+            }
+          }
+          Iv[u] = A.I[idx];
+          Vv[u] = A.V[idx];
+          rf[u] = A.refractory ? A.refr[idx] : 0;
+          mw[u] = __ldg(mrow + (j >> 5));
+          Am[u] = __ldg(A.net.amp + j);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = jb + u * Ro::NN + gtid;
+        if (j >= j1) continue;
+        const int idx = tb0 + j;
+        T ps, pm;
+        if (P::kSlotWords == 1) {
+          long long qs, qm;
+          unpack2(slot_v[u][0], qs, qm);
+          ps = P::deq(qs, c.inv_scale);
+          pm = P::deq(qm, c.inv_scale);
+        } else {
+          ps = P::deq(slot_v[u][0], c.inv_scale);
+          pm = P::deq(slot_v[u][1], c.inv_scale);
+        }
+        if (!A.exact) pm = (T)0;
+        const T drive = ((mw[u] >> (j & 31)) & 1u) ? Am[u] : (T)0;
+        T i, v_new, a, v, t_spk;
+        if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, Iv[u], Vv[u], drive, rf[u], i, v_new, a, v,
+                     t_spk)) {
+          if (t_spk != t_spk) {
+            raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, j);
+          } else {
+            int pos = atomicAdd(&s_n, 1);
+            SpikeRec<T> rec;
+            rec.idx = idx;
+            rec.t = t_spk;
+            rec.a = a;
+            rec.vh = v;
+            if (pos < kCapN) s_own[pos] = rec;
+            else spill[pos - kCapN] = rec;
+          }
+        }
+        A.I[idx] = i;
+        A.V[idx] = v_new;
+        if (A.refractory) A.refr[idx] = rf[u];
+        if (A.v_trace) A.v_trace[(size_t)(m - A.m0) * A.total + idx] = v_new;
+      }
+    }
+  }
+  group_sync(Ro::kBarN, Ro::NN);
+  if (gtid == 0) tl_mark_any(A.tl, m, A.G, cta, 4);
+  // Clear the popped accumulator (RingQueue._pop_raw zeroes the slot,
+  // queues.py:114-117), in a separate pass: a store next to the pending
+  // load of the same line stalled the pop loop ~8x.  acc[m&1] receives no
+  // red.add in this phase (the event side writes acc[(m+1)&1]).
+  const bool cleared = P::kSlotWords == 1 && acc_pop && (A.N & 3) == 0 && !dirty;   // by the vector update
+  if (acc_pop && !cleared) {
+    long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
+    if (P::kSlotWords == 1 && ((begin | end) & 1) == 0) {
+      for (long long idx = begin + 2 * gtid; idx < end; idx += 2 * Ro::NN)
+        *reinterpret_cast<longlong2*>(accm + idx) = make_longlong2(0, 0);
+    } else {
+      for (int idx = (int)begin + gtid; idx < end; idx += Ro::NN) {
+        if (P::kSlotWords == 1) {
+          st_slot(accm + idx, 0);
+        } else {
+          st_slot(accm + 2 * (size_t)idx, 0);
+          st_slot(accm + 2 * (size_t)idx + 1, 0);
+        }
+      }
+    }
+    if (dirty) {
+      const int row = m % A.R;
+      for (int idx = (int)begin + gtid; idx < end; idx += Ro::NN) {
+        const int b = c.divN.div(idx);   // rare path (bucket overflow)
+        const size_t so = ((size_t)b * A.R + row) * A.N + (idx - b * A.N);
+        if (P::kSlotWords == 1) {
+          st_slot(A.ring + so, 0);
+        } else {
+          st_slot(A.ring + 2 * so, 0);
+          st_slot(A.ring + 2 * so + 1, 0);
+        }
+      }
+    }
+  }
+  const int nspk = s_n;
+  // ---------------- spike log: one chunk per (step, CTA); the chunks of a
+  // step are contiguous because every reservation of step m happens between
+  // the two barriers around phase m.  Counters per trial (spikes, events;
+  // donothing drops every event, queues.py:42-45).
+  if (gtid == 0) {
+    unsigned long long off = nspk ? atomicAdd(A.log_count, (unsigned long long)nspk) : 0ULL;
+    if (nspk && (long long)(off + nspk) > A.log_cap) {
+      raise_error(A.err, EQ_ERR_CAPACITY, m, -1, -1);
+      off = 0;
+    }
+    s_off = (long long)off;
+    A.chunk_off[(size_t)m * A.G + cta] = (long long)off;
+    A.chunk_cnt[(size_t)m * A.G + cta] = nspk;
+  }
+  group_sync(Ro::kBarN, Ro::NN);
+  const bool log_ok = s_off + nspk <= A.log_cap;
+  for (int k = gtid; k < nspk; k += Ro::NN) {
+    const SpikeRec<T> rec = k < kCapN ? s_own[k] : spill[k - kCapN];
+    const int b = c.divN.div(rec.idx);
+    const int i = rec.idx - b * A.N;
+    const long long r0 = __ldg(A.net.rowptr + A.src_off + i);
+    const unsigned long long len = (unsigned long long)(__ldg(A.net.rowptr + A.src_off + i + 1) - r0);
+    if (log_ok) {
+      A.log[s_off + k] = rec;
+      A.log_r0[s_off + k] = r0;
+      A.log_len[s_off + k] = (int)len;
+    }
+    const int tb = b - b_first;
+    if (tb < kTr) {
+      atomicAdd(&s_ctr[tb][0], 1ULL);
+      atomicAdd(&s_ctr[tb][1], len);
+      if (A.kind == EQ_KIND_DONOTHING) atomicAdd(&s_ctr[tb][2], len);
+    } else {
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), len);
+      if (A.kind == EQ_KIND_DONOTHING)
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), len);
+    }
+  }
+  group_sync(Ro::kBarN, Ro::NN);
+  if (gtid == 0) {
+    s_n = 0;
+    tl_mark_any(A.tl, m, A.G, cta, 6);
+  }
+}
+
 template <typename T, int NT, int U, int NF = NT / 2>
 __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   typedef Prec<T> P;
@@ -476,235 +722,8 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
     } else if (m < A.m1) {
       // ======================== neuron side
       const int gtid = tid - Ro::NF;
-      const bool dirty = A.kind == EQ_KIND_RING && ld_volatile(A.ring_dirty + m % A.R) != 0;
-      // ---------------- (b) neuron update: pop, synapse, membrane, crossing.
-      // Walked per trial segment of the owned range so the row pointers are
-      // computed once per segment, not per neuron.
-      const int mm = m < A.net.t_mask ? m : A.net.t_mask - 1;   // network.py:155 rows[-1]
-      const long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
-      const int b_last = (int)((end - 1) / A.N);
-      for (int b = b_first; b <= b_last; ++b) {
-        const int tb0 = b * A.N;
-        const int j0 = (int)(begin > tb0 ? begin - tb0 : 0);
-        const int j1 = (int)(end < (long long)tb0 + A.N ? end - tb0 : A.N);
-        const uint32_t* mrow = A.net.mask + ((size_t)b * A.net.t_mask + mm) * A.net.words;
-        if (P::kSlotWords == 1 && A.kind == EQ_KIND_RING && (A.N & 3) == 0 && !dirty) {
-          // fp32 fast path: four neurons per thread with 16-byte accesses
-          // (segment bounds are multiples of 4 when N % 4 == 0: ranges are
-          // warp-aligned).  Same per-neuron arithmetic as the scalar path.
-          for (int jq = j0 + 4 * gtid; jq < j1; jq += 4 * Ro::NN) {
-            const int idx = tb0 + jq;
-            const longlong2 a01 = *reinterpret_cast<const longlong2*>(accm + idx);
-            const longlong2 a23 = *reinterpret_cast<const longlong2*>(accm + idx + 2);
-            const float4 I4 = *reinterpret_cast<const float4*>(A.I + idx);
-            const float4 V4 = *reinterpret_cast<const float4*>(A.V + idx);
-            const float4 M4 = __ldg(reinterpret_cast<const float4*>(A.net.amp + jq));
-            const unsigned mw = __ldg(mrow + (jq >> 5)) >> (jq & 31);
-            int4 R4 = make_int4(0, 0, 0, 0);
-            if (A.refractory) R4 = *reinterpret_cast<const int4*>(A.refr + idx);
-            const long long av[4] = {a01.x, a01.y, a23.x, a23.y};
-            const float Iv4[4] = {I4.x, I4.y, I4.z, I4.w};
-            const float Vv4[4] = {V4.x, V4.y, V4.z, V4.w};
-            const float Av4[4] = {M4.x, M4.y, M4.z, M4.w};
-            int rf4[4] = {R4.x, R4.y, R4.z, R4.w};
-            float In[4], Vn[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              long long qs, qm;
-              unpack2(av[q], qs, qm);
-              const T ps = P::deq(qs, c.inv_scale);
-              const T pm = A.exact ? P::deq(qm, c.inv_scale) : (T)0;
-              const T drive = ((mw >> q) & 1u) ? (T)Av4[q] : (T)0;
-              T i, v_new, a, v, t_spk;
-              if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, (T)Iv4[q], (T)Vv4[q], drive, rf4[q], i, v_new,
-                           a, v, t_spk)) {
-                if (t_spk != t_spk) {
-                  raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, jq + q);
-                } else {
-                  int pos = atomicAdd(&s_n, 1);
-                  SpikeRec<T> rec;
-                  rec.idx = idx + q;
-                  rec.t = t_spk;
-                  rec.a = a;
-                  rec.vh = v;
-                  if (pos < kCapN) s_own[pos] = rec;
-                  else spill[pos - kCapN] = rec;
-                }
-              }
-              In[q] = (float)i;
-              Vn[q] = (float)v_new;
-            }
-            *reinterpret_cast<float4*>(A.I + idx) = make_float4(In[0], In[1], In[2], In[3]);
-            *reinterpret_cast<float4*>(A.V + idx) = make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
-            // RingQueue._pop_raw zeroes the slot (queues.py:114-117): the load has been
-            // consumed, so this store does not wait behind it
-            long long* accz = const_cast<long long*>(accm) + idx;
-            *reinterpret_cast<longlong2*>(accz) = make_longlong2(0, 0);
-            *reinterpret_cast<longlong2*>(accz + 2) = make_longlong2(0, 0);
-            if (A.refractory)
-              *reinterpret_cast<int4*>(A.refr + idx) = make_int4(rf4[0], rf4[1], rf4[2], rf4[3]);
-            if (A.v_trace)
-              *reinterpret_cast<float4*>(A.v_trace + (size_t)(m - A.m0) * A.total + idx) =
-                  make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
-          }
-          continue;
-        }
-        for (int jb = j0; jb < j1; jb += Ro::NN * U) {
-          long long slot_v[U][2];
-          T Iv[U], Vv[U], Am[U];
-          int rf[U];
-          unsigned mw[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int j = jb + u * Ro::NN + gtid;
-            slot_v[u][0] = slot_v[u][1] = 0;
-            if (j < j1) {
-              const int idx = tb0 + j;
-              if (A.kind == EQ_KIND_RING) {
-                if (P::kSlotWords == 1) {
-                  slot_v[u][0] = ld_slot(accm + idx);
-                } else {
-                  slot_v[u][0] = ld_slot(accm + 2 * (size_t)idx);
-                  slot_v[u][1] = ld_slot(accm + 2 * (size_t)idx + 1);
-                }
-                if (dirty) {                       // a bucket overflowed into the DRAM row
-                  size_t so = ((size_t)b * A.R + (size_t)(m % A.R)) * A.N + j;
-                  if (P::kSlotWords == 1) {
-                    slot_v[u][0] += ld_slot(A.ring + so);
-                  } else {
-                    slot_v[u][0] += ld_slot(A.ring + 2 * so);
-                    slot_v[u][1] += ld_slot(A.ring + 2 * so + 1);
-                  }
-                }
-              }
-              Iv[u] = A.I[idx];
-              Vv[u] = A.V[idx];
-              rf[u] = A.refractory ? A.refr[idx] : 0;
-              mw[u] = __ldg(mrow + (j >> 5));
-              Am[u] = __ldg(A.net.amp + j);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int j = jb + u * Ro::NN + gtid;
-            if (j >= j1) continue;
-            const int idx = tb0 + j;
-            T ps, pm;
-            if (P::kSlotWords == 1) {
-              long long qs, qm;
-              unpack2(slot_v[u][0], qs, qm);
-              ps = P::deq(qs, c.inv_scale);
-              pm = P::deq(qm, c.inv_scale);
-            } else {
-              ps = P::deq(slot_v[u][0], c.inv_scale);
-              pm = P::deq(slot_v[u][1], c.inv_scale);
-            }
-            if (!A.exact) pm = (T)0;
-            const T drive = ((mw[u] >> (j & 31)) & 1u) ? Am[u] : (T)0;
-            T i, v_new, a, v, t_spk;
-            if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, Iv[u], Vv[u], drive, rf[u], i, v_new, a, v,
-                         t_spk)) {
-              if (t_spk != t_spk) {
-                raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, j);
-              } else {
-                int pos = atomicAdd(&s_n, 1);
-                SpikeRec<T> rec;
-                rec.idx = idx;
-                rec.t = t_spk;
-                rec.a = a;
-                rec.vh = v;
-                if (pos < kCapN) s_own[pos] = rec;
-                else spill[pos - kCapN] = rec;
-              }
-            }
-            A.I[idx] = i;
-            A.V[idx] = v_new;
-            if (A.refractory) A.refr[idx] = rf[u];
-            if (A.v_trace) A.v_trace[(size_t)(m - A.m0) * A.total + idx] = v_new;
-          }
-        }
-      }
-      group_sync(Ro::kBarN, Ro::NN);
-      if (gtid == 0) tl_mark_any(A.tl, m, A.G, cta, 4);
-      // Clear the popped accumulator (RingQueue._pop_raw zeroes the slot,
-      // queues.py:114-117), in a separate pass: a store next to the pending
-      // load of the same line stalled the pop loop ~8x.  acc[m&1] receives no
-      // red.add in this phase (the event side writes acc[(m+1)&1]).
-      const bool cleared = P::kSlotWords == 1 && A.kind == EQ_KIND_RING && (A.N & 3) == 0 && !dirty;   // by the vector update
-      if (A.kind == EQ_KIND_RING && !cleared) {
-        long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
-        if (P::kSlotWords == 1 && ((begin | end) & 1) == 0) {
-          for (long long idx = begin + 2 * gtid; idx < end; idx += 2 * Ro::NN)
-            *reinterpret_cast<longlong2*>(accm + idx) = make_longlong2(0, 0);
-        } else {
-          for (int idx = (int)begin + gtid; idx < end; idx += Ro::NN) {
-            if (P::kSlotWords == 1) {
-              st_slot(accm + idx, 0);
-            } else {
-              st_slot(accm + 2 * (size_t)idx, 0);
-              st_slot(accm + 2 * (size_t)idx + 1, 0);
-            }
-          }
-        }
-        if (dirty) {
-          const int row = m % A.R;
-          for (int idx = (int)begin + gtid; idx < end; idx += Ro::NN) {
-            const int b = c.divN.div(idx);   // rare path (bucket overflow)
-            const size_t so = ((size_t)b * A.R + row) * A.N + (idx - b * A.N);
-            if (P::kSlotWords == 1) {
-              st_slot(A.ring + so, 0);
-            } else {
-              st_slot(A.ring + 2 * so, 0);
-              st_slot(A.ring + 2 * so + 1, 0);
-            }
-          }
-        }
-      }
-      const int nspk = s_n;
-      // ---------------- spike log: one chunk per (step, CTA); the chunks of a
-      // step are contiguous because every reservation of step m happens between
-      // the two barriers around phase m.  Counters per trial (spikes, events;
-      // donothing drops every event, queues.py:42-45).
-      if (gtid == 0) {
-        unsigned long long off = nspk ? atomicAdd(A.log_count, (unsigned long long)nspk) : 0ULL;
-        if (nspk && (long long)(off + nspk) > A.log_cap) {
-          raise_error(A.err, EQ_ERR_CAPACITY, m, -1, -1);
-          off = 0;
-        }
-        s_off = (long long)off;
-        A.chunk_off[(size_t)m * A.G + cta] = (long long)off;
-        A.chunk_cnt[(size_t)m * A.G + cta] = nspk;
-      }
-      group_sync(Ro::kBarN, Ro::NN);
-      const bool log_ok = s_off + nspk <= A.log_cap;
-      for (int k = gtid; k < nspk; k += Ro::NN) {
-        const SpikeRec<T> rec = k < kCapN ? s_own[k] : spill[k - kCapN];
-        const int b = c.divN.div(rec.idx);
-        const int i = rec.idx - b * A.N;
-        const long long r0 = __ldg(A.net.rowptr + A.src_off + i);
-        const unsigned long long len = (unsigned long long)(__ldg(A.net.rowptr + A.src_off + i + 1) - r0);
-        if (log_ok) {
-          A.log[s_off + k] = rec;
-          A.log_r0[s_off + k] = r0;
-          A.log_len[s_off + k] = (int)len;
-        }
-        const int tb = b - b_first;
-        if (tb < kTr) {
-          atomicAdd(&s_ctr[tb][0], 1ULL);
-          atomicAdd(&s_ctr[tb][1], len);
-          if (A.kind == EQ_KIND_DONOTHING) atomicAdd(&s_ctr[tb][2], len);
-        } else {
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
-          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), len);
-          if (A.kind == EQ_KIND_DONOTHING)
-            atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), len);
-        }
-      }
-      group_sync(Ro::kBarN, Ro::NN);
-      if (gtid == 0) {
-        s_n = 0;
-        tl_mark_any(A.tl, m, A.G, cta, 6);
-      }
+      neuron_side<T, NT, U, NF>(A, m, cta, gtid, begin, end, b_first, A.kind == EQ_KIND_RING, s_own, s_n, s_off,
+                                s_ctr, spill);
     }
     __syncthreads();
     if (m == A.m1) break;
