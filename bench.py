@@ -368,6 +368,16 @@ def run_ours(args):
     bwd_bytes = alg_bytes(neuron_steps, spikes, events, "bwd")
     dom = ("k_forward", fwd_bytes, fwd_avg) if fwd_avg >= bwd_avg else ("k_backward", bwd_bytes, bwd_avg)
     achieved = dom[1] / (dom[2] / 1e3) / 1e9
+    # DRAM bytes per launch of that kernel from the committed ncu --set full capture of this workload
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1c_traffic.json")) as f:
+            tr = json.load(f)
+        if (args.config == "C3" and B == 16 and args.kind == "ring" and args.precision == 32
+                and T == 1000 and args.delays is None):
+            traffic = tr.get(dom[0])
+    except Exception:
+        traffic = None
 
     if rank != 0:
         if world > 1:
@@ -408,7 +418,8 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (queue storage %.2f GB/GPU)" % (B * (eng.horizon + 1) * net.n * 8 / 1e9),
                    "parallelism": f"trial-dp{world}"},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
-                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": "profiles/r1c_traffic.json" if traffic else None,
                      "alg_bytes_per_launch": dom[1], "avg_launch_ms": dom[2],
                      "fwd_ms": fwd_avg, "bwd_ms": bwd_avg},
         "cpu_baseline": cpu,

@@ -83,6 +83,38 @@ __global__ void k_init(uint32_t* idx, int m, uint32_t seed) {
 
 int main(int argc, char** argv) {
   const int M = 711000;
+  if (argc > 1 && argv[1][0] == 'r') {   // per-warp region size: a warp's 32 lanes fall in one region
+    uint32_t* idx; cudaMalloc(&idx, M * 4);
+    float* out; cudaMalloc(&out, 4);
+    k_init<<<(M + 255) / 256, 256>>>(idx, M, 7);
+    std::vector<uint32_t> h(M);
+    cudaMemcpy(h.data(), idx, M * 4, cudaMemcpyDeviceToHost);
+    const size_t n = (size_t)845 * (1 << 20) / 8;
+    float2* a; cudaMalloc(&a, n * 8); cudaMemset(a, 0, n * 8);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    // the kernel's lane k of a warp is gather index i = tid + e*stride: consecutive k in one warp share tid/32
+    const int stride = 592 * 256;
+    for (size_t region : {(size_t)53 << 20, (size_t)8 << 20, (size_t)800 << 10, (size_t)64 << 10}) {
+      const size_t rn = region / 8;
+      std::vector<uint32_t> g(M);
+      for (int k = 0; k < M; ++k) {
+        const int tid = k % stride, e = k / stride;
+        const uint32_t warp_key = (uint32_t)((tid / 32) * 7919u + e * 104729u);
+        const size_t base = ((size_t)(warp_key * 2654435761u) % (n / rn)) * rn;
+        g[k] = (uint32_t)(base + h[k] % rn);
+      }
+      uint32_t* gi; cudaMalloc(&gi, M * 4);
+      cudaMemcpy(gi, g.data(), M * 4, cudaMemcpyHostToDevice);
+      k_gather_v<0><<<592, 256>>>(a, n, gi, M, out);
+      cudaEventRecord(e0);
+      for (int r = 0; r < 20; ++r) k_gather_v<0><<<592, 256>>>(a, n, gi, M, out);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("845 MB, warp lanes within %8zu KB regions: %7.2f us per 711k\n", region >> 10, ms / 20 * 1e3);
+      cudaFree(gi);
+    }
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 's') {   // locality: 16 trial rings of 53 MB, gathers grouped by ring
     uint32_t* idx; cudaMalloc(&idx, M * 4);
     float* out; cudaMalloc(&out, 4);
