@@ -804,7 +804,8 @@ struct BwdShared {
 template <typename T, int NT, int NF, bool kImp, int kCapB, int kEv>
 __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, const int cta, const int gtid,
                                             const long long s0, const long long s1, SpikeRec<T>* s_rec,
-                                            long long* s_r0, int* s_pre, T* s_lt, T* s_gtp) {
+                                            long long* s_r0, int* s_pre, T* s_lt, T* s_gtp,
+                                            const bool prestaged = false) {
   typedef typename Prec<T>::T2 T2;
   typedef Roles<NT, NF> Ro;
   const StepConsts<T>& c = A.c;
@@ -815,7 +816,8 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
   const int me_fixed = m - 1;
   for (long long k0 = s0; k0 < s1; k0 += kCapB) {
     const int nb = (int)(s1 - k0 < kCapB ? s1 - k0 : kCapB);
-    stage_spikes<T>(lg, lr0, llen, k0, nb, s_rec, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
+    // a single-batch share may have been staged by the neuron side during the previous phase
+    if (!prestaged) stage_spikes<T>(lg, lr0, llen, k0, nb, s_rec, s_r0, s_pre, gtid, Ro::NF, Ro::kBarF);
     for (int k = gtid; k < nb; k += Ro::NF) s_lt[k] = (T)0;
     group_sync(Ro::kBarF, Ro::NF);
     if (k0 == s0) tl_mark(A.tl, m, A.G, cta, 4);
@@ -896,9 +898,12 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
   typedef Roles<NT, NF> Ro;
   constexpr int kCapB = BwdShared<T>::kCapB;
   constexpr int kEv = BwdShared<T>::kEv;
-  __shared__ SpikeRec<T> s_rec[kCapB];
-  __shared__ long long s_r0[kCapB];
-  __shared__ int s_pre[kCapB + 1];
+  // staging of the event side's spike batch, double-buffered by phase parity:
+  // the neuron side pre-stages the next phase's share when it finishes early
+  __shared__ SpikeRec<T> s_rec[2][kCapB];
+  __shared__ long long s_r0[2][kCapB];
+  __shared__ int s_pre[2][kCapB + 1];
+  __shared__ int s_ready[2];                  // phase whose share buffer k holds (or -1)
   __shared__ T s_lt[kCapB];
   __shared__ T s_gtp[kEv];
   extern __shared__ unsigned int s_bits[];   // one bit per owned neuron-trial, then uint16 chunk positions
@@ -910,6 +915,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
   unsigned short* s_pos = reinterpret_cast<unsigned short*>(s_bits + nwords);
   const StepConsts<T> c = A.c;
   for (int k = tid; k < nwords; k += NT) s_bits[k] = 0u;
+  if (tid < 2) s_ready[tid] = -1;
   __syncthreads();
 
   // Phase m (m = m_run-1 .. 0): [event side] R-fanout of step m-1 (its events
@@ -924,9 +930,11 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
       const int gtid = tid;
       if (m >= 1) {
         const int me = m - 1;
+        const int cur = m & 1;
         const long long L0 = A.step_start[me], S = A.step_start[me + 1] - L0;
         bwd_rfanout<T, NT, NF, false, kCapB, kEv>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G,
-                                                  s_rec, s_r0, s_pre, s_lt, s_gtp);
+                                                  s_rec[cur], s_r0[cur], s_pre[cur], s_lt, s_gtp,
+                                                  s_ready[cur] == m);
       }
       tl_mark(A.tl, m, A.G, cta, 1);
     } else {
@@ -1061,6 +1069,18 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
         s_bits[loc >> 5] = 0u;
       }
       if (gtid == 0) tl_mark_any(A.tl, m, A.G, cta, 6);
+      // pre-stage the event side's share of the next phase (R-fanout of step
+      // m-2) into the other buffer: the event side is the critical path
+      if (m - 1 >= A.m_lo && m - 1 >= 1) {
+        const int nxt = (m - 1) & 1;
+        const long long L0 = A.step_start[m - 2], S = A.step_start[m - 1] - L0;
+        const long long s0 = L0 + S * cta / A.G, s1 = L0 + S * (cta + 1) / A.G;
+        if (s1 - s0 <= kCapB) {
+          stage_spikes<T>(A.log, A.log_r0, A.log_len, s0, (int)(s1 - s0), s_rec[nxt], s_r0[nxt], s_pre[nxt], gtid,
+                          Ro::NN, Ro::kBarN);
+          if (gtid == 0) s_ready[nxt] = m - 1;
+        }
+      }
     }
     __syncthreads();
     tl_mark(A.tl, m, A.G, cta, 2);
