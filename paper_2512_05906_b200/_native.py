@@ -54,6 +54,7 @@ def lib() -> ctypes.CDLL:
         "eq_forward": (ctypes.c_int, [H, vp, vp, vp, vp]),
         "eq_backward": (ctypes.c_int, [H, vp, vp, vp, vp, vp, vp]),
         "eq_get_state": (ctypes.c_int, [H, vp, vp, vp]),
+        "eq_forward_jvp": (ctypes.c_int, [H, i32, vp, vp, vp, vp, vp]),
         "eq_backward_begin": (ctypes.c_int, [H, vp, vp, vp, vp, vp, vp]),
         "eq_backward_window": (ctypes.c_int, [H, i32, vp]),
         "eq_set_partition": (ctypes.c_int, [H, i32, i32]),
@@ -91,7 +92,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive",
-            "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_get_state", "eq_backward_begin", "eq_backward_window",
+            "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_get_state", "eq_forward_jvp", "eq_backward_begin", "eq_backward_window",
             "eq_set_partition", "eq_set_frac_bits", "eq_export_spikes", "eq_import_spikes",
             "eq_get_import_adjoints", "eq_add_spike_adjoints", "eq_counters", "eq_spike_count",
             "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",

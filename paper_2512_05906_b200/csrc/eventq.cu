@@ -17,6 +17,7 @@
 #include "eq_device.cuh"
 #include "eq_ring.cuh"
 #include "eq_bounded.cuh"
+#include "eq_jvp.cuh"
 
 #include <cub/cub.cuh>
 
@@ -1233,6 +1234,94 @@ int eq_forward(eq_handle* h, void* v_out, void* i_out, void* v_trace, void* stre
   if (v_out) EQ_CUDA(h, cudaMemcpyAsync(v_out, h->V, h->total * h->tsize, cudaMemcpyDeviceToDevice, s));
   if (i_out) EQ_CUDA(h, cudaMemcpyAsync(i_out, h->I, h->total * h->tsize, cudaMemcpyDeviceToDevice, s));
   return EQ_OK;
+}
+
+int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const int64_t* dir_index, double* v_out,
+                   double* v_tangent, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  const eq_config& c = h->cfg;
+  if (c.precision != 64 || c.kind != EQ_KIND_RING || !c.exact_delivery)
+    return fail(h, EQ_ERR_CONFIGURATION, "forward-mode runs need precision 64, the ring kind and exact delivery");
+  if (h->partitioned) return fail(h, EQ_ERR_CONFIGURATION, "forward-mode runs on partitioned networks are not supported");
+  if (!h->net_set || !h->drive_set) return fail(h, EQ_ERR_CONFIGURATION, "network and drive must be set");
+  if (n_dir < 1 || !dir_kind || !dir_index || !v_tangent)
+    return fail(h, EQ_ERR_CONFIGURATION, "need >= 1 direction and a tangent output");
+  for (int d = 0; d < n_dir; ++d) {
+    const long long lim = dir_kind[d] == 2 ? c.n_neurons : h->E;
+    if (dir_kind[d] < 0 || dir_kind[d] > 2 || dir_index[d] < 0 || dir_index[d] >= lim)
+      return fail(h, EQ_ERR_CONFIGURATION, "direction " + std::to_string(d) + " is not a weight/delay edge or a "
+                                               "drive neuron");
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = eq_reset(h, stream);
+  if (rc) return rc;
+  const int N = c.n_neurons, B = c.n_trials, D = n_dir;
+  const size_t td = (size_t)B * D * N;
+  void *tI = nullptr, *tV = nullptr, *tslot = nullptr, *dk = nullptr, *di = nullptr, *sidx = nullptr, *st = nullptr,
+       *std_ = nullptr, *sn = nullptr, *off = nullptr, *nev = nullptr;
+  struct Scratch {
+    eq_handle* h;
+    std::vector<void*> p;
+    ~Scratch() { for (void* x : p) release(h, x); }
+  } scr{h, {}};
+  const int cap = (int)std::min<long long>(h->total, 1 << 30);
+  for (auto pr : std::vector<std::pair<void**, size_t>>{
+           {&tI, td * 8}, {&tV, td * 8}, {&tslot, td * h->R * 4 * 8}, {&dk, (size_t)D * 4}, {&di, (size_t)D * 8},
+           {&sidx, (size_t)cap * 4}, {&st, (size_t)cap * 8}, {&std_, (size_t)cap * D * 8}, {&sn, 16},
+           {&off, ((size_t)cap + 1) * 8}, {&nev, 16}}) {
+    EQ_CUDA(h, alloc(h, pr.first, pr.second));
+    scr.p.push_back(*pr.first);
+  }
+  EQ_CUDA(h, cudaMemsetAsync(tI, 0, td * 8, s));
+  EQ_CUDA(h, cudaMemsetAsync(tV, 0, td * 8, s));
+  EQ_CUDA(h, cudaMemsetAsync(tslot, 0, td * h->R * 4 * 8, s));
+  EQ_CUDA(h, cudaMemcpyAsync(dk, dir_kind, (size_t)D * 4, cudaMemcpyHostToDevice, s));
+  EQ_CUDA(h, cudaMemcpyAsync(di, dir_index, (size_t)D * 8, cudaMemcpyHostToDevice, s));
+  JvpArgs A;
+  A.N = N;
+  A.B = B;
+  A.D = D;
+  A.R = h->R;
+  A.refractory = c.refractory_steps;
+  A.total = h->total;
+  A.c = consts<double>(h);
+  A.net = netview<double>(h);
+  A.I = (double*)h->I;
+  A.V = (double*)h->V;
+  A.refr = h->refr;
+  A.ring = h->ring;
+  A.tI = (double*)tI;
+  A.tV = (double*)tV;
+  A.tslot = (double*)tslot;
+  A.dkind = (const int*)dk;
+  A.dindex = (const long long*)di;
+  A.spk_idx = (int*)sidx;
+  A.spk_t = (double*)st;
+  A.spk_tdot = (double*)std_;
+  A.spk_n = (int*)sn;
+  A.spk_cap = cap;
+  A.counters = h->counters;
+  A.err = h->err_dev;
+  const int ub = (int)((h->total + 255) / 256);
+  for (int m = 0; m < c.t_steps; ++m) {
+    A.m = m;
+    EQ_CUDA(h, cudaMemsetAsync(sn, 0, 4, s));
+    k_jvp_update<<<ub, 256, 0, s>>>(A);
+    k_jvp_offsets<<<1, 1024, 0, s>>>(A, (long long*)off, (long long*)nev);
+    k_jvp_fanout<<<1184, 256, 0, s>>>(A, (const long long*)nev, (const long long*)off);
+    h->launches += 3;
+  }
+  EQ_CUDA(h, cudaGetLastError());
+  if (v_out) EQ_CUDA(h, cudaMemcpyAsync(v_out, h->V, h->total * 8, cudaMemcpyDeviceToDevice, s));
+  // [B][D][N] -> [D][B][N]
+  for (int d = 0; d < D; ++d)
+    for (int b = 0; b < B; ++b)
+      EQ_CUDA(h, cudaMemcpyAsync(v_tangent + ((size_t)d * B + b) * N, (double*)tV + ((size_t)b * D + d) * N,
+                                 (size_t)N * 8, cudaMemcpyDeviceToDevice, s));
+  rc = check_err(h, s);
+  h->steps_done = 0;   // the spike log / queues of eq_run are not populated by this path
+  return rc;
 }
 
 int eq_get_state(eq_handle* h, void* v_out, void* i_out, void* stream) {

@@ -126,6 +126,23 @@ class Engine:
             out["v_trace"] = tr
         return out
 
+    def forward_jvp(self, kinds, indices):
+        """Forward mode for D seeded directions at once (network.py:668-683):
+        kinds[d] in {"weight", "delay", "drive"}, indices[d] = CSR edge
+        (weight/delay) or neuron (drive).  Runs the whole drive from rest;
+        returns (v [B, n], v_tangent [D, B, n]) in float64."""
+        code = {"weight": 0, "delay": 1, "drive": 2}
+        k = np.asarray([code[x] if isinstance(x, str) else int(x) for x in kinds], dtype=np.int32)
+        ix = np.asarray(indices, dtype=np.int64)
+        if k.shape != ix.shape or k.ndim != 1:
+            raise ConfigurationError("kinds and indices must be 1-d of equal length")
+        v = torch.empty(self.B, self.n, dtype=torch.float64, device=self.device)
+        vt = torch.empty(len(k), self.B, self.n, dtype=torch.float64, device=self.device)
+        _native.check(self.h, self.L.eq_forward_jvp(self.h, len(k), k.ctypes.data_as(ctypes.c_void_p),
+                                                     ix.ctypes.data_as(ctypes.c_void_p), _ptr(v), _ptr(vt),
+                                                     self.stream))
+        return v, vt
+
     def state(self) -> Dict[str, torch.Tensor]:
         """Current membrane and synaptic current, [n_trials, n]."""
         v = torch.empty(self.B, self.n, dtype=self.dtype, device=self.device)

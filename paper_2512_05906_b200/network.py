@@ -302,6 +302,37 @@ def forward_gradient(params: NetworkParams, direction: SeedDirection, t_steps: i
     return res.loss.tangent, res
 
 
+def forward_gradients(params: NetworkParams, directions, t_steps: int, drive=None) -> np.ndarray:
+    """The reference's forward mode (network.py:668-683) for many directions in
+    ONE batched JVP run on the GPU (eq_forward_jvp; fp64, ring kind): returns
+    d loss / d theta for each SeedDirection — an independent cross-check of
+    the reverse pass (tests/test_gpu_jvp.py)."""
+    directions = list(directions)
+    state = build_rsnn(params, precision=64)
+    for dr in directions:
+        build_rsnn(params, seed=dr)            # the reference's seed validation
+    p = state.params
+    act, amp = _drive_arrays(drive, p.n, t_steps, p.dt)
+    eng = state._ensure(t_steps)
+    eng.set_drive(pack_mask(act)[None], amp)
+    kinds, idx = [], []
+    for dr in directions:
+        kinds.append(dr.param)
+        idx.append(dr.i if dr.param == "drive" else _edge_index(p.n, dr.i, dr.j))
+    v, vt = eng.forward_jvp(kinds, idx)
+    v = v[0].cpu().numpy()
+    target = np.zeros(p.n) if p.v_target is None else np.asarray(p.v_target, dtype=float)
+    g = 2.0 * (v - target)
+    out = np.empty(len(directions))
+    for d in range(len(directions)):         # sequential dual sum, network.py:486-489
+        t = vt[d, 0].cpu().numpy()
+        acc = 0.0
+        for j in range(p.n):
+            acc = acc + g[j] * t[j]
+        out[d] = acc
+    return out
+
+
 def full_gradient(params: NetworkParams, t_steps: int, drive=None, precision: int = 64):
     """All directions at once: dL/dW and dL/dD as dense (n, n) (diagonal 0) and
     dL/d amplitude (n,)."""
