@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libeventq_b200.so")
 SOURCES = ["eventq.cu", "eq_queues.cu"]
-HEADERS = ["eq_device.cuh", "eq_ring.cuh", "eq_bounded.cuh"]
+HEADERS = ["eq_device.cuh", "eq_ring.cuh", "eq_bounded.cuh", "eq_jvp.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
