@@ -13,6 +13,7 @@
  *                                  (validation :213-268, horizon :188-198,
  *                                   queue wiring + capacities :321-332)
  *   eq_set_drive                <- PoissonDrive.materialize    pkg/src/eventq/network.py:123-155
+ *   eq_poisson_drive            <- PoissonDrive (generated on the device)  network.py:98-155
  *   eq_run                      <- network_step(state, drive)  pkg/src/eventq/network.py:336-445
  *                                  (n_steps calls, persistent on device)
  *   eq_forward                  <- simulate(state, T, drive) / PrimalRSNN.run
@@ -93,6 +94,17 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
  * word j/32 = neuron j receives `amplitude[j]` on that step) and amplitude
  * float|double[n].  Device pointers. */
 int eq_set_drive(eq_handle* h, const uint32_t* mask, const void* amplitude, void* stream);
+
+/* On-device PoissonDrive (reference PoissonDrive.__init__ + materialize,
+ * pkg/src/eventq/network.py:98-155): writes the packed active-step mask
+ * [n_trials][t_steps][ceil(n/32)] (device pointer, the layout eq_set_drive
+ * takes) for pulse trains t = Exp(mean); while t < t_steps*dt: pulse
+ * [t, t+pulse_duration), t += pulse_duration + Exp(mean), sampled as steps
+ * [ceil(s/dt), ceil(e/dt)).  Exponentials come from a counter-based
+ * Philox4x32-10 stream per (trial, neuron) keyed by `seed` (same statistics as
+ * the reference's numpy draws, not the same numbers).  No handle needed. */
+int eq_poisson_drive(int32_t n, int32_t n_trials, int32_t t_steps, double dt, double mean_interval,
+                     double pulse_duration, uint64_t seed, uint32_t* mask_out, void* stream);
 
 /* Reset all state to rest (v = v_reset, i = 0, queues empty, step 0). */
 int eq_reset(eq_handle* h, void* stream);

@@ -661,3 +661,63 @@ void eqo_math(int which, const double* in, double* out, int64_t n) {
   }
 }
 }
+
+extern "C" {
+/* On-device PoissonDrive restated (paper_2512_05906_b200/csrc/eq_drive.cu):
+ * the reference's pulse-train walk (pkg/src/eventq/network.py:113-120) and
+ * grid sampling (:138-143) with per-(trial, neuron) Philox4x32-10 streams
+ * (Salmon et al., SC'11; Random123 round constants) instead of numpy's PCG64. */
+void eqo_philox4x32_10(const uint32_t* ctr_in, const uint32_t* key, uint32_t* out) {
+  uint32_t x0 = ctr_in[0], x1 = ctr_in[1], x2 = ctr_in[2], x3 = ctr_in[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * x0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * x2;
+    const uint32_t y0 = (uint32_t)(p1 >> 32) ^ x1 ^ k0;
+    const uint32_t y1 = (uint32_t)p1;
+    const uint32_t y2 = (uint32_t)(p0 >> 32) ^ x3 ^ k1;
+    const uint32_t y3 = (uint32_t)p0;
+    x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+void eqo_poisson_drive(int32_t n, int32_t n_trials, int32_t t_steps, double dt, double mean, double dur,
+                       uint64_t seed, uint32_t* mask) {
+  const int words = (n + 31) / 32;
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  const double t_total = (double)t_steps * dt;
+  std::fill(mask, mask + (size_t)n_trials * t_steps * words, 0u);
+  for (int b = 0; b < n_trials; ++b)
+    for (int i = 0; i < n; ++i) {
+      uint32_t call = 0;
+      std::vector<double> pend;   // draws of the current Philox call not yet used
+      auto draw = [&]() {
+        if (pend.empty()) {
+          const uint32_t c[4] = {call++, (uint32_t)i, (uint32_t)b, 0x5d0f1eedu};
+          uint32_t o[4];
+          eqo_philox4x32_10(c, key, o);
+          const double inv53 = 1.0 / 9007199254740992.0;
+          const double ua = ((double)(o[0] >> 5) * 67108864.0 + (double)(o[1] >> 6) + 0.5) * inv53;
+          const double ub = ((double)(o[2] >> 5) * 67108864.0 + (double)(o[3] >> 6) + 0.5) * inv53;
+          pend.push_back(-mean * eq_log(ub));
+          pend.push_back(-mean * eq_log(ua));
+        }
+        const double v = pend.back();
+        pend.pop_back();
+        return v;
+      };
+      double t = draw();                                   // network.py:116
+      while (t < t_total) {                                // :117
+        const double s = t, e = s + dur;
+        const long long lo = std::min<long long>(t_steps, std::max<long long>(0, (long long)std::ceil(s / dt)));
+        const long long hi = std::min<long long>(t_steps, std::max<long long>(0, (long long)std::ceil(e / dt)));
+        for (long long m = lo; m < hi; ++m)
+          mask[((size_t)b * t_steps + m) * words + (i >> 5)] |= 1u << (i & 31);
+        t += dur + draw();                                 // :118
+      }
+    }
+}
+}  // extern "C"

@@ -71,6 +71,8 @@ def lib():
         L.eqo_get_counters.argtypes = [vp] * 2
         L.eqo_get_pending.argtypes = [vp] * 3
         L.eqo_threads.restype = ctypes.c_int
+        L.eqo_philox4x32_10.argtypes = [vp] * 3
+        L.eqo_poisson_drive.argtypes = [ctypes.c_int32] * 3 + [ctypes.c_double] * 3 + [ctypes.c_uint64, vp]
         _lib = L
     return _lib
 
@@ -194,3 +196,20 @@ class OracleSession:
 
 def threads() -> int:
     return lib().eqo_threads()
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    """Philox4x32-10 block (restated in eq_oracle.cpp; Random123 KATs pin it)."""
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().eqo_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def poisson_drive(n: int, n_trials: int, t_steps: int, dt: float, mean_interval: float,
+                  pulse_duration: float, seed: int) -> np.ndarray:
+    """CPU restatement of eq_poisson_drive: packed mask uint32 [B][T][ceil(n/32)]."""
+    out = np.zeros((n_trials, t_steps, (n + 31) // 32), dtype=np.uint32)
+    lib().eqo_poisson_drive(n, n_trials, t_steps, dt, mean_interval, pulse_duration, seed, _p(out))
+    return out

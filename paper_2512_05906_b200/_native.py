@@ -49,6 +49,8 @@ def lib() -> ctypes.CDLL:
         "eq_version": (ctypes.c_char_p, []),
         "eq_set_network": (ctypes.c_int, [H, vp, vp, vp, vp, i64, vp]),
         "eq_set_drive": (ctypes.c_int, [H, vp, vp, vp]),
+        "eq_poisson_drive": (ctypes.c_int, [i32, i32, i32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_uint64, vp, vp]),
         "eq_reset": (ctypes.c_int, [H, vp]),
         "eq_run": (ctypes.c_int, [H, i32, vp, vp]),
         "eq_forward": (ctypes.c_int, [H, vp, vp, vp, vp]),
@@ -91,7 +93,7 @@ def lib() -> ctypes.CDLL:
     return L
 
 
-EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive",
+EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive", "eq_poisson_drive",
             "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_get_state", "eq_forward_jvp", "eq_backward_begin", "eq_backward_window",
             "eq_set_partition", "eq_set_frac_bits", "eq_export_spikes", "eq_import_spikes",
             "eq_get_import_adjoints", "eq_add_spike_adjoints", "eq_counters", "eq_spike_count",

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libeventq_b200.so")
-SOURCES = ["eventq.cu", "eq_queues.cu"]
+SOURCES = ["eventq.cu", "eq_queues.cu", "eq_drive.cu"]
 HEADERS = ["eq_device.cuh", "eq_ring.cuh", "eq_bounded.cuh", "eq_jvp.cuh"]
 
 NVCC_FLAGS = [

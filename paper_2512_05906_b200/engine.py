@@ -115,6 +115,14 @@ class Engine:
         self._drive = (m, a)
         _native.check(self.h, self.L.eq_set_drive(self.h, _ptr(m), _ptr(a), self.stream))
 
+    def set_poisson_drive(self, amp, mean_interval: float, pulse_duration: float, seed: int) -> None:
+        """Drive generated on the device (eq_poisson_drive): the reference's
+        PoissonDrive (network.py:98-155) pulse trains with a Philox stream per
+        (trial, neuron) — same statistics as the reference's draws."""
+        m = poisson_drive_device(self.n, self.B, self.T, self.lif.dt, mean_interval, pulse_duration, seed,
+                                 device=self.device, stream=self.stream)
+        self.set_drive(m, amp)
+
     # ------------------------------------------------------------ running
     def forward(self, record_v: bool = False) -> Dict[str, torch.Tensor]:
         v = torch.empty(self.B, self.n, dtype=self.dtype, device=self.device)
@@ -270,3 +278,19 @@ class Engine:
     @property
     def launch_count(self) -> int:
         return int(self.L.eq_launch_count(self.h))
+
+
+def poisson_drive_device(n: int, n_trials: int, t_steps: int, dt: float, mean_interval: float,
+                         pulse_duration: float, seed: int, device=0, stream=None) -> torch.Tensor:
+    """Packed active-step masks int32 [B][T][ceil(n/32)] generated on the GPU
+    (eq_poisson_drive); bitwise equal to oracle.poisson_drive."""
+    L = _native.lib()
+    words = (n + 31) // 32
+    m = torch.empty((n_trials, t_steps, words), dtype=torch.int32, device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(m.device).cuda_stream
+    rc = L.eq_poisson_drive(n, n_trials, t_steps, dt, mean_interval, pulse_duration, seed, _ptr(m), s)
+    if rc != 0:
+        raise ConfigurationError(
+            f"eq_poisson_drive: invalid arguments (n={n}, trials={n_trials}, steps={t_steps}, dt={dt}, "
+            f"mean_interval={mean_interval}, pulse_duration={pulse_duration})")
+    return m
