@@ -79,10 +79,26 @@ __device__ __forceinline__ bool key_less(int da, int sa, int db, int sb) {
   return da < db || (da == db && sa < sb);
 }
 
-// Insert one event (reference order) into the owner's queue; false = dropped.
+// Per-target queues in HBM.  Every structure operation is a chain of
+// dependent memory round trips, so the device structures are laid out to keep
+// the chains short (the accepted sets and popped sums do not depend on the
+// structure: pops sum fixed-point payloads, acceptance depends on the count):
+//   heap    — min-heap on (due, insertion seq), 8-ary: a level's children are
+//             8 adjacent entries read in one round trip, depth log8(cap);
+//   sorted  — circular array, stable insertion (:351-366) (a chunked shift,
+//             8 keys per round trip, measured no faster at capacity 64);
+//   FIFO    — circular buffer, pops read 4 head entries per round trip.
+constexpr int kHeapD = 8;
+
+template <typename T>
+__device__ __forceinline__ int2 qkey(const QEv<T>* p) {   // {tag, due}: the entry's first 8 bytes
+  return *reinterpret_cast<const int2*>(p);
+}
+
+// Insert one event (reference order) into the owner's queue.
+// Returns 0 accepted, 1 dropped (full), 2 capability error (FIFO order).
 template <typename T>
 __device__ __forceinline__ int queue_insert(int kind, int cap, QEv<T>* q, int4& mt, QEv<T> ev) {
-  // returns 0 accepted, 1 dropped, 2 capability error
   if (kind == EQ_KIND_FIFORING && ev.due < mt.z) return 2;      // queues.py:220-224
   if (mt.x == cap) return 1;                                     // :225-226, :514-515, :344-345
   if (kind == EQ_KIND_FIFORING) {
@@ -95,15 +111,15 @@ __device__ __forceinline__ int queue_insert(int kind, int cap, QEv<T>* q, int4& 
   } else if (kind == EQ_KIND_BINARYHEAP) {
     ev.tag = mt.y++;                                             // insertion seq, :517-518
     int i = mt.x++;
-    while (i > 0) {                                              // sift up, :522-528
-      const int parent = (i - 1) >> 1;
+    while (i > 0) {                                              // sift up (:522-528), 8-ary
+      const int parent = (i - 1) / kHeapD;
       const QEv<T> pv = q[parent];
       if (!key_less(ev.due, ev.tag, pv.due, pv.tag)) break;
       q[i] = pv;
       i = parent;
     }
     q[i] = ev;
-    mt.w = q[0].due;
+    mt.w = i == 0 ? ev.due : mt.w;
   } else {  // sorted array, circular with head mt.y; stable for equal due (:351-366)
     int k = mt.x;
     while (k > 0) {
@@ -120,8 +136,7 @@ __device__ __forceinline__ int queue_insert(int kind, int cap, QEv<T>* q, int4& 
     if (di >= cap) di -= cap;
     q[di] = ev;
     mt.x += 1;
-    int h = mt.y;
-    mt.w = q[h].due;
+    if (k == 0) mt.w = ev.due;
   }
   return 0;
 }
@@ -135,53 +150,85 @@ __device__ __forceinline__ void queue_pop(int kind, int cap, QEv<T>* q, int4& mt
     while (mt.x > 0 && q[0].due == now) {                        // :555-568
       q[0].add_to(s, mm);
       const int last = --mt.x;
-      const QEv<T> item = q[last];
       if (last > 0) {
+        const QEv<T> item = q[last];
         int i = 0;
-        const int half = last >> 1;
-        while (i < half) {                                       // sift down, :541-551
-          int child = 2 * i + 1;
-          const int right = child + 1;
-          QEv<T> cv = q[child];
-          if (right < last) {
-            const QEv<T> rv = q[right];
-            if (key_less(rv.due, rv.tag, cv.due, cv.tag)) {
-              child = right;
-              cv = rv;
+        while (true) {                                           // sift down (:541-551), 8-ary
+          const int c0 = kHeapD * i + 1;
+          if (c0 >= last) break;
+          const int cn = last - c0 < kHeapD ? last - c0 : kHeapD;
+          int2 kk[kHeapD];
+#pragma unroll
+          for (int e = 0; e < kHeapD; ++e) kk[e] = e < cn ? qkey(q + c0 + e) : make_int2(0x7fffffff, 0x7fffffff);
+          int best = 0, bd = kk[0].y, bt = kk[0].x;
+#pragma unroll
+          for (int e = 1; e < kHeapD; ++e)
+            if (key_less(kk[e].y, kk[e].x, bd, bt)) {
+              best = e;
+              bd = kk[e].y;
+              bt = kk[e].x;
             }
-          }
-          if (!key_less(cv.due, cv.tag, item.due, item.tag)) break;
-          q[i] = cv;
-          i = child;
+          if (!key_less(bd, bt, item.due, item.tag)) break;
+          q[i] = q[c0 + best];                                   // L1 hit: its line was just read
+          i = c0 + best;
         }
         q[i] = item;
       }
     }
     mt.w = mt.x ? q[0].due : 0x7fffffff;
-  } else {  // FIFO and sorted: due run at the head (:245-254, :378-386)
-    while (mt.x > 0 && q[mt.y].due == now) {
-      q[mt.y].add_to(s, mm);
-      mt.y += 1;
-      if (mt.y == cap) mt.y = 0;
-      mt.x -= 1;
+  } else {  // FIFO and sorted: due run at the head (:245-254, :378-386), 4 entries per round trip
+    while (mt.x > 0) {
+      const int nb = mt.x < 4 ? mt.x : 4;
+      QEv<T> ev[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int pi = mt.y + e;
+        if (pi >= cap) pi -= cap;
+        if (e < nb) ev[e] = q[pi];
+      }
+      int taken = 0, next = 0x7fffffff;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (e < nb && e == taken && ev[e].due == now) {
+          ev[e].add_to(s, mm);
+          ++taken;
+        } else if (e < nb && e == taken) {
+          next = ev[e].due;                                      // first entry not due: the new head
+        }
+      }
+      mt.y += taken;
+      if (mt.y >= cap) mt.y -= cap;
+      mt.x -= taken;
+      if (taken < nb) {
+        mt.w = next;
+        return;
+      }
+      if (nb < 4) break;                                         // emptied
     }
     mt.w = mt.x ? q[mt.y].due : 0x7fffffff;
   }
 }
 
-// Owner-side insertion of one target's arrivals of step `ms` (parity ms & 1).
+// Owner-side insertion of one target's arrivals of step `ms` (parity ms & 1),
+// in ascending in-edge order (= the reference's source order).
 template <typename T>
 __device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int j, int idx, int ms, int4& mt,
-                                                unsigned long long& drops) {
+                                                unsigned long long& drops, long long w0, long long w1,
+                                                long long cs) {
   const int par = ms & 1;
-  const long long w0 = A.word_off[j], w1 = A.word_off[j + 1];
   unsigned* arr = A.arr + ((size_t)par * A.f.B + b) * A.W;
-  const QEv<T>* stg = A.stage + ((size_t)par * A.f.B + b) * A.E + A.csc_off[j];
-  const unsigned short* srow = A.stage_row + ((size_t)par * A.f.B + b) * A.E + A.csc_off[j];
+  const QEv<T>* stg = A.stage + ((size_t)par * A.f.B + b) * A.E + cs;
+  const unsigned short* srow = A.stage_row + ((size_t)par * A.f.B + b) * A.E + cs;
   QEv<T>* q = A.q + (size_t)idx * A.cap;
-  for (long long w = w0; w < w1; ++w) {
-    unsigned bits = arr[w];
+  for (long long wb = w0; wb < w1; wb += 4) {
+   unsigned bw[4];
+#pragma unroll
+   for (int e = 0; e < 4; ++e) bw[e] = wb + e < w1 ? arr[wb + e] : 0u;   // four words per round trip
+#pragma unroll
+   for (int e = 0; e < 4; ++e) {
+    unsigned bits = bw[e];
     if (!bits) continue;
+    const long long w = wb + e;
     arr[w] = 0u;
     while (bits) {
       const int bit = __ffs(bits) - 1;
@@ -199,11 +246,12 @@ __device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int 
         else raise_error(A.f.err, EQ_ERR_CAPACITY, ms, b, j);
       }
     }
+   }
   }
 }
 
 template <typename T, int NT, int U>
-__global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
+__global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
   typedef Prec<T> P;
   constexpr int kCap = FwdShared<NT, T>::kCap;
   constexpr int kTr = FwdShared<NT>::kTrials;
@@ -237,16 +285,24 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
       if (idx >= end) continue;
       const int b = c.divN.div(idx);
       const int j = idx - b * F.N;
+      // every load that does not depend on the queue first: one round trip
       int4 mt = A.meta[idx];
+      const bool ins = m - 1 >= A.insert_first && m >= 1;
+      unsigned* fl = A.flags + ((size_t)((m - 1) & 1) * F.B + b) * fwords;
+      const unsigned flw = ins ? fl[j >> 5] : 0u;
+      const long long aw0 = __ldg(A.word_off + j), aw1 = __ldg(A.word_off + j + 1), acs = __ldg(A.csc_off + j);
+      const T I0 = F.I[idx], V0 = F.V[idx];
+      int rf = F.refractory ? F.refr[idx] : 0;
+      const bool drv = !last && drive_bit(F.net, b, m, j);
+      const T ampj = __ldg(F.net.amp + j);
       bool dirty = false;
-      if (m - 1 >= A.insert_first && m >= 1) {
-        unsigned* fl = A.flags + ((size_t)((m - 1) & 1) * F.B + b) * fwords;
+      if (ins) {
         const unsigned bit = 1u << (j & 31);
-        if (fl[j >> 5] & bit) {
+        if (flw & bit) {
           // a flag word can straddle two CTAs' ranges when N % 32 != 0: clear our bit only
           atomicAnd(fl + (j >> 5), ~bit);
           unsigned long long d = 0;
-          insert_arrivals<T>(A, b, j, idx, m - 1, mt, d);
+          insert_arrivals<T>(A, b, j, idx, m - 1, mt, d, aw0, aw1, acs);
           const int tb = b - b_first;
           if (d) {
             if (tb < kTr) atomicAdd(&s_ctr[tb][2], d);
@@ -267,10 +323,9 @@ __global__ void __launch_bounds__(NT) k_forward_bounded(BndArgs<T> A) {
       if (dirty) A.meta[idx] = mt;
       T ps = P::deq(qs, c.inv_scale), pm = P::deq(qm, c.inv_scale);
       if (!F.exact) pm = (T)0;
-      int rf = F.refractory ? F.refr[idx] : 0;
-      const T drive = drive_bit(F.net, b, m, j) ? __ldg(F.net.amp + j) : (T)0;
+      const T drive = drv ? ampj : (T)0;
       T i, v_new, a, v, t_spk;
-      if (lif_step(c, F.exact != 0, F.refractory, m, ps, pm, F.I[idx], F.V[idx], drive, rf, i, v_new, a, v, t_spk)) {
+      if (lif_step(c, F.exact != 0, F.refractory, m, ps, pm, I0, V0, drive, rf, i, v_new, a, v, t_spk)) {
         if (t_spk != t_spk) {
           raise_error(F.err, EQ_ERR_GRAZING, m + 1, b, j);
         } else {
