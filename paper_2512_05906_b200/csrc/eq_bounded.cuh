@@ -10,15 +10,16 @@
 // Parallel fan-out cannot produce that order, so an arrival is not inserted by
 // its producer.  Instead:
 //
-//   phase m, producer (the CTA that detected the crossing): for each event of
-//     edge x -> target j write a staging record at the edge's in-edge slot
-//     csc_off[j] + in_pos[x] and set bit in_pos[x] of j's arrival bitmap
-//     (plus j's bit in a dense per-target "has arrivals" word);
-//   phase m+1, owner of j, before pop(m+1): walk j's arrival bits in ascending
-//     order (= ascending x) and insert in exactly the reference order — FIFO
-//     tail-key check (CapabilityError), drop when full, structure insert.
+//   phase m, producer (the CTA that detected the crossing): each event of
+//     edge x -> target j is appended to j's arrival list (a slot from an
+//     atomic per-target counter, inside j's in-edge segment csc_off[j]..: it
+//     cannot overflow) as one 32-byte record {x, log position, due, row
+//     offset, payload} — one full sector per event, no partial writes;
+//   phase m+1, owner of j, before pop(m+1): read j's (few) arrivals and insert
+//     them in ascending x, exactly the reference order — FIFO tail-key check
+//     (CapabilityError), drop when full, structure insert.
 //
-// Staging and bitmaps are double-buffered by step parity (phase m+1 producers
+// Lists and counters are double-buffered by step parity (phase m+1 producers
 // write step m+1 while owners read step m).  The final step's arrivals are
 // inserted after a last barrier so the queue contents after a run equal the
 // reference's.  Pops and sums are fixed point (order-free), as for the ring.
@@ -54,18 +55,28 @@ template <> struct alignas(16) QEv<double> {
   }
 };
 
+// one arrival (32 bytes, one sector): edge x (the reference's arrival order
+// within a step is ascending x), log position of the source spike, due step,
+// row offset of x in the source's CSR row (drop bookkeeping), payload
+template <typename T> struct Arrival;
+template <> struct alignas(32) Arrival<float> {
+  int x, tag, due, ro;
+  long long p;
+  long long pad;
+};
+template <> struct alignas(32) Arrival<double> {
+  int x, tag, due, ro;
+  long long ps, pm;
+};
+
 template <typename T>
 struct BndArgs {
   FwdArgs<T> f;
   int cap;                    // events per queue
-  const int* in_pos;          // [E] rank of edge x among its target's in-edges
-  const long long* csc_off;   // [N+1] in-edge slot offsets
-  const long long* word_off;  // [N+1] arrival-bitmap word offsets
-  long long E, W;             // edges, bitmap words per trial
-  QEv<T>* stage;              // [2][B][E]
-  unsigned short* stage_row;  // [2][B][E] row offsets of staged events
-  unsigned* arr;              // [2][B][W]
-  unsigned* flags;            // [2][B][words]
+  const long long* csc_off;   // [N+1] in-edge segment offsets
+  long long E;
+  Arrival<T>* alist;          // [2][B][E] arrival lists, target j at csc_off[j]
+  int* acnt;                  // [2][B][N] arrivals per target
   QEv<T>* q;                  // [B*N][cap]
   int4* meta;                 // [B*N] {count, head|seq, tail_key, next_due}
   long long* ev_base;         // [log_cap] flat event id of each logged spike's first edge
@@ -209,44 +220,45 @@ __device__ __forceinline__ void queue_pop(int kind, int cap, QEv<T>* q, int4& mt
   }
 }
 
-// Owner-side insertion of one target's arrivals of step `ms` (parity ms & 1),
-// in ascending in-edge order (= the reference's source order).
+// Owner-side insertion of target j's `n` arrivals of step `ms` (parity ms & 1)
+// in ascending x (= the reference's source order): each round takes the
+// smallest x above the last one (the list is read once; rounds hit L1).
 template <typename T>
-__device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int j, int idx, int ms, int4& mt,
-                                                unsigned long long& drops, long long w0, long long w1,
-                                                long long cs) {
-  const int par = ms & 1;
-  unsigned* arr = A.arr + ((size_t)par * A.f.B + b) * A.W;
-  const QEv<T>* stg = A.stage + ((size_t)par * A.f.B + b) * A.E + cs;
-  const unsigned short* srow = A.stage_row + ((size_t)par * A.f.B + b) * A.E + cs;
+__device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int j, int idx, int ms, int n,
+                                                long long cs, int4& mt, unsigned long long& drops) {
+  const Arrival<T>* lst = A.alist + ((size_t)(ms & 1) * A.f.B + b) * A.E + cs;
   QEv<T>* q = A.q + (size_t)idx * A.cap;
-  for (long long wb = w0; wb < w1; wb += 4) {
-   unsigned bw[4];
-#pragma unroll
-   for (int e = 0; e < 4; ++e) bw[e] = wb + e < w1 ? arr[wb + e] : 0u;   // four words per round trip
-#pragma unroll
-   for (int e = 0; e < 4; ++e) {
-    unsigned bits = bw[e];
-    if (!bits) continue;
-    const long long w = wb + e;
-    arr[w] = 0u;
-    while (bits) {
-      const int bit = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const int pos = (int)((w - w0) * 32 + bit);
-      QEv<T> ev = stg[pos];
-      const int log_pos = ev.tag;
-      const int rc = queue_insert<T>(A.f.kind, A.cap, q, mt, ev);
-      if (rc == 2) {
-        raise_error(A.f.err, EQ_ERR_CAPABILITY, ms + 1, b, j);
-      } else if (rc == 1) {
-        drops += 1;
-        const long long id = A.ev_base[log_pos] + srow[pos];
-        if (id < A.drop_cap) atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
-        else raise_error(A.f.err, EQ_ERR_CAPACITY, ms, b, j);
+  int last_x = -1;
+  for (int r = 0; r < n; ++r) {
+    int best = -1, bx = 0x7fffffff;
+    for (int k = 0; k < n; ++k) {
+      const int x = lst[k].x;
+      if (x > last_x && x < bx) {
+        bx = x;
+        best = k;
       }
     }
-   }
+    last_x = bx;
+    const Arrival<T> a = lst[best];
+    QEv<T> ev;
+    ev.tag = a.tag;
+    ev.due = a.due;
+    if constexpr (sizeof(T) == 4) {
+      ev.p = a.p;
+    } else {
+      ev.ps = a.ps;
+      ev.pm = a.pm;
+      ev.pad = 0;
+    }
+    const int rc = queue_insert<T>(A.f.kind, A.cap, q, mt, ev);
+    if (rc == 2) {
+      raise_error(A.f.err, EQ_ERR_CAPABILITY, ms + 1, b, j);
+    } else if (rc == 1) {
+      drops += 1;
+      const long long id = A.ev_base[a.tag] + a.ro;
+      if (id < A.drop_cap) atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
+      else raise_error(A.f.err, EQ_ERR_CAPACITY, ms, b, j);
+    }
   }
 }
 
@@ -272,7 +284,6 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
   const StepConsts<T> c = F.c;
   SpikeRec<T>* spill = F.scratch + (size_t)cta * F.per;
   if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
-  const int fwords = (F.N + 31) / 32;
 
   for (int m = F.m0; m <= F.m1; ++m) {
     const bool last = (m == F.m1);   // extra pass: insert the final step's arrivals only
@@ -288,21 +299,19 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
       // every load that does not depend on the queue first: one round trip
       int4 mt = A.meta[idx];
       const bool ins = m - 1 >= A.insert_first && m >= 1;
-      unsigned* fl = A.flags + ((size_t)((m - 1) & 1) * F.B + b) * fwords;
-      const unsigned flw = ins ? fl[j >> 5] : 0u;
-      const long long aw0 = __ldg(A.word_off + j), aw1 = __ldg(A.word_off + j + 1), acs = __ldg(A.csc_off + j);
+      int* cntp = A.acnt + ((size_t)((m - 1) & 1) * F.B + b) * F.N + j;
+      const int narr = ins ? *cntp : 0;
+      const long long acs = __ldg(A.csc_off + j);
       const T I0 = F.I[idx], V0 = F.V[idx];
       int rf = F.refractory ? F.refr[idx] : 0;
       const bool drv = !last && drive_bit(F.net, b, m, j);
       const T ampj = __ldg(F.net.amp + j);
       bool dirty = false;
-      if (ins) {
-        const unsigned bit = 1u << (j & 31);
-        if (flw & bit) {
-          // a flag word can straddle two CTAs' ranges when N % 32 != 0: clear our bit only
-          atomicAnd(fl + (j >> 5), ~bit);
+      if (narr > 0) {
+        {
+          *cntp = 0;
           unsigned long long d = 0;
-          insert_arrivals<T>(A, b, j, idx, m - 1, mt, d, aw0, aw1, acs);
+          insert_arrivals<T>(A, b, j, idx, m - 1, narr, acs, mt, d);
           const int tb = b - b_first;
           if (d) {
             if (tb < kTr) atomicAdd(&s_ctr[tb][2], d);
@@ -420,25 +429,23 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
           ws = w;
           wm = (T)0;
         }
-        const int pos = __ldg(A.in_pos + x);
-        QEv<T> ev;
-        ev.tag = (int)(s_off + k0 + k);
-        ev.due = ds;
+        // append to the target's arrival list (slot from its counter; the
+        // segment holds all in-edges, so it cannot overflow)
+        const int slot = atomicAdd(A.acnt + ((size_t)par * F.B + b) * F.N + jt, 1);
+        Arrival<T> ar;
+        ar.x = (int)x;
+        ar.tag = (int)(s_off + k0 + k);
+        ar.due = ds;
+        ar.ro = ro;
         const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
         if constexpr (sizeof(T) == 4) {
-          ev.p = pack2(q1, q2);
+          ar.p = pack2(q1, q2);
+          ar.pad = 0;
         } else {
-          ev.ps = q1;
-          ev.pm = q2;
-          ev.pad = 0;
+          ar.ps = q1;
+          ar.pm = q2;
         }
-        const size_t so = ((size_t)par * F.B + b) * A.E + A.csc_off[jt] + pos;
-        A.stage[so] = ev;
-        A.stage_row[so] = (unsigned short)ro;
-        unsigned* arr = A.arr + ((size_t)par * F.B + b) * A.W + A.word_off[jt];
-        atomicOr(arr + (pos >> 5), 1u << (pos & 31));
-        unsigned* fl = A.flags + ((size_t)par * F.B + b) * fwords;
-        atomicOr(fl + (jt >> 5), 1u << (jt & 31));
+        A.alist[((size_t)par * F.B + b) * A.E + __ldg(A.csc_off + jt) + slot] = ar;
       }
     }
     __syncthreads();

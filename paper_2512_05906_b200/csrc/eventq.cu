@@ -103,14 +103,9 @@ struct eq_handle {
   bool bounded = false;
   int cap = 0;                 // physical events per queue
   long long cap_ref = 0;       // the reference's capacity (acceptance rule)
-  int* in_pos = nullptr;
   long long* csc_off = nullptr;
-  long long* word_off = nullptr;
-  long long W = 0;
-  void* stage = nullptr;
-  unsigned short* stage_row = nullptr;
-  unsigned* arr = nullptr;
-  unsigned* flags = nullptr;
+  void* alist = nullptr;       // [2][B][E] arrival lists (Arrival<T>)
+  int* acnt = nullptr;         // [2][B][N] arrivals per target
   void* q = nullptr;
   int4* meta = nullptr;
   long long* ev_base = nullptr;
@@ -411,23 +406,6 @@ __global__ void k_pending(const long long* ring, int B, int R, int N, int H, int
   }
 }
 
-__global__ void k_iota(int* v, long long n) {
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
-    v[k] = (int)k;
-}
-
-// in_pos[x] = rank of edge x among its target's in-edges (sorted stably by x)
-__global__ void k_in_pos(const int* sorted_col, const int* sorted_x, const long long* csc_off, long long E,
-                         int* in_pos) {
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < E; k += (long long)gridDim.x * blockDim.x)
-    in_pos[sorted_x[k]] = (int)(k - csc_off[sorted_col[k]]);
-}
-
-__global__ void k_words_of(const int* indeg, int N, long long* words) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < N) words[j] = (indeg[j] + 31) / 32;
-}
-
 __global__ void k_meta_init(int4* meta, long long n) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
     meta[k] = make_int4(0, 0, -1, 0x7fffffff);
@@ -626,15 +604,10 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
     BndArgs<T> Bk;
     Bk.f = A;
     Bk.cap = h->cap;
-    Bk.in_pos = h->in_pos;
     Bk.csc_off = h->csc_off;
-    Bk.word_off = h->word_off;
     Bk.E = h->E;
-    Bk.W = h->W;
-    Bk.stage = (QEv<T>*)h->stage;
-    Bk.stage_row = h->stage_row;
-    Bk.arr = h->arr;
-    Bk.flags = h->flags;
+    Bk.alist = (Arrival<T>*)h->alist;
+    Bk.acnt = h->acnt;
     Bk.q = (QEv<T>*)h->q;
     Bk.meta = h->meta;
     Bk.ev_base = h->ev_base;
@@ -858,57 +831,18 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   if (qbytes > ((size_t)96 << 30))
     return fail(h, EQ_ERR_CONFIGURATION, "queue storage " + std::to_string(qbytes >> 20) +
                                              " MiB exceeds 96 GiB; set eq_config.capacity");
-  // stable sort of (target, edge) pairs -> csc order
-  void *keys_out = nullptr, *vals_in = nullptr, *vals_out = nullptr, *tmp = nullptr;
-  EQ_CUDA(h, alloc(h, &keys_out, E * sizeof(int)));
-  EQ_CUDA(h, alloc(h, &vals_in, E * sizeof(int)));
-  EQ_CUDA(h, alloc(h, &vals_out, E * sizeof(int)));
-  k_iota<<<592, 256, 0, s>>>((int*)vals_in, E);
+  // csc_off = exclusive scan of in-degree: target j's arrival list is its
+  // in-edge segment [csc_off[j], csc_off[j+1]) (no step delivers more)
   size_t tmp_bytes = 0;
-  int end_bit = 1;
-  while ((1LL << end_bit) < N) ++end_bit;
-  EQ_CUDA(h, cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, h->col, (int*)keys_out, (const int*)vals_in,
-                                             (int*)vals_out, (int)E, 0, end_bit, s));
-  EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
-  EQ_CUDA(h, cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, h->col, (int*)keys_out, (const int*)vals_in,
-                                             (int*)vals_out, (int)E, 0, end_bit, s));
-  release(h, tmp);
-  // csc_off = exclusive scan of in-degree; word_off = exclusive scan of ceil(indeg/32)
+  void* tmp = nullptr;
   EQ_CUDA(h, ensure(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
-  EQ_CUDA(h, ensure(h, (void**)&h->word_off, (size_t)(N + 1) * sizeof(long long)));
-  void *deg64 = nullptr, *words = nullptr;
-  EQ_CUDA(h, alloc(h, &deg64, (size_t)(N + 1) * sizeof(long long)));
-  EQ_CUDA(h, alloc(h, &words, (size_t)(N + 1) * sizeof(long long)));
-  EQ_CUDA(h, cudaMemsetAsync(deg64, 0, (size_t)(N + 1) * sizeof(long long), s));
-  EQ_CUDA(h, cudaMemsetAsync(words, 0, (size_t)(N + 1) * sizeof(long long), s));
-  k_words_of<<<(N + 255) / 256, 256, 0, s>>>(indeg, N, (long long*)words);
-  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const long long*)words, h->word_off, N + 1, s));
-  EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
-  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, (const long long*)words, h->word_off, N + 1, s));
-  release(h, tmp);
-  tmp_bytes = 0;
   EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, indeg, h->csc_off, N + 1, s));
   EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
   EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, indeg, h->csc_off, N + 1, s));
   release(h, tmp);
-  release(h, deg64);
-  EQ_CUDA(h, ensure(h, (void**)&h->in_pos, E * sizeof(int)));
-  k_in_pos<<<592, 256, 0, s>>>((const int*)keys_out, (const int*)vals_out, h->csc_off, E, h->in_pos);
-  h->launches += 4;
-  long long wtot = 0;
-  EQ_CUDA(h, cudaMemcpyAsync(&wtot, h->word_off + N, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  EQ_CUDA(h, cudaStreamSynchronize(s));
-  release(h, words);
-  release(h, keys_out);
-  release(h, vals_in);
-  release(h, vals_out);
-  h->W = wtot;
-  const size_t qe = c.precision == 32 ? sizeof(QEv<float>) : sizeof(QEv<double>);
-  const int fwords = (N + 31) / 32;
-  EQ_CUDA(h, ensure(h, &h->stage, (size_t)2 * B * E * qe));
-  EQ_CUDA(h, ensure(h, (void**)&h->stage_row, (size_t)2 * B * E * sizeof(unsigned short)));
-  EQ_CUDA(h, ensure(h, (void**)&h->arr, (size_t)2 * B * h->W * sizeof(unsigned)));
-  EQ_CUDA(h, ensure(h, (void**)&h->flags, (size_t)2 * B * fwords * sizeof(unsigned)));
+  h->launches += 1;
+  EQ_CUDA(h, ensure(h, &h->alist, (size_t)2 * B * E * sizeof(Arrival<float>)));   // 32 bytes in both precisions
+  EQ_CUDA(h, ensure(h, (void**)&h->acnt, (size_t)2 * B * N * sizeof(int)));
   EQ_CUDA(h, ensure(h, &h->q, qbytes));
   EQ_CUDA(h, ensure(h, (void**)&h->meta, (size_t)B * N * sizeof(int4)));
   EQ_CUDA(h, ensure(h, (void**)&h->ev_base, (size_t)h->log_cap * sizeof(long long)));
@@ -1190,8 +1124,7 @@ int eq_reset(eq_handle* h, void* stream) {
   EQ_CUDA(h, cudaMemsetAsync(h->step_start, 0, sizeof(long long), s));
   if (h->bounded) {
     const int B = h->cfg.n_trials, N = h->cfg.n_neurons;
-    EQ_CUDA(h, cudaMemsetAsync(h->arr, 0, (size_t)2 * B * h->W * sizeof(unsigned), s));
-    EQ_CUDA(h, cudaMemsetAsync(h->flags, 0, (size_t)2 * B * ((N + 31) / 32) * sizeof(unsigned), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->acnt, 0, (size_t)2 * B * N * sizeof(int), s));
     EQ_CUDA(h, cudaMemsetAsync(h->ev_count, 0, sizeof(unsigned long long), s));
     EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
     k_meta_init<<<592, 256, 0, s>>>(h->meta, (long long)B * N);
