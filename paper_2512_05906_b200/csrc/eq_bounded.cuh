@@ -307,6 +307,18 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
       const bool drv = !last && drive_bit(F.net, b, m, j);
       const T ampj = __ldg(F.net.amp + j);
       bool dirty = false;
+      if (narr > 0 || (!last && mt.x > 0 && mt.w == m)) {
+        // the queue lines this step's inserts and pops will walk, fetched into
+        // L2 together: the structure's dependent chains then miss DRAM once
+        const char* qb = reinterpret_cast<const char*>(A.q + (size_t)idx * A.cap);
+        const int span = mt.x + narr < A.cap ? mt.x + narr : A.cap;
+        const int first = F.kind == EQ_KIND_BINARYHEAP ? 0 : mt.y;
+        for (int e = 0; e < span; e += 128 / (int)sizeof(QEv<T>)) {
+          int k = first + e;
+          if (k >= A.cap) k -= A.cap;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + (size_t)k * sizeof(QEv<T>)));
+        }
+      }
       if (narr > 0) {
         {
           *cntp = 0;
