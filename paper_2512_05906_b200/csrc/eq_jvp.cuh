@@ -14,7 +14,10 @@
 //   fan-out    tt = tdot + d'_e, W' = w'_e e^{-phi/tau}, Q += (w e^{-phi/tau}) tt
 //                                                           (network.py:429-437, jumps.py:83-87)
 // Tangent slot sums are double atomics (order-dependent in the last bits; the
-// JVP is compared with a tolerance).  Two launches per step: update, fan-out.
+// JVP is compared with a tolerance).  Four kernels per step (update, offsets,
+// fan-out, next) read the step from device memory; the host captures a block
+// of steps once as a CUDA graph and replays it (the run is launch-bound
+// otherwise: ~6 us of host time per kernel at C1).
 #pragma once
 
 #include "eq_ring.cuh"
@@ -22,7 +25,8 @@
 namespace eq {
 
 struct JvpArgs {
-  int N, B, D, R, refractory, m;
+  int N, B, D, R, refractory;
+  int* m_dev;             // current step (device-side, so a CUDA graph of steps replays unchanged)
   long long total;
   StepConsts<double> c;
   NetView<double> net;
@@ -49,7 +53,7 @@ __global__ void k_jvp_update(JvpArgs A) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= A.total) return;
   const StepConsts<double>& c = A.c;
-  const int m = A.m;
+  const int m = *A.m_dev;
   const int b = (int)(idx / A.N);
   const int j = (int)(idx - (long long)b * A.N);
   // primal pop + clear (RingQueue._pop_raw, queues.py:109-120)
@@ -133,7 +137,7 @@ __global__ void k_jvp_fanout(JvpArgs A, const long long* n_events_p, const long 
     const int j = A.net.col[x];
     const double w = A.net.w[x], d = A.net.d[x];
     const double t_post = A.spk_t[k] + d;                   // jumps.py:83-87
-    const int ds = delivery_step_coded(t_post, A.net.dcode[x], c.dt, A.m);
+    const int ds = delivery_step_coded(t_post, A.net.dcode[x], c.dt, *A.m_dev);
     const double phi = (double)ds * c.dt - t_post;
     const double es = eq_exp_t(-phi * c.inv_tau_s), em = eq_exp_t(-phi * c.inv_tau_m);
     const double ws = w * es, wm = w * em;
@@ -154,6 +158,12 @@ __global__ void k_jvp_fanout(JvpArgs A, const long long* n_events_p, const long 
       }
     }
   }
+}
+
+// End of a step: advance the device-side step and empty the spike list.
+__global__ void k_jvp_next(JvpArgs A) {
+  *A.m_dev += 1;
+  *A.spk_n = 0;
 }
 
 // Exclusive prefix of the step's spikes' out-degrees (one block).

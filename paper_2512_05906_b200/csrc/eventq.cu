@@ -1192,7 +1192,7 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
   const int N = c.n_neurons, B = c.n_trials, D = n_dir;
   const size_t td = (size_t)B * D * N;
   void *tI = nullptr, *tV = nullptr, *tslot = nullptr, *dk = nullptr, *di = nullptr, *sidx = nullptr, *st = nullptr,
-       *std_ = nullptr, *sn = nullptr, *off = nullptr, *nev = nullptr;
+       *std_ = nullptr, *sn = nullptr, *off = nullptr, *nev = nullptr, *mdev = nullptr;
   struct Scratch {
     eq_handle* h;
     std::vector<void*> p;
@@ -1202,7 +1202,7 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
   for (auto pr : std::vector<std::pair<void**, size_t>>{
            {&tI, td * 8}, {&tV, td * 8}, {&tslot, td * h->R * 4 * 8}, {&dk, (size_t)D * 4}, {&di, (size_t)D * 8},
            {&sidx, (size_t)cap * 4}, {&st, (size_t)cap * 8}, {&std_, (size_t)cap * D * 8}, {&sn, 16},
-           {&off, ((size_t)cap + 1) * 8}, {&nev, 16}}) {
+           {&off, ((size_t)cap + 1) * 8}, {&nev, 16}, {&mdev, 16}}) {
     EQ_CUDA(h, alloc(h, pr.first, pr.second));
     scr.p.push_back(*pr.first);
   }
@@ -1236,15 +1236,53 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
   A.spk_cap = cap;
   A.counters = h->counters;
   A.err = h->err_dev;
+  A.m_dev = (int*)mdev;
+  EQ_CUDA(h, cudaMemsetAsync(mdev, 0, 4, s));
+  EQ_CUDA(h, cudaMemsetAsync(sn, 0, 4, s));
   const int ub = (int)((h->total + 255) / 256);
-  for (int m = 0; m < c.t_steps; ++m) {
-    A.m = m;
-    EQ_CUDA(h, cudaMemsetAsync(sn, 0, 4, s));
-    k_jvp_update<<<ub, 256, 0, s>>>(A);
-    k_jvp_offsets<<<1, 1024, 0, s>>>(A, (long long*)off, (long long*)nev);
-    k_jvp_fanout<<<1184, 256, 0, s>>>(A, (const long long*)nev, (const long long*)off);
-    h->launches += 3;
+  auto step = [&](cudaStream_t q) {
+    k_jvp_update<<<ub, 256, 0, q>>>(A);
+    k_jvp_offsets<<<1, 1024, 0, q>>>(A, (long long*)off, (long long*)nev);
+    k_jvp_fanout<<<1184, 256, 0, q>>>(A, (const long long*)nev, (const long long*)off);
+    k_jvp_next<<<1, 1, 0, q>>>(A);
+  };
+  // a block of kGraphSteps steps captured once on a private stream and
+  // replayed; the remainder launched directly; ordered with the caller's stream
+  constexpr int kGraphSteps = 50;
+  const int nblk = c.t_steps / kGraphSteps;
+  cudaStream_t gs = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool ok = nblk >= 2 && cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming) == cudaSuccess;
+  if (ok) {
+    ok = cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      for (int k = 0; k < kGraphSteps; ++k) step(gs);
+      ok = cudaStreamEndCapture(gs, &graph) == cudaSuccess &&
+           cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    }
   }
+  if (ok) {
+    EQ_CUDA(h, cudaEventRecord(ev0, s));
+    EQ_CUDA(h, cudaStreamWaitEvent(gs, ev0, 0));
+    for (int k = 0; k < nblk; ++k) EQ_CUDA(h, cudaGraphLaunch(exec, gs));
+    for (int m = nblk * kGraphSteps; m < c.t_steps; ++m) step(gs);
+    EQ_CUDA(h, cudaEventRecord(ev1, gs));
+    EQ_CUDA(h, cudaStreamWaitEvent(s, ev1, 0));
+  } else {
+    cudaGetLastError();
+    for (int m = 0; m < c.t_steps; ++m) step(s);
+  }
+  h->launches += 4LL * c.t_steps;
+  if (gs) cudaStreamSynchronize(gs);   // the graph and stream outlive their launches
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (gs) cudaStreamDestroy(gs);
   EQ_CUDA(h, cudaGetLastError());
   if (v_out) EQ_CUDA(h, cudaMemcpyAsync(v_out, h->V, h->total * 8, cudaMemcpyDeviceToDevice, s));
   // [B][D][N] -> [D][B][N]
