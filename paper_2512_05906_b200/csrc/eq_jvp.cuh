@@ -14,8 +14,9 @@
 //   fan-out    tt = tdot + d'_e, W' = w'_e e^{-phi/tau}, Q += (w e^{-phi/tau}) tt
 //                                                           (network.py:429-437, jumps.py:83-87)
 // Tangent slot sums are double atomics (order-dependent in the last bits; the
-// JVP is compared with a tolerance).  Four kernels per step (update, offsets,
-// fan-out, next) read the step from device memory; the host captures a block
+// JVP is compared with a tolerance).  Five kernels per step (primal update,
+// tangent update per (neuron, direction), offsets, fan-out per (event,
+// direction), next) read the step from device memory; the host captures a block
 // of steps once as a CUDA graph and replays it (the run is launch-bound
 // otherwise: ~6 us of host time per kernel at C1).
 #pragma once
@@ -42,12 +43,16 @@ struct JvpArgs {
   int* spk_idx;           // [cap] flat neuron-trial of each spike of this step
   double* spk_t;          // [cap]
   double* spk_tdot;       // [cap][D]
+  double *pa, *pv, *pr, *pku;   // [total] primal intermediates of this step (a, v-hat, r, e^{-u/tau_m})
+  int2* pinfo;            // [total] {on | crossed << 1, spike slot}
   int* spk_n;             // spikes of this step
   int spk_cap;
   long long* counters;    // [B][3]
   int* err;
 };
 
+// Primal step of every neuron (one thread each); the quantities the tangent
+// recurrences need are kept per neuron for k_jvp_tangent.
 __global__ void k_jvp_update(JvpArgs A) {
   typedef Prec<double> P;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -73,13 +78,11 @@ __global__ void k_jvp_update(JvpArgs A) {
   }
   const bool crossed = spike;   // lif_step reports a crossing only outside refractoriness
   double ku = 0.0, r = 0.0;
+  int slot = -1;
   if (crossed) {
     r = (c.v_th - a) / (v - a);                             // neuro.py:196-201 (same ops as lif_step)
     const double uu = (double)(m + 1) * c.dt - t_spk;
     ku = eq_exp_t(-uu / c.tau_m);
-  }
-  int slot = -1;
-  if (crossed) {
     slot = atomicAdd(A.spk_n, 1);
     if (slot < A.spk_cap) {
       A.spk_idx[slot] = (int)idx;
@@ -89,31 +92,51 @@ __global__ void k_jvp_update(JvpArgs A) {
       slot = -1;
     }
   }
-  for (int d = 0; d < A.D; ++d) {
-    const size_t ts = ((size_t)b * A.D + d) * A.N + j;
-    double* sl = A.tslot + ((((size_t)b * A.D + d) * A.R + (size_t)(m % A.R)) * A.N + j) * 4;
-    const double Ws = sl[0], Qs = sl[1], Wm = sl[2], Qm = sl[3];
-    sl[0] = sl[1] = sl[2] = sl[3] = 0.0;
-    double tI = A.tI[ts];
-    tI = (tI + Ws + Qs / c.tau_s) * c.k_s;                  // apply_jump_pulse + dual_exp_decay
-    const double ta = tI + ((on && A.dkind[d] == 2 && A.dindex[d] == j) ? 1.0 : 0.0);
-    const double tv = A.tV[ts] + c.cc * (Wm + Qm / c.tau_m - Ws - Qs / c.tau_s);
-    double tvn = ta + (tv - ta) * c.k_m;
-    if (crossed) {
-      const double num_p = c.v_th - a, num_t = -ta;
-      const double den_p = v - a, den_t = tv - ta;
-      const double r_t = (num_t * den_p - num_p * den_t) / (den_p * den_p);
-      const double tdot = -c.tau_m * r_t / r;
-      const double rest_p = c.v_reset - a, rest_t = -ta;
-      tvn = ta + (rest_t * ku + rest_p * (ku * tdot / c.tau_m));
-      if (slot >= 0) A.spk_tdot[(size_t)slot * A.D + d] = tdot;
-    }
-    A.tI[ts] = tI;
-    A.tV[ts] = tvn;
-  }
+  A.pa[idx] = a;
+  A.pv[idx] = v;
+  A.pr[idx] = r;
+  A.pku[idx] = ku;
+  A.pinfo[idx] = make_int2((on ? 1 : 0) | (crossed ? 2 : 0), slot);
   A.I[idx] = i;
   A.V[idx] = v_new;
   if (A.refractory) A.refr[idx] = rf;
+}
+
+// Tangent step: one thread per (trial, direction, neuron), neuron fastest
+// (coalesced tangent state and slots).
+__global__ void k_jvp_tangent(JvpArgs A) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= A.total * A.D) return;
+  const StepConsts<double>& c = A.c;
+  const int m = *A.m_dev;
+  const int j = (int)(t % A.N);
+  const long long bd = t / A.N;                             // b * D + d
+  const int d = (int)(bd % A.D);
+  const int b = (int)(bd / A.D);
+  const long long idx = (long long)b * A.N + j;
+  const int2 info = A.pinfo[idx];
+  const bool on = info.x & 1, crossed = info.x & 2;
+  const size_t ts = (size_t)bd * A.N + j;
+  double* sl = A.tslot + (((size_t)bd * A.R + (size_t)(m % A.R)) * A.N + j) * 4;
+  const double Ws = sl[0], Qs = sl[1], Wm = sl[2], Qm = sl[3];
+  sl[0] = sl[1] = sl[2] = sl[3] = 0.0;
+  double tI = A.tI[ts];
+  tI = (tI + Ws + Qs / c.tau_s) * c.k_s;                    // apply_jump_pulse + dual_exp_decay
+  const double ta = tI + ((on && A.dkind[d] == 2 && A.dindex[d] == j) ? 1.0 : 0.0);
+  const double tv = A.tV[ts] + c.cc * (Wm + Qm / c.tau_m - Ws - Qs / c.tau_s);
+  double tvn = ta + (tv - ta) * c.k_m;
+  if (crossed) {
+    const double a = A.pa[idx], v = A.pv[idx], r = A.pr[idx], ku = A.pku[idx];
+    const double num_p = c.v_th - a, num_t = -ta;
+    const double den_p = v - a, den_t = tv - ta;
+    const double r_t = (num_t * den_p - num_p * den_t) / (den_p * den_p);
+    const double tdot = -c.tau_m * r_t / r;
+    const double rest_p = c.v_reset - a, rest_t = -ta;
+    tvn = ta + (rest_t * ku + rest_p * (ku * tdot / c.tau_m));
+    if (info.y >= 0) A.spk_tdot[(size_t)info.y * A.D + d] = tdot;
+  }
+  A.tI[ts] = tI;
+  A.tV[ts] = tvn;
 }
 
 // One thread per (spike, out-edge) of this step's spikes.
@@ -121,9 +144,11 @@ __global__ void k_jvp_fanout(JvpArgs A, const long long* n_events_p, const long 
   typedef Prec<double> P;
   const StepConsts<double>& c = A.c;
   const int n = *A.spk_n < A.spk_cap ? *A.spk_n : A.spk_cap;
-  const long long n_events = *n_events_p;
-  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < n_events;
-       f += (long long)gridDim.x * blockDim.x) {
+  const long long n_items = *n_events_p * A.D;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < n_items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const long long f = it / A.D;                           // event; direction fastest across lanes
+    const int dd = (int)(it - f * A.D);
     int lo = 0, hi = n;                                     // spike k: ev_off[k] <= f < ev_off[k+1]
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -141,21 +166,21 @@ __global__ void k_jvp_fanout(JvpArgs A, const long long* n_events_p, const long 
     const double phi = (double)ds * c.dt - t_post;
     const double es = eq_exp_t(-phi * c.inv_tau_s), em = eq_exp_t(-phi * c.inv_tau_m);
     const double ws = w * es, wm = w * em;
-    const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + j;
-    red_add(A.ring + 2 * so, P::q(ws, c.scale));
-    red_add(A.ring + 2 * so + 1, P::q(wm, c.scale));
-    for (int dd = 0; dd < A.D; ++dd) {
-      const double tt = A.spk_tdot[(size_t)k * A.D + dd] + ((A.dkind[dd] == 1 && A.dindex[dd] == x) ? 1.0 : 0.0);
-      const double wt = (A.dkind[dd] == 0 && A.dindex[dd] == x) ? 1.0 : 0.0;
-      double* sl = A.tslot + ((((size_t)b * A.D + dd) * A.R + (size_t)(ds % A.R)) * A.N + j) * 4;
-      if (wt != 0.0) {
-        atomicAdd(sl + 0, wt * es);                         // DualScalar.scale: (p c, t c)
-        atomicAdd(sl + 2, wt * em);
-      }
-      if (tt != 0.0) {
-        atomicAdd(sl + 1, ws * tt);                         // wtt += p * time_tangent
-        atomicAdd(sl + 3, wm * tt);
-      }
+    if (dd == 0) {
+      const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + j;
+      red_add(A.ring + 2 * so, P::q(ws, c.scale));
+      red_add(A.ring + 2 * so + 1, P::q(wm, c.scale));
+    }
+    const double tt = A.spk_tdot[(size_t)k * A.D + dd] + ((A.dkind[dd] == 1 && A.dindex[dd] == x) ? 1.0 : 0.0);
+    const double wt = (A.dkind[dd] == 0 && A.dindex[dd] == x) ? 1.0 : 0.0;
+    double* sl = A.tslot + ((((size_t)b * A.D + dd) * A.R + (size_t)(ds % A.R)) * A.N + j) * 4;
+    if (wt != 0.0) {
+      atomicAdd(sl + 0, wt * es);                           // DualScalar.scale: (p c, t c)
+      atomicAdd(sl + 2, wt * em);
+    }
+    if (tt != 0.0) {
+      atomicAdd(sl + 1, ws * tt);                           // wtt += p * time_tangent
+      atomicAdd(sl + 3, wm * tt);
     }
   }
 }

@@ -134,6 +134,7 @@ struct eq_handle {
   double* bw_gw = nullptr;
   double* bw_gd = nullptr;
   double* bw_gamp = nullptr;
+  void* jvp_buf[24] = {};                         // eq_forward_jvp scratch
   std::vector<void*> owned;
   std::vector<std::pair<void*, size_t>> sizes;   // reusable buffers
 };
@@ -1192,19 +1193,21 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
   const int N = c.n_neurons, B = c.n_trials, D = n_dir;
   const size_t td = (size_t)B * D * N;
   void *tI = nullptr, *tV = nullptr, *tslot = nullptr, *dk = nullptr, *di = nullptr, *sidx = nullptr, *st = nullptr,
-       *std_ = nullptr, *sn = nullptr, *off = nullptr, *nev = nullptr, *mdev = nullptr;
-  struct Scratch {
-    eq_handle* h;
-    std::vector<void*> p;
-    ~Scratch() { for (void* x : p) release(h, x); }
-  } scr{h, {}};
+       *std_ = nullptr, *sn = nullptr, *off = nullptr, *nev = nullptr, *mdev = nullptr, *pa = nullptr, *pv = nullptr,
+       *pr = nullptr, *pku = nullptr, *pinfo = nullptr;
+  // scratch kept in the handle between runs (grow-only, like the other buffers)
   const int cap = (int)std::min<long long>(h->total, 1 << 30);
-  for (auto pr : std::vector<std::pair<void**, size_t>>{
+  const std::vector<std::pair<void**, size_t>> list{
            {&tI, td * 8}, {&tV, td * 8}, {&tslot, td * h->R * 4 * 8}, {&dk, (size_t)D * 4}, {&di, (size_t)D * 8},
            {&sidx, (size_t)cap * 4}, {&st, (size_t)cap * 8}, {&std_, (size_t)cap * D * 8}, {&sn, 16},
-           {&off, ((size_t)cap + 1) * 8}, {&nev, 16}, {&mdev, 16}}) {
-    EQ_CUDA(h, alloc(h, pr.first, pr.second));
-    scr.p.push_back(*pr.first);
+           {&off, ((size_t)cap + 1) * 8}, {&nev, 16}, {&mdev, 16}, {&pa, (size_t)h->total * 8},
+           {&pv, (size_t)h->total * 8}, {&pr, (size_t)h->total * 8}, {&pku, (size_t)h->total * 8},
+           {&pinfo, (size_t)h->total * 8}};
+  if (list.size() > sizeof(h->jvp_buf) / sizeof(void*)) return fail(h, EQ_ERR_CUDA, "jvp scratch table too small");
+  for (const auto& pr : list) {
+    void** slot = &h->jvp_buf[&pr - &*list.begin()];
+    EQ_CUDA(h, ensure(h, slot, pr.second));
+    *pr.first = *slot;
   }
   EQ_CUDA(h, cudaMemsetAsync(tI, 0, td * 8, s));
   EQ_CUDA(h, cudaMemsetAsync(tV, 0, td * 8, s));
@@ -1237,11 +1240,19 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
   A.counters = h->counters;
   A.err = h->err_dev;
   A.m_dev = (int*)mdev;
+  A.pa = (double*)pa;
+  A.pv = (double*)pv;
+  A.pr = (double*)pr;
+  A.pku = (double*)pku;
+  A.pinfo = (int2*)pinfo;
   EQ_CUDA(h, cudaMemsetAsync(mdev, 0, 4, s));
   EQ_CUDA(h, cudaMemsetAsync(sn, 0, 4, s));
   const int ub = (int)((h->total + 255) / 256);
+  const long long tb = (h->total * D + 255) / 256;
+  if (tb > 0x7fffffffLL) return fail(h, EQ_ERR_CONFIGURATION, "too many directions x neuron-trials");
   auto step = [&](cudaStream_t q) {
     k_jvp_update<<<ub, 256, 0, q>>>(A);
+    k_jvp_tangent<<<(unsigned)tb, 256, 0, q>>>(A);
     k_jvp_offsets<<<1, 1024, 0, q>>>(A, (long long*)off, (long long*)nev);
     k_jvp_fanout<<<1184, 256, 0, q>>>(A, (const long long*)nev, (const long long*)off);
     k_jvp_next<<<1, 1, 0, q>>>(A);
@@ -1276,7 +1287,7 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
     cudaGetLastError();
     for (int m = 0; m < c.t_steps; ++m) step(s);
   }
-  h->launches += 4LL * c.t_steps;
+  h->launches += 5LL * c.t_steps;
   if (gs) cudaStreamSynchronize(gs);   // the graph and stream outlive their launches
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
