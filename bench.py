@@ -34,6 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+TRAFFIC_FILE = "r1d_traffic.json"   # DRAM bytes per launch from the committed ncu capture of the default workload
 
 
 def read_peaks():
@@ -371,9 +372,9 @@ def run_ours(args):
     # DRAM bytes per launch of that kernel from the committed ncu --set full capture of this workload
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1c_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_FILE)) as f:
             tr = json.load(f)
-        if (args.config == "C3" and B == 16 and args.kind == "ring" and args.precision == 32
+        if (args.config == "C3" and B == tr.get("trials") and args.kind == "ring" and args.precision == 32
                 and T == 1000 and args.delays is None):
             traffic = tr.get(dom[0])
     except Exception:
@@ -419,7 +420,7 @@ def run_ours(args):
                    "parallelism": f"trial-dp{world}"},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "traffic_source": "profiles/r1c_traffic.json" if traffic else None,
+                     "traffic_source": "profiles/" + TRAFFIC_FILE if traffic else None,
                      "alg_bytes_per_launch": dom[1], "avg_launch_ms": dom[2],
                      "fwd_ms": fwd_avg, "bwd_ms": bwd_avg},
         "cpu_baseline": cpu,
@@ -440,7 +441,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--trials", type=int, default=16)
+    ap.add_argument("--trials", type=int, default=24)   # trials per GPU: 24 measured best of 8..48 (DESIGN 6.1)
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--cpu-trials", type=int, default=0)
     ap.add_argument("--cpu-steps", type=int, default=0)
