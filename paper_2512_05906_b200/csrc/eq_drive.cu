@@ -73,9 +73,12 @@ __device__ __forceinline__ double next_exp(Walk& w, uint32_t i, uint32_t b, uint
 
 // One warp per (trial, 32-neuron mask word), lane = neuron within the word;
 // a CTA of 32 warps covers 32 consecutive words and writes 32 steps at a time
-// through a shared-memory tile as 128-byte row segments (one 4-byte store per
-// word and step would be a partial-sector write each).
+// through a shared-memory tile as 128-byte row segments.  Pulses are generated
+// kPulses at a time per lane, all lanes together (the per-pulse Philox + log
+// would otherwise run one lane at a time inside the step loop), and consumed
+// from a per-lane list as the steps advance.
 constexpr int kTileSteps = 32;
+constexpr int kPulses = 48;
 __global__ void __launch_bounds__(1024) k_poisson_drive(int n, int B, int T, int words, double dt, double mean,
                                                         double dur, double t_total, uint32_t k0, uint32_t k1,
                                                         uint32_t* mask) {
@@ -92,23 +95,42 @@ __global__ void __launch_bounds__(1024) k_poisson_drive(int n, int B, int T, int
   w.has_spare = false;
   w.lo = w.hi = 0x7fffffff;
   w.t = live ? next_exp(w, (uint32_t)i, (uint32_t)b, k0, k1, mean) : t_total;
-  auto advance = [&]() {
-    if (w.t < t_total) {                                   // network.py:117 (while t < t_total)
-      const double s = w.t, e = s + dur;                  // :119-120
-      w.lo = (int)fmin(fmax(ceil(s / dt), 0.0), (double)T);   // materialize :140-141
-      w.hi = (int)fmin(fmax(ceil(e / dt), 0.0), (double)T);
+  int2 pl[kPulses];   // this lane's next pulses as active-step ranges
+  int np = 0, pi = 0;
+  auto refill = [&]() {   // up to kPulses more pulses (network.py:117-120, materialize :140-141)
+    np = 0;
+    pi = 0;
+    while (np < kPulses && w.t < t_total) {
+      const double s = w.t, e = s + dur;
+      const int lo = (int)fmin(fmax(ceil(s / dt), 0.0), (double)T);
+      const int hi = (int)fmin(fmax(ceil(e / dt), 0.0), (double)T);
       w.t = s + (dur + next_exp(w, (uint32_t)i, (uint32_t)b, k0, k1, mean));   // :118 t += dur + Exp
-    } else {
-      w.lo = w.hi = 0x7fffffff;
+      if (hi > lo) pl[np++] = make_int2(lo, hi);   // pulses empty on the grid are never active
     }
   };
-  advance();
+  refill();
+  int lo = 0x7fffffff, hi = 0x7fffffff;
+  if (np > 0) {
+    lo = pl[0].x;
+    hi = pl[0].y;
+  }
   uint32_t* out = mask + (size_t)b * T * words;
   for (int m0 = 0; m0 < T; m0 += kTileSteps) {
     for (int mm = 0; mm < kTileSteps; ++mm) {
       const int m = m0 + mm;
-      while (w.hi <= m && w.lo != 0x7fffffff) advance();  // pulses may be empty on the grid
-      const bool on = live && w.lo <= m && m < w.hi;
+      while (hi <= m) {                                    // next pulse of this lane
+        if (++pi >= np) {
+          if (w.t < t_total) refill();
+          else np = 0;
+          if (np == 0) {
+            lo = hi = 0x7fffffff;
+            break;
+          }
+        }
+        lo = pl[pi].x;
+        hi = pl[pi].y;
+      }
+      const bool on = live && lo <= m && m < hi;
       const unsigned bits = __ballot_sync(0xffffffffu, on);
       if (lane == 0) tile[mm][wp] = bits;
     }
