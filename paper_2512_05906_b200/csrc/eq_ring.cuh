@@ -788,6 +788,20 @@ struct BwdArgs {
   unsigned* bar;
 };
 
+// Random 8/16-byte reverse-slot gather: ask L2 for a 64-byte fill instead of
+// the default 128 (fewer DRAM bytes per useful byte; the DRAM is ~56% busy in
+// the reverse pass at 24 trials, profiles/r1d_c3x24.md).
+__device__ __forceinline__ float2 ld_gather(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.L2::64B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_gather(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.L2::64B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 template <typename T>
 struct BwdShared {
   static constexpr int kCapB = sizeof(T) == 4 ? 512 : 256;   // spikes per batch
@@ -866,7 +880,7 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
             const T phi = (T)st * c.dt - t_post;
             const T es = eq_exp_t(-phi * c.inv_tau_s);
             const T em = eq_exp_t(-phi * c.inv_tau_m);
-            const T2 L = A.lam[((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]];
+            const T2 L = ld_gather(A.lam + ((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]);
             const T g_w = es * L.x + em * L.y;
             g_tp = w * (es * L.x * c.inv_tau_s + em * L.y * c.inv_tau_m);
             red_add_f64(A.gw + xx[e], (double)g_w);
