@@ -1019,8 +1019,9 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
               nv[q] = (float)lvh;
             }
             float4* lr4 = reinterpret_cast<float4*>(lam_row + jq);
-            lr4[0] = make_float4(ls[0], lm[0], ls[1], lm[1]);
-            lr4[1] = make_float4(ls[2], lm[2], ls[3], lm[3]);
+            // read back only by random gathers 1..H phases later (from DRAM): streaming stores
+            __stcs(lr4, make_float4(ls[0], lm[0], ls[1], lm[1]));
+            __stcs(lr4 + 1, make_float4(ls[2], lm[2], ls[3], lm[3]));
             *reinterpret_cast<float4*>(A.lamI + idx) = make_float4(ni[0], ni[1], ni[2], ni[3]);
             *reinterpret_cast<float4*>(A.lamV + idx) = make_float4(nv[0], nv[1], nv[2], nv[3]);
           }
