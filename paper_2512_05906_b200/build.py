@@ -50,7 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
+    extra = os.environ.get("EQ_NVCC_EXTRA", "").split()   # A/B builds (e.g. -DEQ_SPLIT_F64=192)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
     env = dict(os.environ)
     # the image's CXX wrapper lacks some runtime specs; nvcc's host compiler is the system gcc
     cmd[1:1] = ["-ccbin", "/usr/bin/g++"] if os.path.exists("/usr/bin/g++") else []

@@ -29,6 +29,15 @@ constexpr int kNT = 512;   // threads per CTA of the persistent kernels
 constexpr int kU = 4;      // neurons per thread in flight per round
 constexpr int kSplitF = 288;  // forward event-side threads per CTA (measured: 224..384, profiles/)
 constexpr int kSplitB = 352;  // reverse event-side threads per CTA (measured: 224..448, profiles/)
+// fp64: the neuron side is the slower one (scalar paths, 16-byte slots), so it gets more threads
+#ifndef EQ_SPLIT_F64
+#define EQ_SPLIT_F64 224
+#endif
+#ifndef EQ_SPLIT_B64
+#define EQ_SPLIT_B64 256
+#endif
+template <typename T> constexpr int split_f() { return sizeof(T) == 4 ? kSplitF : EQ_SPLIT_F64; }
+template <typename T> constexpr int split_b() { return sizeof(T) == 4 ? kSplitB : EQ_SPLIT_B64; }
 
 
 struct DeviceGuard {
@@ -648,7 +657,7 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
       h->launches += 1;
       if (n_steps == 0) return check_err(h, s);   // flush: deliver the imports, no step
     }
-    const void* kf = (const void*)k_forward<T, kNT, kU, kSplitF>;
+    const void* kf = (const void*)k_forward<T, kNT, kU, split_f<T>()>;
     EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, 0, s));
   }
   h->launches += 1;
@@ -731,7 +740,7 @@ int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
   A.bar = h->bar;
   size_t smem = bwd_smem(h->per);
   void* args[] = {&A};
-  const void* kb = (const void*)k_backward<T, kNT, kU, kSplitB>;
+  const void* kb = (const void*)k_backward<T, kNT, kU, split_b<T>()>;
   // static + dynamic smem beyond 48 KB needs the opt-in (the static part alone is ~41 KB)
   EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   EQ_CUDA(h, cudaLaunchCooperativeKernel(kb, dim3(h->G), dim3(kNT), args, smem, s));
@@ -760,8 +769,8 @@ int setup_geometry(eq_handle* h) {
     kf = (const void*)k_forward<float, kNT, kU, kSplitF>;
     kb = (const void*)k_backward<float, kNT, kU, kSplitB>;
   } else {
-    kf = (const void*)k_forward<double, kNT, kU, kSplitF>;
-    kb = (const void*)k_backward<double, kNT, kU, kSplitB>;
+    kf = (const void*)k_forward<double, kNT, kU, split_f<double>()>;
+    kb = (const void*)k_backward<double, kNT, kU, split_b<double>()>;
   }
   EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf, kNT, 0));
   {

@@ -52,16 +52,17 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--kind", default="ring")
     ap.add_argument("--capacity", type=int, default=0)
+    ap.add_argument("--precision", type=int, default=32)
     args = ap.parse_args()
     net, mask, amp, T = bench.make_inputs(args.config, args.trials, 0)
     T = args.steps
     mask = np.ascontiguousarray(mask[:, :T])
-    eng = Engine(net.n, args.trials, T, precision=32, kind=args.kind, capacity=args.capacity)
+    eng = Engine(net.n, args.trials, T, precision=args.precision, kind=args.kind, capacity=args.capacity)
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     eng.set_drive(mask, amp)
     for _ in range(2):
         out = eng.forward()
-        eng.backward((2 * (out["v"] - 0.25)).float(), want_amp=False)
+        eng.backward(2 * (out["v"] - 0.25), want_amp=False)
     torch.cuda.synchronize()
     G, _ = eng.geometry
     for which, label in ((0, "forward"), (1, "reverse")):
