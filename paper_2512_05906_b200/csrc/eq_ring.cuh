@@ -467,6 +467,59 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
       }
       continue;
     }
+    if (P::kSlotWords == 2 && acc_pop && (A.N & 1) == 0 && !dirty) {
+      // fp64 fast path: two neurons per thread with 16-byte accesses (a neuron's
+      // two int64 slot words are one longlong2); same per-neuron arithmetic
+      for (int jq = j0 + 2 * gtid; jq < j1; jq += 2 * Ro::NN) {
+        const int idx = tb0 + jq;
+        long long* accz = const_cast<long long*>(accm) + 2 * (size_t)idx;
+        const longlong2 s0 = *reinterpret_cast<const longlong2*>(accz);
+        const longlong2 s1 = *reinterpret_cast<const longlong2*>(accz + 2);
+        const double2 I2 = *reinterpret_cast<const double2*>(A.I + idx);
+        const double2 V2 = *reinterpret_cast<const double2*>(A.V + idx);
+        const double2 M2 = __ldg(reinterpret_cast<const double2*>(A.net.amp + jq));
+        const unsigned mw = __ldg(mrow + (jq >> 5)) >> (jq & 31);
+        int2 R2 = make_int2(0, 0);
+        if (A.refractory) R2 = *reinterpret_cast<const int2*>(A.refr + idx);
+        const long long qs2[2] = {s0.x, s1.x}, qm2[2] = {s0.y, s1.y};
+        const double Iv2[2] = {I2.x, I2.y}, Vv2[2] = {V2.x, V2.y}, Av2[2] = {M2.x, M2.y};
+        int rf2[2] = {R2.x, R2.y};
+        double In[2], Vn[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const T ps = P::deq(qs2[q], c.inv_scale);
+          const T pm = A.exact ? P::deq(qm2[q], c.inv_scale) : (T)0;
+          const T drive = ((mw >> q) & 1u) ? (T)Av2[q] : (T)0;
+          T i, v_new, a, v, t_spk;
+          if (lif_step(c, A.exact != 0, A.refractory, m, ps, pm, (T)Iv2[q], (T)Vv2[q], drive, rf2[q], i, v_new,
+                       a, v, t_spk)) {
+            if (t_spk != t_spk) {
+              raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, jq + q);
+            } else {
+              int pos = atomicAdd(&s_n, 1);
+              SpikeRec<T> rec;
+              rec.idx = idx + q;
+              rec.t = t_spk;
+              rec.a = a;
+              rec.vh = v;
+              if (pos < kCapN) s_own[pos] = rec;
+              else spill[pos - kCapN] = rec;
+            }
+          }
+          In[q] = (double)i;
+          Vn[q] = (double)v_new;
+        }
+        *reinterpret_cast<double2*>(A.I + idx) = make_double2(In[0], In[1]);
+        *reinterpret_cast<double2*>(A.V + idx) = make_double2(Vn[0], Vn[1]);
+        // RingQueue._pop_raw zeroes the slot (queues.py:114-117)
+        *reinterpret_cast<longlong2*>(accz) = make_longlong2(0, 0);
+        *reinterpret_cast<longlong2*>(accz + 2) = make_longlong2(0, 0);
+        if (A.refractory) *reinterpret_cast<int2*>(A.refr + idx) = make_int2(rf2[0], rf2[1]);
+        if (A.v_trace)
+          *reinterpret_cast<double2*>(A.v_trace + (size_t)(m - A.m0) * A.total + idx) = make_double2(Vn[0], Vn[1]);
+      }
+      continue;
+    }
     for (int jb = j0; jb < j1; jb += Ro::NN * U) {
       long long slot_v[U][2];
       T Iv[U], Vv[U], Am[U];
@@ -548,7 +601,7 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
   // queues.py:114-117), in a separate pass: a store next to the pending
   // load of the same line stalled the pop loop ~8x.  acc[m&1] receives no
   // red.add in this phase (the event side writes acc[(m+1)&1]).
-  const bool cleared = P::kSlotWords == 1 && acc_pop && (A.N & 3) == 0 && !dirty;   // by the vector update
+  const bool cleared = acc_pop && !dirty && (P::kSlotWords == 1 ? (A.N & 3) == 0 : (A.N & 1) == 0);   // by the vector update
   if (acc_pop && !cleared) {
     long long* accm = A.acc + (size_t)(m & 1) * A.total * P::kSlotWords;
     if (P::kSlotWords == 1 && ((begin | end) & 1) == 0) {
