@@ -1080,6 +1080,60 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
           }
           continue;
         }
+        if (sizeof(T) == 8 && (A.N & 1) == 0 && ((j0 | j1) & 1) == 0) {
+          // fp64 fast path: two neurons per thread, 16-byte accesses
+          for (int jq = j0 + 2 * gtid; jq < j1; jq += 2 * Ro::NN) {
+            const int idx = tb0 + jq;
+            const double2 LV2 = *reinterpret_cast<const double2*>(A.lamV + idx);
+            const double2 LI2 = *reinterpret_cast<const double2*>(A.lamI + idx);
+            const double lvv[2] = {LV2.x, LV2.y};
+            const double liv[2] = {LI2.x, LI2.y};
+            double nv[2], ni[2], ls[2], lm[2];
+            unsigned mw = 0;
+            if (A.gamp_bt) mw = __ldg(mrow + (jq >> 5)) >> (jq & 31);
+            const int loc0 = idx - (int)begin;
+            const unsigned sb = (s_bits[loc0 >> 5] >> (loc0 & 31)) & 0x3u;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const T lv = (T)lvv[q];
+              T la, lvh;
+              if ((sb >> q) & 1u) {
+                int k = s_pos[loc0 + q];
+                if (k == 0xffff) {
+                  k = 0;
+                  while (k < cnt && A.log[off + k].idx != idx + q) ++k;
+                }
+                SpikeRec<T> rec = A.log[off + k];
+                const T lt0 = (m + 1 < A.m_run ? A.lt_log[off + k] : (T)0) + (A.lt_rem ? A.lt_rem[off + k] : (T)0);
+                T t = rec.t, a = rec.a, vh = rec.vh;
+                T uu = (T)(m + 1) * c.dt - t;
+                T ku = eq_exp_t(-uu / c.tau_m);
+                T r = (c.v_th - a) / (vh - a);
+                T lt = lt0 + lv * (c.v_reset - a) * ku / c.tau_m;
+                T lr = -c.tau_m * lt / r;
+                T den = vh - a;
+                T den2 = den * den;
+                la = lv * ((T)1 - ku) + lr * (c.v_th - vh) / den2;
+                lvh = -lr * (c.v_th - a) / den2;
+              } else {
+                la = lv * ((T)1 - c.k_m);
+                lvh = lv * c.k_m;
+              }
+              const T lip = (T)liv[q] + la;
+              if (A.gamp_bt && ((mw >> q) & 1u)) A.gamp_bt[idx + q] += (double)la;
+              ls[q] = (double)(c.k_s * lip - c.cc * lvh);
+              lm[q] = (double)(c.cc * lvh);
+              ni[q] = (double)(c.k_s * lip);
+              nv[q] = (double)lvh;
+            }
+            double2* lr2 = reinterpret_cast<double2*>(lam_row + jq);
+            __stcs(lr2, make_double2(ls[0], lm[0]));
+            __stcs(lr2 + 1, make_double2(ls[1], lm[1]));
+            *reinterpret_cast<double2*>(A.lamI + idx) = make_double2(ni[0], ni[1]);
+            *reinterpret_cast<double2*>(A.lamV + idx) = make_double2(nv[0], nv[1]);
+          }
+          continue;
+        }
         for (int jb = j0; jb < j1; jb += Ro::NN * U) {
           T LV[U], LI[U];
 #pragma unroll
