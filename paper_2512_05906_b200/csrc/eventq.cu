@@ -31,7 +31,7 @@ constexpr int kSplitF = 288;  // forward event-side threads per CTA (measured: 2
 constexpr int kSplitB = 352;  // reverse event-side threads per CTA (measured: 224..448, profiles/)
 // fp64: the neuron side is the slower one (scalar paths, 16-byte slots), so it gets more threads
 #ifndef EQ_SPLIT_F64
-#define EQ_SPLIT_F64 224
+#define EQ_SPLIT_F64 288
 #endif
 #ifndef EQ_SPLIT_B64
 #define EQ_SPLIT_B64 256
