@@ -891,7 +891,7 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
     const int total = s_pre[nb];
     for (int w0 = 0; w0 < total; w0 += kEv) {
       const int wend = total - w0 < kEv ? total : w0 + kEv;
-      constexpr int EV = 4;
+      constexpr int EV = 3;
       for (int f0 = w0 + gtid; f0 < wend; f0 += EV * Ro::NF) {
         int jj[EV], kk[EV];
         long long xx[EV];
