@@ -273,7 +273,7 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
                   (unsigned long long)(s_pre[k + 1] - s_pre[k]));
       }
     }
-    constexpr int EV = 4;
+    constexpr int EV = 3;
     for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
       int jj[EV], kk[EV];
       T ww[EV], dd[EV];
