@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         const longlong2* bk = reinterpret_cast<const longlong2*>(
             A.bk + ((size_t)cta * A.NB + bin) * A.cap_b * bk_words<T>());
         long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
-        constexpr int DV = 4;
+        constexpr int DV = 8;
         for (int q = gtid; q < n; q += DV * Ro::NF) {
           longlong2 ev[DV], ev2[DV];
 #pragma unroll
