@@ -87,6 +87,7 @@ struct FwdArgs {
   // src_off + j; spikes imported from other partitions (emitted in the
   // previous exchange window) are fanned out in the launch's first phase
   int src_off;
+  int smem_state;            // I, V of the owned range kept in shared memory for the launch
   const SpikeRec<T>* imp;    // idx = trial*N (flat base of the trial), a = (T)emit step
   const long long* imp_r0;
   const int* imp_len;
@@ -388,7 +389,11 @@ template <typename T, int NT, int U, int NF>
 __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, const int cta, const int gtid,
                                             const long long begin, const long long end, const int b_first,
                                             const bool acc_pop, SpikeRec<T>* s_own, int& s_n, long long& s_off,
-                                            unsigned long long (*s_ctr)[3], SpikeRec<T>* spill) {
+                                            unsigned long long (*s_ctr)[3], SpikeRec<T>* spill, T* s_st = nullptr) {
+  // s_st: the CTA's I and V kept in shared memory across the launch ([per] I,
+  // then [per] V, indexed by idx - begin), or null (state in HBM)
+  T* const gI = s_st ? s_st - begin : A.I;
+  T* const gV = s_st ? s_st + A.per - begin : A.V;
   typedef Prec<T> P;
   typedef Roles<NT, NF> Ro;
   constexpr int kCapN = FwdShared<NT, T>::kCap / 2;
@@ -414,8 +419,8 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
         const int idx = tb0 + jq;
         const longlong2 a01 = *reinterpret_cast<const longlong2*>(accm + idx);
         const longlong2 a23 = *reinterpret_cast<const longlong2*>(accm + idx + 2);
-        const float4 I4 = *reinterpret_cast<const float4*>(A.I + idx);
-        const float4 V4 = *reinterpret_cast<const float4*>(A.V + idx);
+        const float4 I4 = *reinterpret_cast<const float4*>(gI + idx);
+        const float4 V4 = *reinterpret_cast<const float4*>(gV + idx);
         const float4 M4 = __ldg(reinterpret_cast<const float4*>(A.net.amp + jq));
         const unsigned mw = __ldg(mrow + (jq >> 5)) >> (jq & 31);
         int4 R4 = make_int4(0, 0, 0, 0);
@@ -452,8 +457,8 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
           In[q] = (float)i;
           Vn[q] = (float)v_new;
         }
-        *reinterpret_cast<float4*>(A.I + idx) = make_float4(In[0], In[1], In[2], In[3]);
-        *reinterpret_cast<float4*>(A.V + idx) = make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
+        *reinterpret_cast<float4*>(gI + idx) = make_float4(In[0], In[1], In[2], In[3]);
+        *reinterpret_cast<float4*>(gV + idx) = make_float4(Vn[0], Vn[1], Vn[2], Vn[3]);
         // RingQueue._pop_raw zeroes the slot (queues.py:114-117): the load has been
         // consumed, so this store does not wait behind it
         long long* accz = const_cast<long long*>(accm) + idx;
@@ -548,8 +553,8 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
               }
             }
           }
-          Iv[u] = A.I[idx];
-          Vv[u] = A.V[idx];
+          Iv[u] = gI[idx];
+          Vv[u] = gV[idx];
           rf[u] = A.refractory ? A.refr[idx] : 0;
           mw[u] = __ldg(mrow + (j >> 5));
           Am[u] = __ldg(A.net.amp + j);
@@ -588,8 +593,8 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
             else spill[pos - kCapN] = rec;
           }
         }
-        A.I[idx] = i;
-        A.V[idx] = v_new;
+        gI[idx] = i;
+        gV[idx] = v_new;
         if (A.refractory) A.refr[idx] = rf[u];
         if (A.v_trace) A.v_trace[(size_t)(m - A.m0) * A.total + idx] = v_new;
       }
@@ -708,6 +713,14 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   if (A.kind == EQ_KIND_RING)
     for (int k = tid; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
   if (tid == 0) s_n = 0;
+  // state in shared memory for the launch (A.smem_state): I then V of the owned range
+  extern __shared__ __align__(16) unsigned char s_dynf[];
+  T* s_st = A.smem_state ? reinterpret_cast<T*>(s_dynf) : nullptr;
+  if (s_st)
+    for (long long k = tid; k < end - begin; k += NT) {
+      s_st[k] = A.I[begin + k];
+      s_st[A.per + k] = A.V[begin + k];
+    }
   __syncthreads();
 
   // Phase m: (a) [event side] deliver this CTA's bucket m+1 and fan out its
@@ -776,7 +789,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
       // ======================== neuron side
       const int gtid = tid - Ro::NF;
       neuron_side<T, NT, U, NF>(A, m, cta, gtid, begin, end, b_first, A.kind == EQ_KIND_RING, s_own, s_n, s_off,
-                                s_ctr, spill);
+                                s_ctr, spill, s_st);
     }
     __syncthreads();
     if (m == A.m1) break;
@@ -788,6 +801,11 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
     if (ld_volatile(A.err) != 0) break;
   }
   __syncthreads();
+  if (s_st)
+    for (long long k = tid; k < end - begin; k += NT) {
+      A.I[begin + k] = s_st[k];
+      A.V[begin + k] = s_st[A.per + k];
+    }
   if (A.kind == EQ_KIND_RING)
     for (int k = tid; k < A.NB; k += NT) A.bk_cnt[(size_t)cta * A.NB + k] = s_bin[k];
   if (tid < kTr) {

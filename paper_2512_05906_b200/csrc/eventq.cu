@@ -29,6 +29,7 @@ constexpr int kNT = 512;   // threads per CTA of the persistent kernels
 constexpr int kU = 4;      // neurons per thread in flight per round
 constexpr int kSplitF = 288;  // forward event-side threads per CTA (measured: 224..384, profiles/)
 constexpr int kSplitB = 352;  // reverse event-side threads per CTA (measured: 224..448, profiles/)
+constexpr size_t kStateSmem = 72 * 1024;   // forward state in shared memory up to this size per CTA
 // fp64: the neuron side is the slower one (scalar paths, 16-byte slots), so it gets more threads
 #ifndef EQ_SPLIT_F64
 #define EQ_SPLIT_F64 288
@@ -551,6 +552,11 @@ int check_err(eq_handle* h, cudaStream_t s) {
   return fail(h, e[0], buf);
 }
 
+bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] == '1';
+}
+
 std::array<long long, 4>* find_block(eq_handle* h, int start) {
   for (auto& b : h->imp_blocks)
     if (b[0] == start && b[2] > 0) return &b;
@@ -595,6 +601,7 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
   A.counters = h->counters;
   A.v_trace = (T*)v_trace;
   A.src_off = h->src_off;
+  A.smem_state = 0;
   A.imp = nullptr;
   A.imp_r0 = nullptr;
   A.imp_len = nullptr;
@@ -658,7 +665,19 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
       if (n_steps == 0) return check_err(h, s);   // flush: deliver the imports, no step
     }
     const void* kf = (const void*)k_forward<T, kNT, kU, split_f<T>()>;
-    EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, 0, s));
+    // fp32: I and V of each CTA's range in shared memory for the whole launch
+    // when two CTAs per SM still fit (state 2 x per x 4 B next to ~39 KB static)
+    const size_t st_bytes = (size_t)2 * h->per * sizeof(T);
+    size_t dyn = 0;
+    if (sizeof(T) == 4 && st_bytes <= kStateSmem && !getenv_flag("EQ_NO_SMEM_STATE")) {
+      EQ_CUDA(h, cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st_bytes));
+      int occ = 0;   // the cooperative grid must stay co-resident
+      EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kNT, st_bytes));
+      if ((long long)occ * h->n_sm >= h->G) dyn = st_bytes;
+    }
+    FwdArgs<T>* ap = &A;
+    ap->smem_state = dyn > 0;
+    EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, dyn, s));
   }
   h->launches += 1;
   int rc = check_err(h, s);
