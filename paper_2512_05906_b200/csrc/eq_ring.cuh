@@ -862,15 +862,55 @@ struct BwdArgs {
 // Random 8/16-byte reverse-slot gather: ask L2 for a 64-byte fill instead of
 // the default 128 (fewer DRAM bytes per useful byte; the DRAM is ~56% busy in
 // the reverse pass at 24 trials, profiles/r1d_c3x24.md).
+// L2 cache policies of the reverse pass (bit 0: gathers evict-first, bit 1:
+// gradient reds evict-last with fraction EQ_HINT_FRAC).  A/B on one box, C3 x 24
+// trials: none 49.1 ms, gathers only 45.95, both (fraction 0.5) 45.75, both
+// (1.0) 45.53 (profiles/r1g_ab_hint.txt).
+#ifndef EQ_HINT
+#define EQ_HINT 3
+#endif
+#ifndef EQ_HINT_FRAC
+#define EQ_HINT_FRAC 1.0
+#endif
+#define EQ_STR2(x) #x
+#define EQ_STR(x) EQ_STR2(x)
 __device__ __forceinline__ float2 ld_gather(const float2* p) {
   float2 v;
+#if EQ_HINT & 1
+  // the gathered line is rarely hit again before eviction (1.2 GB live ring): evict first
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.L2::cache_hint.L2::64B.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+#else
   asm volatile("ld.global.L2::64B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+#endif
   return v;
 }
 __device__ __forceinline__ double2 ld_gather(const double2* p) {
   double2 v;
+#if EQ_HINT & 1
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.L2::cache_hint.L2::64B.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+#else
   asm volatile("ld.global.L2::64B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+#endif
   return v;
+}
+// Per-edge gradient reductions of the reverse pass (dL/dw, dL/dd: 2 x 8 B x E,
+// 160 MB at C3): with EQ_HINT & 2 they are kept in L2 evict-last (a fraction
+// EQ_HINT_FRAC of the accesses), so the ring gathers evict them last.
+__device__ __forceinline__ void red_grad(double* p, double v) {
+#if EQ_HINT & 2
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, " EQ_STR(EQ_HINT_FRAC) ";" : "=l"(pol));
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
+               : "memory");
+#else
+  red_add_f64(p, v);
+#endif
 }
 
 template <typename T>
@@ -954,8 +994,8 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
             const T2 L = ld_gather(A.lam + ((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]);
             const T g_w = es * L.x + em * L.y;
             g_tp = w * (es * L.x * c.inv_tau_s + em * L.y * c.inv_tau_m);
-            red_add_f64(A.gw + xx[e], (double)g_w);
-            red_add_f64(A.gd + xx[e], (double)g_tp);
+            red_grad(A.gw + xx[e], (double)g_w);
+            red_grad(A.gd + xx[e], (double)g_tp);
           }
           s_gtp[f - w0] = g_tp;
         }
