@@ -100,6 +100,12 @@ __device__ __forceinline__ bool key_less(int da, int sa, int db, int sb) {
 //             8 keys per round trip, measured no faster at capacity 64);
 //   FIFO    — circular buffer, pops read 4 head entries per round trip.
 constexpr int kHeapD = 8;
+// EQ_PF_NEXT=1: prefetch the next owned queue's lines one iteration ahead.
+// Measured slower (C3 x 16 heap cap 64 fwd 163 -> 188 ms, sorted 208 -> 230,
+// profiles/r1g_ab_prefetch_next.txt); kept as an A/B knob, off.
+#ifndef EQ_PF_NEXT
+#define EQ_PF_NEXT 0
+#endif
 
 template <typename T>
 __device__ __forceinline__ int2 qkey(const QEv<T>* p) {   // {tag, due}: the entry's first 8 bytes
@@ -307,18 +313,37 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
       const bool drv = !last && drive_bit(F.net, b, m, j);
       const T ampj = __ldg(F.net.amp + j);
       bool dirty = false;
-      if (narr > 0 || (!last && mt.x > 0 && mt.w == m)) {
-        // the queue lines this step's inserts and pops will walk, fetched into
-        // L2 together: the structure's dependent chains then miss DRAM once
-        const char* qb = reinterpret_cast<const char*>(A.q + (size_t)idx * A.cap);
-        const int span = mt.x + narr < A.cap ? mt.x + narr : A.cap;
-        const int first = F.kind == EQ_KIND_BINARYHEAP ? 0 : mt.y;
-        for (int e = 0; e < span; e += 128 / (int)sizeof(QEv<T>)) {
-          int k = first + e;
-          if (k >= A.cap) k -= A.cap;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + (size_t)k * sizeof(QEv<T>)));
+      // the queue lines a step's inserts and pops will walk, fetched into L2
+      // together: the structure's dependent chains then miss DRAM once
+      auto prefetch_queue = [&](int qidx, const int4& qm, int qn) {
+        if (qn > 0 || (!last && qm.x > 0 && qm.w == m)) {
+          const char* qb = reinterpret_cast<const char*>(A.q + (size_t)qidx * A.cap);
+          const int span = qm.x + qn < A.cap ? qm.x + qn : A.cap;
+          const int first = F.kind == EQ_KIND_BINARYHEAP ? 0 : qm.y;
+          for (int e = 0; e < span; e += 128 / (int)sizeof(QEv<T>)) {
+            int k = first + e;
+            if (k >= A.cap) k -= A.cap;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + (size_t)k * sizeof(QEv<T>)));
+          }
+        }
+      };
+#if EQ_PF_NEXT
+      // software pipeline over the thread's queues: the next owned queue's lines
+      // are requested now, so its chains start from L2 instead of one DRAM miss
+      if (base == begin) prefetch_queue(idx, mt, narr);
+      {
+        const long long nx = (long long)idx + NT;
+        if (nx < end) {
+          const int nidx = (int)nx;
+          const int nb = c.divN.div(nidx);
+          const int4 nmt = A.meta[nidx];
+          const int nn = ins ? A.acnt[((size_t)((m - 1) & 1) * F.B + nb) * F.N + (nidx - nb * F.N)] : 0;
+          prefetch_queue(nidx, nmt, nn);
         }
       }
+#else
+      prefetch_queue(idx, mt, narr);
+#endif
       if (narr > 0) {
         {
           *cntp = 0;
