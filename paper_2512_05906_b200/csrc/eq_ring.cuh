@@ -23,6 +23,24 @@
 
 namespace eq {
 
+// Forward delivery into the L2-resident fixed-point accumulator (2 x B x N x 8 B,
+// 38 MB at C3 x 24).  EQ_ACC_HINT=1 marks it evict-last (A/B knob).
+#ifndef EQ_ACC_HINT
+#define EQ_ACC_HINT 0
+#endif
+#ifndef EQ_BK_ST
+#define EQ_BK_ST 0
+#endif
+__device__ __forceinline__ void red_acc(long long* p, long long v) {
+#if EQ_ACC_HINT
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+#else
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#endif
+}
+
 template <typename T>
 struct StepConsts {
   T dt, tau_m, tau_s, v_th, v_reset, k_m, k_s, cc;
@@ -338,12 +356,21 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
         const int pos = atomicAdd(&s_bin[bn], 1);
         if (pos < A.cap_b) {
           longlong2* o = reinterpret_cast<longlong2*>(bk_cta + ((size_t)bn * A.cap_b + pos) * bk_words<T>());
+#if EQ_BK_ST
+          if (P::kSlotWords == 1) {                         // A/B: default store policy
+            *o = make_longlong2(tgt, pack2(q1, q2));
+          } else {
+            o[0] = make_longlong2(tgt, q1);
+            o[1] = make_longlong2(q2, 0);
+          }
+#else
           if (P::kSlotWords == 1) {                         // read once, ~H/2 steps later: streaming
             __stcs(o, make_longlong2(tgt, pack2(q1, q2)));
           } else {
             __stcs(o, make_longlong2(tgt, q1));
             __stcs(o + 1, make_longlong2(q2, 0));
           }
+#endif
         } else {                                            // bucket full: DRAM ring row
           const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
           if (P::kSlotWords == 1) {
@@ -766,10 +793,10 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
           for (int e = 0; e < DV; ++e) {
             if (ev[e].x < 0) continue;
             if (P::kSlotWords == 1) {
-              red_add(accn + ev[e].x, ev[e].y);
+              red_acc(accn + ev[e].x, ev[e].y);
             } else {
-              red_add(accn + 2 * (size_t)ev[e].x, ev[e].y);
-              red_add(accn + 2 * (size_t)ev[e].x + 1, ev2[e].x);
+              red_acc(accn + 2 * (size_t)ev[e].x, ev[e].y);
+              red_acc(accn + 2 * (size_t)ev[e].x + 1, ev2[e].x);
             }
           }
         }
