@@ -976,7 +976,10 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
     const int total = s_pre[nb];
     for (int w0 = 0; w0 < total; w0 += kEv) {
       const int wend = total - w0 < kEv ? total : w0 + kEv;
-      constexpr int EV = 3;
+#ifndef EQ_REV_EV
+#define EQ_REV_EV 2
+#endif
+      constexpr int EV = EQ_REV_EV;   // events in flight per thread (2: bwd 45.9 -> 43.6 ms vs 3, profiles/r1g_ab_rev*.txt)
       for (int f0 = w0 + gtid; f0 < wend; f0 += EV * Ro::NF) {
         int jj[EV], kk[EV];
         long long xx[EV];

@@ -28,7 +28,10 @@ namespace {
 constexpr int kNT = 512;   // threads per CTA of the persistent kernels
 constexpr int kU = 4;      // neurons per thread in flight per round
 constexpr int kSplitF = 288;  // forward event-side threads per CTA (measured: 224..384, profiles/)
-constexpr int kSplitB = 352;  // reverse event-side threads per CTA (measured: 224..448, profiles/)
+#ifndef EQ_SPLIT_B32
+#define EQ_SPLIT_B32 352
+#endif
+constexpr int kSplitB = EQ_SPLIT_B32;  // reverse event-side threads per CTA (measured: 224..448, profiles/)
 constexpr size_t kStateSmem = 72 * 1024;   // forward state in shared memory up to this size per CTA
 // fp64: the neuron side is the slower one (scalar paths, 16-byte slots), so it gets more threads
 #ifndef EQ_SPLIT_F64
