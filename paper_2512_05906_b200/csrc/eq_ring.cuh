@@ -292,7 +292,10 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
                   (unsigned long long)(s_pre[k + 1] - s_pre[k]));
       }
     }
-    constexpr int EV = 3;
+#ifndef EQ_FWD_EV
+#define EQ_FWD_EV 3
+#endif
+    constexpr int EV = EQ_FWD_EV;
     for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
       int jj[EV], kk[EV];
       T ww[EV], dd[EV];
@@ -943,7 +946,10 @@ __device__ __forceinline__ void red_grad(double* p, double v) {
 template <typename T>
 struct BwdShared {
   static constexpr int kCapB = sizeof(T) == 4 ? 512 : 256;   // spikes per batch
-  static constexpr int kEv = sizeof(T) == 4 ? 4096 : 2048;    // events per reduction window
+#ifndef EQ_REV_WIN
+#define EQ_REV_WIN 4096
+#endif
+  static constexpr int kEv = sizeof(T) == 4 ? EQ_REV_WIN : 2048;    // events per reduction window
 };
 
 // R-fanout of log records [s0, s1): the CTA's share of step
