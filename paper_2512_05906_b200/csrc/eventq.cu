@@ -38,7 +38,7 @@ constexpr size_t kStateSmem = 72 * 1024;   // forward state in shared memory up 
 #define EQ_SPLIT_F64 288
 #endif
 #ifndef EQ_SPLIT_B64
-#define EQ_SPLIT_B64 256
+#define EQ_SPLIT_B64 288   // 256 -> 288 with EV 2: fp64 bwd 59.6-61.1 -> 59.1 ms (profiles/r1h_ab_4.txt)
 #endif
 template <typename T> constexpr int split_f() { return sizeof(T) == 4 ? kSplitF : EQ_SPLIT_F64; }
 template <typename T> constexpr int split_b() { return sizeof(T) == 4 ? kSplitB : EQ_SPLIT_B64; }
