@@ -899,6 +899,9 @@ struct BwdArgs {
 #ifndef EQ_HINT
 #define EQ_HINT 3
 #endif
+#ifndef EQ_GATHER_NA
+#define EQ_GATHER_NA 0   // A/B: gathers bypass L1 allocation
+#endif
 #ifndef EQ_HINT_FRAC
 #define EQ_HINT_FRAC 1.0
 #endif
@@ -910,8 +913,13 @@ __device__ __forceinline__ float2 ld_gather(const float2* p) {
   // the gathered line is rarely hit again before eviction (1.2 GB live ring): evict first
   unsigned long long pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#if EQ_GATHER_NA
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.L2::64B.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+#else
   asm volatile("ld.global.L2::cache_hint.L2::64B.v2.f32 {%0, %1}, [%2], %3;"
                : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+#endif
 #else
   asm volatile("ld.global.L2::64B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
 #endif
