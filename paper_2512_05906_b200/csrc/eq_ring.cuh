@@ -28,6 +28,9 @@ namespace eq {
 #ifndef EQ_ACC_HINT
 #define EQ_ACC_HINT 0
 #endif
+#ifndef EQ_BIN_AGG
+#define EQ_BIN_AGG 0
+#endif
 #ifndef EQ_BK_ST
 #define EQ_BK_ST 0
 #endif
@@ -356,7 +359,20 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
           }
           bn = ds % A.NB;
         }
+#if EQ_BIN_AGG
+        // warp-aggregated bucket slot allocation (A/B knob): one shared atomic per
+        // distinct bin in the warp (slot order is free: the sums are fixed point)
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, bn);
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&s_bin[bn], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const int pos = base + __popc(peers & ((1u << lane) - 1u));
+#else
         const int pos = atomicAdd(&s_bin[bn], 1);
+#endif
         if (pos < A.cap_b) {
           longlong2* o = reinterpret_cast<longlong2*>(bk_cta + ((size_t)bn * A.cap_b + pos) * bk_words<T>());
 #if EQ_BK_ST
