@@ -46,21 +46,44 @@ def read_peaks():
 
 
 # ---------------------------------------------------------------- algorithmic bytes
-# SURVEY.md §8(d) / BASELINE.md §4 (fp32, ring, exact delivery, reverse mode):
-#   per neuron-step 60 B = fwd 36 [slot 8 read + 8 clear, drive 4, I/V 16] + bwd 24 [adjoints 16, slot 8]
-#   per spike 32 B       = fwd 16 (record write) + bwd 16 (record read)
-#   per event 64 B       = fwd 28 [CSR 12, slot RMW 16] + bwd 36 [CSR 12, gather 8, (g_w,g_d) RMW 16]
-FWD_B = (36.0, 16.0, 28.0)
-BWD_B = (24.0, 16.0, 36.0)
-# bounded kinds (FIFO / heap / sorted), same rules: per event the fwd moves
-# CSR 12 + the event record {due, W_s, W_m} 12 written at enqueue and 12 read at pop = 36 B;
-# per neuron-step the queue meta {count, head, tail, next due} 16 B replaces the slot's 16 B
-FWD_B_BOUNDED = (36.0, 16.0, 36.0)
+# SURVEY.md §8(d) / BASELINE.md §4, written for element size t (4 fp32 / 8 fp64)
+# and fixed-point slot word q (int32 fp32 / int64 fp64); at t = q = 4 these are
+# the survey's fp32 figures (ring, exact delivery, reverse mode):
+#   per neuron-step   fwd [slot 2q read + 2q clear, drive 4, I/V 4t] = 36 B
+#                     bwd [adjoints 4t, reverse slot 2t]             = 24 B
+#   per spike         record {t, a, v_hat} 3t + id 4, written fwd, read bwd = 16 + 16 B
+#   per event         fwd [CSR 4 + 2t, slot RMW 4q]                  = 28 B
+#                     bwd [CSR 4 + 2t, gather 2t, (g_w, g_d) RMW 4t] = 36 B
+# bounded kinds (FIFO / heap / sorted), same rules: per event the fwd moves CSR
+# 4 + 2t plus the event record {due 4, W_s q, W_m q} written at enqueue and read
+# at pop; per neuron-step the queue meta 16 B replaces the slot's 4q.
+def byte_model(precision=32, bounded=False):
+    t = 4 if precision == 32 else 8
+    q = t
+    fwd_ns = (16 if bounded else 4 * q) + 4 + 4 * t
+    fwd_ev = (4 + 2 * t) + (2 * (4 + 2 * q) if bounded else 4 * q)
+    spike = 3 * t + 4
+    return {"fwd": (fwd_ns, spike, fwd_ev), "bwd": (6 * t, spike, (4 + 2 * t) + 2 * t + 4 * t)}
 
 
-def alg_bytes(neuron_steps, spikes, events, which, bounded=False):
-    a = (FWD_B_BOUNDED if bounded else FWD_B) if which == "fwd" else BWD_B
+def alg_bytes(neuron_steps, spikes, events, which, bounded=False, precision=32):
+    a = byte_model(precision, bounded and which == "fwd")[which]
     return a[0] * neuron_steps + a[1] * spikes + a[2] * events
+
+
+def host_label():
+    """CPU model and logical core count of this host (the reference's
+    bench.platform_label, pkg/src/eventq/bench.py:48-60, names the host too)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{model} x {os.cpu_count()} logical cores"
 
 
 class ClockSampler:
@@ -185,6 +208,10 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
+    # torchrun pins OMP_NUM_THREADS=1 per rank; the CPU arm alone on this host
+    # uses every core (read by the OpenMP runtime when the oracle loads)
+    if world > 1 or os.environ.get("OMP_NUM_THREADS") == "1":
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     from oracle import oracle as orc
     trials = args.cpu_trials or min(orc.threads(), 16)
     net, mask, amp, T = make_inputs(args.config, trials, 0, delay_steps=args.delays)
@@ -202,6 +229,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": f"{args.config} {args.kind} fwd+bwd (sample)", **info},
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": info["cores"], "kind": "port",
+                         "host": host_label(),
                          "sample": f"{info['trials']} trials x {info['steps']} steps of {args.config}"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -209,6 +237,43 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- our arm
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> None:
+    """`bench.py --gpus N` run as a plain process (no WORLD_SIZE): start N ranks
+    on this node with torch.distributed.run and exit with their status.  NCCL
+    logs its communicator setup (NCCL_DEBUG=INFO) so the transport is on record."""
+    import subprocess
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def launch_selftest(args):
+    """Launcher check without GPUs (tests/test_bench_launch.py): every rank
+    joins a gloo group and all-reduces its rank; rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"launched {world} ranks for --gpus {args.gpus}")
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank)])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "rank_sum": float(t.item())}), flush=True)
+    dist.destroy_process_group()
+
 
 def run_ours(args):
     import torch
@@ -218,6 +283,8 @@ def run_ours(args):
     from paper_2512_05906_b200 import workload as wl
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} is running with WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -370,8 +437,8 @@ def run_ours(args):
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     fwd_avg, bwd_avg = statistics.mean(fwd), statistics.mean(bwd)
     bounded = args.kind in ("fiforing", "binaryheap", "sortedarray")
-    fwd_bytes = alg_bytes(neuron_steps, spikes, events, "fwd", bounded)
-    bwd_bytes = alg_bytes(neuron_steps, spikes, events, "bwd")
+    fwd_bytes = alg_bytes(neuron_steps, spikes, events, "fwd", bounded, args.precision)
+    bwd_bytes = alg_bytes(neuron_steps, spikes, events, "bwd", False, args.precision)
     fwd_name = "k_forward_bounded" if bounded else "k_forward"
     dom = (fwd_name, fwd_bytes, fwd_avg) if fwd_avg >= bwd_avg else ("k_backward", bwd_bytes, bwd_avg)
     achieved = dom[1] / (dom[2] / 1e3) / 1e9
@@ -395,7 +462,7 @@ def run_ours(args):
         try:
             v, info = cpu_reference_sample(net, mask, amp, T, max_trials=args.cpu_trials, steps=args.cpu_steps,
                                            kind=args.kind, capacity=args.capacity)
-            cpu = {"value": v, "unit": "events/s", "cores": info["cores"], "kind": "port",
+            cpu = {"value": v, "unit": "events/s", "cores": info["cores"], "kind": "port", "host": host_label(),
                    "sample": f"{info['trials']} trials x {info['steps']} steps of {args.config}, "
                              f"fwd+bwd, OpenMP over trials ({info['seconds']:.1f} s)"}
         except Exception as exc:  # the checker must not sink the bench line
@@ -428,7 +495,11 @@ def run_ours(args):
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": "profiles/" + TRAFFIC_FILE if traffic else None,
                      "alg_bytes_per_launch": dom[1], "avg_launch_ms": dom[2],
-                     "fwd_ms": fwd_avg, "bwd_ms": bwd_avg},
+                     "fwd_ms": fwd_avg, "bwd_ms": bwd_avg,
+                     # the north-star target is stated for forward + reverse together
+                     "fwd_bwd": {"alg_bytes": fwd_bytes + bwd_bytes, "ms": fwd_avg + bwd_avg,
+                                 "achieved": (fwd_bytes + bwd_bytes) / ((fwd_avg + bwd_avg) / 1e3) / 1e9,
+                                 "frac": (fwd_bytes + bwd_bytes) / ((fwd_avg + bwd_avg) / 1e3) / 1e9 / peak}},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "events/s", "h2d_bytes_per_step": int(mask.nbytes),
                 "d2h_bytes_per_step": int(2 * 4 * net.n_edges + 8)},
@@ -457,8 +528,13 @@ def main():
     ap.add_argument("--capacity", type=int, default=0, help="bounded kinds: events per queue")
     ap.add_argument("--delays", type=lambda s: tuple(int(x) for x in s.split(",")), default=None,
                     help="delay range in steps lo,hi (FIFO needs lo == hi)")
+    ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and (args.impl == "ours" or args.launch_selftest):
+        relaunch_under_torchrun(args)
+    if args.launch_selftest:
+        launch_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

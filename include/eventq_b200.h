@@ -204,6 +204,14 @@ int64_t eq_launch_count(const eq_handle* h);
  * the grid barrier, [3] after it, [4..7] kernel-specific sub-phase marks (0 = unset).
  * Only when the environment had EQ_TIMELINE=1 at eq_create. */
 int eq_debug_timeline(eq_handle* h, int which, uint64_t* host_out);
+/* Spike-log capacity (records) and how many times eq_run grew it: the log
+ * starts at eq_config.max_spikes (or the default) and doubles whenever one more
+ * step could overflow it; the run pauses at that step boundary and resumes. */
+int64_t eq_log_capacity(const eq_handle* h, int32_t* n_grows);
+/* Test hook (ring kind): events per calendar bucket per CTA before a bucket
+ * spills into the DRAM overflow ring, 1 <= cap <= the allocated size; takes
+ * effect from the next eq_reset.  Small values force the spill path. */
+int eq_debug_set_bucket_capacity(eq_handle* h, int64_t cap);
 
 /* ------------------------------------------------------------------------
  * Queue operator API: a batch of Q independent queues of one kind that step

@@ -36,21 +36,41 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stamp_path(lib: str) -> str:
+    return lib + ".flags"
+
+
+def _stale(lib: str, flags: str) -> bool:
+    """Rebuild when a source is newer than the library OR the library was built
+    with different nvcc flags (the stamp file next to it records them)."""
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    try:
+        with open(_stamp_path(lib)) as f:
+            if f.read() != flags:
+                return True
+    except OSError:
+        return True
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps += [os.path.join(HERE, "..", "include", f) for f in ("eq_math.h", "eventq_b200.h")]
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    extra = os.environ.get("EQ_NVCC_EXTRA", "").split()   # A/B builds (e.g. -DEQ_SPLIT_F64=192)
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Build the library.  A/B builds (EQ_NVCC_EXTRA, e.g. -DEQ_REV_EV=3) never
+    touch the canonical lib/libeventq_b200.so: they need an explicit output
+    path (``out`` or EQ_AB_OUT) and are loaded with EQ_LIB_PATH."""
+    extra = os.environ.get("EQ_NVCC_EXTRA", "").split()
+    out = out or os.environ.get("EQ_AB_OUT")
+    if extra and not out:
+        raise RuntimeError("EQ_NVCC_EXTRA builds need EQ_AB_OUT=<path>: the default library stays the default build")
+    lib = os.path.abspath(out) if out else LIB
+    flags = " ".join(NVCC_FLAGS + extra)
+    if not force and not _stale(lib, flags):
+        return lib
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    tmp = lib + ".tmp"
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
     env = dict(os.environ)
     # the image's CXX wrapper lacks some runtime specs; nvcc's host compiler is the system gcc
@@ -61,8 +81,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    with open(_stamp_path(lib), "w") as f:
+        f.write(flags)
+    return lib
 
 
 if __name__ == "__main__":

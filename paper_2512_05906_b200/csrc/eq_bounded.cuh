@@ -79,8 +79,7 @@ struct BndArgs {
   int* acnt;                  // [2][B][N] arrivals per target
   QEv<T>* q;                  // [B*N][cap]
   int4* meta;                 // [B*N] {count, head|seq, tail_key, next_due}
-  long long* ev_base;         // [log_cap] flat event id of each logged spike's first edge
-  unsigned long long* ev_count;  // run-wide event id counter
+  int maxdeg;                 // event id = log position * maxdeg + row offset
   unsigned* drop_bits;        // [drop_cap/32]
   long long drop_cap;
   int insert_first;           // first step whose arrivals this launch inserts
@@ -100,12 +99,6 @@ __device__ __forceinline__ bool key_less(int da, int sa, int db, int sb) {
 //             8 keys per round trip, measured no faster at capacity 64);
 //   FIFO    — circular buffer, pops read 4 head entries per round trip.
 constexpr int kHeapD = 8;
-// EQ_PF_NEXT=1: prefetch the next owned queue's lines one iteration ahead.
-// Measured slower (C3 x 16 heap cap 64 fwd 163 -> 188 ms, sorted 208 -> 230,
-// profiles/r1g_ab_prefetch_next.txt); kept as an A/B knob, off.
-#ifndef EQ_PF_NEXT
-#define EQ_PF_NEXT 0
-#endif
 
 template <typename T>
 __device__ __forceinline__ int2 qkey(const QEv<T>* p) {   // {tag, due}: the entry's first 8 bytes
@@ -261,7 +254,7 @@ __device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int 
       raise_error(A.f.err, EQ_ERR_CAPABILITY, ms + 1, b, j);
     } else if (rc == 1) {
       drops += 1;
-      const long long id = A.ev_base[a.tag] + a.ro;
+      const long long id = (long long)a.tag * A.maxdeg + a.ro;
       if (id < A.drop_cap) atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
       else raise_error(A.f.err, EQ_ERR_CAPACITY, ms, b, j);
     }
@@ -278,7 +271,6 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
   __shared__ int s_pre[kCap + 1];
   __shared__ int s_n;
   __shared__ long long s_off;
-  __shared__ long long s_evoff;
   __shared__ unsigned long long s_ctr[kTr][3];
   FwdArgs<T>& F = A.f;
 
@@ -291,8 +283,9 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
   SpikeRec<T>* spill = F.scratch + (size_t)cta * F.per;
   if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
 
-  for (int m = F.m0; m <= F.m1; ++m) {
-    const bool last = (m == F.m1);   // extra pass: insert the final step's arrivals only
+  int m1 = F.m1;   // lowered at a barrier when the spike log could overflow (pause_due)
+  for (int m = F.m0; m <= m1; ++m) {
+    const bool last = (m == m1);   // extra pass: insert the final step's arrivals only
     if (tid == 0) s_n = 0;
     __syncthreads();
     if (!last) tl_mark(F.tl, m, F.G, cta, 0);
@@ -327,23 +320,9 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
           }
         }
       };
-#if EQ_PF_NEXT
-      // software pipeline over the thread's queues: the next owned queue's lines
-      // are requested now, so its chains start from L2 instead of one DRAM miss
-      if (base == begin) prefetch_queue(idx, mt, narr);
-      {
-        const long long nx = (long long)idx + NT;
-        if (nx < end) {
-          const int nidx = (int)nx;
-          const int nb = c.divN.div(nidx);
-          const int4 nmt = A.meta[nidx];
-          const int nn = ins ? A.acnt[((size_t)((m - 1) & 1) * F.B + nb) * F.N + (nidx - nb * F.N)] : 0;
-          prefetch_queue(nidx, nmt, nn);
-        }
-      }
-#else
+      // (prefetching the NEXT owned queue one iteration ahead measured slower:
+      // C3 x 16 heap fwd 163 -> 188 ms, profiles/r1g_ab_prefetch_next.txt)
       prefetch_queue(idx, mt, narr);
-#endif
       if (narr > 0) {
         {
           *cntp = 0;
@@ -440,10 +419,6 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
       warp0_scan(s_pre, nb);
       __syncthreads();
       const int total = s_pre[nb];
-      if (tid == 0) s_evoff = (long long)atomicAdd(A.ev_count, (unsigned long long)total);
-      __syncthreads();
-      if (log_ok)
-        for (int k = tid; k < nb; k += NT) A.ev_base[s_off + k0 + k] = s_evoff + s_pre[k];
       const int par = m & 1;
       for (int f = tid; f < total; f += NT) {
         const int k = find_row(s_pre, nb, f);
@@ -490,7 +465,9 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
     if (!grid_sync(F.bar, F.G, F.err, F.step_start + m + 1, F.log_count)) break;
     tl_mark(F.tl, m, F.G, cta, 3);
     if (ld_volatile(F.err) != 0) break;
+    if (m + 1 < m1 && pause_due(F, m)) m1 = m + 1;
   }
+  if (cta == 0 && tid == 0) F.err[4] = m1;
   // per-trial counters
   __syncthreads();
   if (tid < kTr) {

@@ -128,26 +128,8 @@ __device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-// Grid-wide barrier for a cooperative (co-resident) launch.  bar[0] = arrival
-// count, bar[32] = generation (separate 128-byte lines so spinning readers do
-// not queue behind arrivals).  Arrival is an acq_rel atomic (cumulative over
-// the CTA's writes ordered before it by bar.sync); waiters spin with relaxed
-// loads (no L1 invalidation per poll) and take one acquire fence on exit.  No
-// seq_cst fences: MEMBAR.SC.GPU on 296 CTAs per step cost ~100 us here.  A 20 s
-// watchdog turns a wedged barrier into EQ_ERR_CUDA instead of a hung GPU.
-// Two-level grid barrier for a cooperative (co-resident) launch: CTAs arrive
-// on a per-group counter (16 CTAs per group, own 128-byte line), the last of
-// each group arrives on the top counter, the last group releases a new
-// generation.  Arrivals are acq_rel atomics (cumulative over the CTA's writes
-// ordered before them by bar.sync); waiters spin with relaxed loads (no L1
-// invalidation per poll) and take one acquire fence on exit.  No seq_cst
-// fences (MEMBAR.SC.GPU on 296 CTAs per step cost ~100 us here).  A 20 s
-// watchdog turns a wedged barrier into EQ_ERR_CUDA instead of a hung GPU.
-// Layout of `bar`: [0] top count, [32] generation, [64 + 32*g] group counts.
-// publish_dst/src (optional): the final arriver copies *src to *dst before the
-// release, so every CTA sees a value that no CTA can change until the next
-// phase (used to publish the spike-log end of the finished step);
-// zero_u64 / zero_i32 (optional): reset by the final arriver.
+// `bar` holds kBarWords words (only bar[0] is used by grid_sync; the rest
+// keeps the word on its own 128-byte line).
 constexpr unsigned kBarWords = 64;
 
 // Grid barrier: one arrival atomic per CTA on a single word whose top bit

@@ -352,7 +352,9 @@ __global__ void k_fill_int(int* v, long long n, int x) {
     v[k] = x;
 }
 
-int ensure_scratch(eq_queues* h, long long n) {
+// Scratch for one enqueue batch; the iota initialisation is stream-ordered on
+// the caller's stream s, which the sort that reads it uses next.
+int ensure_scratch(eq_queues* h, long long n, cudaStream_t s) {
   if (n <= h->scratch_n) return EQ_OK;
   for (void* p : {(void*)h->sq, (void*)h->sidx, (void*)h->iota, (void*)h->tmp}) {
     if (p) {
@@ -364,7 +366,7 @@ int ensure_scratch(eq_queues* h, long long n) {
   QCUDA(h, qalloc(h, (void**)&h->sq, cap * sizeof(int)));
   QCUDA(h, qalloc(h, (void**)&h->sidx, cap * sizeof(int)));
   QCUDA(h, qalloc(h, (void**)&h->iota, cap * sizeof(int)));
-  k_iota32<<<256, 256>>>(h->iota, cap);
+  k_iota32<<<256, 256, 0, s>>>(h->iota, cap);
   size_t tb = 0;
   int end_bit = 1;
   while ((1LL << end_bit) < h->Q) ++end_bit;
@@ -380,7 +382,7 @@ template <typename T>
 int enqueue_impl(eq_queues* h, const int32_t* queue, const int32_t* due, const void* w, const void* dw,
                  const void* tt, int64_t n, uint8_t* accepted, cudaStream_t s) {
   if (n <= 0) return EQ_OK;
-  int rc = ensure_scratch(h, n);
+  int rc = ensure_scratch(h, n, s);
   if (rc) return rc;
   int end_bit = 1;
   while ((1LL << end_bit) < h->Q) ++end_bit;

@@ -24,24 +24,10 @@
 namespace eq {
 
 // Forward delivery into the L2-resident fixed-point accumulator (2 x B x N x 8 B,
-// 38 MB at C3 x 24).  EQ_ACC_HINT=1 marks it evict-last (A/B knob).
-#ifndef EQ_ACC_HINT
-#define EQ_ACC_HINT 0
-#endif
-#ifndef EQ_BIN_AGG
-#define EQ_BIN_AGG 0
-#endif
-#ifndef EQ_BK_ST
-#define EQ_BK_ST 0
-#endif
+// 38 MB at C3 x 24).  An evict-last policy on these reds measured no gain
+// (profiles/r1g_ab_fwd_policies.txt): the accumulator stays in L2 anyway.
 __device__ __forceinline__ void red_acc(long long* p, long long v) {
-#if EQ_ACC_HINT
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
-#else
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-#endif
 }
 
 template <typename T>
@@ -359,37 +345,17 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
           }
           bn = ds % A.NB;
         }
-#if EQ_BIN_AGG
-        // warp-aggregated bucket slot allocation (A/B knob): one shared atomic per
-        // distinct bin in the warp (slot order is free: the sums are fixed point)
-        const unsigned act = __activemask();
-        const unsigned peers = __match_any_sync(act, bn);
-        const int lane = threadIdx.x & 31;
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&s_bin[bn], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        const int pos = base + __popc(peers & ((1u << lane) - 1u));
-#else
+        // one shared atomic per event (a warp-aggregated variant with
+        // __match_any_sync measured slower: fwd 32.2 -> 37.7 ms, profiles/r1h_ab_bin_agg.txt)
         const int pos = atomicAdd(&s_bin[bn], 1);
-#endif
         if (pos < A.cap_b) {
           longlong2* o = reinterpret_cast<longlong2*>(bk_cta + ((size_t)bn * A.cap_b + pos) * bk_words<T>());
-#if EQ_BK_ST
-          if (P::kSlotWords == 1) {                         // A/B: default store policy
-            *o = make_longlong2(tgt, pack2(q1, q2));
-          } else {
-            o[0] = make_longlong2(tgt, q1);
-            o[1] = make_longlong2(q2, 0);
-          }
-#else
           if (P::kSlotWords == 1) {                         // read once, ~H/2 steps later: streaming
             __stcs(o, make_longlong2(tgt, pack2(q1, q2)));
           } else {
             __stcs(o, make_longlong2(tgt, q1));
             __stcs(o + 1, make_longlong2(q2, 0));
           }
-#endif
         } else {                                            // bucket full: DRAM ring row
           const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + jj[e];
           if (P::kSlotWords == 1) {
@@ -729,6 +695,14 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
   }
 }
 
+// After the barrier of phase m: could the next step overflow the spike log?
+// (one step logs at most `total` spikes).  Read from the value the barrier
+// published, so every CTA decides the same.
+template <typename T>
+__device__ __forceinline__ bool pause_due(const FwdArgs<T>& A, int m) {
+  return ld_published(A.step_start + m + 1) + A.total > A.log_cap;
+}
+
 template <typename T, int NT, int U, int NF = NT / 2>
 __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   typedef Prec<T> P;
@@ -776,8 +750,12 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   // land at steps >= m+1, never in acc[m&1], and acc[(m+1)&1] is popped only
   // after the barrier.  A last pass m = m1 fans out the final step so the
   // queue contents after the run are complete.
-  for (int m = A.m0; m <= A.m1; ++m) {
-    tl_mark(A.tl, m < A.m1 ? m : A.m1 - 1, A.G, cta, m < A.m1 ? 0 : 7);
+  // m1 may be lowered at a barrier (pause_due): the launch then ends at a step
+  // boundary with the spike log one step short of full, the host grows it and
+  // relaunches from there (eq_run resumes bitwise, tests/test_gpu_parity.py)
+  int m1 = A.m1;
+  for (int m = A.m0; m <= m1; ++m) {
+    tl_mark(A.tl, m < m1 ? m : m1 - 1, A.G, cta, m < m1 ? 0 : 7);
     if (tid < Ro::NF) {
       // ======================== event side
       const int gtid = tid;
@@ -822,7 +800,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         group_sync(Ro::kBarF, Ro::NF);
         if (gtid == 0) s_bin[bin] = 0;
       }
-      if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 5);
+      if (m < m1) tl_mark(A.tl, m, A.G, cta, 5);
       // ---------------- (a2) fan-out of step m-1 (and imported spikes): fwd_fanout
       if (A.kind == EQ_KIND_RING && m > A.m0) {
         const int me = m - 1;                          // emitting step
@@ -830,22 +808,24 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
         fwd_fanout<T, NT, NF, false>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G, s_spk, s_r0,
                                      s_pre, s_bin);
       }
-      if (m < A.m1) tl_mark(A.tl, m, A.G, cta, 1);
-    } else if (m < A.m1) {
+      if (m < m1) tl_mark(A.tl, m, A.G, cta, 1);
+    } else if (m < m1) {
       // ======================== neuron side
       const int gtid = tid - Ro::NF;
       neuron_side<T, NT, U, NF>(A, m, cta, gtid, begin, end, b_first, A.kind == EQ_KIND_RING, s_own, s_n, s_off,
                                 s_ctr, spill, s_st);
     }
     __syncthreads();
-    if (m == A.m1) break;
+    if (m == m1) break;
     tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err, A.step_start + m + 1, A.log_count, nullptr,
                    A.kind == EQ_KIND_RING ? A.ring_dirty + m % A.R : nullptr))
       break;
     tl_mark(A.tl, m, A.G, cta, 3);
     if (ld_volatile(A.err) != 0) break;
+    if (m + 1 < m1 && pause_due(A, m)) m1 = m + 1;   // same published value on every CTA
   }
+  if (cta == 0 && tid == 0) A.err[4] = m1;            // the step this launch reached
   __syncthreads();
   if (s_st)
     for (long long k = tid; k < end - begin; k += NT) {
@@ -887,7 +867,7 @@ struct BwdArgs {
   const long long* chunk_off;
   const int* chunk_cnt;
   const long long* step_start;  // [m] first log record of step m
-  const long long* ev_base;     // bounded kinds: flat event id of each log record's first edge
+  int maxdeg;                   // bounded kinds: event id = log position * maxdeg + row offset
   const unsigned* drop_bits;    // bounded kinds: dropped events (contribute nothing); null for ring
   int no_events;                // donothing: every event was dropped
   // partitioned network: dL/dt_spk contributions of the other partitions'
@@ -905,66 +885,34 @@ struct BwdArgs {
   unsigned* bar;
 };
 
-// Random 8/16-byte reverse-slot gather: ask L2 for a 64-byte fill instead of
-// the default 128 (fewer DRAM bytes per useful byte; the DRAM is ~56% busy in
-// the reverse pass at 24 trials, profiles/r1d_c3x24.md).
-// L2 cache policies of the reverse pass (bit 0: gathers evict-first, bit 1:
-// gradient reds evict-last with fraction EQ_HINT_FRAC).  A/B on one box, C3 x 24
-// trials: none 49.1 ms, gathers only 45.95, both (fraction 0.5) 45.75, both
-// (1.0) 45.53 (profiles/r1g_ab_hint.txt).
-#ifndef EQ_HINT
-#define EQ_HINT 3
-#endif
-#ifndef EQ_GATHER_NA
-#define EQ_GATHER_NA 0   // A/B: gathers bypass L1 allocation
-#endif
-#ifndef EQ_HINT_FRAC
-#define EQ_HINT_FRAC 1.0
-#endif
-#define EQ_STR2(x) #x
-#define EQ_STR(x) EQ_STR2(x)
+// Random 8/16-byte reverse-slot gather: a 64-byte L2 fill instead of the
+// default 128 (fewer DRAM bytes per useful byte), marked evict-first: the
+// gathered line is rarely hit again before eviction (1.2 GB live ring), so it
+// must not displace the per-edge gradient accumulators.  Per-edge gradient
+// reductions (dL/dw, dL/dd: 2 x 8 B x E, 160 MB at C3) are evict-last.
+// A/B on one box, C3 x 24 trials: no policy 49.1 ms, gathers evict-first
+// 45.95, both 45.53 (profiles/r1g_ab_hint.txt).
 __device__ __forceinline__ float2 ld_gather(const float2* p) {
   float2 v;
-#if EQ_HINT & 1
-  // the gathered line is rarely hit again before eviction (1.2 GB live ring): evict first
   unsigned long long pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-#if EQ_GATHER_NA
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.L2::64B.v2.f32 {%0, %1}, [%2], %3;"
-               : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
-#else
   asm volatile("ld.global.L2::cache_hint.L2::64B.v2.f32 {%0, %1}, [%2], %3;"
                : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
-#endif
-#else
-  asm volatile("ld.global.L2::64B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-#endif
   return v;
 }
 __device__ __forceinline__ double2 ld_gather(const double2* p) {
   double2 v;
-#if EQ_HINT & 1
   unsigned long long pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("ld.global.L2::cache_hint.L2::64B.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-#else
-  asm volatile("ld.global.L2::64B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-#endif
   return v;
 }
-// Per-edge gradient reductions of the reverse pass (dL/dw, dL/dd: 2 x 8 B x E,
-// 160 MB at C3): with EQ_HINT & 2 they are kept in L2 evict-last (a fraction
-// EQ_HINT_FRAC of the accesses), so the ring gathers evict them last.
 __device__ __forceinline__ void red_grad(double* p, double v) {
-#if EQ_HINT & 2
   unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, " EQ_STR(EQ_HINT_FRAC) ";" : "=l"(pol));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
                : "memory");
-#else
-  red_add_f64(p, v);
-#endif
 }
 
 template <typename T>
@@ -1044,7 +992,7 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
           T g_tp = (T)0;
           bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
           if (live && A.drop_bits) {                       // dropped by a bounded queue
-            const long long id = A.ev_base[k0 + kk[e]] + (f - s_pre[kk[e]]);
+            const long long id = (k0 + kk[e]) * (long long)A.maxdeg + (f - s_pre[kk[e]]);
             live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
           }
           if (live) {

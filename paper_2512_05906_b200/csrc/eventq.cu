@@ -26,6 +26,7 @@ using namespace eq;
 namespace {
 
 constexpr int kNT = 512;   // threads per CTA of the persistent kernels
+constexpr int kErrWords = 8;  // device error word: [0] code, [1] step, [2] trial, [3] neuron, [4] step reached
 constexpr int kU = 4;      // neurons per thread in flight per round
 constexpr int kSplitF = 288;  // forward event-side threads per CTA (measured: 224..384, profiles/)
 #ifndef EQ_SPLIT_B32
@@ -78,7 +79,6 @@ struct eq_handle {
   unsigned short* dcode = nullptr;   // per-edge delivery codes
   void* edges = nullptr;             // packed EdgeRec<T>[E] (snapshot of col/w/d at eq_set_network)
   bool net_set = false, drive_set = false;
-  bool l2_set = false;
   size_t tsize = 4;
   // forward state
   void* I = nullptr;
@@ -86,11 +86,13 @@ struct eq_handle {
   int32_t* refr = nullptr;
   long long* ring = nullptr;
   size_t ring_words = 0;
+  bool ring_clean = false;   // false: the next reset clears the whole ring (fresh buffer, or a JVP run used it)
   // calendar (ring kind)
   long long* acc = nullptr;
   long long* bk = nullptr;
   int* bk_cnt = nullptr;
   long long cap_b = 0;
+  long long cap_b_alloc = 0;   // cap_b the bucket storage was sized for
   int NB = 0;
   int* ring_dirty = nullptr;
   void* scratch = nullptr;
@@ -98,6 +100,8 @@ struct eq_handle {
   long long* log_r0 = nullptr;
   int* log_len = nullptr;
   long long log_cap = 0;
+  long long log_used = 0;      // host copy of *log_count after the last forward launch
+  int log_grows = 0;           // spike-log reallocations (eq_run resumed after each)
   unsigned long long* log_count = nullptr;
   long long* chunk_off = nullptr;
   int* chunk_cnt = nullptr;
@@ -121,8 +125,7 @@ struct eq_handle {
   int* acnt = nullptr;         // [2][B][N] arrivals per target
   void* q = nullptr;
   int4* meta = nullptr;
-  long long* ev_base = nullptr;
-  unsigned long long* ev_count = nullptr;
+  int maxdeg = 1;               // largest CSR row (bounded kinds: event id = log position * maxdeg + row offset)
   unsigned* drop_bits = nullptr;
   long long drop_cap = 0;
   unsigned long long* tl_f = nullptr;   // debug timelines (EQ_TIMELINE=1)
@@ -244,8 +247,8 @@ NetView<T> netview(const eq_handle* h) {
 // ------------------------------------------------------------ small kernels
 
 // Network validation + statistics, one thread per source row.
-// stats[0] = max ceil(d/dt); stats[1] = first bad edge (flat index) for
-// ConfigurationError, stats[2] = code of that error; insum = fixed-point
+// stats[0] = max ceil(d/dt); stats[1] = first bad edge (flat index) << 2 | code
+// of that ConfigurationError; stats[4] = longest row; insum = fixed-point
 // sum of |w| per target (2^-40 units; deterministic integer adds).
 template <typename T>
 __global__ void k_net_stats(int n_rows, int N, int src_off, const int64_t* rowptr, const int32_t* col, const T* w,
@@ -278,6 +281,7 @@ __global__ void k_net_stats(int n_rows, int N, int src_off, const int64_t* rowpt
               (unsigned long long)__double2ll_rn(fabs((double)w[x]) * 1099511627776.0));
   }
   atomicMax(stats, (long long)hmax);
+  atomicMax(stats + 4, (long long)(r1 - r0));
 }
 
 template <typename T>
@@ -342,9 +346,6 @@ __global__ void k_decode_spikes(const SpikeRec<T>* log, const long long* chunk_o
   }
 }
 
-// Calendar ring contents pending after a run at step `now`: acc[now&1] holds
-// due `now`, acc[(now+1)&1] due now+1, bucket (now+h)%NB due now+h (h >= 2),
-// plus flagged DRAM ring rows (bucket overflow).  out int64 [B*N][H][2].
 // Calendar ring contents pending after a run at step `now`: acc[now&1] holds
 // due `now`, acc[(now+1)&1] due now+1, the CTAs' buckets (now+h)%NB due now+h
 // (h >= 2), plus flagged DRAM ring rows (bucket overflow).  out int64 [B*N][H][2].
@@ -418,6 +419,19 @@ __global__ void k_pending(const long long* ring, int B, int R, int N, int H, int
     out[2 * k] = qs;
     out[2 * k + 1] = qm;
   }
+}
+
+// Reset of the ring kind's DRAM overflow rows: only rows a bucket overflow
+// flagged hold anything (every popped row is cleared by its pop), so only those
+// are zeroed — not the whole B x R x N ring (1.27 GB at C3 x 24).
+// grid: x over the row's words, y = b * R + r.
+__global__ void k_clear_dirty_rows(long long* ring, int* ring_dirty, int R, long long row_words) {
+  const int r = blockIdx.y % R;
+  if (ring_dirty[r] == 0) return;
+  long long* row = ring + (size_t)blockIdx.y * row_words;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < row_words;
+       k += (long long)gridDim.x * blockDim.x)
+    row[k] = 0;
 }
 
 __global__ void k_meta_init(int4* meta, long long n) {
@@ -531,10 +545,19 @@ size_t bwd_smem(long long per) {
   return (size_t)((per + 31) / 32) * sizeof(unsigned) + (size_t)((per + 1) / 2) * sizeof(unsigned);
 }
 
-int check_err(eq_handle* h, cudaStream_t s) {
-  int e[4];
+// Wait for the stream and map the device error word to a status + message.
+// `reached` (forward launches): the step the launch ended at (err[4]); the
+// spike-log fill is cached in h->log_used on the same synchronisation.
+int check_err(eq_handle* h, cudaStream_t s, int* reached = nullptr) {
+  int e[kErrWords];
+  unsigned long long used = 0;
   EQ_CUDA(h, cudaMemcpyAsync(e, h->err_dev, sizeof e, cudaMemcpyDeviceToHost, s));
+  if (reached) EQ_CUDA(h, cudaMemcpyAsync(&used, h->log_count, sizeof used, cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));
+  if (reached) {
+    *reached = e[4];
+    h->log_used = (long long)used;
+  }
   if (e[0] == 0) return EQ_OK;
   char buf[256];
   switch (e[0]) {
@@ -566,8 +589,55 @@ std::array<long long, 4>* find_block(eq_handle* h, int start) {
   return nullptr;
 }
 
+// Grow the spike log (and the per-record arrays, and the bounded kinds' drop
+// bits, which are indexed by log position) to hold at least `need` records;
+// the first log_used records are kept.
+int grow_log(eq_handle* h, long long need, cudaStream_t s) {
+  const long long ncap = std::max<long long>(need, 2 * h->log_cap);
+  const size_t rec = h->cfg.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
+  const long long used = h->log_used;
+  void *lg = nullptr, *r0 = nullptr, *len = nullptr, *lt = nullptr, *ltr = nullptr;
+  EQ_CUDA(h, alloc(h, &lg, (size_t)ncap * rec));
+  EQ_CUDA(h, alloc(h, &r0, (size_t)ncap * sizeof(long long)));
+  EQ_CUDA(h, alloc(h, &len, (size_t)ncap * sizeof(int)));
+  EQ_CUDA(h, alloc(h, &lt, (size_t)ncap * h->tsize));
+  EQ_CUDA(h, alloc(h, &ltr, (size_t)ncap * h->tsize));
+  if (used > 0) {
+    EQ_CUDA(h, cudaMemcpyAsync(lg, h->log, (size_t)used * rec, cudaMemcpyDeviceToDevice, s));
+    EQ_CUDA(h, cudaMemcpyAsync(r0, h->log_r0, (size_t)used * sizeof(long long), cudaMemcpyDeviceToDevice, s));
+    EQ_CUDA(h, cudaMemcpyAsync(len, h->log_len, (size_t)used * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  }
+  if (h->bounded) {
+    const long long ndrop = (ncap * h->maxdeg + 31) / 32 * 32;
+    void* db = nullptr;
+    EQ_CUDA(h, alloc(h, &db, (size_t)ndrop / 8));
+    EQ_CUDA(h, cudaMemsetAsync(db, 0, (size_t)ndrop / 8, s));
+    EQ_CUDA(h, cudaMemcpyAsync(db, h->drop_bits, (size_t)h->drop_cap / 8, cudaMemcpyDeviceToDevice, s));
+    EQ_CUDA(h, cudaStreamSynchronize(s));
+    release(h, h->drop_bits);
+    h->drop_bits = (unsigned*)db;
+    h->drop_cap = ndrop;
+  }
+  EQ_CUDA(h, cudaStreamSynchronize(s));
+  release(h, h->log);
+  release(h, h->log_r0);
+  release(h, h->log_len);
+  release(h, h->lt_log);
+  release(h, h->lt_rem);
+  h->log = lg;
+  h->log_r0 = (long long*)r0;
+  h->log_len = (int*)len;
+  h->lt_log = lt;
+  h->lt_rem = ltr;
+  h->log_cap = ncap;
+  h->log_grows += 1;
+  return EQ_OK;
+}
+
+// One persistent launch over steps [steps_done, steps_done + n_steps); it may
+// end early at a step boundary when the spike log could overflow (*reached).
 template <typename T>
-int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
+int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s, int* reached) {
   FwdArgs<T> A;
   A.N = h->cfg.n_neurons;
   A.B = h->cfg.n_trials;
@@ -630,8 +700,7 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
     Bk.acnt = h->acnt;
     Bk.q = (QEv<T>*)h->q;
     Bk.meta = h->meta;
-    Bk.ev_base = h->ev_base;
-    Bk.ev_count = h->ev_count;
+    Bk.maxdeg = h->maxdeg;
     Bk.drop_bits = h->drop_bits;
     Bk.drop_cap = h->drop_cap;
     Bk.insert_first = h->steps_done;
@@ -640,26 +709,6 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
                                            bargs, 0, s));
   } else {
     void* args[] = {&A};
-    if (h->cfg.kind == EQ_KIND_RING && !h->l2_set && getenv("EQ_L2_PERSIST")) {
-      // keep the two accumulator rows L2-resident (every event's red.add lands there)
-      int maxp = 0;
-      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
-      size_t bytes = (size_t)2 * h->total * P_words<T>() * sizeof(long long);
-      size_t win = std::min<size_t>(bytes, (size_t)maxp);
-      if (win > 0) {
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, win);
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.base_ptr = h->acc;
-        v.accessPolicyWindow.num_bytes = win;
-        v.accessPolicyWindow.hitRatio = 1.0f;
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
-        h->l2_set = true;
-      }
-    }
-    // warp split (event side / neuron side) measured at C3 x 16 trials:
-    // 384/128 balances the forward's sides (timeline, profiles/)
     if (A.imp_n > 0) {   // other partitions' spikes of the last window, due >= m0+1
       FwdArgs<T> Ai = A;
       Ai.tl = nullptr;
@@ -683,21 +732,45 @@ int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
     EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, dyn, s));
   }
   h->launches += 1;
-  int rc = check_err(h, s);
-  if (rc == EQ_OK || rc == EQ_ERR_GRAZING) h->steps_done += n_steps;
-  return rc;
+  return check_err(h, s, reached);
+}
+
+// eq_run's launches: as many persistent launches as the spike log needs (one
+// unless it fills up; then it grows and the run resumes at the step reached).
+template <typename T>
+int launch_forward(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s) {
+  int done = 0;
+  while (true) {
+    if (n_steps > 0 && h->log_used + h->total > h->log_cap) {
+      int rc = grow_log(h, h->log_used + 2 * h->total, s);
+      if (rc) return rc;
+    }
+    if (done > 0) EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
+    void* vt = v_trace ? (char*)v_trace + (size_t)done * h->total * h->tsize : nullptr;
+    int reached = h->steps_done + (n_steps - done);
+    int rc = launch_forward_once<T>(h, n_steps - done, vt, s, &reached);
+    if (rc != EQ_OK) {
+      if (rc == EQ_ERR_GRAZING) h->steps_done += n_steps - done;
+      return rc;
+    }
+    if (n_steps == 0) return EQ_OK;
+    if (reached <= h->steps_done || reached > h->steps_done + (n_steps - done))
+      return fail(h, EQ_ERR_CUDA, "forward launch reported step " + std::to_string(reached));
+    done += reached - h->steps_done;
+    h->steps_done = reached;
+    if (done == n_steps) return EQ_OK;
+  }
 }
 
 template <typename T>
 int backward_begin(eq_handle* h, const void* v_bar, const void* i_bar, double* gw, double* gd, double* gamp,
                    cudaStream_t s) {
-  typedef typename Prec<T>::T2 T2;
-  const int N = h->cfg.n_neurons, B = h->cfg.n_trials;
   const long long total = h->total;
   EQ_CUDA(h, cudaMemcpyAsync(h->lamV, v_bar, total * sizeof(T), cudaMemcpyDeviceToDevice, s));
   if (i_bar) EQ_CUDA(h, cudaMemcpyAsync(h->lamI, i_bar, total * sizeof(T), cudaMemcpyDeviceToDevice, s));
   else EQ_CUDA(h, cudaMemsetAsync(h->lamI, 0, total * sizeof(T), s));
-  EQ_CUDA(h, cudaMemsetAsync(h->lam, 0, (size_t)B * h->R * N * sizeof(T2), s));
+  // no clear of the reverse ring: R-fanout reads only rows of steps < m_run,
+  // each written by R-neuron of its step earlier in the reverse sweep
   EQ_CUDA(h, cudaMemsetAsync(gw, 0, h->E * sizeof(double), s));
   EQ_CUDA(h, cudaMemsetAsync(gd, 0, h->E * sizeof(double), s));
   if (gamp) EQ_CUDA(h, cudaMemsetAsync(h->gamp_bt, 0, total * sizeof(double), s));
@@ -741,7 +814,7 @@ int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
   A.chunk_off = h->chunk_off;
   A.chunk_cnt = h->chunk_cnt;
   A.step_start = h->step_start;
-  A.ev_base = h->bounded ? h->ev_base : nullptr;
+  A.maxdeg = h->maxdeg;
   A.drop_bits = h->bounded ? h->drop_bits : nullptr;
   A.no_events = h->cfg.kind == EQ_KIND_DONOTHING;
   A.lt_rem = h->partitioned ? (const T*)h->lt_rem : nullptr;
@@ -877,10 +950,8 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   EQ_CUDA(h, ensure(h, (void**)&h->acnt, (size_t)2 * B * N * sizeof(int)));
   EQ_CUDA(h, ensure(h, &h->q, qbytes));
   EQ_CUDA(h, ensure(h, (void**)&h->meta, (size_t)B * N * sizeof(int4)));
-  EQ_CUDA(h, ensure(h, (void**)&h->ev_base, (size_t)h->log_cap * sizeof(long long)));
-  EQ_CUDA(h, ensure(h, (void**)&h->ev_count, sizeof(unsigned long long)));
-  // one bit per event of the run: spike-log capacity x mean out-degree x 2
-  h->drop_cap = ((long long)h->log_cap * std::max<long long>(1, 2 * E / N) + 31) / 32 * 32;
+  // one drop bit per possible event of a logged spike: grows with the log
+  h->drop_cap = ((long long)h->log_cap * h->maxdeg + 31) / 32 * 32;
   EQ_CUDA(h, ensure(h, (void**)&h->drop_bits, (size_t)h->drop_cap / 8));
   return EQ_OK;
 }
@@ -937,8 +1008,6 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   }
   h->n_sm = prop.multiProcessorCount;
   h->n_src = c.n_neurons;
-  if (const char* g = getenv("EQ_L2_FETCH"))   // experiment knob: L2 fetch granularity hint (bytes)
-    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(g));
   *out = h;
   int rc = setup_geometry(h);
   if (rc) return rc;
@@ -950,7 +1019,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   EQ_CUDA(h, alloc(h, &h->lamI, h->total * T));
   EQ_CUDA(h, alloc(h, (void**)&h->gamp_bt, h->total * sizeof(double)));
   EQ_CUDA(h, alloc(h, (void**)&h->counters, (size_t)c.n_trials * 3 * sizeof(long long)));
-  EQ_CUDA(h, alloc(h, (void**)&h->err_dev, 4 * sizeof(int)));
+  EQ_CUDA(h, alloc(h, (void**)&h->err_dev, kErrWords * sizeof(int)));
   EQ_CUDA(h, alloc(h, (void**)&h->bar, kBarWords * sizeof(unsigned)));
   EQ_CUDA(h, alloc(h, (void**)&h->log_count, sizeof(unsigned long long)));
   const size_t rec = c.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
@@ -999,8 +1068,8 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   EQ_CUDA(h, alloc(h, &insum, (size_t)N * sizeof(long long)));
   EQ_CUDA(h, alloc(h, &inocc, (size_t)N * sizeof(long long)));
   EQ_CUDA(h, alloc(h, &indeg, (size_t)(N + 1) * sizeof(int)));   // +1: exclusive scan reads n+1
-  EQ_CUDA(h, alloc(h, &stats, 4 * sizeof(long long)));
-  long long init[4] = {1, -1LL, 0, 0};
+  EQ_CUDA(h, alloc(h, &stats, 5 * sizeof(long long)));
+  long long init[5] = {1, -1LL, 0, 0, 1};
   init[1] = (long long)~0ULL;
   EQ_CUDA(h, cudaMemsetAsync(insum, 0, (size_t)N * sizeof(long long), s));
   EQ_CUDA(h, cudaMemsetAsync(inocc, 0, (size_t)N * sizeof(long long), s));
@@ -1018,7 +1087,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   k_max_ll<<<256, 256, 0, s>>>((const long long*)insum, N, (long long*)stats + 2);
   k_max_ll<<<256, 256, 0, s>>>((const long long*)inocc, N, (long long*)stats + 3);
   h->launches += 3;
-  long long st[4];
+  long long st[5];
   EQ_CUDA(h, cudaMemcpyAsync(st, stats, sizeof st, cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));
   release(h, insum);
@@ -1059,6 +1128,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
     return fail(h, EQ_ERR_CONFIGURATION, buf);
   }
   h->horizon = (int)st[0] + 1;           // network.py:188-198
+  h->maxdeg = (int)std::max<long long>(1, st[4]);
   h->R = h->horizon + 1;                 // + one slot for in-phase pop/scatter overlap
   // fixed-point fraction bits: largest F with 4*max_in*2^F <= 2^(bits-2)
   double max_in = std::ldexp((double)st[2], -40);
@@ -1093,7 +1163,11 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   // queue storage
   size_t words = c.kind == EQ_KIND_RING ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
   h->ring_words = words;
-  EQ_CUDA(h, ensure(h, (void**)&h->ring, words * sizeof(long long)));
+  {
+    long long* before = h->ring;
+    EQ_CUDA(h, ensure(h, (void**)&h->ring, words * sizeof(long long)));
+    if (h->ring != before) h->ring_clean = false;
+  }
   if (c.kind == EQ_KIND_RING) {
     const int wd = c.precision == 32 ? 1 : 2;
     h->NB = h->R;
@@ -1106,6 +1180,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
     long long avg_deg = std::max<long long>(1, n_edges / N);
     h->cap_b = std::max<long long>(256, (h->total * avg_deg / 64 + h->G - 1) / h->G);
     if (h->cap_b > (1LL << 30)) h->cap_b = 1LL << 30;
+    h->cap_b_alloc = h->cap_b;
     EQ_CUDA(h, ensure(h, (void**)&h->acc, (size_t)2 * h->total * wd * sizeof(long long)));
     EQ_CUDA(h, ensure(h, (void**)&h->bk, (size_t)h->G * h->NB * h->cap_b * (wd == 1 ? 2 : 4) * sizeof(long long)));
     EQ_CUDA(h, ensure(h, (void**)&h->bk_cnt, (size_t)h->G * h->NB * sizeof(int)));
@@ -1135,12 +1210,24 @@ int eq_reset(eq_handle* h, void* stream) {
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t T = h->tsize;
-  EQ_CUDA(h, cudaMemsetAsync(h->ring, 0, h->ring_words * sizeof(long long), s));
   if (h->cfg.kind == EQ_KIND_RING) {
     const int wd = h->cfg.precision == 32 ? 1 : 2;
+    if (!h->ring_clean) {
+      EQ_CUDA(h, cudaMemsetAsync(h->ring, 0, h->ring_words * sizeof(long long), s));
+      h->ring_clean = true;
+    } else {
+      const long long row_words = (long long)h->cfg.n_neurons * wd;
+      k_clear_dirty_rows<<<dim3((unsigned)std::min<long long>((row_words + 255) / 256, 64),
+                              (unsigned)(h->cfg.n_trials * h->R)), 256, 0, s>>>(h->ring, h->ring_dirty, h->R,
+                                                                                row_words);
+      h->launches += 1;
+    }
     EQ_CUDA(h, cudaMemsetAsync(h->acc, 0, (size_t)2 * h->total * wd * sizeof(long long), s));
     EQ_CUDA(h, cudaMemsetAsync(h->bk_cnt, 0, (size_t)h->G * h->NB * sizeof(int), s));
     EQ_CUDA(h, cudaMemsetAsync(h->ring_dirty, 0, (size_t)h->R * sizeof(int), s));
+  } else if (!h->ring_clean) {
+    EQ_CUDA(h, cudaMemsetAsync(h->ring, 0, h->ring_words * sizeof(long long), s));
+    h->ring_clean = true;
   }
   EQ_CUDA(h, cudaMemsetAsync(h->I, 0, h->total * T, s));
   if (h->cfg.precision == 32)
@@ -1150,19 +1237,19 @@ int eq_reset(eq_handle* h, void* stream) {
   h->launches += 1;
   EQ_CUDA(h, cudaMemsetAsync(h->refr, 0, h->total * sizeof(int32_t), s));
   EQ_CUDA(h, cudaMemsetAsync(h->counters, 0, (size_t)h->cfg.n_trials * 3 * sizeof(long long), s));
-  EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, 4 * sizeof(int), s));
+  EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, kErrWords * sizeof(int), s));
   EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
   EQ_CUDA(h, cudaMemsetAsync(h->log_count, 0, sizeof(unsigned long long), s));
   EQ_CUDA(h, cudaMemsetAsync(h->step_start, 0, sizeof(long long), s));
   if (h->bounded) {
     const int B = h->cfg.n_trials, N = h->cfg.n_neurons;
     EQ_CUDA(h, cudaMemsetAsync(h->acnt, 0, (size_t)2 * B * N * sizeof(int), s));
-    EQ_CUDA(h, cudaMemsetAsync(h->ev_count, 0, sizeof(unsigned long long), s));
     EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
     k_meta_init<<<592, 256, 0, s>>>(h->meta, (long long)B * N);
     h->launches += 1;
   }
   h->steps_done = 0;
+  h->log_used = 0;
   h->imp_n = 0;
   h->imp_blocks.clear();
   h->bwd_cursor = -1;
@@ -1334,6 +1421,7 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
                                  (size_t)N * 8, cudaMemcpyDeviceToDevice, s));
   rc = check_err(h, s);
   h->steps_done = 0;   // the spike log / queues of eq_run are not populated by this path
+  h->ring_clean = false;   // its pending events sit in unflagged ring rows
   return rc;
 }
 
@@ -1485,7 +1573,7 @@ int eq_import_spikes(eq_handle* h, const void* recs, int64_t n, void* stream) {
   EQ_CUDA(h, cudaMemcpyAsync(e, h->err_dev, sizeof e, cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));
   if (e[0]) {
-    EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, 4 * sizeof(int), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->err_dev, 0, kErrWords * sizeof(int), s));
     char buf[200];
     snprintf(buf, sizeof buf, "imported spike (source %d, trial %d, step %d) is not a remote spike of an "
                               "earlier step", e[3], e[2], e[1]);
@@ -1608,6 +1696,22 @@ int eq_geometry(const eq_handle* h, int32_t* ctas, int32_t* threads) {
   return EQ_OK;
 }
 int64_t eq_launch_count(const eq_handle* h) { return h ? h->launches : -1; }
+
+int64_t eq_log_capacity(const eq_handle* h, int32_t* n_grows) {
+  if (!h) return -1;
+  if (n_grows) *n_grows = h->log_grows;
+  return h->log_cap;
+}
+
+int eq_debug_set_bucket_capacity(eq_handle* h, int64_t cap) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (h->cfg.kind != EQ_KIND_RING || !h->net_set)
+    return fail(h, EQ_ERR_CONFIGURATION, "bucket capacity: ring kind after eq_set_network only");
+  if (cap < 1 || cap > h->cap_b_alloc)
+    return fail(h, EQ_ERR_CONFIGURATION, "bucket capacity outside [1, " + std::to_string(h->cap_b_alloc) + "]");
+  h->cap_b = cap;
+  return EQ_OK;
+}
 
 /* Debug: per-step, per-CTA phase timestamps (ns) of the last forward (which=0)
  * or reverse (which=1) run, [t_steps][ctas][4]; needs EQ_TIMELINE=1 at create. */

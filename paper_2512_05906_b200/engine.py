@@ -60,6 +60,9 @@ class Engine:
         _native.check(self.h, code)
         self._net = None
         self._drive = None
+        # bumped by every call that changes the recorded forward run (spike log,
+        # queues): a reverse pass saved against an older run id is stale
+        self.run_id = 0
         # partitioned network (paper_2512_05906_b200.partition): this engine owns
         # neurons [offset, offset + n) of an n_global-neuron network
         self.n_global, self.offset = (n, 0) if partition is None else (int(partition[0]), int(partition[1]))
@@ -99,6 +102,7 @@ class Engine:
         if w.numel() != E or d.numel() != E:
             raise ConfigurationError("weight/delay must have one entry per edge")
         self._net = (rp, cl, w, d)
+        self.run_id += 1                     # eq_set_network resets the run
         _native.check(self.h, self.L.eq_set_network(self.h, _ptr(rp), _ptr(cl), _ptr(w), _ptr(d), E,
                                                       self.stream))
         self.n_edges = E
@@ -128,6 +132,7 @@ class Engine:
         v = torch.empty(self.B, self.n, dtype=self.dtype, device=self.device)
         i = torch.empty_like(v)
         tr = torch.empty(self.T, self.B, self.n, dtype=self.dtype, device=self.device) if record_v else None
+        self.run_id += 1
         _native.check(self.h, self.L.eq_forward(self.h, _ptr(v), _ptr(i), _ptr(tr), self.stream))
         out = {"v": v, "i": i}
         if record_v:
@@ -146,6 +151,7 @@ class Engine:
             raise ConfigurationError("kinds and indices must be 1-d of equal length")
         v = torch.empty(self.B, self.n, dtype=torch.float64, device=self.device)
         vt = torch.empty(len(k), self.B, self.n, dtype=torch.float64, device=self.device)
+        self.run_id += 1
         _native.check(self.h, self.L.eq_forward_jvp(self.h, len(k), k.ctypes.data_as(ctypes.c_void_p),
                                                      ix.ctypes.data_as(ctypes.c_void_p), _ptr(v), _ptr(vt),
                                                      self.stream))
@@ -159,9 +165,11 @@ class Engine:
         return {"v": v, "i": i}
 
     def reset(self) -> None:
+        self.run_id += 1
         _native.check(self.h, self.L.eq_reset(self.h, self.stream))
 
     def run(self, n_steps: int, v_trace: Optional[torch.Tensor] = None) -> None:
+        self.run_id += 1
         _native.check(self.h, self.L.eq_run(self.h, n_steps, _ptr(v_trace), self.stream))
 
     def backward(self, v_bar: torch.Tensor, i_bar: Optional[torch.Tensor] = None, want_amp: bool = True):
@@ -278,6 +286,17 @@ class Engine:
     @property
     def launch_count(self) -> int:
         return int(self.L.eq_launch_count(self.h))
+
+    def log_capacity(self):
+        """(spike-log capacity in records, times eq_run grew it)."""
+        g = ctypes.c_int32()
+        cap = int(self.L.eq_log_capacity(self.h, ctypes.byref(g)))
+        return cap, g.value
+
+    def debug_set_bucket_capacity(self, cap: int) -> None:
+        """Test hook: shrink the ring kind's calendar buckets so events spill
+        into the DRAM overflow ring (the rarely-taken path); next reset on."""
+        _native.check(self.h, self.L.eq_debug_set_bucket_capacity(self.h, int(cap)))
 
 
 def poisson_drive_device(n: int, n_trials: int, t_steps: int, dt: float, mean_interval: float,

@@ -28,7 +28,7 @@ from typing import Callable, List, Optional, Sequence, Tuple, Union
 import numpy as np
 import torch
 
-from .errors import ConfigurationError, GrazingCrossingError, NonSmoothDirectionError
+from .errors import ConfigurationError, EventQError, GrazingCrossingError, NonSmoothDirectionError
 from .events import DualScalar, QueueKind
 from .queues import coerce_kind
 from .workload import LIFConfig, Network, pack_mask
@@ -409,6 +409,7 @@ class RSNNFunction(torch.autograd.Function):
         engine.set_drive(mask, amplitude.detach())
         out = engine.forward()
         ctx.engine = engine
+        ctx.run_id = engine.run_id
         ctx.dtypes = (weight.dtype, delay.dtype, amplitude.dtype)
         ctx.needs_amp = ctx.needs_input_grad[2]
         return out["v"]
@@ -416,6 +417,12 @@ class RSNNFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, v_bar):
         eng = ctx.engine
+        if eng.run_id != ctx.run_id:
+            # the engine holds ONE recorded run (spike log + queues); a later
+            # forward on it (gradient accumulation, two losses, checkpointing)
+            # replaced the run this backward belongs to
+            raise EventQError("RSNNFunction.backward: the engine ran another forward since this one "
+                              f"(run {eng.run_id} != {ctx.run_id}); use one engine per pending backward")
         gw, gd, ga = eng.backward(v_bar.contiguous(), want_amp=ctx.needs_amp)
         dw, dd, da = ctx.dtypes
         return (gw.to(dw), gd.to(dd), None if ga is None else ga.to(da), None, None, None, None)
