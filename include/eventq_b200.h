@@ -49,7 +49,7 @@ enum {
   EQ_KIND_FIFORING = 1,    /* FIFORingQueue   queues.py:184-260 */
   EQ_KIND_BINARYHEAP = 2,  /* BinaryHeapQueue queues.py:481-571 */
   EQ_KIND_SORTEDARRAY = 3, /* SortedArrayQueue queues.py:308-403 */
-  EQ_KIND_LOSSYRING = 4,   /* LossyRingQueue  queues.py:126-181 (queue API only) */
+  EQ_KIND_LOSSYRING = 4,   /* LossyRingQueue  queues.py:126-181 (networks: network.py:321-328) */
   EQ_KIND_DONOTHING = 5    /* DoNothingQueue  queues.py:26-52   */
 };
 

@@ -17,6 +17,10 @@
  *                        (network.py:429-437)
  *   ring ............... queues.py:55-123 (slot = step % capacity, capability
  *                        error when step - now >= capacity :94-98)
+ *   lossy ring ......... queues.py:126-181 (slot = step % capacity with no
+ *                        capability check: a delay past the buffer aliases to
+ *                        an earlier step), wired by network.py:321-328 with
+ *                        capacity `queue_capacity or horizon*(n-1)+1`
  *   fifo/heap/sorted ... queues.py:184-260, 481-571, 308-403: all three drop the
  *                        INCOMING event when full and pop every due event; their
  *                        accepted sets are identical, so one
@@ -25,7 +29,11 @@
  *   donothing .......... queues.py:26-52 (drops everything)
  *   reverse mode ....... SURVEY.md Appendix B — the transpose of the reference's
  *                        forward-mode tangent recurrences (the reference has no
- *                        VJP; its JVP, network.py:668-683, is the pin)
+ *                        VJP; its JVP, network.py:668-683, is the pin); with
+ *                        exact_delivery=False the transpose of the plain
+ *                        delivery tangents: synapse jump W' + Q/tau_s
+ *                        (jumps.py:116-126), membrane -Q/tau_m (neuro.py:146-149,
+ *                        network.py:403-408), Q = sum w * (t_spk' + d')
  *
  * Two arithmetic modes:
  *   mode 0 "reference": double, glibc exp/log, slot sums in the reference's
@@ -52,7 +60,7 @@
 
 namespace {
 
-enum Kind { K_RING = 0, K_FIFO = 1, K_HEAP = 2, K_SORTED = 3, K_DONOTHING = 5 };
+enum Kind { K_RING = 0, K_FIFO = 1, K_HEAP = 2, K_SORTED = 3, K_LOSSY = 4, K_DONOTHING = 5 };
 enum Status { OK = 0, E_CONFIG = 1, E_CAPABILITY = 2, E_CAUSALITY = 3, E_GRAZING = 4, E_INTERNAL = 5 };
 
 struct Cfg {
@@ -175,11 +183,13 @@ struct Trial {
 
   Trial(const Session& s, int trial) : S(s), c(s.cfg), b(trial) {
     N = c.n;
-    R = S.horizon;
+    // lossy ring: slot = step % capacity; any capacity >= horizon behaves as a
+    // horizon-slot ring (no step in flight aliases), so storage is min of both
+    R = c.kind == K_LOSSY ? std::min(S.capacity, S.horizon) : S.horizon;
     I.assign(N, (T)0);
     V.assign(N, (T)c.v_reset);
     refr.assign(N, 0);
-    if (c.kind == K_RING) {
+    if (c.kind == K_RING || c.kind == K_LOSSY) {
       if (DEV) ring_f.assign((size_t)R * N * 2, 0);
       else ring_r.assign((size_t)R * N * 2, 0.0);
       ring_occ.assign((size_t)R * N, 0);
@@ -192,7 +202,7 @@ struct Trial {
   // pop slot `now` for neuron j -> (ps, pm)
   inline void pop(int j, int now, T& ps, T& pm) {
     ps = (T)0; pm = (T)0;
-    if (c.kind == K_RING) {
+    if (c.kind == K_RING || c.kind == K_LOSSY) {
       size_t k = (size_t)(now % R) * N + j;
       if (DEV) {
         ps = from_fixed<T, A>(ring_f[2 * k], c.frac_bits);
@@ -230,8 +240,8 @@ struct Trial {
       return false;
     }
     if (c.kind == K_DONOTHING) return false;
-    if (c.kind == K_RING) {
-      if (dstep - now >= R) {
+    if (c.kind == K_RING || c.kind == K_LOSSY) {
+      if (c.kind == K_RING && dstep - now >= R) {
         e.code = E_CAPABILITY;
         e.msg = "ring: delay of " + std::to_string(dstep - now + 1) + " steps exceeds buffer capacity " + std::to_string(R);
         return false;
@@ -340,7 +350,7 @@ struct Trial {
           bool ok = enqueue(j, now, dstep, ws, wm);
           if (e.code != OK) return;
           if (!ok) n_drop += 1;
-          acc.push_back(ok || c.kind == K_RING ? 1 : 0);
+          acc.push_back(ok || c.kind == K_RING || c.kind == K_LOSSY ? 1 : 0);
         }
       }
     }
@@ -376,15 +386,29 @@ int run_forward(Session& s) {
     s.counters[3 * b + 2] = tr.n_drop;
     // canonical pending contents: due steps T .. T+horizon-1
     int H = s.horizon;
+    if (c.kind == K_FIFO || c.kind == K_HEAP || c.kind == K_SORTED) {   // one pass over each pool
+      for (int j = 0; j < N; ++j) {
+        for (auto& ev : tr.pool[j]) {
+          const int k = ev.due - c.t_steps;
+          if (k < 0 || k >= H) continue;
+          size_t o = (((size_t)b * N + j) * H + k) * 2;
+          if (DEV) { s.pending[o] += ev.fs; s.pending[o + 1] += ev.fm; }
+          else { s.pending_ref[o] += ev.rs; s.pending_ref[o + 1] += ev.rm; }
+        }
+      }
+      continue;
+    }
     for (int j = 0; j < N; ++j) {
       for (int k = 0; k < H; ++k) {
         int due = c.t_steps + k;
         typename FixedOf<T>::type fs = 0, fm = 0;
         double rs = 0.0, rm = 0.0;
-        if (c.kind == K_RING) {
+        if (c.kind == K_RING || (c.kind == K_LOSSY && k < tr.R)) {
+          // (a lossy ring's slot k >= R would alias an earlier due step)
           size_t q = (size_t)(due % tr.R) * N + j;
           if (DEV) { fs = tr.ring_f[2 * q]; fm = tr.ring_f[2 * q + 1]; }
           else { rs = tr.ring_r[2 * q]; rm = tr.ring_r[2 * q + 1]; }
+        } else if (c.kind == K_LOSSY) {
         } else if (c.kind != K_DONOTHING) {
           for (auto& ev : tr.pool[j]) if (ev.due == due) { fs += ev.fs; fm += ev.fm; rs += ev.rs; rm += ev.rm; }
         }
@@ -417,16 +441,21 @@ template <typename T, bool DEV>
 int run_backward(Session& s, const double* vbar, const double* ibar, double* gw, double* gd, double* gamp) {
   const Cfg& c = s.cfg;
   if (c.kind == K_DONOTHING) { /* every event dropped: only the neuron recurrences remain */ }
-  if (!c.exact_delivery) { s.err = "backward requires exact_delivery"; return E_CONFIG; }
+  const bool exact = c.exact_delivery != 0;
   int B = c.n_trials, N = c.n, TT = c.t_steps;
   size_t E = s.col.size();
   const T dt = (T)c.dt, tau_m = (T)c.tau_m, tau_s = (T)c.tau_syn;
   const T v_th = (T)c.v_th, v_reset = (T)c.v_reset;
   const T k_m = (T)std::exp(-c.dt / c.tau_m);
   const T k_s = (T)std::exp(-c.dt / c.tau_syn);
-  const T cc = (T)(c.tau_syn / (c.tau_m - c.tau_syn));
+  // exact delivery: Lambda_m = c * lambda_vhat is the membrane twin payload's
+  // adjoint; plain delivery: Lambda_m = -lambda_vhat carries the membrane's
+  // -Q/tau_m tangent term, and there is no bump (c = 0)
+  const T cc = exact ? (T)(c.tau_syn / (c.tau_m - c.tau_syn)) : (T)0;
+  const T cm = exact ? cc : (T)-1;
   const T inv_s = (T)(1.0 / c.tau_syn), inv_m = (T)(1.0 / c.tau_m);
   const int R = s.horizon + 1;
+  const int lossy_cap = c.kind == K_LOSSY ? s.capacity : 0;
   std::fill(gw, gw + E, 0.0);
   std::fill(gd, gd + E, 0.0);
   std::fill(gamp, gamp + N, 0.0);
@@ -477,13 +506,20 @@ int run_backward(Session& s, const double* vbar, const double* ibar, double* gw,
             T dd = (T)s.d[x];
             T t_post = t + dd;
             int32_t st = delivery<T, DEV>(t_post, dd, dt, m);
-            if (st >= TT || !okv[x - r0]) { lt_sum = lt_sum + (T)0; continue; }
-            T phi = (T)st * dt - t_post;
-            T es = xexp<T, DEV>(DEV ? -phi * inv_s : -phi / tau_s);
-            T em = xexp<T, DEV>(DEV ? -phi * inv_m : -phi / tau_m);
-            size_t o = (size_t)(st % R) * N + j;
+            // the step the event is popped at: st, or for a lossy ring the
+            // first step >= m+1 in st's residue class mod capacity
+            int32_t sp = st;
+            if (lossy_cap > 0 && st - (m + 1) >= lossy_cap) sp = (m + 1) + (st - (m + 1)) % lossy_cap;
+            if (sp >= TT || !okv[x - r0]) { lt_sum = lt_sum + (T)0; continue; }
+            T es = (T)1, em = (T)1;
+            if (exact) {
+              T phi = (T)st * dt - t_post;
+              es = xexp<T, DEV>(DEV ? -phi * inv_s : -phi / tau_s);
+              em = xexp<T, DEV>(DEV ? -phi * inv_m : -phi / tau_m);
+            }
+            size_t o = (size_t)(sp % R) * N + j;
             T as = Ls[o], am = Lm[o];
-            T g_w = es * as + em * am;
+            T g_w = exact ? es * as + em * am : as;
             T g_tp = DEV ? w * (es * as * inv_s + em * am * inv_m) : w * (es * as / tau_s + em * am / tau_m);
             lw[x] += (double)g_w;
             ld[x] += (double)g_tp;
@@ -516,7 +552,7 @@ int run_backward(Session& s, const double* vbar, const double* ibar, double* gw,
           T lip = lI[j] + la;
           if (drive_on(s, b, m, j)) la_acc[j] += (double)la;
           size_t o = (size_t)(m % R) * N + j;
-          Lm[o] = cc * lvh;
+          Lm[o] = cm * lvh;
           Ls[o] = k_s * lip - cc * lvh;
           lI[j] = k_s * lip;
           lV[j] = lvh;
@@ -572,7 +608,7 @@ int eqo_set_network(void* h, const int64_t* rowptr, const int32_t* col, const do
     hmax = std::max(hmax, q);
   }
   s->horizon = hmax + 1;
-  if (c.kind == K_FIFO || c.kind == K_HEAP || c.kind == K_SORTED)
+  if (c.kind == K_FIFO || c.kind == K_HEAP || c.kind == K_SORTED || c.kind == K_LOSSY)
     s->capacity = c.capacity > 0 ? c.capacity : s->horizon * (N - 1) + 1;  // network.py:327
   return OK;
 }

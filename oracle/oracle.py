@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "build", "libeqoracle.so")
 _lib = None
 
-KINDS = {"ring": 0, "fiforing": 1, "binaryheap": 2, "sortedarray": 3, "donothing": 5}
+KINDS = {"ring": 0, "fiforing": 1, "binaryheap": 2, "sortedarray": 3, "lossyring": 4, "donothing": 5}
 STATUS = {0: "ok", 1: "ConfigurationError", 2: "CapabilityError", 3: "CausalityError",
           4: "GrazingCrossingError", 5: "InternalError"}
 

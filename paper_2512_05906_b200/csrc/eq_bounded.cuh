@@ -72,7 +72,8 @@ template <> struct alignas(32) Arrival<double> {
 template <typename T>
 struct BndArgs {
   FwdArgs<T> f;
-  int cap;                    // events per queue
+  int cap;                    // events per queue (lossy ring: physical slots = min(capacity, horizon) + 1)
+  int cap_ref;                // lossy ring: the reference's capacity (aliasing modulus)
   const long long* csc_off;   // [N+1] in-edge segment offsets
   long long E;
   Arrival<T>* alist;          // [2][B][E] arrival lists, target j at csc_off[j]
@@ -295,16 +296,33 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
       if (idx >= end) continue;
       const int b = c.divN.div(idx);
       const int j = idx - b * F.N;
+      long long qs = 0, qm = 0;
+      if (F.kind == EQ_KIND_LOSSYRING) {
+        // LossyRingQueue._pop_raw (queues.py:109-120 via :178): read and zero
+        // slot m of the target's ring; producers added into it directly
+        if (last) continue;
+        long long* sl = F.ring + ((size_t)b * A.cap + (size_t)(m % A.cap)) * F.N * P::kSlotWords + (size_t)j * P::kSlotWords;
+        if (P::kSlotWords == 1) {
+          unpack2(sl[0], qs, qm);
+          sl[0] = 0;
+        } else {
+          qs = sl[0];
+          qm = sl[1];
+          sl[0] = 0;
+          sl[1] = 0;
+        }
+      }
+      const T I0 = F.I[idx], V0 = F.V[idx];
+      int rf = F.refractory ? F.refr[idx] : 0;
+      const bool drv = !last && drive_bit(F.net, b, m, j);
+      const T ampj = __ldg(F.net.amp + j);
+      if (F.kind != EQ_KIND_LOSSYRING) {
       // every load that does not depend on the queue first: one round trip
       int4 mt = A.meta[idx];
       const bool ins = m - 1 >= A.insert_first && m >= 1;
       int* cntp = A.acnt + ((size_t)((m - 1) & 1) * F.B + b) * F.N + j;
       const int narr = ins ? *cntp : 0;
       const long long acs = __ldg(A.csc_off + j);
-      const T I0 = F.I[idx], V0 = F.V[idx];
-      int rf = F.refractory ? F.refr[idx] : 0;
-      const bool drv = !last && drive_bit(F.net, b, m, j);
-      const T ampj = __ldg(F.net.amp + j);
       bool dirty = false;
       // the queue lines a step's inserts and pops will walk, fetched into L2
       // together: the structure's dependent chains then miss DRAM once
@@ -340,12 +358,12 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
         if (dirty) A.meta[idx] = mt;
         continue;
       }
-      long long qs = 0, qm = 0;
       if (mt.x > 0 && mt.w == m) {
         queue_pop<T>(F.kind, A.cap, A.q + (size_t)idx * A.cap, mt, m, qs, qm);
         dirty = true;
       }
       if (dirty) A.meta[idx] = mt;
+      }
       T ps = P::deq(qs, c.inv_scale), pm = P::deq(qm, c.inv_scale);
       if (!F.exact) pm = (T)0;
       const T drive = drv ? ampj : (T)0;
@@ -441,6 +459,26 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
           ws = w;
           wm = (T)0;
         }
+        const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
+        if (F.kind == EQ_KIND_LOSSYRING) {
+          // LossyRingQueue.enqueue (queues.py:160-176): slot = step % capacity,
+          // i.e. the event is popped at the first step >= now = m+1 in its due
+          // step's residue class; add straight into that slot (order-free fixed
+          // point).  The ring has capacity+1 physical slots so slot m, popped
+          // in this phase by other CTAs, is never a target here.
+          int off = ds - (m + 1);
+          if (off >= A.cap_ref) off %= A.cap_ref;
+          const int se = m + 1 + off;
+          long long* sl = F.ring + ((size_t)b * A.cap + (size_t)(se % A.cap)) * F.N * P::kSlotWords +
+                          (size_t)jt * P::kSlotWords;
+          if (P::kSlotWords == 1) {
+            red_add(sl, pack2(q1, q2));
+          } else {
+            red_add(sl, q1);
+            red_add(sl + 1, q2);
+          }
+          continue;
+        }
         // append to the target's arrival list (slot from its counter; the
         // segment holds all in-edges, so it cannot overflow)
         const int slot = atomicAdd(A.acnt + ((size_t)par * F.B + b) * F.N + jt, 1);
@@ -449,7 +487,6 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
         ar.tag = (int)(s_off + k0 + k);
         ar.due = ds;
         ar.ro = ro;
-        const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
         if constexpr (sizeof(T) == 4) {
           ar.p = pack2(q1, q2);
           ar.pad = 0;

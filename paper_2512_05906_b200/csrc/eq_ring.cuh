@@ -33,6 +33,7 @@ __device__ __forceinline__ void red_acc(long long* p, long long v) {
 template <typename T>
 struct StepConsts {
   T dt, tau_m, tau_s, v_th, v_reset, k_m, k_s, cc;
+  T cm;                     // reverse: Lambda_m = cm * lambda_vhat (cc exact, -1 plain delivery)
   T inv_tau_m, inv_tau_s;   // (T)(1/tau) for the per-event exponents (device-mode contract)
   T scale, inv_scale;       // 2^F, 2^-F (exact powers of two)
   FastDiv divN;             // idx -> trial
@@ -852,6 +853,11 @@ struct BwdArgs {
   int m_run;          // steps simulated since reset (the reverse pass walks m_run-1 .. 0)
   int m_hi, m_lo;     // this launch's phases: m_hi-1 .. m_lo (one exchange window, or all)
   int R, refractory;
+  int exact;          // exact delivery (else plain: payload w, Lambda_m = -lambda_vhat)
+  int lossy_cap;      // lossy ring: the reference's capacity (events pop at the first step
+                      // >= m+1 in the due step's residue class), 0 otherwise
+  int serial;         // R-fanout(m-1) after R-neuron(m) behind a grid barrier (lossy ring:
+                      // an event of step m-1 may pop at step m, whose reverse row R-neuron(m) writes)
   StepConsts<T> c;
   NetView<T> net;
   T* lamV;
@@ -989,18 +995,25 @@ __device__ __forceinline__ void bwd_rfanout(const BwdArgs<T>& A, const int m, co
           const T w = ww[e], d = dd[e];
           const T t_post = rec.t + d;
           const int st = delivery_step_coded(t_post, cc[e], c.dt, me);
+          int sp = st;                                     // the step the event is popped at
+          if (A.lossy_cap > 0 && st - (me + 1) >= A.lossy_cap) sp = me + 1 + (st - (me + 1)) % A.lossy_cap;
           T g_tp = (T)0;
-          bool live = st < A.m_run && !A.no_events;        // never popped / dropped: no effect
+          bool live = sp < A.m_run && !A.no_events;        // never popped / dropped: no effect
           if (live && A.drop_bits) {                       // dropped by a bounded queue
             const long long id = (k0 + kk[e]) * (long long)A.maxdeg + (f - s_pre[kk[e]]);
             live = !((A.drop_bits[id >> 5] >> (id & 31)) & 1u);
           }
           if (live) {
-            const T phi = (T)st * c.dt - t_post;
-            const T es = eq_exp_t(-phi * c.inv_tau_s);
-            const T em = eq_exp_t(-phi * c.inv_tau_m);
-            const T2 L = ld_gather(A.lam + ((size_t)b * A.R + (size_t)(st % A.R)) * A.N + jj[e]);
-            const T g_w = es * L.x + em * L.y;
+            T es = (T)1, em = (T)1;
+            if (A.exact) {
+              const T phi = (T)st * c.dt - t_post;
+              es = eq_exp_t(-phi * c.inv_tau_s);
+              em = eq_exp_t(-phi * c.inv_tau_m);
+            }
+            const T2 L = ld_gather(A.lam + ((size_t)b * A.R + (size_t)(sp % A.R)) * A.N + jj[e]);
+            // plain delivery: W' enters the synapse jump alone, Q = sum w tt
+            // enters synapse (+Q/tau_s) and membrane (-Q/tau_m, in Lambda_m)
+            const T g_w = A.exact ? es * L.x + em * L.y : L.x;
             g_tp = w * (es * L.x * c.inv_tau_s + em * L.y * c.inv_tau_m);
             red_grad(A.gw + xx[e], (double)g_w);
             red_grad(A.gd + xx[e], (double)g_tp);
@@ -1055,9 +1068,14 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
   // read reverse slots of steps >= m+1, all final); [neuron side] R-neuron(m),
   // which writes reverse slot m only and reads dL/dt_spk of its own spikes of
   // step m, produced by the event side of phase m+1.
-  for (int m = A.m_hi - 1; m >= A.m_lo; --m) {
+  bool ok = true;
+  for (int m = A.m_hi - 1; m >= A.m_lo && ok; --m) {
     tl_mark(A.tl, m, A.G, cta, 0);
-    if (tid < Ro::NF) {
+    // serial mode (lossy ring): pass 0 = R-neuron(m), grid barrier, pass 1 =
+    // R-fanout(m-1); otherwise one pass with both sides concurrent
+    for (int pass = A.serial ? 0 : 1; pass < 2; ++pass) {
+    const bool ev_pass = pass == 1, nr_pass = !A.serial || pass == 0;
+    if (tid < Ro::NF && ev_pass) {
       // ======================== event side: R-fanout(m-1), shared evenly by
       // the whole grid (whole spikes per CTA): bwd_rfanout
       const int gtid = tid;
@@ -1070,7 +1088,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
                                                   s_ready[cur] == m);
       }
       tl_mark(A.tl, m, A.G, cta, 1);
-    } else {
+    } else if (tid >= Ro::NF && nr_pass) {
       // ======================== neuron side: R-neuron(m)
       const int gtid = tid - Ro::NF;
       const long long off = A.chunk_off[(size_t)m * A.G + cta];
@@ -1133,7 +1151,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
               const T lip = (T)liv[q] + la;
               if (A.gamp_bt && ((mw >> q) & 1u)) A.gamp_bt[idx + q] += (double)la;
               ls[q] = (float)(c.k_s * lip - c.cc * lvh);
-              lm[q] = (float)(c.cc * lvh);
+              lm[q] = (float)(c.cm * lvh);
               ni[q] = (float)(c.k_s * lip);
               nv[q] = (float)lvh;
             }
@@ -1188,7 +1206,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
               const T lip = (T)liv[q] + la;
               if (A.gamp_bt && ((mw >> q) & 1u)) A.gamp_bt[idx + q] += (double)la;
               ls[q] = (double)(c.k_s * lip - c.cc * lvh);
-              lm[q] = (double)(c.cc * lvh);
+              lm[q] = (double)(c.cm * lvh);
               ni[q] = (double)(c.k_s * lip);
               nv[q] = (double)lvh;
             }
@@ -1244,7 +1262,7 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
             if (A.gamp_bt && ((__ldg(mrow + (j >> 5)) >> (j & 31)) & 1u)) A.gamp_bt[idx] += (double)la;
             T2 L;
             L.x = c.k_s * lip - c.cc * lvh;
-            L.y = c.cc * lvh;
+            L.y = c.cm * lvh;
             lam_row[j] = L;
             A.lamI[idx] = c.k_s * lip;
             A.lamV[idx] = lvh;
@@ -1270,6 +1288,10 @@ __global__ void __launch_bounds__(NT, 2) k_backward(BwdArgs<T> A) {
         }
       }
     }
+    if (A.serial && pass == 0 && !grid_sync(A.bar, A.G, A.err)) ok = false;
+    if (!ok) break;
+    }
+    if (!ok) break;
     __syncthreads();
     tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err)) break;

@@ -118,6 +118,11 @@ struct eq_handle {
   double* gamp_bt = nullptr;
   // bounded kinds (fifo / heap / sorted)
   bool bounded = false;
+  // lossy ring: run by the bounded kernel's step structure (an event may pop
+  // one step after its emission), slots in `ring` as [B][lossy_slots][N]
+  bool lossy = false;
+  int lossy_slots = 0;         // physical slots: min(capacity, horizon) + 1
+  long long lossy_cap = 0;     // the reference's capacity (aliasing modulus)
   int cap = 0;                 // physical events per queue
   long long cap_ref = 0;       // the reference's capacity (acceptance rule)
   long long* csc_off = nullptr;
@@ -220,6 +225,7 @@ StepConsts<T> consts(const eq_handle* h) {
   k.k_m = (T)std::exp(-c.dt / c.tau_m);
   k.k_s = (T)std::exp(-c.dt / c.tau_syn);
   k.cc = c.exact_delivery ? (T)(c.tau_syn / (c.tau_m - c.tau_syn)) : (T)0;
+  k.cm = c.exact_delivery ? k.cc : (T)-1;
   k.inv_tau_m = (T)(1.0 / c.tau_m);
   k.inv_tau_s = (T)(1.0 / c.tau_syn);
   k.scale = (T)std::ldexp(1.0, h->frac_bits);
@@ -432,6 +438,27 @@ __global__ void k_clear_dirty_rows(long long* ring, int* ring_dirty, int R, long
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < row_words;
        k += (long long)gridDim.x * blockDim.x)
     row[k] = 0;
+}
+
+// Lossy ring contents pending at step `now`: slot (now + h) % S holds the
+// events popped at now + h for h < S - 1 (= min(capacity, horizon)); larger h
+// alias to earlier steps and stay empty.  out int64 [B*N][H][2].
+__global__ void k_pending_lossy(const long long* ring, int W, int S, int B, int N, int H, int now, long long* out) {
+  const long long total = (long long)B * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(idx / N), j = (int)(idx - (long long)b * N);
+    for (int h = 0; h < H; ++h) {
+      long long qs = 0, qm = 0;
+      if (h < S - 1) {
+        const long long* sl = ring + (((size_t)b * S + (size_t)((now + h) % S)) * N + j) * W;
+        if (W == 1) unpack2(sl[0], qs, qm);
+        else { qs = sl[0]; qm = sl[1]; }
+      }
+      out[(idx * H + h) * 2] = qs;
+      out[(idx * H + h) * 2 + 1] = qm;
+    }
+  }
 }
 
 __global__ void k_meta_init(int4* meta, long long n) {
@@ -690,10 +717,11 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
   A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
-  if (h->bounded) {
+  if (h->bounded || h->lossy) {
     BndArgs<T> Bk;
     Bk.f = A;
-    Bk.cap = h->cap;
+    Bk.cap = h->lossy ? h->lossy_slots : h->cap;
+    Bk.cap_ref = h->lossy ? (int)std::min<long long>(h->lossy_cap, 1LL << 30) : 0;
     Bk.csc_off = h->csc_off;
     Bk.E = h->E;
     Bk.alist = (Arrival<T>*)h->alist;
@@ -816,6 +844,9 @@ int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
   A.step_start = h->step_start;
   A.maxdeg = h->maxdeg;
   A.drop_bits = h->bounded ? h->drop_bits : nullptr;
+  A.exact = h->cfg.exact_delivery;
+  A.lossy_cap = h->lossy ? (int)std::min<long long>(h->lossy_cap, 1LL << 30) : 0;
+  A.serial = h->lossy && h->lossy_cap < h->horizon;   // aliasing can pop an event one step after emission
   A.no_events = h->cfg.kind == EQ_KIND_DONOTHING;
   A.lt_rem = h->partitioned ? (const T*)h->lt_rem : nullptr;
   A.imp = nullptr;
@@ -985,10 +1016,11 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
   if (!(c.tau_syn > 0.0)) return bad("tau_syn must be positive, got " + std::to_string(c.tau_syn));
   if (!(c.v_th > c.v_reset)) return bad("threshold must sit above reset");
   if (c.kind != EQ_KIND_RING && c.kind != EQ_KIND_DONOTHING && c.kind != EQ_KIND_FIFORING &&
-      c.kind != EQ_KIND_BINARYHEAP && c.kind != EQ_KIND_SORTEDARRAY)
+      c.kind != EQ_KIND_BINARYHEAP && c.kind != EQ_KIND_SORTEDARRAY && c.kind != EQ_KIND_LOSSYRING)
     return bad("unknown queue kind " + std::to_string(c.kind));
   if (c.capacity < 0) return bad("capacity must be >= 1, got " + std::to_string(c.capacity));
   h->bounded = c.kind == EQ_KIND_FIFORING || c.kind == EQ_KIND_BINARYHEAP || c.kind == EQ_KIND_SORTEDARRAY;
+  h->lossy = c.kind == EQ_KIND_LOSSYRING;
   if (c.exact_delivery && std::fabs(c.tau_m - c.tau_syn) < 1e-3 * c.tau_m)
     return bad("exact delivery splits the membrane/synapse eigenmodes and needs tau_m != tau_syn");
   h->total = (long long)c.n_neurons * c.n_trials;
@@ -1162,6 +1194,13 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   h->launches += 1;
   // queue storage
   size_t words = c.kind == EQ_KIND_RING ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
+  if (h->lossy) {
+    // LossyRingQueue capacity as the reference wires it (network.py:327):
+    // queue_capacity or horizon*(n-1)+1; >= horizon never aliases
+    h->lossy_cap = c.capacity > 0 ? c.capacity : (long long)h->horizon * (N - 1) + 1;
+    h->lossy_slots = (int)std::min<long long>(h->lossy_cap, h->horizon) + 1;
+    words = (size_t)c.n_trials * h->lossy_slots * N * (c.precision == 32 ? 1 : 2);
+  }
   h->ring_words = words;
   {
     long long* before = h->ring;
@@ -1225,7 +1264,7 @@ int eq_reset(eq_handle* h, void* stream) {
     EQ_CUDA(h, cudaMemsetAsync(h->acc, 0, (size_t)2 * h->total * wd * sizeof(long long), s));
     EQ_CUDA(h, cudaMemsetAsync(h->bk_cnt, 0, (size_t)h->G * h->NB * sizeof(int), s));
     EQ_CUDA(h, cudaMemsetAsync(h->ring_dirty, 0, (size_t)h->R * sizeof(int), s));
-  } else if (!h->ring_clean) {
+  } else if (!h->ring_clean || h->lossy) {   // a lossy ring's pending events sit in its slots
     EQ_CUDA(h, cudaMemsetAsync(h->ring, 0, h->ring_words * sizeof(long long), s));
     h->ring_clean = true;
   }
@@ -1446,7 +1485,6 @@ int eq_backward_begin(eq_handle* h, const void* v_bar, const void* i_bar, double
                       double* grad_amp, void* stream) {
   if (!h) return EQ_ERR_CONFIGURATION;
   if (h->steps_done < 1) return fail(h, EQ_ERR_CONFIGURATION, "backward needs a forward run first");
-  if (!h->cfg.exact_delivery) return fail(h, EQ_ERR_CONFIGURATION, "reverse mode requires exact_delivery");
   if (!v_bar || !grad_w || !grad_d) return fail(h, EQ_ERR_CONFIGURATION, "v_bar, grad_w, grad_d are required");
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1662,7 +1700,10 @@ int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream) {
   size_t n = (size_t)B * N * H * 2;
   void* buf = nullptr;
   EQ_CUDA(h, alloc(h, &buf, n * sizeof(long long)));
-  if (h->bounded) {
+  if (h->lossy) {
+    k_pending_lossy<<<592, 256, 0, s>>>(h->ring, h->cfg.precision == 32 ? 1 : 2, h->lossy_slots, B, N, H,
+                                        h->steps_done, (long long*)buf);
+  } else if (h->bounded) {
     if (h->cfg.precision == 32)
       k_pending_bounded<float><<<592, 256, 0, s>>>((const QEv<float>*)h->q, h->meta, h->cfg.kind, h->cap,
                                                     (long long)B * N, H, h->steps_done, (long long*)buf);

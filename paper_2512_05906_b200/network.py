@@ -212,10 +212,10 @@ def build_rsnn(params: NetworkParams, seed: Optional[SeedDirection] = None, rng_
     if kind is QueueKind.BGPQ:
         raise ConfigurationError("bgpq is registered but unsupported: its value is GPU group parallelism, "
                                  "which a serial build cannot express")
-    if kind not in (QueueKind.RING, QueueKind.FIFORING, QueueKind.BINARYHEAP, QueueKind.SORTEDARRAY,
-                    QueueKind.DONOTHING):
+    if kind not in (QueueKind.RING, QueueKind.LOSSYRING, QueueKind.FIFORING, QueueKind.BINARYHEAP,
+                    QueueKind.SORTEDARRAY, QueueKind.DONOTHING):
         raise ConfigurationError(f"{kind.value} networks are out of scope of the B200 build "
-                                 "(ring, fiforing, binaryheap, sortedarray, donothing)")
+                                 "(ring, lossyring, fiforing, binaryheap, sortedarray, donothing)")
     off = ~np.eye(n, dtype=bool)
     bad = np.argwhere(off & (d < params.dt))
     if len(bad):

@@ -70,15 +70,15 @@ def ref_params(net: wl.Network, kind: str, capacity=None, v_target=0.25, dense_d
 
 def run_case(name: str, net: wl.Network, kind: str, t_steps: int, mask: np.ndarray,
              amp: np.ndarray, capacity=None, directions=(), record=True, refractory=0,
-             dense_delay=DT):
+             dense_delay=DT, exact=True):
     t0 = time.time()
-    params = ref_params(net, kind, capacity, refractory=refractory, dense_delay=dense_delay)
+    params = ref_params(net, kind, capacity, refractory=refractory, dense_delay=dense_delay, exact=exact)
     res = simulate(build_rsnn(params), t_steps, drive_fn(mask[0], amp, net.n), record=record)
     # loss tangent-free; raster rows (step, neuron)
     raster = np.array(res.raster, dtype=np.int32).reshape(-1, 2) if record else np.zeros((0, 2), np.int32)
     out = dict(
         kind=kind, n=net.n, t_steps=t_steps, capacity=-1 if capacity is None else capacity,
-        refractory=refractory, dense_delay=dense_delay,
+        refractory=refractory, dense_delay=dense_delay, exact=exact,
         digest=input_digest(net, mask, amp),
         raster=raster, loss=res.loss.primal, spike_count=res.spike_count,
         drop_count=res.drop_count, enqueued_count=res.enqueued_count,
@@ -127,7 +127,7 @@ def main():
         net, mask, amp = case.inputs()
         dirs = golden_cases.pick_directions(net, case.seed, *case.n_dirs)
         run_case(case.name, net, case.kind, case.t_steps, mask, amp, capacity=case.capacity,
-                 directions=dirs, refractory=case.refractory)
+                 directions=dirs, refractory=case.refractory, exact=case.exact)
 
 
 if __name__ == "__main__":

@@ -33,6 +33,7 @@ class Case:
     refractory: int = 0
     n_dirs: Tuple[int, int, int] = (0, 0, 0)   # weight, delay, drive directions
     slow: bool = False
+    exact: bool = True                         # NetworkParams.exact_delivery
 
     def inputs(self):
         net = wl.random_network(self.n, self.k_out, self.seed, dt=DT, w_mean=self.w_mean,
@@ -46,10 +47,10 @@ class Case:
         return self.k_out >= self.n - 1
 
 
-def _dense(name, n, kind, cap, homog, seed, T, dirs=(0, 0, 0), refr=0, dl=None):
+def _dense(name, n, kind, cap, homog, seed, T, dirs=(0, 0, 0), refr=0, dl=None, exact=True):
     if dl is None:
         dl = (16, 16) if homog else (14, 30)
-    return Case(name, n, n - 1, kind, T, seed, 0.3, 0.1, dl, 1000 + seed, cap, refr, dirs)
+    return Case(name, n, n - 1, kind, T, seed, 0.3, 0.1, dl, 1000 + seed, cap, refr, dirs, exact=exact)
 
 
 CASES: List[Case] = [
@@ -64,6 +65,17 @@ CASES: List[Case] = [
     _dense("dense_ring_n40", 40, "ring", None, False, 6, 1000, (3, 3, 1)),
     _dense("dense_ring_refr3_n10", 10, "ring", None, False, 7, 1000, (2, 2, 1), refr=3, dl=(2, 20)),
     Case("sparse_ring_n100", 100, 10, "ring", 1000, 8, 0.03, 0.01, (1, 16), 1000, None, 0, (4, 4, 2)),
+    # LossyRingQueue networks (network.py:321-328, queues.py:126-181): capacity
+    # below the horizon (31) aliases delays into earlier steps; default capacity
+    # (horizon*(n-1)+1) is lossless
+    _dense("dense_lossy_cap6_n10", 10, "lossyring", 6, False, 9, 1200, (3, 3, 1)),
+    _dense("dense_lossy_n8", 8, "lossyring", None, False, 10, 1000, (2, 2, 1)),
+    # plain step-aligned delivery (exact_delivery=False, network.py:403-408)
+    _dense("dense_ring_plain_n10", 10, "ring", None, False, 11, 1200, (3, 3, 1), exact=False),
+    _dense("dense_lossy_cap5_plain_n10", 10, "lossyring", 5, False, 12, 1000, (2, 2, 1), exact=False),
+    _dense("dense_sorted_plain_cap3_n12", 12, "sortedarray", 3, False, 13, 1000, (2, 2, 1), exact=False),
+    Case("sparse_ring_plain_n100", 100, 10, "ring", 1000, 14, 0.03, 0.01, (1, 16), 1014, None, 0, (3, 3, 1),
+         exact=False),
     # BASELINE config 1: 1k neurons, K=100, delays 1..16 steps, ring, T=1000
     Case("c1_ring", 1000, 100, "ring", 1000, 0, 0.003, 0.001, (1, 16), 1000, None, 0, (2, 2, 1),
          slow=True),

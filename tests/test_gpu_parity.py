@@ -24,18 +24,18 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-def _engine(net, mask, amp, B, T, precision, kind="ring", refractory=0, capacity=0):
+def _engine(net, mask, amp, B, T, precision, kind="ring", refractory=0, capacity=0, exact=True):
     from paper_2512_05906_b200.engine import Engine
-    lif = wl.LIFConfig(refractory_steps=refractory)
-    eng = Engine(net.n, B, T, kind=kind, precision=precision, lif=lif, capacity=capacity)
+    lif = wl.LIFConfig(refractory_steps=refractory, exact_delivery=exact)
+    eng = Engine(net.n, B, T, kind=kind, precision=precision, lif=lif, capacity=capacity or 0)
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     eng.set_drive(mask, amp)
     return eng
 
 
-def _oracle(net, mask, amp, B, T, precision, F, kind="ring", refractory=0, mode="device"):
+def _oracle(net, mask, amp, B, T, precision, F, kind="ring", refractory=0, mode="device", capacity=0, exact=True):
     s = OracleSession(n=net.n, n_trials=B, t_steps=T, kind=kind, mode=mode, precision=precision,
-                      frac_bits=F, refractory_steps=refractory)
+                      frac_bits=F, refractory_steps=refractory, capacity=capacity or 0, exact_delivery=exact)
     s.set_network(net.rowptr, net.col, net.weight, net.delay)
     s.set_drive(mask, amp)
     return s
@@ -46,11 +46,12 @@ def _sorted_spikes(d):
     return np.stack([d["trial"][order], d["step"][order], d["neuron"][order]], 1), d["t"][order]
 
 
-def _compare_forward(net, mask, amp, B, T, precision, refractory=0, backward=True):
-    eng = _engine(net, mask, amp, B, T, precision, refractory=refractory)
+def _compare_forward(net, mask, amp, B, T, precision, refractory=0, backward=True, kind="ring", capacity=0,
+                     exact=True):
+    eng = _engine(net, mask, amp, B, T, precision, kind=kind, refractory=refractory, capacity=capacity, exact=exact)
     out = eng.forward()
     F = eng.frac_bits
-    s = _oracle(net, mask, amp, B, T, precision, F, refractory=refractory)
+    s = _oracle(net, mask, amp, B, T, precision, F, kind=kind, refractory=refractory, capacity=capacity, exact=exact)
     ref = s.forward()
     assert s.horizon == eng.horizon
     got = eng.spikes()
@@ -78,12 +79,31 @@ def _compare_forward(net, mask, amp, B, T, precision, refractory=0, backward=Tru
     return eng, out
 
 
+RING_LIKE = ["dense_ring_n8", "dense_ring_n40", "dense_ring_refr3_n10", "sparse_ring_n100",
+             # lossy ring networks and plain (non-exact) delivery, forward and reverse
+             "dense_lossy_cap6_n10", "dense_lossy_n8", "dense_ring_plain_n10", "dense_lossy_cap5_plain_n10",
+             "sparse_ring_plain_n100"]
+
+
 @pytest.mark.parametrize("precision", [32, 64])
-@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_n40", "dense_ring_refr3_n10", "sparse_ring_n100"])
+@pytest.mark.parametrize("name", RING_LIKE)
 def test_golden_inputs_bitwise_vs_oracle(name, precision):
     case = BY_NAME[name]
     net, mask, amp = case.inputs()
-    _compare_forward(net, mask, amp, 1, case.t_steps, precision, refractory=case.refractory)
+    _compare_forward(net, mask, amp, 1, case.t_steps, precision, refractory=case.refractory, kind=case.kind,
+                     capacity=case.capacity, exact=case.exact)
+
+
+@pytest.mark.parametrize("kind,cap", [("lossyring", 9), ("lossyring", 0)])
+@pytest.mark.parametrize("exact", [True, False])
+def test_lossy_multi_trial_bitwise_vs_oracle(kind, cap, exact):
+    """Sparse net, 3 trials, delays 1..20 (horizon 21): capacity 9 aliases
+    (events pop up to 12 steps early, some one step after their emission);
+    capacity 0 = the reference default, lossless (== ring)."""
+    net = wl.random_network(300, 30, 19, delay_steps=(1, 20), w_mean=0.02, w_std=0.01)
+    B, T = 3, 400
+    mask = wl.drive_masks(300, B, T, 1e-3, seed0=78)
+    _compare_forward(net, mask, np.full(300, 12.0), B, T, 32, kind=kind, capacity=cap, exact=exact)
 
 
 @pytest.mark.parametrize("precision", [32, 64])
@@ -100,8 +120,7 @@ def test_c1_full_size_bitwise_vs_oracle(precision):
     _compare_forward(wk.net, wk.mask, wk.amp, wk.n_trials, wk.t_steps, precision)
 
 
-@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_n40", "dense_ring_refr3_n10", "sparse_ring_n100",
-                                  "c1_ring"])
+@pytest.mark.parametrize("name", RING_LIKE + ["c1_ring"])
 def test_fp64_gpu_vs_reference_fixture(name):
     """Python reference outputs (fixtures) vs the GPU in fp64."""
     case = BY_NAME[name]
@@ -110,7 +129,8 @@ def test_fp64_gpu_vs_reference_fixture(name):
         pytest.skip("fixture missing")
     g = np.load(path)
     net, mask, amp = case.inputs()
-    eng = _engine(net, mask, amp, 1, case.t_steps, 64, refractory=case.refractory)
+    eng = _engine(net, mask, amp, 1, case.t_steps, 64, kind=case.kind, refractory=case.refractory,
+                  capacity=case.capacity, exact=case.exact)
     out = eng.forward()
     sp = eng.spikes()
     raster = np.stack([sp["step"], sp["neuron"]], 1)
@@ -183,17 +203,14 @@ def test_configuration_errors_name_the_edge():
 # ---------------------------------------------------------------- bounded kinds
 
 BOUNDED = ["dense_heap_n8", "dense_sorted_n8", "dense_fifo_n8", "dense_heap_cap3_n12", "dense_sorted_cap3_n12",
-           "dense_fifo_cap2_n12"]
+           "dense_fifo_cap2_n12", "dense_sorted_plain_cap3_n12"]
 
 
-def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=True):
-    from paper_2512_05906_b200.engine import Engine
-    eng = Engine(net.n, B, T, kind=kind, precision=precision, capacity=capacity or 0)
-    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
-    eng.set_drive(mask, amp)
+def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=True, exact=True):
+    eng = _engine(net, mask, amp, B, T, precision, kind=kind, capacity=capacity, exact=exact)
     out = eng.forward()
     s = OracleSession(n=net.n, n_trials=B, t_steps=T, kind=kind, mode="device", precision=precision,
-                      frac_bits=eng.frac_bits, capacity=capacity or 0)
+                      frac_bits=eng.frac_bits, capacity=capacity or 0, exact_delivery=exact)
     s.set_network(net.rowptr, net.col, net.weight, net.delay)
     s.set_drive(mask, amp)
     ref = s.forward()
@@ -213,7 +230,16 @@ def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=T
 def test_bounded_kinds_bitwise_vs_oracle(name, precision):
     case = BY_NAME[name]
     net, mask, amp = case.inputs()
-    _compare_bounded(net, mask, amp, 1, case.t_steps, precision, case.kind, case.capacity)
+    eng, out, _ = _compare_bounded(net, mask, amp, 1, case.t_steps, precision, case.kind, case.capacity,
+                                   exact=case.exact)
+    # reverse: bitwise at one trial, dropped events skipped exactly
+    vbar = (2.0 * (out["v"].double() - 0.25)).to(out["v"].dtype)
+    gw, gd, ga = (x.cpu().numpy() for x in eng.backward(vbar))
+    s = _oracle(net, mask, amp, 1, case.t_steps, precision, eng.frac_bits, kind=case.kind, capacity=case.capacity,
+                exact=case.exact)
+    s.forward()
+    ow, od, oa = s.backward(vbar.double().cpu().numpy())
+    assert np.array_equal(gw, ow) and np.array_equal(gd, od) and np.array_equal(ga, oa)
 
 
 @pytest.mark.parametrize("name", BOUNDED)
@@ -221,10 +247,7 @@ def test_bounded_fp64_vs_reference_fixture(name):
     case = BY_NAME[name]
     g = np.load(os.path.join(GOLDEN, name + ".npz"))
     net, mask, amp = case.inputs()
-    from paper_2512_05906_b200.engine import Engine
-    eng = Engine(net.n, 1, case.t_steps, kind=case.kind, precision=64, capacity=case.capacity or 0)
-    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
-    eng.set_drive(mask, amp)
+    eng = _engine(net, mask, amp, 1, case.t_steps, 64, kind=case.kind, capacity=case.capacity, exact=case.exact)
     out = eng.forward()
     sp = eng.spikes()
     raster = np.stack([sp["step"], sp["neuron"]], 1)

@@ -46,7 +46,8 @@ def _load(case):
 def _session(case, net, mask, amp, mode, precision=64, record_v=False, F=0):
     s = OracleSession(n=case.n, n_trials=1, t_steps=case.t_steps, kind=case.kind, mode=mode,
                       precision=precision, capacity=case.capacity or 0,
-                      refractory_steps=case.refractory, record_v=record_v, frac_bits=F)
+                      refractory_steps=case.refractory, record_v=record_v, frac_bits=F,
+                      exact_delivery=case.exact)
     s.set_network(net.rowptr, net.col, net.weight, net.delay)
     s.set_drive(mask, amp)
     return s
