@@ -84,6 +84,11 @@ struct BndArgs {
   unsigned* drop_bits;        // [drop_cap/32]
   long long drop_cap;
   int insert_first;           // first step whose arrivals this launch inserts
+  // shared-memory staged queues (eq_bq.cuh, capacity <= kBqMaxCap)
+  unsigned* keys;             // [B*N][C]
+  void* pay;                  // [B*N][C] fixed-point payloads
+  int C;                      // storage capacity (capacity rounded up to 4)
+  int lanes;                  // queues per warp batch
 };
 
 __device__ __forceinline__ bool key_less(int da, int sa, int db, int sb) {
@@ -262,6 +267,128 @@ __device__ __forceinline__ void insert_arrivals(const BndArgs<T>& A, int b, int 
   }
 }
 
+// Spike log of step m for this CTA (one chunk per (step, CTA)) and the fan-out
+// of its crossings: every event of edge x -> target j is appended to j's
+// arrival list for insertion by j's owner at phase m+1 (lossy ring: added
+// straight into the target's slot).  Shared by the bounded-kind kernels.
+template <typename T, int NT>
+__device__ __forceinline__ void bounded_log_fanout(const BndArgs<T>& A, const int m, const int cta, const int tid,
+                                                   const int nspk, const int b_first, SpikeRec<T>* s_spk,
+                                                   long long* s_r0, int* s_pre, SpikeRec<T>* spill, long long& s_off,
+                                                   unsigned long long (*s_ctr)[3]) {
+  typedef Prec<T> P;
+  constexpr int kCap = FwdShared<NT, T>::kCap;
+  constexpr int kTr = FwdShared<NT>::kTrials;
+  const FwdArgs<T>& F = A.f;
+  const StepConsts<T>& c = F.c;
+    // ---------------- spike log + event-id range for this (step, CTA)
+    if (tid == 0) {
+      unsigned long long off = nspk ? atomicAdd(F.log_count, (unsigned long long)nspk) : 0ULL;
+      if (nspk && (long long)(off + nspk) > F.log_cap) {
+        raise_error(F.err, EQ_ERR_CAPACITY, m, -1, -1);
+        off = 0;
+      }
+      s_off = (long long)off;
+      F.chunk_off[(size_t)m * F.G + cta] = (long long)off;
+      F.chunk_cnt[(size_t)m * F.G + cta] = nspk;
+    }
+    __syncthreads();
+    const bool log_ok = s_off + nspk <= F.log_cap;
+    if (log_ok)
+      for (int k = tid; k < nspk; k += NT) F.log[s_off + k] = k < kCap ? s_spk[k] : spill[k - kCap];
+    // ---------------- fan-out: stage each event at its in-edge slot
+    for (int k0 = 0; k0 < nspk; k0 += kCap) {
+      const int nb = nspk - k0 < kCap ? nspk - k0 : kCap;
+      __syncthreads();
+      if (k0 > 0)
+        for (int k = tid; k < nb; k += NT) s_spk[k] = spill[k0 - kCap + k];
+      __syncthreads();
+      for (int k = tid; k < nb; k += NT) {
+        const int b = c.divN.div(s_spk[k].idx);
+        const int i = s_spk[k].idx - b * F.N;
+        const long long r0 = __ldg(F.net.rowptr + i);
+        const int len = (int)(__ldg(F.net.rowptr + i + 1) - r0);
+        s_r0[k] = r0;
+        s_pre[k + 1] = len;
+        if (log_ok) {
+          F.log_r0[s_off + k0 + k] = r0;
+          F.log_len[s_off + k0 + k] = len;
+        }
+        const int tb = b - b_first;
+        if (tb < kTr) {
+          atomicAdd(&s_ctr[tb][0], 1ULL);
+          atomicAdd(&s_ctr[tb][1], (unsigned long long)len);
+        } else {
+          atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b), 1ULL);
+          atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 1), (unsigned long long)len);
+        }
+      }
+      __syncthreads();
+      warp0_scan(s_pre, nb);
+      __syncthreads();
+      const int total = s_pre[nb];
+      const int par = m & 1;
+      for (int f = tid; f < total; f += NT) {
+        const int k = find_row(s_pre, nb, f);
+        const int ro = f - s_pre[k];
+        const long long x = s_r0[k] + ro;
+        const SpikeRec<T> rec = s_spk[k];
+        const int b = c.divN.div(rec.idx);
+        const EdgeRec<T> ed = ld_edge(F.net.er + x);
+        const int jt = ed.col;
+        const T w = ed.w;
+        const T d = ed.d;
+        const T t_post = rec.t + d;
+        const int ds = delivery_step_coded(t_post, (unsigned short)ed.code, c.dt, m);
+        T ws, wm;
+        if (F.exact) {
+          const T phi = (T)ds * c.dt - t_post;
+          ws = w * eq_exp_t(-phi * c.inv_tau_s);
+          wm = w * eq_exp_t(-phi * c.inv_tau_m);
+        } else {
+          ws = w;
+          wm = (T)0;
+        }
+        const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
+        if (F.kind == EQ_KIND_LOSSYRING) {
+          // LossyRingQueue.enqueue (queues.py:160-176): slot = step % capacity,
+          // i.e. the event is popped at the first step >= now = m+1 in its due
+          // step's residue class; add straight into that slot (order-free fixed
+          // point).  The ring has capacity+1 physical slots so slot m, popped
+          // in this phase by other CTAs, is never a target here.
+          int off = ds - (m + 1);
+          if (off >= A.cap_ref) off %= A.cap_ref;
+          const int se = m + 1 + off;
+          long long* sl = F.ring + ((size_t)b * A.cap + (size_t)(se % A.cap)) * F.N * P::kSlotWords +
+                          (size_t)jt * P::kSlotWords;
+          if (P::kSlotWords == 1) {
+            red_add(sl, pack2(q1, q2));
+          } else {
+            red_add(sl, q1);
+            red_add(sl + 1, q2);
+          }
+          continue;
+        }
+        // append to the target's arrival list (slot from its counter; the
+        // segment holds all in-edges, so it cannot overflow)
+        const int slot = atomicAdd(A.acnt + ((size_t)par * F.B + b) * F.N + jt, 1);
+        Arrival<T> ar;
+        ar.x = (int)x;
+        ar.tag = (int)(s_off + k0 + k);
+        ar.due = ds;
+        ar.ro = ro;
+        if constexpr (sizeof(T) == 4) {
+          ar.p = pack2(q1, q2);
+          ar.pad = 0;
+        } else {
+          ar.ps = q1;
+          ar.pm = q2;
+        }
+        A.alist[((size_t)par * F.B + b) * A.E + __ldg(A.csc_off + jt) + slot] = ar;
+      }
+    }
+}
+
 template <typename T, int NT, int U>
 __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
   typedef Prec<T> P;
@@ -391,112 +518,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
     if (last) break;
     tl_mark(F.tl, m, F.G, cta, 1);
     const int nspk = s_n;
-    // ---------------- spike log + event-id range for this (step, CTA)
-    if (tid == 0) {
-      unsigned long long off = nspk ? atomicAdd(F.log_count, (unsigned long long)nspk) : 0ULL;
-      if (nspk && (long long)(off + nspk) > F.log_cap) {
-        raise_error(F.err, EQ_ERR_CAPACITY, m, -1, -1);
-        off = 0;
-      }
-      s_off = (long long)off;
-      F.chunk_off[(size_t)m * F.G + cta] = (long long)off;
-      F.chunk_cnt[(size_t)m * F.G + cta] = nspk;
-    }
-    __syncthreads();
-    const bool log_ok = s_off + nspk <= F.log_cap;
-    if (log_ok)
-      for (int k = tid; k < nspk; k += NT) F.log[s_off + k] = k < kCap ? s_spk[k] : spill[k - kCap];
-    // ---------------- fan-out: stage each event at its in-edge slot
-    for (int k0 = 0; k0 < nspk; k0 += kCap) {
-      const int nb = nspk - k0 < kCap ? nspk - k0 : kCap;
-      __syncthreads();
-      if (k0 > 0)
-        for (int k = tid; k < nb; k += NT) s_spk[k] = spill[k0 - kCap + k];
-      __syncthreads();
-      for (int k = tid; k < nb; k += NT) {
-        const int b = c.divN.div(s_spk[k].idx);
-        const int i = s_spk[k].idx - b * F.N;
-        const long long r0 = __ldg(F.net.rowptr + i);
-        const int len = (int)(__ldg(F.net.rowptr + i + 1) - r0);
-        s_r0[k] = r0;
-        s_pre[k + 1] = len;
-        if (log_ok) {
-          F.log_r0[s_off + k0 + k] = r0;
-          F.log_len[s_off + k0 + k] = len;
-        }
-        const int tb = b - b_first;
-        if (tb < kTr) {
-          atomicAdd(&s_ctr[tb][0], 1ULL);
-          atomicAdd(&s_ctr[tb][1], (unsigned long long)len);
-        } else {
-          atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b), 1ULL);
-          atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 1), (unsigned long long)len);
-        }
-      }
-      __syncthreads();
-      warp0_scan(s_pre, nb);
-      __syncthreads();
-      const int total = s_pre[nb];
-      const int par = m & 1;
-      for (int f = tid; f < total; f += NT) {
-        const int k = find_row(s_pre, nb, f);
-        const int ro = f - s_pre[k];
-        const long long x = s_r0[k] + ro;
-        const SpikeRec<T> rec = s_spk[k];
-        const int b = c.divN.div(rec.idx);
-        const EdgeRec<T> ed = ld_edge(F.net.er + x);
-        const int jt = ed.col;
-        const T w = ed.w;
-        const T d = ed.d;
-        const T t_post = rec.t + d;
-        const int ds = delivery_step_coded(t_post, (unsigned short)ed.code, c.dt, m);
-        T ws, wm;
-        if (F.exact) {
-          const T phi = (T)ds * c.dt - t_post;
-          ws = w * eq_exp_t(-phi * c.inv_tau_s);
-          wm = w * eq_exp_t(-phi * c.inv_tau_m);
-        } else {
-          ws = w;
-          wm = (T)0;
-        }
-        const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
-        if (F.kind == EQ_KIND_LOSSYRING) {
-          // LossyRingQueue.enqueue (queues.py:160-176): slot = step % capacity,
-          // i.e. the event is popped at the first step >= now = m+1 in its due
-          // step's residue class; add straight into that slot (order-free fixed
-          // point).  The ring has capacity+1 physical slots so slot m, popped
-          // in this phase by other CTAs, is never a target here.
-          int off = ds - (m + 1);
-          if (off >= A.cap_ref) off %= A.cap_ref;
-          const int se = m + 1 + off;
-          long long* sl = F.ring + ((size_t)b * A.cap + (size_t)(se % A.cap)) * F.N * P::kSlotWords +
-                          (size_t)jt * P::kSlotWords;
-          if (P::kSlotWords == 1) {
-            red_add(sl, pack2(q1, q2));
-          } else {
-            red_add(sl, q1);
-            red_add(sl + 1, q2);
-          }
-          continue;
-        }
-        // append to the target's arrival list (slot from its counter; the
-        // segment holds all in-edges, so it cannot overflow)
-        const int slot = atomicAdd(A.acnt + ((size_t)par * F.B + b) * F.N + jt, 1);
-        Arrival<T> ar;
-        ar.x = (int)x;
-        ar.tag = (int)(s_off + k0 + k);
-        ar.due = ds;
-        ar.ro = ro;
-        if constexpr (sizeof(T) == 4) {
-          ar.p = pack2(q1, q2);
-          ar.pad = 0;
-        } else {
-          ar.ps = q1;
-          ar.pm = q2;
-        }
-        A.alist[((size_t)par * F.B + b) * A.E + __ldg(A.csc_off + jt) + slot] = ar;
-      }
-    }
+    bounded_log_fanout<T, NT>(A, m, cta, tid, nspk, b_first, s_spk, s_r0, s_pre, spill, s_off, s_ctr);
     __syncthreads();
     tl_mark(F.tl, m, F.G, cta, 2);
     if (!grid_sync(F.bar, F.G, F.err, F.step_start + m + 1, F.log_count)) break;

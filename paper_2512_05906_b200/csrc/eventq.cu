@@ -17,6 +17,7 @@
 #include "eq_device.cuh"
 #include "eq_ring.cuh"
 #include "eq_bounded.cuh"
+#include "eq_bq.cuh"
 #include "eq_jvp.cuh"
 
 #include <cub/cub.cuh>
@@ -130,6 +131,10 @@ struct eq_handle {
   int* acnt = nullptr;         // [2][B][N] arrivals per target
   void* q = nullptr;
   int4* meta = nullptr;
+  bool staged = false;         // capacity <= kBqMaxCap: shared-memory staged queues (eq_bq.cuh)
+  int C = 0;                   // their storage capacity
+  unsigned* qkeys = nullptr;
+  void* qpay = nullptr;
   int maxdeg = 1;               // largest CSR row (bounded kinds: event id = log position * maxdeg + row offset)
   unsigned* drop_bits = nullptr;
   long long drop_cap = 0;
@@ -567,6 +572,9 @@ __global__ void k_add_lt(T* lt_rem, const long long* step_start, int lo, const T
 
 // ------------------------------------------------------------ launches
 
+// staged bounded-queue kernel: key staging of every warp
+constexpr size_t bq_smem() { return (size_t)(kNT / 32) * kBqWarpWords * sizeof(unsigned); }
+
 // reverse kernel dynamic smem: spiker bitmap + uint16 chunk position per owned neuron
 size_t bwd_smem(long long per) {
   return (size_t)((per + 31) / 32) * sizeof(unsigned) + (size_t)((per + 1) / 2) * sizeof(unsigned);
@@ -732,9 +740,19 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
     Bk.drop_bits = h->drop_bits;
     Bk.drop_cap = h->drop_cap;
     Bk.insert_first = h->steps_done;
+    Bk.keys = h->qkeys;
+    Bk.pay = h->qpay;
+    Bk.C = h->C;
+    Bk.lanes = h->C > 0 ? std::min(32, kBqWarpWords / h->C) : 0;
     void* bargs[] = {&Bk};
-    EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_forward_bounded<T, kNT, kU>, dim3(h->G), dim3(kNT),
-                                           bargs, 0, s));
+    if (h->staged) {
+      const void* kq = (const void*)k_forward_bq<T, kNT, kU>;
+      EQ_CUDA(h, cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bq_smem()));
+      EQ_CUDA(h, cudaLaunchCooperativeKernel(kq, dim3(h->G), dim3(kNT), bargs, bq_smem(), s));
+    } else {
+      EQ_CUDA(h, cudaLaunchCooperativeKernel((const void*)k_forward_bounded<T, kNT, kU>, dim3(h->G), dim3(kNT),
+                                             bargs, 0, s));
+    }
   } else {
     void* args[] = {&A};
     if (A.imp_n > 0) {   // other partitions' spikes of the last window, due >= m0+1
@@ -905,6 +923,11 @@ int setup_geometry(eq_handle* h) {
                                             : (const void*)k_forward_bounded<double, kNT, kU>;
     EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, kq, kNT, 0));
     occ_f = std::min(occ_f, occ_q);
+    const void* kb2 = h->cfg.precision == 32 ? (const void*)k_forward_bq<float, kNT, kU>
+                                             : (const void*)k_forward_bq<double, kNT, kU>;
+    EQ_CUDA(h, cudaFuncSetAttribute(kb2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bq_smem()));
+    EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, kb2, kNT, bq_smem()));
+    occ_f = std::min(occ_f, occ_q);
   }
   int occ = std::max(1, occ_f);
   for (; occ >= 1; --occ) {
@@ -979,7 +1002,15 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   h->launches += 1;
   EQ_CUDA(h, ensure(h, &h->alist, (size_t)2 * B * E * sizeof(Arrival<float>)));   // 32 bytes in both precisions
   EQ_CUDA(h, ensure(h, (void**)&h->acnt, (size_t)2 * B * N * sizeof(int)));
-  EQ_CUDA(h, ensure(h, &h->q, qbytes));
+  h->staged = h->cap <= kBqMaxCap;
+  if (h->staged) {
+    h->C = (h->cap + 3) / 4 * 4;
+    const size_t pb = c.precision == 32 ? sizeof(long long) : sizeof(longlong2);
+    EQ_CUDA(h, ensure(h, (void**)&h->qkeys, (size_t)B * N * h->C * sizeof(unsigned)));
+    EQ_CUDA(h, ensure(h, &h->qpay, (size_t)B * N * h->C * pb));
+  } else {
+    EQ_CUDA(h, ensure(h, &h->q, qbytes));
+  }
   EQ_CUDA(h, ensure(h, (void**)&h->meta, (size_t)B * N * sizeof(int4)));
   // one drop bit per possible event of a logged spike: grows with the log
   h->drop_cap = ((long long)h->log_cap * h->maxdeg + 31) / 32 * 32;
@@ -1284,7 +1315,10 @@ int eq_reset(eq_handle* h, void* stream) {
     const int B = h->cfg.n_trials, N = h->cfg.n_neurons;
     EQ_CUDA(h, cudaMemsetAsync(h->acnt, 0, (size_t)2 * B * N * sizeof(int), s));
     EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
-    k_meta_init<<<592, 256, 0, s>>>(h->meta, (long long)B * N);
+    if (h->staged)
+      k_meta_init_bq<<<592, 256, 0, s>>>(h->meta, (long long)B * N, h->cfg.kind == EQ_KIND_FIFORING);
+    else
+      k_meta_init<<<592, 256, 0, s>>>(h->meta, (long long)B * N);
     h->launches += 1;
   }
   h->steps_done = 0;
@@ -1703,6 +1737,13 @@ int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream) {
   if (h->lossy) {
     k_pending_lossy<<<592, 256, 0, s>>>(h->ring, h->cfg.precision == 32 ? 1 : 2, h->lossy_slots, B, N, H,
                                         h->steps_done, (long long*)buf);
+  } else if (h->bounded && h->staged) {
+    if (h->cfg.precision == 32)
+      k_pending_bq<float><<<592, 256, 0, s>>>(h->qkeys, (const long long*)h->qpay, h->meta, h->cfg.kind, h->C,
+                                               (long long)B * N, H, h->steps_done, (long long*)buf);
+    else
+      k_pending_bq<double><<<592, 256, 0, s>>>(h->qkeys, (const longlong2*)h->qpay, h->meta, h->cfg.kind, h->C,
+                                                (long long)B * N, H, h->steps_done, (long long*)buf);
   } else if (h->bounded) {
     if (h->cfg.precision == 32)
       k_pending_bounded<float><<<592, 256, 0, s>>>((const QEv<float>*)h->q, h->meta, h->cfg.kind, h->cap,
