@@ -180,6 +180,29 @@ int eq_get_import_adjoints(eq_handle* h, int32_t start_step, void* out, void* st
  * reverse window that contains those steps. */
 int eq_add_spike_adjoints(eq_handle* h, int32_t step_lo, const void* vals, int64_t n, void* stream);
 
+/* Device-resident exchange (no host round trip per window): the partitions
+ * read each other's spike logs and reverse import blocks directly — handles in
+ * one process, on one GPU or on several GPUs with P2P access over NVLink
+ * (enabled here).  peers[k] = partition k's handle (peers[me] == h); call on
+ * every partition after all eq_set_network calls.  Replaces the host-routed
+ * eq_export_spikes / eq_import_spikes / eq_get_import_adjoints /
+ * eq_add_spike_adjoints round trip. */
+int eq_set_peers(eq_handle* h, int32_t n_parts, eq_handle* const* peers, int32_t me);
+/* Forward window w: gather the other partitions' spikes of steps [a_prev,
+ * now) from their logs into import block w (w > 0), fan them out, run n_steps
+ * (0 = only deliver the last window's imports).  Asynchronous: window w of
+ * every partition must be ordered after window w-1 of all of them (one
+ * stream, or events); errors (a full spike log included) surface at eq_sync. */
+int eq_run_window(eq_handle* h, int32_t w, int32_t a_prev, int32_t n_steps, void* stream);
+/* Reverse window w over steps [m_lo, a_next): first the other partitions'
+ * partial dL/dt_spk of this partition's spikes of the window (their import
+ * block w+1, summed in partition order), then the reverse phases down to m_lo,
+ * then this partition's partials of its import block w.  Asynchronous, after
+ * eq_backward_begin; ordered like eq_run_window in reverse. */
+int eq_backward_window_peer(eq_handle* h, int32_t w, int32_t m_lo, int32_t a_next, void* stream);
+/* Wait for the stream and report the device error word of the asynchronous calls. */
+int eq_sync(eq_handle* h, void* stream);
+
 /* Host-side queries (synchronise the stream). */
 int eq_counters(eq_handle* h, int64_t* out /* [n_trials][3] spikes, events, drops */, void* stream);
 int64_t eq_spike_count(eq_handle* h, void* stream);

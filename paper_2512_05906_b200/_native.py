@@ -65,6 +65,10 @@ def lib() -> ctypes.CDLL:
         "eq_import_spikes": (ctypes.c_int, [H, vp, i64, vp]),
         "eq_get_import_adjoints": (ctypes.c_int, [H, i32, vp, vp]),
         "eq_add_spike_adjoints": (ctypes.c_int, [H, i32, vp, i64, vp]),
+        "eq_set_peers": (ctypes.c_int, [H, i32, vp, i32]),
+        "eq_run_window": (ctypes.c_int, [H, i32, i32, i32, vp]),
+        "eq_backward_window_peer": (ctypes.c_int, [H, i32, i32, i32, vp]),
+        "eq_sync": (ctypes.c_int, [H, vp]),
         "eq_counters": (ctypes.c_int, [H, vp, vp]),
         "eq_spike_count": (i64, [H, vp]),
         "eq_get_spikes": (ctypes.c_int, [H, vp, vp, vp, vp, vp]),
@@ -98,7 +102,8 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_network", "eq_set_drive", "eq_poisson_drive",
             "eq_reset", "eq_run", "eq_forward", "eq_backward", "eq_get_state", "eq_forward_jvp", "eq_backward_begin", "eq_backward_window",
             "eq_set_partition", "eq_set_frac_bits", "eq_export_spikes", "eq_import_spikes",
-            "eq_get_import_adjoints", "eq_add_spike_adjoints", "eq_counters", "eq_spike_count",
+            "eq_get_import_adjoints", "eq_add_spike_adjoints", "eq_set_peers", "eq_run_window",
+            "eq_backward_window_peer", "eq_sync", "eq_counters", "eq_spike_count",
             "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",
             "eq_launch_count", "eq_debug_timeline", "eq_log_capacity", "eq_debug_set_bucket_capacity",
             "eq_queues_create", "eq_queues_destroy",

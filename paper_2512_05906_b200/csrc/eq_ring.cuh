@@ -100,6 +100,8 @@ struct FwdArgs {
   const long long* imp_r0;
   const int* imp_len;
   long long imp_n;
+  const long long* imp_dev;  // peer exchange: {first, count} of the import block on the device (overrides imp_n)
+  int no_pause;              // asynchronous windows: a full spike log is an error, not a pause
 };
 
 template <int NT, typename T = float>
@@ -387,7 +389,12 @@ __global__ void __launch_bounds__(NT) k_import_fanout(FwdArgs<T> A) {
   const int cta = blockIdx.x;
   for (int k = threadIdx.x; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
   __syncthreads();
-  fwd_fanout<T, NT, NT, true>(A, A.m0, cta, threadIdx.x, A.imp_n * cta / A.G, A.imp_n * (cta + 1) / A.G, s_spk,
+  long long first = 0, n = A.imp_n;
+  if (A.imp_dev) {
+    first = A.imp_dev[0];
+    n = A.imp_dev[1];
+  }
+  fwd_fanout<T, NT, NT, true>(A, A.m0, cta, threadIdx.x, first + n * cta / A.G, first + n * (cta + 1) / A.G, s_spk,
                               s_r0, s_pre, s_bin);
   __syncthreads();
   for (int k = threadIdx.x; k < A.NB; k += NT) A.bk_cnt[(size_t)cta * A.NB + k] = s_bin[k];
@@ -729,6 +736,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   const int b_first = (int)(begin / A.N);
   const StepConsts<T> c = A.c;
   SpikeRec<T>* spill = A.scratch + (size_t)cta * A.per;
+  if (A.no_pause && ld_volatile(A.err) != 0) return;   // an earlier asynchronous window failed
 
   if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
   if (A.kind == EQ_KIND_RING)
@@ -824,7 +832,13 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
       break;
     tl_mark(A.tl, m, A.G, cta, 3);
     if (ld_volatile(A.err) != 0) break;
-    if (m + 1 < m1 && pause_due(A, m)) m1 = m + 1;   // same published value on every CTA
+    if (m + 1 < m1 && pause_due(A, m)) {             // same published value on every CTA
+      if (A.no_pause) {
+        raise_error(A.err, EQ_ERR_CAPACITY, m + 1, -1, -1);
+        break;
+      }
+      m1 = m + 1;
+    }
   }
   if (cta == 0 && tid == 0) A.err[4] = m1;            // the step this launch reached
   __syncthreads();
@@ -885,6 +899,7 @@ struct BwdArgs {
   const long long* imp_r0;
   const int* imp_len;
   long long imp_n;
+  const long long* imp_dev;     // peer exchange: {first, count} of the import block on the device
   T* imp_lt;
   unsigned long long* tl;  // debug timeline [m][G][4] or null
   int* err;
@@ -1314,8 +1329,13 @@ __global__ void __launch_bounds__(NT) k_import_rfanout(BwdArgs<T> A) {
   __shared__ T s_lt[kCapB];
   __shared__ T s_gtp[kEv];
   const int cta = blockIdx.x;
-  bwd_rfanout<T, NT, NT, true, kCapB, kEv>(A, A.m_lo, cta, threadIdx.x, A.imp_n * cta / A.G,
-                                           A.imp_n * (cta + 1) / A.G, s_rec, s_r0, s_pre, s_lt, s_gtp);
+  long long first = 0, n = A.imp_n;
+  if (A.imp_dev) {
+    first = A.imp_dev[0];
+    n = A.imp_dev[1];
+  }
+  bwd_rfanout<T, NT, NT, true, kCapB, kEv>(A, A.m_lo, cta, threadIdx.x, first + n * cta / A.G,
+                                           first + n * (cta + 1) / A.G, s_rec, s_r0, s_pre, s_lt, s_gtp);
 }
 
 }  // namespace eq

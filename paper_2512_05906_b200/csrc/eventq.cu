@@ -155,6 +155,14 @@ struct eq_handle {
   long long imp_cap = 0, imp_n = 0;
   std::vector<std::array<long long, 4>> imp_blocks;   // {forward launch start step, first, count, fanned out}
   void* lt_rem = nullptr;             // [log_cap] other partitions' dL/dt_spk of own spikes
+  // device-resident peer exchange (eq_set_peers): the partitions read each
+  // other's spike logs and import-adjoint blocks directly (same GPU, or peers
+  // with P2P access over NVLink); no host round trip per window
+  bool peer_mode = false;
+  int peer_me = -1;
+  std::vector<eq_handle*> peers;
+  long long* peer_blk = nullptr;      // [t_cap + 2][2] {first, count} of import block w
+  long long* peer_count = nullptr;    // imports so far (device)
   // reverse pass in windows (eq_backward_begin / eq_backward_window)
   int bwd_cursor = -1;
   double* bw_gw = nullptr;
@@ -562,6 +570,105 @@ __global__ void k_import(const ExRec<T>* in, long long n, const int64_t* rowptr,
   }
 }
 
+// ------------------------------------------------------------ peer exchange (device-resident)
+
+constexpr int kMaxPeers = 16;
+// What a partition's kernels read of every partition (its own entry included):
+// spike log + step index (forward import), import adjoints + block index
+// (reverse).  Device pointers; with several GPUs these are peer addresses
+// reached over NVLink (cudaDeviceEnablePeerAccess in eq_set_peers).
+struct PeerDesc {
+  const void* log;               // SpikeRec<T>[log_cap]
+  const long long* step_start;   // [t_cap + 1]
+  const void* imp_lt;            // T[imp_cap]: partial dL/dt_spk of its imports
+  const long long* blk;          // [t_cap + 2][2] {first, count} of its import block w
+  int N, src_off;
+};
+struct PeerTable {
+  PeerDesc d[kMaxPeers];
+  int P, me;
+};
+
+// Import block of window w for partition `me`: the other partitions' spikes
+// of steps [a_prev, a) read straight from their logs, in partition order then
+// log order, appended at *count as fan-out records (idx = trial base, a = emit
+// step, CSR row of the global source in this partition's CSR).
+template <typename T>
+__global__ void k_gather_peers(PeerTable tab, int a_prev, int a, int N_me, const int64_t* rowptr, SpikeRec<T>* imp,
+                               long long* imp_r0, int* imp_len, const long long* count, long long cap, int* err) {
+  const long long base = *count;
+  long long off[kMaxPeers + 1];
+  off[0] = 0;
+  for (int q = 0; q < tab.P; ++q) {
+    long long n = 0;
+    if (q != tab.me) n = tab.d[q].step_start[a] - tab.d[q].step_start[a_prev];
+    off[q + 1] = off[q] + n;
+  }
+  const long long total = off[tab.P];
+  if (base + total > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(err, EQ_ERR_CAPACITY, a, -1, -1);
+    return;
+  }
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < total;
+       r += (long long)gridDim.x * blockDim.x) {
+    int q = 0;
+    while (off[q + 1] <= r) ++q;
+    const PeerDesc& d = tab.d[q];
+    const long long pos = d.step_start[a_prev] + (r - off[q]);
+    const SpikeRec<T> rec = static_cast<const SpikeRec<T>*>(d.log)[pos];
+    int lo = a_prev, hi = a;                         // emit step: largest m with step_start[m] <= pos
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (d.step_start[mid] <= pos) lo = mid;
+      else hi = mid;
+    }
+    const int trial = rec.idx / d.N;
+    const int src = d.src_off + (rec.idx - trial * d.N);
+    SpikeRec<T> o{};
+    o.idx = trial * N_me;
+    o.t = rec.t;
+    o.a = (T)lo;                                     // exact: steps < 2^24
+    imp[base + r] = o;
+    const long long r0 = rowptr[src];
+    imp_r0[base + r] = r0;
+    imp_len[base + r] = (int)(rowptr[src + 1] - r0);
+  }
+}
+
+__global__ void k_gather_commit(PeerTable tab, int a_prev, int a, long long* count, long long* blk) {
+  long long total = 0;
+  for (int q = 0; q < tab.P; ++q)
+    if (q != tab.me) total += tab.d[q].step_start[a] - tab.d[q].step_start[a_prev];
+  blk[0] = *count;
+  blk[1] = total;
+  *count += total;
+}
+
+// Before partition me's reverse window over steps [a, a_next): the other
+// partitions' partial dL/dt_spk of its spikes of those steps, which each of
+// them computed in import block w+1 (their imports of this window); summed in
+// partition order into lt_rem (the order the host-routed exchange uses).
+template <typename T>
+__global__ void k_sum_peer_adjoints(PeerTable tab, int w, int a, int a_next, T* lt_rem) {
+  const PeerDesc& mine = tab.d[tab.me];
+  const long long k0 = mine.step_start[a], n = mine.step_start[a_next] - k0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    T acc = (T)0;
+    bool first = true;
+    for (int p = 0; p < tab.P; ++p) {
+      if (p == tab.me) continue;
+      long long off = tab.d[p].blk[2 * (w + 1)];     // p's block w+1 holds the others' spikes of [a, a_next)
+      for (int q = 0; q < tab.me; ++q)
+        if (q != p) off += tab.d[q].step_start[a_next] - tab.d[q].step_start[a];
+      const T v = static_cast<const T*>(tab.d[p].imp_lt)[off + k];
+      acc = first ? v : acc + v;
+      first = false;
+    }
+    lt_rem[k0 + k] = (T)0 + acc;
+  }
+}
+
 template <typename T>
 __global__ void k_add_lt(T* lt_rem, const long long* step_start, int lo, const T* vals, long long n) {
   const long long k0 = step_start[lo];
@@ -669,10 +776,9 @@ int grow_log(eq_handle* h, long long need, cudaStream_t s) {
   return EQ_OK;
 }
 
-// One persistent launch over steps [steps_done, steps_done + n_steps); it may
-// end early at a step boundary when the spike log could overflow (*reached).
+// Kernel arguments of a forward launch over steps [steps_done, steps_done + n_steps).
 template <typename T>
-int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s, int* reached) {
+FwdArgs<T> fwd_args(eq_handle* h, int n_steps, void* v_trace) {
   FwdArgs<T> A;
   A.N = h->cfg.n_neurons;
   A.B = h->cfg.n_trials;
@@ -714,6 +820,19 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
   A.imp_r0 = nullptr;
   A.imp_len = nullptr;
   A.imp_n = 0;
+  A.imp_dev = nullptr;
+  A.no_pause = 0;
+  A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
+  A.err = h->err_dev;
+  A.bar = h->bar;
+  return A;
+}
+
+// One persistent launch over steps [steps_done, steps_done + n_steps); it may
+// end early at a step boundary when the spike log could overflow (*reached).
+template <typename T>
+int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s, int* reached) {
+  FwdArgs<T> A = fwd_args<T>(h, n_steps, v_trace);
   std::array<long long, 4>* blk = find_block(h, h->steps_done);
   if (blk && !(*blk)[3]) {
     (*blk)[3] = 1;
@@ -722,9 +841,6 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
     A.imp_len = h->imp_len + (*blk)[1];
     A.imp_n = (*blk)[2];
   }
-  A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
-  A.err = h->err_dev;
-  A.bar = h->bar;
   if (h->bounded || h->lossy) {
     BndArgs<T> Bk;
     Bk.f = A;
@@ -830,7 +946,7 @@ int backward_begin(eq_handle* h, const void* v_bar, const void* i_bar, double* g
 
 // Reverse phases bwd_cursor-1 .. m_lo in one persistent launch.
 template <typename T>
-int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
+int launch_backward(eq_handle* h, int m_lo, cudaStream_t s, int peer_win = -1) {
   typedef typename Prec<T>::T2 T2;
   const int N = h->cfg.n_neurons, B = h->cfg.n_trials;
   EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
@@ -871,8 +987,15 @@ int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
   A.imp_r0 = nullptr;
   A.imp_len = nullptr;
   A.imp_n = 0;
+  A.imp_dev = nullptr;
   A.imp_lt = nullptr;
-  if (std::array<long long, 4>* blk = find_block(h, m_lo)) {
+  if (peer_win > 0) {                                 // peer exchange: the block is on the device
+    A.imp = (const SpikeRec<T>*)h->imp;
+    A.imp_r0 = h->imp_r0;
+    A.imp_len = h->imp_len;
+    A.imp_lt = (T*)h->imp_lt;
+    A.imp_dev = h->peer_blk + 2 * peer_win;
+  } else if (std::array<long long, 4>* blk = find_block(h, m_lo)) {
     A.imp = (const SpikeRec<T>*)h->imp + (*blk)[1];
     A.imp_r0 = h->imp_r0 + (*blk)[1];
     A.imp_len = h->imp_len + (*blk)[1];
@@ -889,7 +1012,7 @@ int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
   EQ_CUDA(h, cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   EQ_CUDA(h, cudaLaunchCooperativeKernel(kb, dim3(h->G), dim3(kNT), args, smem, s));
   h->launches += 1;
-  if (A.imp_n > 0) {   // partial dL/dt_spk of the imported spikes (reverse slots >= m_lo final)
+  if (A.imp_n > 0 || A.imp_dev) {   // partial dL/dt_spk of the imported spikes (reverse slots >= m_lo final)
     BwdArgs<T> Ai = A;
     Ai.tl = nullptr;
     k_import_rfanout<T, kNT><<<h->G, kNT, 0, s>>>(Ai);
@@ -900,6 +1023,7 @@ int launch_backward(eq_handle* h, int m_lo, cudaStream_t s) {
     k_sum_trials<T><<<(N + 255) / 256, 256, 0, s>>>(h->gamp_bt, B, N, h->bw_gamp);
     h->launches += 1;
   }
+  if (peer_win >= 0) return EQ_OK;   // asynchronous windows: errors surface at eq_sync
   return check_err(h, s);
 }
 
@@ -1666,6 +1790,151 @@ int eq_get_import_adjoints(eq_handle* h, int32_t start_step, void* out, void* st
   EQ_CUDA(h, cudaMemcpyAsync(out, (char*)h->imp_lt + (*blk)[1] * h->tsize, (size_t)(*blk)[2] * h->tsize,
                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return EQ_OK;
+}
+
+}  // extern "C"
+
+namespace {
+PeerTable peer_table(const eq_handle* h) {
+  PeerTable t{};
+  t.P = (int)h->peers.size();
+  t.me = h->peer_me;
+  for (int q = 0; q < t.P; ++q) {
+    const eq_handle* p = h->peers[q];
+    t.d[q].log = p->log;
+    t.d[q].step_start = p->step_start;
+    t.d[q].imp_lt = p->imp_lt;
+    t.d[q].blk = p->peer_blk;
+    t.d[q].N = p->cfg.n_neurons;
+    t.d[q].src_off = p->src_off;
+  }
+  return t;
+}
+}  // namespace
+
+extern "C" {
+
+int eq_set_peers(eq_handle* h, int32_t n_parts, eq_handle* const* peers, int32_t me) {
+  if (!h || !peers) return EQ_ERR_CONFIGURATION;
+  if (n_parts < 2 || n_parts > kMaxPeers || me < 0 || me >= n_parts || peers[me] != h)
+    return fail(h, EQ_ERR_CONFIGURATION, "peer table: 2.." + std::to_string(kMaxPeers) +
+                                             " partitions, this handle at index `me`");
+  if (!h->partitioned || !h->net_set) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_partition and eq_set_network first");
+  long long cap = 0;
+  for (int q = 0; q < n_parts; ++q) {
+    const eq_handle* p = peers[q];
+    if (!p || !p->partitioned || !p->net_set || p->cfg.precision != h->cfg.precision ||
+        p->cfg.n_trials != h->cfg.n_trials || p->n_src != h->n_src)
+      return fail(h, EQ_ERR_CONFIGURATION, "peer " + std::to_string(q) + " is not a partition of the same network");
+    if (q != me) cap += p->log_cap;
+  }
+  DeviceGuard g(h->device);
+  for (int q = 0; q < n_parts; ++q) {   // other GPUs' memory over NVLink
+    if (peers[q]->device == h->device) continue;
+    cudaError_t e = cudaDeviceEnablePeerAccess(peers[q]->device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) return cuda_fail(h, e, "cudaDeviceEnablePeerAccess");
+  }
+  // imports can never exceed the other partitions' logs together
+  const size_t rec = h->cfg.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
+  if (cap + 1 > h->imp_cap) {
+    release(h, h->imp);
+    release(h, h->imp_r0);
+    release(h, h->imp_len);
+    release(h, h->imp_lt);
+    EQ_CUDA(h, alloc(h, &h->imp, (size_t)(cap + 1) * rec));
+    EQ_CUDA(h, alloc(h, (void**)&h->imp_r0, (size_t)(cap + 1) * sizeof(long long)));
+    EQ_CUDA(h, alloc(h, (void**)&h->imp_len, (size_t)(cap + 1) * sizeof(int)));
+    EQ_CUDA(h, alloc(h, &h->imp_lt, (size_t)(cap + 1) * h->tsize));
+    h->imp_cap = cap + 1;
+  }
+  EQ_CUDA(h, ensure(h, (void**)&h->peer_blk, (size_t)(h->t_cap + 2) * 2 * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, (void**)&h->peer_count, sizeof(long long)));
+  EQ_CUDA(h, cudaMemset(h->peer_blk, 0, (size_t)(h->t_cap + 2) * 2 * sizeof(long long)));
+  EQ_CUDA(h, cudaMemset(h->peer_count, 0, sizeof(long long)));
+  h->peers.assign(peers, peers + n_parts);
+  h->peer_me = me;
+  h->peer_mode = true;
+  h->imp_n = 0;
+  h->imp_blocks.clear();
+  return EQ_OK;
+}
+
+int eq_run_window(eq_handle* h, int32_t w, int32_t a_prev, int32_t n_steps, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (!h->peer_mode) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_peers must come first");
+  if (n_steps < 0 || w < 0 || w > h->t_cap + 1 || (w > 0 && (a_prev < 0 || a_prev >= h->steps_done)))
+    return fail(h, EQ_ERR_CONFIGURATION, "bad window");
+  if (h->steps_done + n_steps > h->t_cap)
+    return fail(h, EQ_ERR_CONFIGURATION, "window beyond the run's t_steps");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (w == 0) EQ_CUDA(h, cudaMemsetAsync(h->peer_count, 0, sizeof(long long), s));
+  const PeerTable tab = peer_table(h);
+  const bool f32 = h->cfg.precision == 32;
+  if (w > 0) {
+    if (f32)
+      k_gather_peers<float><<<h->G, 256, 0, s>>>(tab, a_prev, h->steps_done, h->cfg.n_neurons, h->rowptr,
+                                                 (SpikeRec<float>*)h->imp, h->imp_r0, h->imp_len, h->peer_count,
+                                                 h->imp_cap, h->err_dev);
+    else
+      k_gather_peers<double><<<h->G, 256, 0, s>>>(tab, a_prev, h->steps_done, h->cfg.n_neurons, h->rowptr,
+                                                  (SpikeRec<double>*)h->imp, h->imp_r0, h->imp_len, h->peer_count,
+                                                  h->imp_cap, h->err_dev);
+    k_gather_commit<<<1, 1, 0, s>>>(tab, a_prev, h->steps_done, h->peer_count, h->peer_blk + 2 * w);
+    h->launches += 2;
+  }
+  auto launch = [&](auto tag) -> int {
+    typedef decltype(tag) T;
+    FwdArgs<T> A = fwd_args<T>(h, n_steps, nullptr);
+    A.no_pause = 1;
+    if (w > 0) {
+      A.imp = (const SpikeRec<T>*)h->imp;
+      A.imp_r0 = h->imp_r0;
+      A.imp_len = h->imp_len;
+      A.imp_dev = h->peer_blk + 2 * w;
+      FwdArgs<T> Ai = A;
+      Ai.tl = nullptr;
+      k_import_fanout<T, kNT><<<h->G, kNT, 0, s>>>(Ai);
+      h->launches += 1;
+    }
+    if (n_steps == 0) return EQ_OK;
+    EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->step_start + h->steps_done + 1, 0xFF, (size_t)n_steps * sizeof(long long), s));
+    void* args[] = {&A};
+    const void* kf = (const void*)k_forward<T, kNT, kU, split_f<T>()>;
+    EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, 0, s));
+    h->launches += 1;
+    h->steps_done += n_steps;
+    return EQ_OK;
+  };
+  return f32 ? launch(float()) : launch(double());
+}
+
+int eq_backward_window_peer(eq_handle* h, int32_t w, int32_t m_lo, int32_t a_next, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (!h->peer_mode) return fail(h, EQ_ERR_CONFIGURATION, "eq_set_peers must come first");
+  if (h->bwd_cursor < 0) return fail(h, EQ_ERR_CONFIGURATION, "eq_backward_begin must come first");
+  if (m_lo < 0 || m_lo >= h->bwd_cursor || a_next < m_lo || a_next > h->steps_done)
+    return fail(h, EQ_ERR_CONFIGURATION, "bad reverse window");
+  DeviceGuard g(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const PeerTable tab = peer_table(h);
+  const bool f32 = h->cfg.precision == 32;
+  if (a_next > m_lo && a_next < h->steps_done) {   // the others' partials of this window's spikes
+    if (f32)
+      k_sum_peer_adjoints<float><<<h->G, 256, 0, s>>>(tab, w, m_lo, a_next, (float*)h->lt_rem);
+    else
+      k_sum_peer_adjoints<double><<<h->G, 256, 0, s>>>(tab, w, m_lo, a_next, (double*)h->lt_rem);
+    h->launches += 1;
+  }
+  return f32 ? launch_backward<float>(h, m_lo, s, w) : launch_backward<double>(h, m_lo, s, w);
+}
+
+int eq_sync(eq_handle* h, void* stream) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  DeviceGuard g(h->device);
+  return check_err(h, (cudaStream_t)stream);
 }
 
 int eq_add_spike_adjoints(eq_handle* h, int32_t step_lo, const void* vals, int64_t n, void* stream) {

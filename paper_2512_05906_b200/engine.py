@@ -236,6 +236,26 @@ class Engine:
         self._adj_keep = v
         _native.check(self.h, self.L.eq_add_spike_adjoints(self.h, int(step_lo), _ptr(v), v.numel(), self.stream))
 
+    # ------------------------------------------------------------ device-resident peer exchange
+    def set_peers(self, engines, me: int) -> None:
+        """Partitions of one network that read each other's spike logs directly
+        (eq_set_peers): engines[k] is partition k, this engine is engines[me]."""
+        arr = (ctypes.c_void_p * len(engines))(*[e.h.value for e in engines])
+        self._peers = list(engines)
+        _native.check(self.h, self.L.eq_set_peers(self.h, len(engines), arr, int(me)))
+
+    def run_window(self, w: int, a_prev: int, n_steps: int) -> None:
+        self.run_id += 1
+        _native.check(self.h, self.L.eq_run_window(self.h, int(w), int(a_prev), int(n_steps), self.stream))
+
+    def backward_window_peer(self, w: int, m_lo: int, a_next: int) -> None:
+        _native.check(self.h, self.L.eq_backward_window_peer(self.h, int(w), int(m_lo), int(a_next), self.stream))
+
+    def sync(self) -> None:
+        """Wait for this engine's stream; raise the device error of any
+        asynchronous window."""
+        _native.check(self.h, self.L.eq_sync(self.h, self.stream))
+
     # ------------------------------------------------------------ queries
     def counters(self) -> np.ndarray:
         out = np.empty((self.B, 3), dtype=np.int64)

@@ -128,6 +128,18 @@ class LocalTransport:
         self.parts = parts
 
 
+class PeerTransport:
+    """All partitions in this process with the device-resident exchange
+    (eq_set_peers): each partition's kernels read the other partitions' spike
+    logs (forward) and import-adjoint blocks (reverse) directly — on one GPU,
+    or on several with P2P access over NVLink — so the window loop makes no
+    host round trip and no copy: windows are ordered by the stream (one device)
+    or by CUDA events (several)."""
+
+    def __init__(self, parts: int):
+        self.parts = parts
+
+
 class DistTransport:
     """One partition per process over torch.distributed (NCCL on B200)."""
 
@@ -182,12 +194,32 @@ class PartitionedNetwork:
         self.tp = transport
         self.P = transport.parts
         self.W = int(window)
-        if isinstance(transport, LocalTransport) and self.ranks != list(range(self.P)):
+        if isinstance(transport, (LocalTransport, PeerTransport)) and self.ranks != list(range(self.P)):
             raise ConfigurationError("a local transport needs every partition")
+        self.peer = isinstance(transport, PeerTransport)
+        if self.peer:
+            for k, e in enumerate(self.engines):
+                e.set_peers(self.engines, k)
         self.counts: List[List[int]] = []     # per forward window: export count of every partition
         self.win: List[Tuple[int, int]] = []
 
     # -- collectives over the partitions, whatever the transport
+    def _order(self) -> None:
+        """Peer exchange on several devices: every partition's next window
+        starts after every partition's current one (events, no host wait)."""
+        devs = {e.device for e in self.engines}
+        if len(devs) < 2:
+            return
+        evs = []
+        for e in self.engines:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(e.device))
+            evs.append(ev)
+        for e in self.engines:
+            st = torch.cuda.current_stream(e.device)
+            for ev in evs:
+                st.wait_event(ev)
+
     def _gather(self, mine: List[torch.Tensor]) -> List[torch.Tensor]:
         if isinstance(self.tp, LocalTransport):
             return mine
@@ -206,6 +238,17 @@ class PartitionedNetwork:
         for e in self.engines:
             e.reset()
         self.counts, self.win = [], windows(t_steps, self.W)
+        if self.peer:
+            for w, (a, b) in enumerate(self.win):
+                a_prev = self.win[w - 1][0] if w else 0
+                for e in self.engines:
+                    e.run_window(w, a_prev, b - a)
+                self._order()
+            for e in self.engines:          # deliver the last window's spikes (queue contents)
+                e.run_window(len(self.win), self.win[-1][0], 0)
+            for e in self.engines:
+                e.sync()
+            return
         for a, b in self.win:
             for e in self.engines:
                 e.run(b - a)
@@ -220,6 +263,16 @@ class PartitionedNetwork:
 
     def backward(self, v_bars: Sequence[torch.Tensor], want_amp: bool = True):
         grads = [e.backward_begin(vb, None, want_amp) for e, vb in zip(self.engines, v_bars)]
+        if self.peer:
+            self._order()
+            for w in range(len(self.win) - 1, -1, -1):
+                a, b = self.win[w]
+                for e in self.engines:
+                    e.backward_window_peer(w, a, b)
+                self._order()
+            for e in self.engines:
+                e.sync()
+            return grads
         for wi in range(len(self.win) - 1, -1, -1):
             a, _ = self.win[wi]
             for e in self.engines:

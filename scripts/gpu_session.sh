@@ -1,8 +1,28 @@
-set -x
+#!/bin/bash
+# One gpurun session.  Usage: bash scripts/gpu_session.sh TAG [parts...]
+#   parts: tests (full -m gpu suite), bench (short C3 bench line), variants (C2 + C4 sweep)
+TAG=${1:-r2}; shift
+PARTS=${@:-tests bench}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1500 python -m pytest tests -m gpu -q -x --durations=25 --ignore=tests/test_gpu_parity_r2.py > gpurun_out/r2a_gpu_main.log 2>&1; echo "main rc=$?"
-tail -30 gpurun_out/r2a_gpu_main.log
-timeout 1800 python -m pytest tests/test_gpu_parity_r2.py -m gpu -q --durations=25 > gpurun_out/r2a_gpu_r2.log 2>&1; echo "r2 rc=$?"
-tail -40 gpurun_out/r2a_gpu_r2.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/r2a_bench.log 2>&1; echo "bench rc=$?"
-tail -3 gpurun_out/r2a_bench.log
+for p in $PARTS; do
+  case $p in
+    tests)
+      timeout 2400 python -m pytest tests -m gpu -q --durations=15 > gpurun_out/${TAG}_gpu_tests.log 2>&1
+      echo "tests rc=$?"; tail -25 gpurun_out/${TAG}_gpu_tests.log ;;
+    quick)
+      timeout 1200 python -m pytest tests -m gpu -q -x --durations=10 --deselect tests/test_gpu_parity_r2.py::test_c4_full_size_bounded_with_drops_bitwise > gpurun_out/${TAG}_gpu_quick.log 2>&1
+      echo "quick rc=$?"; tail -25 gpurun_out/${TAG}_gpu_quick.log ;;
+    bench)
+      timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/${TAG}_bench.log 2>&1
+      echo "bench rc=$?"; tail -1 gpurun_out/${TAG}_bench.log ;;
+    variants)
+      C4=1 timeout 2400 bash scripts/variant_sweep.sh gpurun_out/${TAG}_variants.jsonl 3 3
+      echo "variants rc=$?"
+      python -c "
+import json
+for l in open('gpurun_out/${TAG}_variants.jsonl'):
+    d=json.loads(l); r=d['roofline']; c=d['config']
+    print(c['workload'][:70], '%.3e'%d['value'], 'fwd %.1f bwd %.1f frac %.3f drops %d'%(r['fwd_ms'], r['bwd_ms'], r['frac'], c['drops_per_gpu']))
+" ;;
+  esac
+done

