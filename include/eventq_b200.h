@@ -75,6 +75,9 @@ typedef struct eq_config {
   int32_t capacity;         /* bounded kinds: events per queue; 0 = reference default */
   int64_t max_spikes;       /* spike-log capacity over the run; 0 = default */
   double dt, tau_m, tau_syn, v_th, v_reset;
+  int32_t max_ctas;         /* persistent grid size cap (0 = 2 per SM); partitions that run
+                               concurrently on one GPU split its SMs this way */
+  int32_t reserved;
 } eq_config;
 
 typedef struct eq_handle eq_handle;

@@ -88,7 +88,7 @@ struct BndArgs {
   unsigned* keys;             // [B*N][C]
   void* pay;                  // [B*N][C] fixed-point payloads
   int C;                      // storage capacity (capacity rounded up to 4)
-  int lanes;                  // queues per warp batch
+  int* qdue;                  // [B*N] next due step of each queue
 };
 
 __device__ __forceinline__ bool key_less(int da, int sa, int db, int sb) {

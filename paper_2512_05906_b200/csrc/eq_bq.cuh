@@ -1,30 +1,34 @@
 // eq_bq.cuh — the bounded queue kinds, FIFORing (queues.py:184-260),
-// BinaryHeap (queues.py:481-571) and SortedArray (queues.py:308-403), as
-// per-neuron queues STAGED IN SHARED MEMORY for each step's operations and
-// kept in HBM between steps (capacities up to kBqMaxCap; larger ones use the
-// HBM-resident structures of eq_bounded.cuh).
+// BinaryHeap (queues.py:481-571) and SortedArray (queues.py:308-403), for
+// capacities up to kBqMaxCap: per-neuron queues kept in HBM between steps and
+// STAGED IN SHARED MEMORY for each step's operations (larger capacities use
+// the HBM-resident structures of eq_bounded.cuh).
 //
 // Queue q = trial * N + j, storage capacity C (the capacity rounded up to 4):
-//   keys[q][C]  uint32 (due mod 2^24) << 8 | slot   — the structure itself
-//                (binary min-heap on due / circular sorted array / circular FIFO)
+//   keys[q][C]  uint32 (due mod 2^24) << 8 | slot, entries [0, count):
+//               binary min-heap on due / array sorted by due (stable) / FIFO
+//               in arrival order — only these 4-byte keys move
 //   pay[q][C]   fixed-point payload of slot s (fp32: packed (qm << 32) + qs;
-//                fp64: {qs, qm}); heap and sorted keep payloads in place and move
-//                only 4-byte keys; FIFO's slot is its circular position
-//   meta[q]     int4 {count | head << 16, next due, free-slot mask lo / FIFO tail
-//                key, free-slot mask hi}
+//               fp64: {qs, qm}), written once at insert, read once at pop
+//   meta[q]     int4 {count, occupied-slot mask lo, mask hi, FIFO tail key}
+//   qdue[q]     the queue's next due step (INT_MAX when empty)
 //
-// Phase m, warp-cooperative: a warp takes a batch of L consecutive queues (one
-// per lane).  The lanes whose queue will change this step (arrivals that can
-// be accepted, or a pop due) copy its key array into the warp's shared-memory
-// staging area with cp.async, all at once — one memory round trip for the
-// batch instead of one per heap level / shifted entry — then insert the
-// arrivals of step m-1 in ascending edge order (the reference's source order,
-// with its accept-while-not-full rule: queues.py:225-226, :514-515, :344-345),
-// pop every event due at m, sum the popped payloads (loaded in groups, not one
-// dependent load per entry) and write the staged keys back.  A full queue
-// drops its arrivals without being staged.  Because pops sum fixed-point
-// payloads, ties among equal due steps may sit in any order: the accepted sets,
-// popped sums and pending contents equal the reference's (tests/).
+// Phase m of k_forward_bq, one grid barrier per step:
+//   1. queue pass, over the CTA's queues in chunks: a vectorised scan of qdue
+//      and the arrival counters finds the busy queues (a pop due at m, or
+//      arrivals of step m-1) and compacts them into a shared-memory list;
+//      rounds of one busy queue per thread then stage its keys with cp.async
+//      (every thread's copies in flight at once), insert the arrivals in
+//      ascending edge order with the reference's accept-while-not-full rule
+//      (queues.py:225-226, :514-515, :344-345), pop every event due at m, sum
+//      the popped payloads into the step's accumulator acc[m & 1] and write
+//      the keys back.  A full queue drops its arrivals without being staged.
+//   2. neuron pass: eq_ring.cuh's neuron_side (vectorised LIF over all owned
+//      neurons, popping acc[m & 1]) — the ring kind's code, unchanged.
+//   3. fan-out of the CTA's own crossings of step m (from its log chunk) into
+//      the targets' arrival lists, for insertion at phase m+1.
+// Pops sum fixed-point payloads, so ties among equal due steps may sit in any
+// order: accepted sets, popped sums and pending contents equal the reference's.
 #pragma once
 
 #include "eq_bounded.cuh"
@@ -32,7 +36,6 @@
 namespace eq {
 
 constexpr int kBqMaxCap = 64;         // largest capacity staged in shared memory
-constexpr int kBqWarpWords = 1024;    // staging words per warp (4 KB)
 
 template <typename T> struct BqPay;
 template <> struct BqPay<float> { typedef long long type; };    // packed (qm << 32) + qs
@@ -50,8 +53,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 struct BqState {
-  int count, head, tail;      // tail: FIFO tail key (queues.py:220-224)
-  unsigned long long mask;    // heap / sorted: occupied payload slots
+  int count, tail;            // tail: FIFO tail key (queues.py:220-224)
+  unsigned long long mask;    // occupied payload slots
 };
 
 __device__ __forceinline__ void bq_add(long long v, long long& qs, long long& qm) { qs += v; }
@@ -60,29 +63,23 @@ __device__ __forceinline__ void bq_add(longlong2 v, long long& qs, long long& qm
   qm += v.y;
 }
 
-// Insert one event (called in reference order).  0 accepted, 1 dropped
-// (full), 2 capability error (FIFO order).  The payload goes straight to HBM.
+// Insert one event (called in reference order) into the staged keys.  0
+// accepted, 1 dropped (full), 2 capability error (FIFO order).  The payload
+// goes straight to its slot in HBM.
 template <typename PT>
-__device__ __forceinline__ int bq_insert(int kind, int cap, int C, unsigned* sk, BqState& st, int m, int due, PT p,
+__device__ __forceinline__ int bq_insert(int kind, int cap, unsigned* sk, BqState& st, int m, int due, PT p,
                                          PT* pay) {
   if (kind == EQ_KIND_FIFORING && due < st.tail) return 2;     // queues.py:220-224
   if (st.count == cap) return 1;                               // :225-226, :514-515, :344-345
-  if (kind == EQ_KIND_FIFORING) {
-    int pos = st.head + st.count;
-    if (pos >= C) pos -= C;
-    sk[pos] = bq_key(due, pos);
-    pay[pos] = p;
-    st.count += 1;
-    st.tail = due;
-    return 0;
-  }
   const int slot = __ffsll((long long)~st.mask) - 1;           // a free slot: count < cap <= C <= 64
   st.mask |= 1ull << slot;
   pay[slot] = p;
   const unsigned key = bq_key(due, slot);
   const unsigned rk = bq_rel(key, m);
-  if (kind == EQ_KIND_BINARYHEAP) {                            // sift up (queues.py:521-528)
-    int i = st.count++;
+  int i = st.count++;
+  if (kind == EQ_KIND_FIFORING) {                              // append (queues.py:227-231)
+    st.tail = due;
+  } else if (kind == EQ_KIND_BINARYHEAP) {                     // sift up (queues.py:521-528)
     while (i > 0) {
       const int parent = (i - 1) >> 1;
       const unsigned pk = sk[parent];
@@ -90,29 +87,19 @@ __device__ __forceinline__ int bq_insert(int kind, int cap, int C, unsigned* sk,
       sk[i] = pk;
       i = parent;
     }
-    sk[i] = key;
-  } else {                                                     // sorted: insertion sweep (:351-366)
-    int k = st.count;
-    while (k > 0) {
-      int pi = st.head + k - 1;
-      if (pi >= C) pi -= C;
-      const unsigned pk = sk[pi];
-      if (bq_rel(pk, m) <= rk) break;
-      int di = pi + 1;
-      if (di >= C) di -= C;
-      sk[di] = pk;
-      --k;
+  } else {                                                     // sorted: insertion sweep (:351-366), stable
+    while (i > 0 && bq_rel(sk[i - 1], m) > rk) {
+      sk[i] = sk[i - 1];
+      --i;
     }
-    int di = st.head + k;
-    if (di >= C) di -= C;
-    sk[di] = key;
-    st.count += 1;
   }
+  sk[i] = key;
   return 0;
 }
 
-// Pop every event due at m (the minimum); returns the popped slots.
-__device__ __forceinline__ unsigned long long bq_pop(int kind, int C, unsigned* sk, BqState& st, int m) {
+// Pop every event due at m (the minimum) from the staged keys; returns the
+// popped slots (freed in st.mask).
+__device__ __forceinline__ unsigned long long bq_pop(int kind, unsigned* sk, BqState& st, int m) {
   unsigned long long popped = 0;
   if (kind == EQ_KIND_BINARYHEAP) {
     while (st.count > 0 && bq_rel(sk[0], m) == 0) {            // :555-568
@@ -141,15 +128,18 @@ __device__ __forceinline__ unsigned long long bq_pop(int kind, int C, unsigned* 
         sk[i] = item;
       }
     }
-    st.mask &= ~popped;
   } else {                                                     // due run at the head (:245-254, :378-398)
-    while (st.count > 0 && bq_rel(sk[st.head], m) == 0) {
-      popped |= 1ull << bq_slot(sk[st.head]);
-      st.head = st.head + 1 == C ? 0 : st.head + 1;
-      st.count -= 1;
+    int p = 0;
+    while (p < st.count && bq_rel(sk[p], m) == 0) {
+      popped |= 1ull << bq_slot(sk[p]);
+      ++p;
     }
-    if (kind != EQ_KIND_FIFORING) st.mask &= ~popped;
+    if (p > 0) {
+      for (int k = p; k < st.count; ++k) sk[k - p] = sk[k];
+      st.count -= p;
+    }
   }
+  st.mask &= ~popped;
   return popped;
 }
 
@@ -178,181 +168,270 @@ __device__ __forceinline__ void bq_sum(unsigned long long popped, const PT* pay,
   }
 }
 
-__device__ __forceinline__ int bq_next_due(int kind, const unsigned* sk, const BqState& st, int m) {
-  if (st.count == 0) return 0x7fffffff;
-  return m + (int)bq_rel(sk[kind == EQ_KIND_BINARYHEAP ? 0 : st.head], m);
+constexpr int kBqChunk = 2048;        // queues scanned per chunk (4 per thread at 512 threads)
+constexpr int kBqPoolWords = 8192;    // key staging (32 KB): kBqPoolWords / C queues per round
+
+// Block-wide exclusive scan of one int per thread; returns the total.
+template <int NT>
+__device__ __forceinline__ int block_exclusive_scan(int v, int& excl, int* s_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) s_warp[lane] = w;   // inclusive warp prefix
+  }
+  __syncthreads();
+  const int before = warp > 0 ? s_warp[warp - 1] : 0;
+  excl = before + x - v;
+  const int total = s_warp[NT / 32 - 1];
+  __syncthreads();
+  return total;
+}
+
+template <typename T>
+struct BqView {                 // the staged-queue arrays of BndArgs, typed
+  unsigned* keys;
+  typename BqPay<T>::type* pay;
+  int4* meta;
+  int* qdue;
+};
+
+// One busy queue of phase m (insert the arrivals of step m-1, pop m), keys
+// staged at sk.  Returns nothing; writes acc[m & 1][idx] when events popped.
+template <typename T>
+__device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>& Q, int m, bool last, int idx,
+                                           unsigned* sk, int b_first, unsigned long long (*s_ctr)[3]) {
+  typedef typename BqPay<T>::type PT;
+  const FwdArgs<T>& F = A.f;
+  const int C = A.C, kind = F.kind;
+  constexpr int kTr = FwdShared<512>::kTrials;
+  const int b = F.c.divN.div(idx);
+  const int j = idx - b * F.N;
+  const int4 mt = Q.meta[idx];
+  const int qd = Q.qdue[idx];
+  const bool ins = m - 1 >= A.insert_first && m >= 1;
+  int* cntp = A.acnt + ((size_t)((m - 1) & 1) * F.B + b) * F.N + j;
+  const int narr = ins ? *cntp : 0;
+  const long long acs = narr > 0 ? __ldg(A.csc_off + j) : 0;
+  BqState st;
+  st.count = mt.x;
+  st.mask = ((unsigned long long)(unsigned)mt.z << 32) | (unsigned long long)(unsigned)mt.y;
+  st.tail = mt.w;
+  const bool pop_due = !last && st.count > 0 && qd == m;
+  const bool can_ins = narr > 0 && st.count < A.cap;
+  unsigned* gk = A.keys + (size_t)idx * C;
+  const Arrival<T>* lst = A.alist + ((size_t)((m - 1) & 1) * F.B + b) * A.E + acs;
+  if (pop_due || can_ins) {                          // stage the occupied keys
+    for (int k = 0; k < st.count; k += 4) cp_async16(sk + k, gk + k);
+  }
+  for (int k = 0; k < narr && k < 4; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(lst + k));
+  cp_async_wait_all();
+  PT* const pay = Q.pay + (size_t)idx * C;
+  bool dirty = false;
+  if (narr > 0) {
+    *cntp = 0;
+    unsigned long long drops = 0;
+    int last_x = -1;
+    for (int r = 0; r < narr; ++r) {                 // ascending x = the reference's arrival order
+      int best = r;
+      if (can_ins) {
+        int bx = 0x7fffffff;
+        for (int k = 0; k < narr; ++k) {
+          const int x = lst[k].x;
+          if (x > last_x && x < bx) {
+            bx = x;
+            best = k;
+          }
+        }
+        last_x = bx;
+      }
+      const Arrival<T> a = lst[best];
+      int rc;
+      if (can_ins) {
+        PT p;
+        if constexpr (sizeof(T) == 4) p = a.p;
+        else p = make_longlong2(a.ps, a.pm);
+        rc = bq_insert<PT>(kind, A.cap, sk, st, m, a.due, p, pay);
+        dirty = true;
+      } else {                                       // full: every arrival dropped (FIFO order still checked)
+        rc = (kind == EQ_KIND_FIFORING && a.due < st.tail) ? 2 : 1;
+      }
+      if (rc == 2) {
+        raise_error(F.err, EQ_ERR_CAPABILITY, m, b, j);
+      } else if (rc == 1) {
+        drops += 1;
+        const long long id = (long long)a.tag * A.maxdeg + a.ro;
+        if (id < A.drop_cap) atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
+        else raise_error(F.err, EQ_ERR_CAPACITY, m - 1, b, j);
+      }
+    }
+    if (drops) {
+      const int tb = b - b_first;
+      if (tb < kTr) atomicAdd(&s_ctr[tb][2], drops);
+      else atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 2), drops);
+    }
+  }
+  if (pop_due) {
+    const unsigned long long popped = bq_pop(kind, sk, st, m);
+    long long qs = 0, qm = 0;
+    bq_sum<PT>(popped, pay, qs, qm);
+    if (Prec<T>::kSlotWords == 1) {                  // packed pair, summed mod 2^64
+      F.acc[(size_t)(m & 1) * F.total + idx] = qs;
+    } else {
+      long long* o = F.acc + ((size_t)(m & 1) * F.total + idx) * 2;
+      o[0] = qs;
+      o[1] = qm;
+    }
+    dirty = true;
+  }
+  if (dirty) {
+    for (int k = 0; k < st.count; k += 4)
+      *reinterpret_cast<uint4*>(gk + k) = *reinterpret_cast<const uint4*>(sk + k);
+    Q.meta[idx] = make_int4(st.count, (int)(unsigned)(st.mask & 0xffffffffull), (int)(unsigned)(st.mask >> 32),
+                            st.tail);
+    Q.qdue[idx] = st.count ? m + (int)bq_rel(sk[0], m) : 0x7fffffff;
+  }
+}
+
+// Fan-out of this CTA's crossings of step m (its log chunk) into the targets'
+// arrival lists: one 32-byte record {edge, log position, due, row offset,
+// payload} per event at a slot from the target's counter inside its in-edge
+// segment (cannot overflow), inserted in edge order by the owner at phase m+1.
+template <typename T, int NT>
+__device__ __forceinline__ void bq_fanout(const BndArgs<T>& A, int m, int cta, int tid, SpikeRec<T>* s_spk,
+                                          long long* s_r0, int* s_pre) {
+  typedef Prec<T> P;
+  constexpr int kCap = FwdShared<NT, T>::kCap;
+  const FwdArgs<T>& F = A.f;
+  const StepConsts<T>& c = F.c;
+  const long long L0 = F.chunk_off[(size_t)m * F.G + cta];
+  const int n = F.chunk_cnt[(size_t)m * F.G + cta];
+  if (L0 + n > F.log_cap) return;                    // (the log overflow is already an error)
+  const int par = m & 1;
+  for (int k0 = 0; k0 < n; k0 += kCap) {
+    const int nb = n - k0 < kCap ? n - k0 : kCap;
+    stage_spikes<T>(F.log, F.log_r0, F.log_len, L0 + k0, nb, s_spk, s_r0, s_pre, tid, NT, 3);
+    const int total = s_pre[nb];
+    for (int f = tid; f < total; f += NT) {
+      const int k = find_row(s_pre, nb, f);
+      const int ro = f - s_pre[k];
+      const long long x = s_r0[k] + ro;
+      const SpikeRec<T> rec = s_spk[k];
+      const int b = c.divN.div(rec.idx);
+      const EdgeRec<T> ed = ld_edge(F.net.er + x);
+      const int jt = ed.col;
+      const T t_post = rec.t + ed.d;
+      const int ds = delivery_step_coded(t_post, (unsigned short)ed.code, c.dt, m);
+      T ws, wm;
+      if (F.exact) {
+        const T phi = (T)ds * c.dt - t_post;
+        ws = ed.w * eq_exp_t(-phi * c.inv_tau_s);
+        wm = ed.w * eq_exp_t(-phi * c.inv_tau_m);
+      } else {
+        ws = ed.w;
+        wm = (T)0;
+      }
+      const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
+      const int slot = atomicAdd(A.acnt + ((size_t)par * F.B + b) * F.N + jt, 1);
+      Arrival<T> ar;
+      ar.x = (int)x;
+      ar.tag = (int)(L0 + k0 + k);
+      ar.due = ds;
+      ar.ro = ro;
+      if constexpr (sizeof(T) == 4) {
+        ar.p = pack2(q1, q2);
+        ar.pad = 0;
+      } else {
+        ar.ps = q1;
+        ar.pm = q2;
+      }
+      A.alist[((size_t)par * F.B + b) * A.E + __ldg(A.csc_off + jt) + slot] = ar;
+    }
+  }
 }
 
 template <typename T, int NT, int U>
 __global__ void __launch_bounds__(NT, 2) k_forward_bq(BndArgs<T> A) {
-  typedef Prec<T> P;
-  typedef typename BqPay<T>::type PT;
   constexpr int kCap = FwdShared<NT, T>::kCap;
+  constexpr int kCapN = kCap / 2;
   constexpr int kTr = FwdShared<NT>::kTrials;
-  constexpr int NW = NT / 32;
-  __shared__ SpikeRec<T> s_spk[kCap];
+  __shared__ SpikeRec<T> s_spk[kCap];             // fan-out staging
   __shared__ long long s_r0[kCap];
   __shared__ int s_pre[kCap + 1];
+  __shared__ SpikeRec<T> s_own[kCapN];            // neuron pass
   __shared__ int s_n;
   __shared__ long long s_off;
   __shared__ unsigned long long s_ctr[kTr][3];
-  extern __shared__ __align__(16) unsigned s_keys[];   // [NW][kBqWarpWords] staging
+  __shared__ int s_warp[NT / 32];
+  extern __shared__ __align__(16) unsigned s_dyn[];
+  int* s_busy = reinterpret_cast<int*>(s_dyn);                 // [kBqChunk]
+  unsigned* s_pool = s_dyn + kBqChunk;                         // [kBqPoolWords]
   const FwdArgs<T>& F = A.f;
+  BqView<T> Q;
+  Q.keys = A.keys;
+  Q.pay = reinterpret_cast<typename BqPay<T>::type*>(A.pay);
+  Q.meta = A.meta;
+  Q.qdue = A.qdue;
 
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
   const long long begin = (long long)cta * F.per;
   const long long end = begin + F.per < F.total ? begin + F.per : F.total;
   const int b_first = (int)(begin / F.N);
-  const StepConsts<T> c = F.c;
   SpikeRec<T>* spill = F.scratch + (size_t)cta * F.per;
-  const int C = A.C, L = A.lanes, kind = F.kind;
-  unsigned* const sk = s_keys + warp * kBqWarpWords + lane * C;
-  PT* const payb = reinterpret_cast<PT*>(A.pay);
+  const int C = A.C;
+  const int per_round = kBqPoolWords / C < NT ? kBqPoolWords / C : NT;
+  unsigned* const sk = s_pool + (tid < per_round ? tid : 0) * C;
   if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
+  if (tid == 0) s_n = 0;
+  __syncthreads();
 
   int m1 = F.m1;   // lowered at a barrier when the spike log could overflow (pause_due)
   for (int m = F.m0; m <= m1; ++m) {
     const bool last = (m == m1);   // extra pass: insert the final step's arrivals only
-    if (tid == 0) s_n = 0;
-    __syncthreads();
     if (!last) tl_mark(F.tl, m, F.G, cta, 0);
     const bool ins = m - 1 >= A.insert_first && m >= 1;
-    // ---------------- owner phase, one batch of L consecutive queues per warp
-    for (long long base = begin + (long long)warp * L; base < end; base += (long long)NW * L) {
-      const long long qi = base + lane;
-      const bool act = lane < L && qi < end;
-      const int idx = (int)qi;
-      int b = 0, j = 0, narr = 0, rf = 0;
-      int4 mt = make_int4(0, 0x7fffffff, 0, 0);
-      int* cntp = nullptr;
-      T I0 = (T)0, V0 = (T)0, ampj = (T)0;
-      bool drv = false;
-      if (act) {                                    // independent loads of the lane: one round trip
-        b = c.divN.div(idx);
-        j = idx - b * F.N;
-        mt = A.meta[idx];
-        cntp = A.acnt + ((size_t)((m - 1) & 1) * F.B + b) * F.N + j;
-        narr = ins ? *cntp : 0;
-        if (!last) {
-          I0 = F.I[idx];
-          V0 = F.V[idx];
-          rf = F.refractory ? F.refr[idx] : 0;
-          drv = drive_bit(F.net, b, m, j);
-          ampj = __ldg(F.net.amp + j);
+    const int* acnt = A.acnt + (size_t)((m - 1) & 1) * F.B * F.N;
+    // ---------------- 1. queue pass
+    for (long long cb = begin; cb < end; cb += kBqChunk) {
+      int flags = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long long q = cb + 4 * tid + e;
+        if (q < end && q < cb + kBqChunk) {
+          const bool busy = (!last && Q.qdue[q] == m) || (ins && acnt[q] > 0);
+          flags |= (int)busy << e;
         }
       }
-      BqState st;
-      st.count = mt.x & 0xffff;
-      st.head = (int)((unsigned)mt.x >> 16);
-      st.tail = kind == EQ_KIND_FIFORING ? mt.z : 0;
-      st.mask = kind == EQ_KIND_FIFORING ? 0ull
-                                         : ((unsigned long long)(unsigned)mt.w << 32) | (unsigned long long)(unsigned)mt.z;
-      const bool pop_due = act && !last && st.count > 0 && mt.y == m;
-      const bool can_ins = narr > 0 && st.count < A.cap;
-      const unsigned* gk = A.keys + (size_t)idx * C;
-      if (pop_due || can_ins)                       // stage the key array (all lanes' copies in flight at once)
-        for (int k = 0; k < C; k += 4) cp_async16(sk + k, gk + k);
-      cp_async_wait_all();
-      bool dirty = false;
-      PT* const pay = payb + (size_t)idx * C;
-      if (narr > 0) {
-        *cntp = 0;
-        unsigned long long drops = 0;
-        const Arrival<T>* lst = A.alist + ((size_t)((m - 1) & 1) * F.B + b) * A.E + __ldg(A.csc_off + j);
-        int last_x = -1;
-        for (int r = 0; r < narr; ++r) {             // ascending x = the reference's arrival order
-          int best = 0;
-          if (can_ins) {
-            int bx = 0x7fffffff;
-            for (int k = 0; k < narr; ++k) {
-              const int x = lst[k].x;
-              if (x > last_x && x < bx) {
-                bx = x;
-                best = k;
-              }
-            }
-            last_x = bx;
-          } else {
-            best = r;                                // full queue: order only matters for FIFO's error
-          }
-          const Arrival<T> a = lst[best];
-          PT p;
-          if constexpr (sizeof(T) == 4) p = a.p;
-          else p = make_longlong2(a.ps, a.pm);
-          int rc;
-          if (can_ins) {
-            rc = bq_insert<PT>(kind, A.cap, C, sk, st, m, a.due, p, pay);
-            dirty = true;
-          } else {
-            rc = (kind == EQ_KIND_FIFORING && a.due < st.tail) ? 2 : 1;
-          }
-          if (rc == 2) {
-            raise_error(F.err, EQ_ERR_CAPABILITY, m, b, j);
-          } else if (rc == 1) {
-            drops += 1;
-            const long long id = (long long)a.tag * A.maxdeg + a.ro;
-            if (id < A.drop_cap) atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
-            else raise_error(F.err, EQ_ERR_CAPACITY, m - 1, b, j);
-          }
-        }
-        if (drops) {
-          const int tb = b - b_first;
-          if (tb < kTr) atomicAdd(&s_ctr[tb][2], drops);
-          else atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 2), drops);
-        }
-      }
-      long long qs = 0, qm = 0;
-      if (pop_due) {
-        const unsigned long long popped = bq_pop(kind, C, sk, st, m);
-        bq_sum<PT>(popped, pay, qs, qm);
-        dirty = true;
-      }
-      if (dirty) {
-        unsigned* gkw = const_cast<unsigned*>(gk);
-        for (int k = 0; k < C; k += 4)
-          *reinterpret_cast<uint4*>(gkw + k) = *reinterpret_cast<const uint4*>(sk + k);
-        int4 o;
-        o.x = st.count | (st.head << 16);
-        o.y = bq_next_due(kind, sk, st, m);
-        o.z = kind == EQ_KIND_FIFORING ? st.tail : (int)(unsigned)(st.mask & 0xffffffffull);
-        o.w = kind == EQ_KIND_FIFORING ? 0 : (int)(unsigned)(st.mask >> 32);
-        A.meta[idx] = o;
-      }
-      if (!act || last) continue;
-      if (P::kSlotWords == 1) {
-        const long long packed = qs;
-        unpack2(packed, qs, qm);
-      }
-      T ps = P::deq(qs, c.inv_scale), pm = P::deq(qm, c.inv_scale);
-      if (!F.exact) pm = (T)0;
-      const T drive = drv ? ampj : (T)0;
-      T i, v_new, a, v, t_spk;
-      if (lif_step(c, F.exact != 0, F.refractory, m, ps, pm, I0, V0, drive, rf, i, v_new, a, v, t_spk)) {
-        if (t_spk != t_spk) {
-          raise_error(F.err, EQ_ERR_GRAZING, m + 1, b, j);
-        } else {
-          const int pos = atomicAdd(&s_n, 1);
-          SpikeRec<T> rec;
-          rec.idx = idx;
-          rec.t = t_spk;
-          rec.a = a;
-          rec.vh = v;
-          if (pos < kCap) s_spk[pos] = rec;
-          else spill[pos - kCap] = rec;
-        }
-      }
-      F.I[idx] = i;
-      F.V[idx] = v_new;
-      if (F.refractory) F.refr[idx] = rf;
-      if (F.v_trace) F.v_trace[(size_t)(m - F.m0) * F.total + idx] = v_new;
+      int off;
+      const int nb = block_exclusive_scan<NT>(__popc(flags), off, s_warp);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if ((flags >> e) & 1) s_busy[off++] = (int)(cb + 4 * tid + e);
+      __syncthreads();
+      for (int r0 = 0; r0 < nb; r0 += per_round)
+        if (tid < per_round && r0 + tid < nb) bq_process<T>(A, Q, m, last, s_busy[r0 + tid], sk, b_first, s_ctr);
+      __syncthreads();
     }
-    __syncthreads();
     if (last) break;
     tl_mark(F.tl, m, F.G, cta, 1);
-    const int nspk = s_n;
-    bounded_log_fanout<T, NT>(A, m, cta, tid, nspk, b_first, s_spk, s_r0, s_pre, spill, s_off, s_ctr);
+    // ---------------- 2. neuron pass: pop acc[m & 1], LIF, spike log (eq_ring.cuh)
+    neuron_side<T, NT, U, 0>(F, m, cta, tid, begin, end, b_first, true, s_own, s_n, s_off, s_ctr, spill, nullptr);
+    __syncthreads();
+    // ---------------- 3. fan-out of the crossings of step m
+    bq_fanout<T, NT>(A, m, cta, tid, s_spk, s_r0, s_pre);
     __syncthreads();
     tl_mark(F.tl, m, F.G, cta, 2);
     if (!grid_sync(F.bar, F.G, F.err, F.step_start + m + 1, F.log_count)) break;
@@ -371,28 +450,24 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bq(BndArgs<T> A) {
   }
 }
 
-__global__ void k_meta_init_bq(int4* meta, long long n, int fifo) {
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
-    meta[k] = make_int4(0, 0x7fffffff, fifo ? -1 : 0, 0);   // FIFORingQueue._tail_key = -1
+__global__ void k_meta_init_bq(int4* meta, int* qdue, long long n) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    meta[k] = make_int4(0, 0, 0, -1);                  // FIFORingQueue._tail_key = -1
+    qdue[k] = 0x7fffffff;
+  }
 }
 
 // Pending contents (canonical int64 [B*N][H][2], due now .. now+H-1).
 template <typename T>
-__global__ void k_pending_bq(const unsigned* keys, const typename BqPay<T>::type* pay, const int4* meta, int kind,
-                             int C, long long total, int H, int now, long long* out) {
+__global__ void k_pending_bq(const unsigned* keys, const typename BqPay<T>::type* pay, const int4* meta, int C,
+                             long long total, int H, int now, long long* out) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     long long* o = out + idx * H * 2;
     for (int k = 0; k < 2 * H; ++k) o[k] = 0;
-    const int4 mt = meta[idx];
-    const int count = mt.x & 0xffff, head = (int)((unsigned)mt.x >> 16);
+    const int count = meta[idx].x;
     for (int k = 0; k < count; ++k) {
-      int pos = k;
-      if (kind != EQ_KIND_BINARYHEAP) {
-        pos = head + k;
-        if (pos >= C) pos -= C;
-      }
-      const unsigned key = keys[idx * C + pos];
+      const unsigned key = keys[idx * C + k];
       const int h = (int)bq_rel(key, now);
       if (h >= H) continue;
       long long qs = 0, qm = 0;

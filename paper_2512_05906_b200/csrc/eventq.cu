@@ -135,6 +135,7 @@ struct eq_handle {
   int C = 0;                   // their storage capacity
   unsigned* qkeys = nullptr;
   void* qpay = nullptr;
+  int* qdue = nullptr;
   int maxdeg = 1;               // largest CSR row (bounded kinds: event id = log position * maxdeg + row offset)
   unsigned* drop_bits = nullptr;
   long long drop_cap = 0;
@@ -680,7 +681,7 @@ __global__ void k_add_lt(T* lt_rem, const long long* step_start, int lo, const T
 // ------------------------------------------------------------ launches
 
 // staged bounded-queue kernel: key staging of every warp
-constexpr size_t bq_smem() { return (size_t)(kNT / 32) * kBqWarpWords * sizeof(unsigned); }
+constexpr size_t bq_smem() { return (size_t)(kBqChunk + kBqPoolWords) * sizeof(unsigned); }
 
 // reverse kernel dynamic smem: spiker bitmap + uint16 chunk position per owned neuron
 size_t bwd_smem(long long per) {
@@ -859,7 +860,7 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
     Bk.keys = h->qkeys;
     Bk.pay = h->qpay;
     Bk.C = h->C;
-    Bk.lanes = h->C > 0 ? std::min(32, kBqWarpWords / h->C) : 0;
+    Bk.qdue = h->qdue;
     void* bargs[] = {&Bk};
     if (h->staged) {
       const void* kq = (const void*)k_forward_bq<T, kNT, kU>;
@@ -1065,6 +1066,7 @@ int setup_geometry(eq_handle* h) {
   }
   if (occ < 1) return fail(h, EQ_ERR_CONFIGURATION, "problem too large for one persistent grid");
   h->G = h->n_sm * occ;
+  if (h->cfg.max_ctas > 0 && h->cfg.max_ctas < h->G) h->G = h->cfg.max_ctas;
   // never more CTAs than there are neuron-trials to own
   if ((long long)h->G > h->total) h->G = (int)h->total;
   // ranges in whole warps so a warp's 32 neurons share one drive-mask word
@@ -1132,6 +1134,9 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
     const size_t pb = c.precision == 32 ? sizeof(long long) : sizeof(longlong2);
     EQ_CUDA(h, ensure(h, (void**)&h->qkeys, (size_t)B * N * h->C * sizeof(unsigned)));
     EQ_CUDA(h, ensure(h, &h->qpay, (size_t)B * N * h->C * pb));
+    EQ_CUDA(h, ensure(h, (void**)&h->qdue, (size_t)B * N * sizeof(int)));
+    // the step's popped sums, read by the ring kind's neuron pass
+    EQ_CUDA(h, ensure(h, (void**)&h->acc, (size_t)2 * h->total * (c.precision == 32 ? 1 : 2) * sizeof(long long)));
   } else {
     EQ_CUDA(h, ensure(h, &h->q, qbytes));
   }
@@ -1174,6 +1179,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
       c.kind != EQ_KIND_BINARYHEAP && c.kind != EQ_KIND_SORTEDARRAY && c.kind != EQ_KIND_LOSSYRING)
     return bad("unknown queue kind " + std::to_string(c.kind));
   if (c.capacity < 0) return bad("capacity must be >= 1, got " + std::to_string(c.capacity));
+  if (c.max_ctas < 0) return bad("max_ctas must be >= 0");
   h->bounded = c.kind == EQ_KIND_FIFORING || c.kind == EQ_KIND_BINARYHEAP || c.kind == EQ_KIND_SORTEDARRAY;
   h->lossy = c.kind == EQ_KIND_LOSSYRING;
   if (c.exact_delivery && std::fabs(c.tau_m - c.tau_syn) < 1e-3 * c.tau_m)
@@ -1439,9 +1445,11 @@ int eq_reset(eq_handle* h, void* stream) {
     const int B = h->cfg.n_trials, N = h->cfg.n_neurons;
     EQ_CUDA(h, cudaMemsetAsync(h->acnt, 0, (size_t)2 * B * N * sizeof(int), s));
     EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
-    if (h->staged)
-      k_meta_init_bq<<<592, 256, 0, s>>>(h->meta, (long long)B * N, h->cfg.kind == EQ_KIND_FIFORING);
-    else
+    if (h->staged) {
+      k_meta_init_bq<<<592, 256, 0, s>>>(h->meta, h->qdue, (long long)B * N);
+      EQ_CUDA(h, cudaMemsetAsync(h->acc, 0, (size_t)2 * h->total * (h->cfg.precision == 32 ? 1 : 2) *
+                                                sizeof(long long), s));
+    } else
       k_meta_init<<<592, 256, 0, s>>>(h->meta, (long long)B * N);
     h->launches += 1;
   }
@@ -2008,10 +2016,10 @@ int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream) {
                                         h->steps_done, (long long*)buf);
   } else if (h->bounded && h->staged) {
     if (h->cfg.precision == 32)
-      k_pending_bq<float><<<592, 256, 0, s>>>(h->qkeys, (const long long*)h->qpay, h->meta, h->cfg.kind, h->C,
+      k_pending_bq<float><<<592, 256, 0, s>>>(h->qkeys, (const long long*)h->qpay, h->meta, h->C,
                                                (long long)B * N, H, h->steps_done, (long long*)buf);
     else
-      k_pending_bq<double><<<592, 256, 0, s>>>(h->qkeys, (const longlong2*)h->qpay, h->meta, h->cfg.kind, h->C,
+      k_pending_bq<double><<<592, 256, 0, s>>>(h->qkeys, (const longlong2*)h->qpay, h->meta, h->C,
                                                 (long long)B * N, H, h->steps_done, (long long*)buf);
   } else if (h->bounded) {
     if (h->cfg.precision == 32)

@@ -32,7 +32,8 @@ class Engine:
     def __init__(self, n: int, n_trials: int, t_steps: int, *, kind: str = "ring",
                  precision: int = 32, lif: Optional[LIFConfig] = None, capacity: int = 0,
                  max_spikes: int = 0, device: Optional[int] = None,
-                 partition: Optional[Tuple[int, int]] = None):
+                 partition: Optional[Tuple[int, int]] = None, max_ctas: int = 0,
+                 stream: Optional[torch.cuda.Stream] = None):
         self.L = _native.lib()
         if kind not in _native.KIND_IDS:
             raise ConfigurationError(f"unknown queue kind {kind!r}")
@@ -53,7 +54,9 @@ class Engine:
         cfg.max_spikes = max_spikes
         cfg.dt, cfg.tau_m, cfg.tau_syn = lif.dt, lif.tau_m, lif.tau_syn
         cfg.v_th, cfg.v_reset = lif.v_th, lif.v_reset
+        cfg.max_ctas = max_ctas
         self.cfg = cfg
+        self._stream = stream      # None: the device's current torch stream at each call
         h = ctypes.c_void_p()
         code = self.L.eq_create(ctypes.byref(cfg), device, ctypes.byref(h))
         self.h = h
@@ -82,8 +85,25 @@ class Engine:
             pass
 
     @property
+    def torch_stream(self) -> torch.cuda.Stream:
+        return self._stream if self._stream is not None else torch.cuda.current_stream(self.device)
+
+    @property
     def stream(self):
-        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        """cudaStream_t for an ABI call.  With a private stream (partitions
+        running concurrently) the call is ordered after the caller's current
+        stream (its inputs) and the caller's stream after it (its outputs)."""
+        if self._stream is not None:
+            cur = torch.cuda.current_stream(self.device)
+            if cur.cuda_stream != self._stream.cuda_stream:
+                self._stream.wait_stream(cur)
+                self._join_pending = True
+        return ctypes.c_void_p(self.torch_stream.cuda_stream)
+
+    def _join(self) -> None:
+        if self._stream is not None and getattr(self, "_join_pending", False):
+            torch.cuda.current_stream(self.device).wait_stream(self._stream)
+            self._join_pending = False
 
     def _dev(self, a, dtype) -> torch.Tensor:
         if isinstance(a, torch.Tensor):
@@ -134,6 +154,7 @@ class Engine:
         tr = torch.empty(self.T, self.B, self.n, dtype=self.dtype, device=self.device) if record_v else None
         self.run_id += 1
         _native.check(self.h, self.L.eq_forward(self.h, _ptr(v), _ptr(i), _ptr(tr), self.stream))
+        self._join()
         out = {"v": v, "i": i}
         if record_v:
             out["v_trace"] = tr
@@ -162,6 +183,7 @@ class Engine:
         v = torch.empty(self.B, self.n, dtype=self.dtype, device=self.device)
         i = torch.empty_like(v)
         _native.check(self.h, self.L.eq_get_state(self.h, _ptr(v), _ptr(i), self.stream))
+        self._join()
         return {"v": v, "i": i}
 
     def reset(self) -> None:
@@ -180,6 +202,7 @@ class Engine:
         ga = torch.empty(self.n, dtype=torch.float64, device=self.device) if want_amp else None
         _native.check(self.h, self.L.eq_backward(self.h, _ptr(vb), _ptr(ib), _ptr(gw), _ptr(gd), _ptr(ga),
                                                   self.stream))
+        self._join()
         return gw, gd, ga
 
     def backward_begin(self, v_bar: torch.Tensor, i_bar: Optional[torch.Tensor] = None, want_amp: bool = True):
@@ -254,7 +277,7 @@ class Engine:
     def sync(self) -> None:
         """Wait for this engine's stream; raise the device error of any
         asynchronous window."""
-        _native.check(self.h, self.L.eq_sync(self.h, self.stream))
+        _native.check(self.h, self.L.eq_sync(self.h, ctypes.c_void_p(self.torch_stream.cuda_stream)))
 
     # ------------------------------------------------------------ queries
     def counters(self) -> np.ndarray:
@@ -278,6 +301,7 @@ class Engine:
         if S:
             _native.check(self.h, self.L.eq_get_spikes(self.h, _ptr(step), _ptr(trial), _ptr(neuron), _ptr(t),
                                                         self.stream))
+            self._join()
         st, tr, ne, tt = (x.cpu().numpy() for x in (step, trial, neuron, t))
         order = np.lexsort((ne, st, tr))
         return {"step": st[order], "trial": tr[order], "neuron": ne[order], "t": tt[order]}

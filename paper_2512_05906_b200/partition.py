@@ -205,20 +205,32 @@ class PartitionedNetwork:
 
     # -- collectives over the partitions, whatever the transport
     def _order(self) -> None:
-        """Peer exchange on several devices: every partition's next window
-        starts after every partition's current one (events, no host wait)."""
-        devs = {e.device for e in self.engines}
-        if len(devs) < 2:
+        """Peer exchange on several streams (partitions running concurrently
+        on one GPU's SM subsets, or on several GPUs): every partition's next
+        window starts after every partition's current one — CUDA events, no
+        host wait."""
+        streams = [e.torch_stream for e in self.engines]
+        if len({s.cuda_stream for s in streams}) < 2:
             return
         evs = []
-        for e in self.engines:
+        for st in streams:
             ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(e.device))
+            ev.record(st)
             evs.append(ev)
-        for e in self.engines:
-            st = torch.cuda.current_stream(e.device)
+        for st in streams:
             for ev in evs:
                 st.wait_event(ev)
+
+    def join(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Make `stream` (default: the current stream of the first engine's
+        device) wait for every partition's stream."""
+        stream = stream or torch.cuda.current_stream(self.engines[0].device)
+        for e in self.engines:
+            st = e.torch_stream
+            if st.cuda_stream != stream.cuda_stream:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                stream.wait_event(ev)
 
     def _gather(self, mine: List[torch.Tensor]) -> List[torch.Tensor]:
         if isinstance(self.tp, LocalTransport):
@@ -246,6 +258,7 @@ class PartitionedNetwork:
                 self._order()
             for e in self.engines:          # deliver the last window's spikes (queue contents)
                 e.run_window(len(self.win), self.win[-1][0], 0)
+            self._order()
             for e in self.engines:
                 e.sync()
             return

@@ -37,6 +37,11 @@ def main():
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="peer exchange: every partition on its own stream and SM share (grid = 2*SMs/P), "
+                         "windows ordered by events — the partitions run side by side as on P GPUs")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "host"],
+                    help="single process: device-resident peer exchange (eq_set_peers) or host-routed export/import")
     args = ap.parse_args()
 
     import torch
@@ -44,7 +49,7 @@ def main():
 
     from paper_2512_05906_b200 import workload as wl
     from paper_2512_05906_b200.engine import Engine
-    from paper_2512_05906_b200.partition import (DistTransport, LocalTransport, PartitionedNetwork,
+    from paper_2512_05906_b200.partition import (DistTransport, LocalTransport, PartitionedNetwork, PeerTransport,
                                                  min_delay_steps, partition_csr, slice_mask, split_range)
 
     rank = int(os.environ.get("RANK", "0"))
@@ -68,13 +73,19 @@ def main():
     for r in mine:
         lo, hi = split_range(net.n, P, r)
         rp, cl, w, d, eid = partition_csr(net.rowptr, net.col, net.weight, net.delay, lo, hi)
-        e = Engine(hi - lo, args.trials, args.steps, precision=args.precision, partition=(net.n, lo), device=local)
+        conc = args.concurrent and world == 1 and args.exchange == "peer"
+        sm = torch.cuda.get_device_properties(local).multi_processor_count
+        e = Engine(hi - lo, args.trials, args.steps, precision=args.precision, partition=(net.n, lo), device=local,
+                   max_ctas=(2 * sm) // P if conc else 0, stream=torch.cuda.Stream(local) if conc else None)
         e.set_network(rp, cl, w, d)
         e.set_drive(slice_mask(mask, net.n, lo, hi), amp[lo:hi])
         engines.append(e)
         ranges.append((lo, hi))
         ids.append(eid)
-    tp = DistTransport() if world > 1 else LocalTransport(P)
+    if world > 1:
+        tp = DistTransport()
+    else:
+        tp = PeerTransport(P) if args.exchange == "peer" else LocalTransport(P)
     pn = PartitionedNetwork(engines, mine, tp, window=W)
     stream = torch.cuda.current_stream()
 
@@ -83,10 +94,16 @@ def main():
         b = torch.cuda.Event(enable_timing=True)
         c = torch.cuda.Event(enable_timing=True)
         a.record(stream)
+        for e in engines:                     # partitions on their own streams start after `a`
+            e.torch_stream.wait_event(a)
         pn.forward(args.steps)
+        pn.join(stream)
         b.record(stream)
         vbars = [(2.0 * (e.state()["v"].double() - 0.25)).to(e.dtype) for e in engines]
+        for e in engines:
+            e.torch_stream.wait_event(b)
         pn.backward(vbars, want_amp=False)
+        pn.join(stream)
         c.record(stream)
         torch.cuda.synchronize()
         return a.elapsed_time(b), b.elapsed_time(c)
@@ -102,7 +119,8 @@ def main():
     ctr = sum(e.counters() for e in engines)
     t = torch.tensor([np.mean(fw) + np.mean(bw), np.mean(fw), np.mean(bw)], device="cuda", dtype=torch.float64)
     ev = torch.tensor([float(ctr[:, 1].sum()), float(ctr[:, 0].sum()),
-                       float(sum(sum(c) for c in pn.counts))], device="cuda", dtype=torch.float64)
+                       float(sum(sum(c) for c in pn.counts)) if pn.counts else float(ctr[:, 0].sum()) * (P - 1)],
+                      device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(ev)
@@ -114,6 +132,9 @@ def main():
         "config": {"workload": f"C5: {net.n} LIF neurons, {args.k} syn/neuron, delay {lo_d}..{hi_d} steps, ring, "
                                f"fwd+bwd T={args.steps}, {P} partitions", "trials": args.trials,
                    "processes": world, "partitions": P, "window_steps": W,
+                   "exchange": "nccl-host" if world > 1 else args.exchange,
+                   "concurrent_partitions": bool(args.concurrent and world == 1),
+                   "ctas_per_partition": engines[0].geometry[0],
                    "windows": len(pn.win), "exchanged_spikes": exchanged,
                    "exchange_bytes": exchanged * (16 if args.precision == 32 else 24)},
         "ms_per_pass": ms, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "spikes": spikes, "events": events,

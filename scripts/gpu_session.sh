@@ -26,3 +26,22 @@ for l in open('gpurun_out/${TAG}_variants.jsonl'):
 " ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    partition)
+      timeout 900 python -m pytest tests/test_gpu_partition.py -m gpu -q > gpurun_out/${TAG}_partition.log 2>&1
+      echo "partition rc=$?"; tail -5 gpurun_out/${TAG}_partition.log ;;
+    c5)
+      timeout 900 python scripts/c5_partitioned.py --parts 8 --exchange peer --check > gpurun_out/${TAG}_c5_peer.json 2> gpurun_out/${TAG}_c5_peer.err
+      echo "c5 peer rc=$?"; tail -1 gpurun_out/${TAG}_c5_peer.json; tail -3 gpurun_out/${TAG}_c5_peer.err
+      timeout 900 python scripts/c5_partitioned.py --parts 8 --exchange host > gpurun_out/${TAG}_c5_host.json 2> gpurun_out/${TAG}_c5_host.err
+      echo "c5 host rc=$?"; tail -1 gpurun_out/${TAG}_c5_host.json ;;
+  esac
+done
+for p in $PARTS; do
+  case $p in
+    c5c)
+      timeout 900 python scripts/c5_partitioned.py --parts 8 --exchange peer --concurrent --check > gpurun_out/${TAG}_c5_conc.json 2> gpurun_out/${TAG}_c5_conc.err
+      echo "c5 concurrent rc=$?"; tail -1 gpurun_out/${TAG}_c5_conc.json; tail -3 gpurun_out/${TAG}_c5_conc.err ;;
+  esac
+done

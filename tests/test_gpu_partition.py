@@ -117,6 +117,53 @@ def test_partitioned_run_equals_whole_network(precision, P, window, peer):
         np.testing.assert_allclose(got, ref, rtol=tol, atol=tol * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_concurrent_peer_partitions_equal_whole_network(precision):
+    """Partitions on their own streams and SM shares (grid 2*SMs/P each),
+    running side by side as on P GPUs, windows ordered by CUDA events: same
+    raster, state and queues as the whole network; gradients to rounding."""
+    import torch
+    from paper_2512_05906_b200.engine import Engine
+    B, T, P = 2, 300, 4
+    net, mask, amp = _problem(B=B, T=T, seed=9)
+    whole = _whole(net, mask, amp, B, T, precision)
+    out = whole.forward()
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    engines, ids, ranges = [], [], []
+    for r in range(P):
+        lo, hi = split_range(net.n, P, r)
+        rp, cl, w, d, eid = partition_csr(net.rowptr, net.col, net.weight, net.delay, lo, hi)
+        e = Engine(hi - lo, B, T, precision=precision, partition=(net.n, lo), max_ctas=(2 * sm) // P,
+                   stream=torch.cuda.Stream())
+        e.set_network(rp, cl, w, d)
+        e.set_drive(slice_mask(mask, net.n, lo, hi), amp[lo:hi])
+        engines.append(e)
+        ids.append(eid)
+        ranges.append((lo, hi))
+    assert engines[0].geometry[0] <= (2 * sm) // P
+    pn = PartitionedNetwork(engines, range(P), PeerTransport(P), window=4)
+    pn.forward(T)
+    pn.join()
+    rows, ts = zip(*[_raster(e, lo) for e, (lo, _) in zip(engines, ranges)])
+    got_r, got_t = _sorted(np.concatenate(rows), np.concatenate(ts))
+    ref_r, ref_t = _sorted(*_raster(whole))
+    assert np.array_equal(got_r, ref_r) and np.array_equal(got_t, ref_t)
+    v = out["v"].cpu().numpy()
+    pend = whole.pending()
+    for e, (lo, hi) in zip(engines, ranges):
+        assert np.array_equal(e.state()["v"].cpu().numpy(), v[:, lo:hi])
+        assert np.array_equal(e.pending(), pend[:, lo:hi])
+    vbar = 2.0 * (out["v"].double() - 0.25)
+    gw, gd, _ = (x.cpu().numpy() for x in whole.backward(vbar.to(out["v"].dtype)))
+    grads = pn.backward([vbar[:, lo:hi].to(out["v"].dtype) for lo, hi in ranges])
+    pn.join()
+    pw = np.zeros_like(gw)
+    for (w_, _, _), eid in zip(grads, ids):
+        pw[eid] = w_.cpu().numpy()
+    tol = 1e-10 if precision == 64 else 1e-4
+    np.testing.assert_allclose(pw, gw, rtol=tol, atol=tol * np.abs(gw).max())
+
+
 def test_partitioned_raster_matches_the_oracle():
     from oracle.oracle import OracleSession
     B, T, P = 1, 250, 3
