@@ -275,6 +275,59 @@ def launch_selftest(args):
     dist.destroy_process_group()
 
 
+VARIANTS = (
+    # (label, config, trials, kind, capacity, precision, delays)
+    ("C3 ring fp64 (the reference's arithmetic)", "C3", 24, "ring", 0, 64, None),
+    ("C4 binaryheap[16] (memory pressure, drops)", "C4", 4, "binaryheap", 16, 32, None),
+    ("C4 sortedarray[16] (memory pressure, drops)", "C4", 4, "sortedarray", 16, 32, None),
+)
+
+
+def measure_variant(label, cfg, trials, kind, capacity, precision, delays, steps, warmup, local, peak):
+    """One more workload timed like the headline (device-resident, CUDA events
+    around each pass), reported with its own roofline fraction — the north
+    star asks the heap and sort-based queues to be reported the same way."""
+    import torch
+    from paper_2512_05906_b200.engine import Engine, poisson_drive_device
+    from paper_2512_05906_b200 import workload as wl
+    n, k, drange, _, T = wl.CONFIGS[cfg]
+    net = wl.random_network(n, k, 0, delay_steps=delays or drange)
+    # drive generated on the device (same PoissonDrive statistics, BASELINE.md §4): no host masks at 1M neurons
+    mask = poisson_drive_device(n, trials, T, 1e-3, 16e-3, 12e-3, 1000, device=local)
+    eng = Engine(n, trials, T, kind=kind, capacity=capacity, precision=precision, device=local)
+    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+    eng.set_drive(mask, np.full(n, 12.0))
+    stream = torch.cuda.current_stream()
+    fw, bw = [], []
+    for it in range(warmup + steps):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        out = eng.forward()
+        e[1].record(stream)
+        eng.backward((2.0 * (out["v"] - 0.25)).to(eng.dtype), want_amp=False)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        if it >= warmup:
+            fw.append(e[0].elapsed_time(e[1]))
+            bw.append(e[1].elapsed_time(e[2]))
+    c = eng.counters()
+    spikes, events, drops = int(c[:, 0].sum()), int(c[:, 1].sum()), int(c[:, 2].sum())
+    ns = trials * T * n
+    bounded = kind in ("fiforing", "binaryheap", "sortedarray")
+    fb = alg_bytes(ns, spikes, events, "fwd", bounded, precision)
+    bb = alg_bytes(ns, spikes, events, "bwd", False, precision)
+    f, b = statistics.mean(fw), statistics.mean(bw)
+    dom = ("k_forward_bounded" if bounded else "k_forward", fb, f) if f >= b else ("k_backward", bb, b)
+    ach = dom[1] / (dom[2] / 1e3) / 1e9
+    del eng
+    torch.cuda.empty_cache()
+    return {"workload": label, "value": events / ((f + b) / 1e3), "unit": "events/s", "trials": trials,
+            "dtype": "f32" if precision == 32 else "f64", "fwd_ms": f, "bwd_ms": b, "events": events,
+            "drops": drops, "drop_fraction": drops / max(events, 1),
+            "roofline": {"kernel": dom[0], "achieved": ach, "peak": peak, "frac": ach / peak,
+                         "fwd_bwd_frac": (fb + bb) / ((f + b) / 1e3) / 1e9 / peak}}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -294,7 +347,8 @@ def run_ours(args):
     if args.steps_per_pass:
         T = args.steps_per_pass
         mask = np.ascontiguousarray(mask[:, :T])
-    eng = Engine(net.n, B, T, kind=args.kind, capacity=args.capacity, precision=args.precision, device=local)
+    eng = Engine(net.n, B, T, kind=args.kind, capacity=args.capacity, precision=args.precision, device=local,
+                 staged_queues=args.staged_queues)
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     mask_dev = torch.from_numpy(mask.view(np.int32)).to(dev)
     amp_dev = torch.from_numpy(amp).to(dev, eng.dtype)
@@ -457,6 +511,14 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
+    variants = None
+    if world == 1 and not args.no_variants:
+        variants = []
+        for v in VARIANTS:
+            try:
+                variants.append(measure_variant(*v, steps=min(args.steps, 3), warmup=3, local=local, peak=peak))
+            except Exception as exc:  # a variant must not sink the headline line
+                variants.append({"workload": v[0], "error": str(exc)})
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
@@ -505,6 +567,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(2 * 4 * net.n_edges + 8)},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "variants": variants,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -523,9 +586,12 @@ def main():
     ap.add_argument("--cpu-trials", type=int, default=0)
     ap.add_argument("--cpu-steps", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the C3-fp64 / C4-heap / C4-sorted lines")
     ap.add_argument("--steps-per-pass", type=int, default=0, help="override T (debug)")
     ap.add_argument("--kind", default="ring", choices=["ring", "fiforing", "binaryheap", "sortedarray", "donothing"])
     ap.add_argument("--capacity", type=int, default=0, help="bounded kinds: events per queue")
+    ap.add_argument("--staged-queues", action="store_true",
+                    help="bounded kinds: the shared-memory staged queues with the in-kernel arrival sort")
     ap.add_argument("--delays", type=lambda s: tuple(int(x) for x in s.split(",")), default=None,
                     help="delay range in steps lo,hi (FIFO needs lo == hi)")
     ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)

@@ -77,7 +77,10 @@ typedef struct eq_config {
   double dt, tau_m, tau_syn, v_th, v_reset;
   int32_t max_ctas;         /* persistent grid size cap (0 = 2 per SM); partitions that run
                                concurrently on one GPU split its SMs this way */
-  int32_t reserved;
+  int32_t staged_queues;    /* bounded kinds, capacity <= 64: 1 = queues staged in shared
+                               memory per step with an in-kernel counting sort of the
+                               arrivals (eq_bq.cuh); 0 = HBM-resident structures (default,
+                               measured faster) */
 } eq_config;
 
 typedef struct eq_handle eq_handle;

@@ -25,7 +25,7 @@ class Config(ctypes.Structure):
         ("exact_delivery", ctypes.c_int32), ("capacity", ctypes.c_int32), ("max_spikes", ctypes.c_int64),
         ("dt", ctypes.c_double), ("tau_m", ctypes.c_double), ("tau_syn", ctypes.c_double),
         ("v_th", ctypes.c_double), ("v_reset", ctypes.c_double),
-        ("max_ctas", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("max_ctas", ctypes.c_int32), ("staged_queues", ctypes.c_int32),
     ]
 
 

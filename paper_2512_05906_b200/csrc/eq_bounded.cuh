@@ -89,6 +89,13 @@ struct BndArgs {
   void* pay;                  // [B*N][C] fixed-point payloads
   int C;                      // storage capacity (capacity rounded up to 4)
   int* qdue;                  // [B*N] next due step of each queue
+  // owner inboxes (eq_bq.cuh): arrivals appended per owner CTA, counting-sorted by target
+  void* inbox;                // [2][G][in_cap] InArr<T>
+  int* in_cnt;                // [2][G]
+  long long in_cap;
+  int* aoff;                  // [B*N] end of each queue's arrival run in its CTA's sorted index
+  int* aidx;                  // [G][in_cap] inbox positions sorted by target
+  FastDiv divPer;             // flat target -> owner CTA
 };
 
 __device__ __forceinline__ bool key_less(int da, int sa, int db, int sb) {
@@ -328,63 +335,90 @@ __device__ __forceinline__ void bounded_log_fanout(const BndArgs<T>& A, const in
       __syncthreads();
       const int total = s_pre[nb];
       const int par = m & 1;
-      for (int f = tid; f < total; f += NT) {
-        const int k = find_row(s_pre, nb, f);
-        const int ro = f - s_pre[k];
-        const long long x = s_r0[k] + ro;
-        const SpikeRec<T> rec = s_spk[k];
-        const int b = c.divN.div(rec.idx);
-        const EdgeRec<T> ed = ld_edge(F.net.er + x);
-        const int jt = ed.col;
-        const T w = ed.w;
-        const T d = ed.d;
-        const T t_post = rec.t + d;
-        const int ds = delivery_step_coded(t_post, (unsigned short)ed.code, c.dt, m);
-        T ws, wm;
-        if (F.exact) {
-          const T phi = (T)ds * c.dt - t_post;
-          ws = w * eq_exp_t(-phi * c.inv_tau_s);
-          wm = w * eq_exp_t(-phi * c.inv_tau_m);
-        } else {
-          ws = w;
-          wm = (T)0;
-        }
-        const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
-        if (F.kind == EQ_KIND_LOSSYRING) {
-          // LossyRingQueue.enqueue (queues.py:160-176): slot = step % capacity,
-          // i.e. the event is popped at the first step >= now = m+1 in its due
-          // step's residue class; add straight into that slot (order-free fixed
-          // point).  The ring has capacity+1 physical slots so slot m, popped
-          // in this phase by other CTAs, is never a target here.
-          int off = ds - (m + 1);
-          if (off >= A.cap_ref) off %= A.cap_ref;
-          const int se = m + 1 + off;
-          long long* sl = F.ring + ((size_t)b * A.cap + (size_t)(se % A.cap)) * F.N * P::kSlotWords +
-                          (size_t)jt * P::kSlotWords;
-          if (P::kSlotWords == 1) {
-            red_add(sl, pack2(q1, q2));
+      // EV events in flight per thread: their edge-record loads, then their
+      // slot atomics (the returned slots) are issued back to back
+      constexpr int EV = 1;   // 2 or 3 in flight spill at the 64-register budget and
+                              // measured slower (C4 heap[16] fwd 317 -> 345 ms at 2)
+      for (int f0 = tid; f0 < total; f0 += EV * NT) {
+        int kk[EV], jt[EV], ds[EV], ro[EV], bb[EV];
+        long long xx[EV], q1[EV], q2[EV];
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          const int f = f0 + e * NT;
+          kk[e] = -1;
+          if (f >= total) continue;
+          const int k = find_row(s_pre, nb, f);
+          kk[e] = k;
+          ro[e] = f - s_pre[k];
+          xx[e] = s_r0[k] + ro[e];
+          const EdgeRec<T> ed = ld_edge(F.net.er + xx[e]);
+          const SpikeRec<T> rec = s_spk[k];
+          bb[e] = c.divN.div(rec.idx);
+          jt[e] = ed.col;
+          const T t_post = rec.t + ed.d;
+          ds[e] = delivery_step_coded(t_post, (unsigned short)ed.code, c.dt, m);
+          T ws, wm;
+          if (F.exact) {
+            const T phi = (T)ds[e] * c.dt - t_post;
+            ws = ed.w * eq_exp_t(-phi * c.inv_tau_s);
+            wm = ed.w * eq_exp_t(-phi * c.inv_tau_m);
           } else {
-            red_add(sl, q1);
-            red_add(sl + 1, q2);
+            ws = ed.w;
+            wm = (T)0;
+          }
+          q1[e] = P::q(ws, c.scale);
+          q2[e] = P::q(wm, c.scale);
+        }
+        if (F.kind == EQ_KIND_LOSSYRING) {
+#pragma unroll
+          for (int e = 0; e < EV; ++e) {
+            if (kk[e] < 0) continue;
+            // LossyRingQueue.enqueue (queues.py:160-176): slot = step % capacity,
+            // i.e. the event is popped at the first step >= now = m+1 in its due
+            // step's residue class; add straight into that slot (order-free fixed
+            // point).  The ring has capacity+1 physical slots so slot m, popped
+            // in this phase by other CTAs, is never a target here.
+            int off = ds[e] - (m + 1);
+            if (off >= A.cap_ref) off %= A.cap_ref;
+            const int se = m + 1 + off;
+            long long* sl = F.ring + ((size_t)bb[e] * A.cap + (size_t)(se % A.cap)) * F.N * P::kSlotWords +
+                            (size_t)jt[e] * P::kSlotWords;
+            if (P::kSlotWords == 1) {
+              red_add(sl, pack2(q1[e], q2[e]));
+            } else {
+              red_add(sl, q1[e]);
+              red_add(sl + 1, q2[e]);
+            }
           }
           continue;
         }
         // append to the target's arrival list (slot from its counter; the
         // segment holds all in-edges, so it cannot overflow)
-        const int slot = atomicAdd(A.acnt + ((size_t)par * F.B + b) * F.N + jt, 1);
-        Arrival<T> ar;
-        ar.x = (int)x;
-        ar.tag = (int)(s_off + k0 + k);
-        ar.due = ds;
-        ar.ro = ro;
-        if constexpr (sizeof(T) == 4) {
-          ar.p = pack2(q1, q2);
-          ar.pad = 0;
-        } else {
-          ar.ps = q1;
-          ar.pm = q2;
+        int slot[EV];
+        long long cs[EV];
+#pragma unroll
+        for (int e = 0; e < EV; ++e)
+          if (kk[e] >= 0) {
+            slot[e] = atomicAdd(A.acnt + ((size_t)par * F.B + bb[e]) * F.N + jt[e], 1);
+            cs[e] = __ldg(A.csc_off + jt[e]);
+          }
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          if (kk[e] < 0) continue;
+          Arrival<T> ar;
+          ar.x = (int)xx[e];
+          ar.tag = (int)(s_off + k0 + kk[e]);
+          ar.due = ds[e];
+          ar.ro = ro[e];
+          if constexpr (sizeof(T) == 4) {
+            ar.p = pack2(q1[e], q2[e]);
+            ar.pad = 0;
+          } else {
+            ar.ps = q1[e];
+            ar.pm = q2[e];
+          }
+          A.alist[((size_t)par * F.B + bb[e]) * A.E + cs[e] + slot[e]] = ar;
         }
-        A.alist[((size_t)par * F.B + b) * A.E + __ldg(A.csc_off + jt) + slot] = ar;
       }
     }
 }
@@ -454,7 +488,9 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
       // the queue lines a step's inserts and pops will walk, fetched into L2
       // together: the structure's dependent chains then miss DRAM once
       auto prefetch_queue = [&](int qidx, const int4& qm, int qn) {
-        if (qn > 0 || (!last && qm.x > 0 && qm.w == m)) {
+        // a full queue drops its arrivals without reading the structure:
+        // only pops and accepting inserts walk its lines
+        if ((qn > 0 && qm.x < A.cap) || (!last && qm.x > 0 && qm.w == m)) {
           const char* qb = reinterpret_cast<const char*>(A.q + (size_t)qidx * A.cap);
           const int span = qm.x + qn < A.cap ? qm.x + qn : A.cap;
           const int first = F.kind == EQ_KIND_BINARYHEAP ? 0 : qm.y;

@@ -1,8 +1,12 @@
 // eq_bq.cuh — the bounded queue kinds, FIFORing (queues.py:184-260),
 // BinaryHeap (queues.py:481-571) and SortedArray (queues.py:308-403), for
 // capacities up to kBqMaxCap: per-neuron queues kept in HBM between steps and
-// STAGED IN SHARED MEMORY for each step's operations (larger capacities use
-// the HBM-resident structures of eq_bounded.cuh).
+// STAGED IN SHARED MEMORY for each step's operations, arrivals grouped by an
+// in-kernel counting sort.  Opt-in (eq_config.staged_queues): parity-green
+// like the HBM-resident structures of eq_bounded.cuh, but measured slower on
+// B200 (C2 heap[64] fwd 76 vs 44 ms, C4 heap[16] 506 vs 317 ms: the inbox
+// atomics and the per-round stalls of the queue pass cost more than the
+// dependent HBM round trips they replace — DESIGN.md §6.4).
 //
 // Queue q = trial * N + j, storage capacity C (the capacity rounded up to 4):
 //   keys[q][C]  uint32 (due mod 2^24) << 8 | slot, entries [0, count):
@@ -14,6 +18,13 @@
 //   qdue[q]     the queue's next due step (INT_MAX when empty)
 //
 // Phase m of k_forward_bq, one grid barrier per step:
+//   0. arrival sort: the arrivals of step m-1 sit in this CTA's inbox in
+//      arrival order (every producer appended with one atomic on the owner's
+//      counter, and counted the target); an in-kernel counting sort — one
+//      radix pass on the target, a block scan of the per-target counts, a
+//      scatter of inbox positions — groups them by target (the segmented
+//      sort; the edge order inside a target's segment is the insertion order
+//      below).  Inbox, counts and index stay L2-resident (one step's arrivals).
 //   1. queue pass, over the CTA's queues in chunks: a vectorised scan of qdue
 //      and the arrival counters finds the busy queues (a pop due at m, or
 //      arrivals of step m-1) and compacts them into a shared-memory list;
@@ -26,7 +37,7 @@
 //   2. neuron pass: eq_ring.cuh's neuron_side (vectorised LIF over all owned
 //      neurons, popping acc[m & 1]) — the ring kind's code, unchanged.
 //   3. fan-out of the CTA's own crossings of step m (from its log chunk) into
-//      the targets' arrival lists, for insertion at phase m+1.
+//      the owners' inboxes, for insertion at phase m+1.
 // Pops sum fixed-point payloads, so ties among equal due steps may sit in any
 // order: accepted sets, popped sums and pending contents equal the reference's.
 #pragma once
@@ -51,6 +62,21 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// One arrival in an owner's inbox: edge x (the reference's arrival order
+// within a step is ascending x), due step, flat target, drop-bit id (log
+// position * maxdeg + row offset), fixed-point payload.
+template <typename T> struct InArr;
+template <> struct alignas(32) InArr<float> {
+  int x, due, tgt, pad;
+  long long id;
+  long long p;
+};
+template <> struct alignas(8) InArr<double> {
+  int x, due, tgt, pad;
+  long long id;
+  long long ps, pm;
+};
 
 struct BqState {
   int count, tail;            // tail: FIFO tail key (queues.py:220-224)
@@ -222,9 +248,10 @@ __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>&
   const int4 mt = Q.meta[idx];
   const int qd = Q.qdue[idx];
   const bool ins = m - 1 >= A.insert_first && m >= 1;
-  int* cntp = A.acnt + ((size_t)((m - 1) & 1) * F.B + b) * F.N + j;
+  const int par = (m - 1) & 1;
+  int* cntp = A.acnt + ((size_t)par * F.B + b) * F.N + j;
   const int narr = ins ? *cntp : 0;
-  const long long acs = narr > 0 ? __ldg(A.csc_off + j) : 0;
+  const int a_end = narr > 0 ? A.aoff[idx] : 0;
   BqState st;
   st.count = mt.x;
   st.mask = ((unsigned long long)(unsigned)mt.z << 32) | (unsigned long long)(unsigned)mt.y;
@@ -232,11 +259,12 @@ __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>&
   const bool pop_due = !last && st.count > 0 && qd == m;
   const bool can_ins = narr > 0 && st.count < A.cap;
   unsigned* gk = A.keys + (size_t)idx * C;
-  const Arrival<T>* lst = A.alist + ((size_t)((m - 1) & 1) * F.B + b) * A.E + acs;
+  const int cta = blockIdx.x;
+  const InArr<T>* inb = reinterpret_cast<const InArr<T>*>(A.inbox) + ((size_t)par * F.G + cta) * A.in_cap;
+  const int* ai = A.aidx + (size_t)cta * A.in_cap + (a_end - narr);
   if (pop_due || can_ins) {                          // stage the occupied keys
     for (int k = 0; k < st.count; k += 4) cp_async16(sk + k, gk + k);
   }
-  for (int k = 0; k < narr && k < 4; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(lst + k));
   cp_async_wait_all();
   PT* const pay = Q.pay + (size_t)idx * C;
   bool dirty = false;
@@ -249,7 +277,7 @@ __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>&
       if (can_ins) {
         int bx = 0x7fffffff;
         for (int k = 0; k < narr; ++k) {
-          const int x = lst[k].x;
+          const int x = inb[ai[k]].x;
           if (x > last_x && x < bx) {
             bx = x;
             best = k;
@@ -257,7 +285,7 @@ __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>&
         }
         last_x = bx;
       }
-      const Arrival<T> a = lst[best];
+      const InArr<T> a = inb[ai[best]];
       int rc;
       if (can_ins) {
         PT p;
@@ -272,7 +300,7 @@ __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>&
         raise_error(F.err, EQ_ERR_CAPABILITY, m, b, j);
       } else if (rc == 1) {
         drops += 1;
-        const long long id = (long long)a.tag * A.maxdeg + a.ro;
+        const long long id = a.id;
         if (id < A.drop_cap) atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
         else raise_error(F.err, EQ_ERR_CAPACITY, m - 1, b, j);
       }
@@ -305,10 +333,10 @@ __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>&
   }
 }
 
-// Fan-out of this CTA's crossings of step m (its log chunk) into the targets'
-// arrival lists: one 32-byte record {edge, log position, due, row offset,
-// payload} per event at a slot from the target's counter inside its in-edge
-// segment (cannot overflow), inserted in edge order by the owner at phase m+1.
+// Fan-out of this CTA's crossings of step m (its log chunk) into the owners'
+// inboxes: one record {edge, due, target, drop id, payload} per event at a
+// position from the owner's counter, plus the target's arrival count; the
+// owner sorts and inserts them in edge order at phase m+1.
 template <typename T, int NT>
 __device__ __forceinline__ void bq_fanout(const BndArgs<T>& A, int m, int cta, int tid, SpikeRec<T>* s_spk,
                                           long long* s_r0, int* s_pre) {
@@ -344,20 +372,26 @@ __device__ __forceinline__ void bq_fanout(const BndArgs<T>& A, int m, int cta, i
         wm = (T)0;
       }
       const long long q1 = P::q(ws, c.scale), q2 = P::q(wm, c.scale);
-      const int slot = atomicAdd(A.acnt + ((size_t)par * F.B + b) * F.N + jt, 1);
-      Arrival<T> ar;
+      const int tgt = b * F.N + jt;
+      const int owner = A.divPer.div(tgt);
+      InArr<T> ar;
       ar.x = (int)x;
-      ar.tag = (int)(L0 + k0 + k);
       ar.due = ds;
-      ar.ro = ro;
+      ar.tgt = tgt;
+      ar.pad = 0;
+      ar.id = (L0 + k0 + k) * (long long)A.maxdeg + ro;
       if constexpr (sizeof(T) == 4) {
         ar.p = pack2(q1, q2);
-        ar.pad = 0;
       } else {
         ar.ps = q1;
         ar.pm = q2;
       }
-      A.alist[((size_t)par * F.B + b) * A.E + __ldg(A.csc_off + jt) + slot] = ar;
+      const int pos = atomicAdd(A.in_cnt + par * F.G + owner, 1);
+      if (pos < A.in_cap)
+        reinterpret_cast<InArr<T>*>(A.inbox)[((size_t)par * F.G + owner) * A.in_cap + pos] = ar;
+      else
+        raise_error(F.err, EQ_ERR_CAPACITY, m, b, jt);
+      atomicAdd(A.acnt + (size_t)par * F.B * F.N + tgt, 1);    // the owner's counting sort
     }
   }
 }
@@ -404,6 +438,37 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bq(BndArgs<T> A) {
     if (!last) tl_mark(F.tl, m, F.G, cta, 0);
     const bool ins = m - 1 >= A.insert_first && m >= 1;
     const int* acnt = A.acnt + (size_t)((m - 1) & 1) * F.B * F.N;
+    // ---------------- 0. arrival sort (counting sort of the inbox by target)
+    if (ins) {
+      int carry = 0;
+      for (long long cb = begin; cb < end; cb += kBqChunk) {
+        int c4[4], sum = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const long long q = cb + 4 * tid + e;
+          c4[e] = (q < end && q < cb + kBqChunk) ? acnt[q] : 0;
+          sum += c4[e];
+        }
+        int off;
+        const int tot = block_exclusive_scan<NT>(sum, off, s_warp);
+        off += carry;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const long long q = cb + 4 * tid + e;
+          if (q < end && q < cb + kBqChunk) A.aoff[q] = off;   // run start; the scatter advances it to the end
+          off += c4[e];
+        }
+        carry += tot;
+      }
+      __syncthreads();
+      const int par = (m - 1) & 1;
+      const int n_in = A.in_cnt[par * F.G + cta];
+      const InArr<T>* inb = reinterpret_cast<const InArr<T>*>(A.inbox) + ((size_t)par * F.G + cta) * A.in_cap;
+      int* aix = A.aidx + (size_t)cta * A.in_cap;
+      for (int r = tid; r < n_in && r < A.in_cap; r += NT) aix[atomicAdd(A.aoff + inb[r].tgt, 1)] = r;
+      __syncthreads();
+      if (tid == 0) A.in_cnt[par * F.G + cta] = 0;
+    }
     // ---------------- 1. queue pass
     for (long long cb = begin; cb < end; cb += kBqChunk) {
       int flags = 0;

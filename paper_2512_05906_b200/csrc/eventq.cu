@@ -136,6 +136,11 @@ struct eq_handle {
   unsigned* qkeys = nullptr;
   void* qpay = nullptr;
   int* qdue = nullptr;
+  void* inbox = nullptr;       // [2][G][in_cap] owner inboxes
+  int* in_cnt = nullptr;       // [2][G]
+  long long in_cap = 0;        // max over CTAs of the in-degree sum of its queues (lossless bound)
+  int* aoff = nullptr;         // [B*N]
+  int* aidx = nullptr;         // [G][in_cap]
   int maxdeg = 1;               // largest CSR row (bounded kinds: event id = log position * maxdeg + row offset)
   unsigned* drop_bits = nullptr;
   long long drop_cap = 0;
@@ -861,6 +866,12 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
     Bk.pay = h->qpay;
     Bk.C = h->C;
     Bk.qdue = h->qdue;
+    Bk.inbox = h->inbox;
+    Bk.in_cnt = h->in_cnt;
+    Bk.in_cap = h->in_cap;
+    Bk.aoff = h->aoff;
+    Bk.aidx = h->aidx;
+    Bk.divPer = FastDiv((unsigned)h->per);
     void* bargs[] = {&Bk};
     if (h->staged) {
       const void* kq = (const void*)k_forward_bq<T, kNT, kU>;
@@ -1116,19 +1127,41 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   if (qbytes > ((size_t)96 << 30))
     return fail(h, EQ_ERR_CONFIGURATION, "queue storage " + std::to_string(qbytes >> 20) +
                                              " MiB exceeds 96 GiB; set eq_config.capacity");
-  // csc_off = exclusive scan of in-degree: target j's arrival list is its
-  // in-edge segment [csc_off[j], csc_off[j+1]) (no step delivers more)
-  size_t tmp_bytes = 0;
-  void* tmp = nullptr;
-  EQ_CUDA(h, ensure(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
-  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, indeg, h->csc_off, N + 1, s));
-  EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
-  EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, indeg, h->csc_off, N + 1, s));
-  release(h, tmp);
-  h->launches += 1;
-  EQ_CUDA(h, ensure(h, &h->alist, (size_t)2 * B * E * sizeof(Arrival<float>)));   // 32 bytes in both precisions
   EQ_CUDA(h, ensure(h, (void**)&h->acnt, (size_t)2 * B * N * sizeof(int)));
-  h->staged = h->cap <= kBqMaxCap;
+  h->staged = c.staged_queues != 0 && h->cap <= kBqMaxCap;
+  if (!h->staged) {
+    // csc_off = exclusive scan of in-degree: target j's arrival list is its
+    // in-edge segment [csc_off[j], csc_off[j+1]) (no step delivers more)
+    size_t tmp_bytes = 0;
+    void* tmp = nullptr;
+    EQ_CUDA(h, ensure(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
+    EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, indeg, h->csc_off, N + 1, s));
+    EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
+    EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, indeg, h->csc_off, N + 1, s));
+    release(h, tmp);
+    h->launches += 1;
+    EQ_CUDA(h, ensure(h, &h->alist, (size_t)2 * B * E * sizeof(Arrival<float>)));   // 32 bytes in both precisions
+  } else {
+    // owner inboxes: a step delivers at most one event per in-edge, so a CTA's
+    // inbox needs the in-degree sum of its queues
+    std::vector<int> deg(N);
+    EQ_CUDA(h, cudaMemcpyAsync(deg.data(), indeg, (size_t)N * sizeof(int), cudaMemcpyDeviceToHost, s));
+    EQ_CUDA(h, cudaStreamSynchronize(s));
+    std::vector<long long> pre(N + 1, 0);
+    for (int j = 0; j < N; ++j) pre[j + 1] = pre[j] + deg[j];
+    auto upto = [&](long long idx) { return (idx / N) * pre[N] + pre[idx % N]; };   // sum over flat [0, idx)
+    long long mx = 1;
+    for (int cta = 0; cta < h->G; ++cta) {
+      const long long a = (long long)cta * h->per, b = std::min<long long>(a + h->per, h->total);
+      if (b > a) mx = std::max(mx, upto(b) - upto(a));
+    }
+    h->in_cap = mx;
+    const size_t rec = c.precision == 32 ? sizeof(InArr<float>) : sizeof(InArr<double>);
+    EQ_CUDA(h, ensure(h, &h->inbox, (size_t)2 * h->G * h->in_cap * rec));
+    EQ_CUDA(h, ensure(h, (void**)&h->in_cnt, (size_t)2 * h->G * sizeof(int)));
+    EQ_CUDA(h, ensure(h, (void**)&h->aoff, (size_t)B * N * sizeof(int)));
+    EQ_CUDA(h, ensure(h, (void**)&h->aidx, (size_t)h->G * h->in_cap * sizeof(int)));
+  }
   if (h->staged) {
     h->C = (h->cap + 3) / 4 * 4;
     const size_t pb = c.precision == 32 ? sizeof(long long) : sizeof(longlong2);
@@ -1447,6 +1480,7 @@ int eq_reset(eq_handle* h, void* stream) {
     EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
     if (h->staged) {
       k_meta_init_bq<<<592, 256, 0, s>>>(h->meta, h->qdue, (long long)B * N);
+      EQ_CUDA(h, cudaMemsetAsync(h->in_cnt, 0, (size_t)2 * h->G * sizeof(int), s));
       EQ_CUDA(h, cudaMemsetAsync(h->acc, 0, (size_t)2 * h->total * (h->cfg.precision == 32 ? 1 : 2) *
                                                 sizeof(long long), s));
     } else

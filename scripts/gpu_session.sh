@@ -45,3 +45,23 @@ for p in $PARTS; do
       echo "c5 concurrent rc=$?"; tail -1 gpurun_out/${TAG}_c5_conc.json; tail -3 gpurun_out/${TAG}_c5_conc.err ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    bounded)
+      timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_r2.py -m gpu -q -x -k "(bounded or fifo or log_grows) and not c4" > gpurun_out/${TAG}_bounded.log 2>&1
+      echo "bounded rc=$?"; tail -15 gpurun_out/${TAG}_bounded.log ;;
+    bvariants)
+      OUT=gpurun_out/${TAG}_bvariants.jsonl; : > $OUT
+      for spec in "C2 32 binaryheap 64" "C2 32 sortedarray 64" "C2 32 fiforing 64 32,32" "C4 4 binaryheap 16" "C4 4 sortedarray 32"; do
+        set -- $spec
+        extra=""; [ -n "$5" ] && extra="--delays $5"
+        timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-variants --config $1 --trials $2 --kind $3 --capacity $4 $extra 2>>${OUT%.jsonl}.err | tail -1 >> $OUT
+      done
+      python -c "
+import json
+for l in open('$OUT'):
+    d=json.loads(l); r=d['roofline']; c=d['config']
+    print(c['workload'][:70], '%.3e'%d['value'], 'fwd %.1f bwd %.1f frac %.3f drops %d'%(r['fwd_ms'], r['bwd_ms'], r['frac'], c['drops_per_gpu']))
+" ;;
+  esac
+done

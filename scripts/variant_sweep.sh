@@ -5,7 +5,7 @@ OUT=${1:-gpurun_out/variants.jsonl}
 K=${2:-3}
 W=${3:-3}
 : > "$OUT"
-run() { python bench.py --steps $K --warmup $W --no-cpu "$@" 2>>"${OUT%.jsonl}.err" | tail -1 >> "$OUT"; }
+run() { python bench.py --steps $K --warmup $W --no-cpu --no-variants "$@" 2>>"${OUT%.jsonl}.err" | tail -1 >> "$OUT"; }
 run --config C2 --trials 32 --kind ring
 run --config C2 --trials 32 --kind binaryheap --capacity 64
 run --config C2 --trials 32 --kind sortedarray --capacity 64

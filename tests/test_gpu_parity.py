@@ -24,10 +24,10 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-def _engine(net, mask, amp, B, T, precision, kind="ring", refractory=0, capacity=0, exact=True):
+def _engine(net, mask, amp, B, T, precision, kind="ring", refractory=0, capacity=0, exact=True, staged=False):
     from paper_2512_05906_b200.engine import Engine
     lif = wl.LIFConfig(refractory_steps=refractory, exact_delivery=exact)
-    eng = Engine(net.n, B, T, kind=kind, precision=precision, lif=lif, capacity=capacity or 0)
+    eng = Engine(net.n, B, T, kind=kind, precision=precision, lif=lif, capacity=capacity or 0, staged_queues=staged)
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     eng.set_drive(mask, amp)
     return eng
@@ -206,8 +206,8 @@ BOUNDED = ["dense_heap_n8", "dense_sorted_n8", "dense_fifo_n8", "dense_heap_cap3
            "dense_fifo_cap2_n12", "dense_sorted_plain_cap3_n12"]
 
 
-def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=True, exact=True):
-    eng = _engine(net, mask, amp, B, T, precision, kind=kind, capacity=capacity, exact=exact)
+def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=True, exact=True, staged=False):
+    eng = _engine(net, mask, amp, B, T, precision, kind=kind, capacity=capacity, exact=exact, staged=staged)
     out = eng.forward()
     s = OracleSession(n=net.n, n_trials=B, t_steps=T, kind=kind, mode="device", precision=precision,
                       frac_bits=eng.frac_bits, capacity=capacity or 0, exact_delivery=exact)
@@ -225,13 +225,17 @@ def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=T
     return eng, out, ref
 
 
+@pytest.mark.parametrize("staged", [False, True])
 @pytest.mark.parametrize("precision", [32, 64])
 @pytest.mark.parametrize("name", BOUNDED)
-def test_bounded_kinds_bitwise_vs_oracle(name, precision):
+def test_bounded_kinds_bitwise_vs_oracle(name, precision, staged):
+    """Both implementations of the bounded kinds: HBM-resident structures and
+    (capacity <= 64) the shared-memory staged queues with the in-kernel
+    arrival sort."""
     case = BY_NAME[name]
     net, mask, amp = case.inputs()
     eng, out, _ = _compare_bounded(net, mask, amp, 1, case.t_steps, precision, case.kind, case.capacity,
-                                   exact=case.exact)
+                                   exact=case.exact, staged=staged)
     # reverse: bitwise at one trial, dropped events skipped exactly
     vbar = (2.0 * (out["v"].double() - 0.25)).to(out["v"].dtype)
     gw, gd, ga = (x.cpu().numpy() for x in eng.backward(vbar))
@@ -376,15 +380,16 @@ def test_c3_full_size_trials_are_independent():
     assert np.array_equal(c[0], c[2])
 
 
+@pytest.mark.parametrize("staged", [False, True])
 @pytest.mark.parametrize("kind,cap", [("binaryheap", 8), ("sortedarray", 8), ("binaryheap", 64)])
-def test_bounded_c2_size_bitwise_vs_oracle(kind, cap):
+def test_bounded_c2_size_bitwise_vs_oracle(kind, cap, staged):
     """BASELINE config 2 sizes (10k neurons, K = 100, delays 1..64, T = 1000),
     two trials, fp32: capacity 8 drops most events (the memory-pressure
     regime), capacity 64 almost none.  Raster, V, I, pending queue sums,
     counters bitwise = oracle; the reverse pass skips exactly the dropped
     events (gradients within 1e-12 of scale: fp64 atomics reorder the trial sum)."""
     wk = wl.make_workload("C2", n_trials=2)
-    eng, out, ref = _compare_bounded(wk.net, wk.mask, wk.amp, 2, wk.t_steps, 32, kind, cap)
+    eng, out, ref = _compare_bounded(wk.net, wk.mask, wk.amp, 2, wk.t_steps, 32, kind, cap, staged=staged)
     c = eng.counters()
     if cap == 8:
         assert c[:, 2].sum() > 0.3 * c[:, 1].sum(), "capacity 8 should drop a large share of events"

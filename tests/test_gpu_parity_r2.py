@@ -25,10 +25,10 @@ from paper_2512_05906_b200 import workload as wl
 pytestmark = pytest.mark.gpu
 
 
-def _engine(net, mask, amp, B, T, precision=32, kind="ring", capacity=0, max_spikes=0, exact=True):
+def _engine(net, mask, amp, B, T, precision=32, kind="ring", capacity=0, max_spikes=0, exact=True, staged=False):
     from paper_2512_05906_b200.engine import Engine
     eng = Engine(net.n, B, T, kind=kind, precision=precision, capacity=capacity, max_spikes=max_spikes,
-                 lif=wl.LIFConfig(exact_delivery=exact))
+                 lif=wl.LIFConfig(exact_delivery=exact), staged_queues=staged)
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     eng.set_drive(mask, amp)
     return eng
@@ -103,8 +103,8 @@ def test_bucket_overflow_spills_to_dram_ring_bitwise(precision):
     _assert_forward_equal(eng, out2, ref)
 
 
-@pytest.mark.parametrize("kind,cap", [("ring", 0), ("binaryheap", 4)])
-def test_spike_log_grows_mid_run_bitwise(kind, cap):
+@pytest.mark.parametrize("kind,cap,staged", [("ring", 0, False), ("binaryheap", 4, False), ("binaryheap", 4, True)])
+def test_spike_log_grows_mid_run_bitwise(kind, cap, staged):
     """max_spikes far below the run's spike count: the launch pauses at a step
     boundary whenever one more step could overflow, the log (and for bounded
     kinds the drop bits indexed by it) doubles, the run resumes — bitwise equal
@@ -113,7 +113,7 @@ def test_spike_log_grows_mid_run_bitwise(kind, cap):
     B, T = 2, 400
     mask = wl.drive_masks(500, B, T, 1e-3, seed0=41)
     amp = np.full(500, 12.0)
-    eng = _engine(net, mask, amp, B, T, 32, kind=kind, capacity=cap, max_spikes=1500)
+    eng = _engine(net, mask, amp, B, T, 32, kind=kind, capacity=cap, max_spikes=1500, staged=staged)
     out = eng.forward()
     cap0, grows = eng.log_capacity()
     assert grows >= 1 and cap0 >= eng.spike_count()
@@ -210,9 +210,10 @@ def _c4_inputs():
     return _C4["net"]
 
 
-@pytest.mark.parametrize("kind", ["binaryheap", "sortedarray"])
-@pytest.mark.parametrize("cap", [16, 32])
-def test_c4_full_size_bounded_with_drops_bitwise(kind, cap):
+@pytest.mark.parametrize("kind,cap,staged", [("binaryheap", 16, False), ("binaryheap", 32, False),
+                                              ("sortedarray", 16, False), ("sortedarray", 32, False),
+                                              ("binaryheap", 16, True)])
+def test_c4_full_size_bounded_with_drops_bitwise(kind, cap, staged):
     """C4 at full size — 1M neurons, K = 100, delays 1..256 — with the heap and
     sorted kinds at capacity 16 / 32 (the memory-pressure regime: most events
     are dropped), 2 trials, T = 300, fp32: forward bitwise incl. drops and the
@@ -222,7 +223,7 @@ def test_c4_full_size_bounded_with_drops_bitwise(kind, cap):
     B, T = 2, 300
     mask = poisson_drive_device(net.n, B, T, 1e-3, 16e-3, 12e-3, 77, device=0).cpu().numpy().view(np.uint32)
     amp = np.full(net.n, 12.0)
-    eng = _engine(net, mask, amp, B, T, 32, kind=kind, capacity=cap)
+    eng = _engine(net, mask, amp, B, T, 32, kind=kind, capacity=cap, staged=staged)
     out = eng.forward()
     s = _oracle(net, mask, amp, B, T, 32, eng.frac_bits, kind=kind, capacity=cap)
     ref = s.forward()
