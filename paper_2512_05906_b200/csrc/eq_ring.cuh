@@ -703,6 +703,52 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
   }
 }
 
+// Delivery of this CTA's calendar bucket m+1 into acc[(m+1)&1] (events due at
+// m+1 it appended in earlier phases; the bucket receives no appends in phase
+// m), shared by both warp groups: each warp claims 256-entry chunks from a
+// shared counter as soon as its own side's work is done, so the delivery
+// fills whichever side finishes first instead of lengthening the event side.
+template <typename T>
+__device__ __forceinline__ void deliver_bucket(const FwdArgs<T>& A, const int m, const int cta, const int n,
+                                               int* s_dq) {
+  typedef Prec<T> P;
+  constexpr int DV = 8;
+  const int lane = threadIdx.x & 31;
+  const int bin = (m + 1) % A.NB;
+  const longlong2* bk = reinterpret_cast<const longlong2*>(A.bk + ((size_t)cta * A.NB + bin) * A.cap_b * bk_words<T>());
+  long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
+  while (true) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(s_dq, DV * 32);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    longlong2 ev[DV], ev2[DV];
+#pragma unroll
+    for (int e = 0; e < DV; ++e) {
+      const int k = base + e * 32 + lane;
+      ev[e] = make_longlong2(-1, 0);
+      if (k < n) {
+        if (P::kSlotWords == 1) {
+          ev[e] = __ldcs(bk + k);
+        } else {
+          ev[e] = __ldcs(bk + 2 * (size_t)k);
+          ev2[e] = __ldcs(bk + 2 * (size_t)k + 1);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < DV; ++e) {
+      if (ev[e].x < 0) continue;
+      if (P::kSlotWords == 1) {
+        red_acc(accn + ev[e].x, ev[e].y);
+      } else {
+        red_acc(accn + 2 * (size_t)ev[e].x, ev[e].y);
+        red_acc(accn + 2 * (size_t)ev[e].x + 1, ev2[e].x);
+      }
+    }
+  }
+}
+
 // After the barrier of phase m: could the next step overflow the spike log?
 // (one step logs at most `total` spikes).  Read from the value the barrier
 // published, so every CTA decides the same.
@@ -728,6 +774,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   __shared__ int s_n;
   __shared__ long long s_off;
   __shared__ unsigned long long s_ctr[kTr][3];
+  __shared__ int s_dq;                            // next unclaimed entry of the bucket being delivered
 
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;
@@ -739,6 +786,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   if (A.no_pause && ld_volatile(A.err) != 0) return;   // an earlier asynchronous window failed
 
   if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
+  if (tid == 0) s_dq = 0;
   if (A.kind == EQ_KIND_RING)
     for (int k = tid; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
   if (tid == 0) s_n = 0;
@@ -765,52 +813,23 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   int m1 = A.m1;
   for (int m = A.m0; m <= m1; ++m) {
     tl_mark(A.tl, m < m1 ? m : m1 - 1, A.G, cta, m < m1 ? 0 : 7);
+    // bucket m+1 (complete: phase m appends only to later buckets), delivered
+    // by both sides once their own work is done (deliver_bucket)
+    int dn = 0;
+    if (m > A.m0 && A.kind == EQ_KIND_RING) {
+      dn = s_bin[(m + 1) % A.NB];
+      dn = dn < A.cap_b ? dn : (int)A.cap_b;
+    }
+    // fp64: the neuron side (two neurons per thread, 16-byte slots) finishes
+    // well before the fan-out, so both sides share the delivery (fwd 81.9 ->
+    // 76.8 ms at C3 x 24); fp32: the sides already finish together and the
+    // delivery goes first on the event side (sharing measured 32.8 -> 33.6 ms)
+    constexpr bool kShare = sizeof(T) == 8;
     if (tid < Ro::NF) {
       // ======================== event side
       const int gtid = tid;
-      // ---------------- (a1) deliver this CTA's bucket m+1 into acc[(m+1)&1]
-      // (L2-resident): the events due at m+1 it appended in earlier phases.
-      // Buckets are private per CTA, so appends need no global atomics; the
-      // delivery load is balanced because the fan-out shares are.
-      if (m > A.m0 && A.kind == EQ_KIND_RING) {
-        const int bin = (m + 1) % A.NB;
-        int n = s_bin[bin];
-        n = n < A.cap_b ? n : (int)A.cap_b;
-        const longlong2* bk = reinterpret_cast<const longlong2*>(
-            A.bk + ((size_t)cta * A.NB + bin) * A.cap_b * bk_words<T>());
-        long long* accn = A.acc + (size_t)((m + 1) & 1) * A.total * P::kSlotWords;
-        constexpr int DV = 8;
-        for (int q = gtid; q < n; q += DV * Ro::NF) {
-          longlong2 ev[DV], ev2[DV];
-#pragma unroll
-          for (int e = 0; e < DV; ++e) {
-            const int k = q + e * Ro::NF;
-            ev[e] = make_longlong2(-1, 0);
-            if (k < n) {
-              if (P::kSlotWords == 1) {
-                ev[e] = __ldcs(bk + k);
-              } else {
-                ev[e] = __ldcs(bk + 2 * (size_t)k);
-                ev2[e] = __ldcs(bk + 2 * (size_t)k + 1);
-              }
-            }
-          }
-#pragma unroll
-          for (int e = 0; e < DV; ++e) {
-            if (ev[e].x < 0) continue;
-            if (P::kSlotWords == 1) {
-              red_acc(accn + ev[e].x, ev[e].y);
-            } else {
-              red_acc(accn + 2 * (size_t)ev[e].x, ev[e].y);
-              red_acc(accn + 2 * (size_t)ev[e].x + 1, ev2[e].x);
-            }
-          }
-        }
-        group_sync(Ro::kBarF, Ro::NF);
-        if (gtid == 0) s_bin[bin] = 0;
-      }
-      if (m < m1) tl_mark(A.tl, m, A.G, cta, 5);
-      // ---------------- (a2) fan-out of step m-1 (and imported spikes): fwd_fanout
+      if (!kShare) deliver_bucket<T>(A, m, cta, dn, &s_dq);
+      // ---------------- fan-out of step m-1: fwd_fanout
       if (A.kind == EQ_KIND_RING && m > A.m0) {
         const int me = m - 1;                          // emitting step
         const long long L0 = ld_published(A.step_start + me), S = ld_published(A.step_start + me + 1) - L0;
@@ -818,13 +837,21 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
                                      s_pre, s_bin);
       }
       if (m < m1) tl_mark(A.tl, m, A.G, cta, 1);
-    } else if (m < m1) {
+      if (kShare) deliver_bucket<T>(A, m, cta, dn, &s_dq);
+      if (m < m1) tl_mark(A.tl, m, A.G, cta, 5);
+    } else {
       // ======================== neuron side
       const int gtid = tid - Ro::NF;
-      neuron_side<T, NT, U, NF>(A, m, cta, gtid, begin, end, b_first, A.kind == EQ_KIND_RING, s_own, s_n, s_off,
-                                s_ctr, spill, s_st);
+      if (m < m1)
+        neuron_side<T, NT, U, NF>(A, m, cta, gtid, begin, end, b_first, A.kind == EQ_KIND_RING, s_own, s_n, s_off,
+                                  s_ctr, spill, s_st);
+      if (kShare) deliver_bucket<T>(A, m, cta, dn, &s_dq);
     }
     __syncthreads();
+    if (tid == 0) {
+      s_dq = 0;
+      if (dn > 0 || (m > A.m0 && A.kind == EQ_KIND_RING)) s_bin[(m + 1) % A.NB] = 0;
+    }
     if (m == m1) break;
     tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err, A.step_start + m + 1, A.log_count, nullptr,

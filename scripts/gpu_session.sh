@@ -65,3 +65,30 @@ for l in open('$OUT'):
 " ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    sanitize)
+      bash scripts/sanitize.sh gpurun_out/${TAG}_sanitize ;;
+    fullbench)
+      timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_fullbench.log 2>&1
+      echo "fullbench rc=$?"; tail -1 gpurun_out/${TAG}_fullbench.log ;;
+  esac
+done
+for p in $PARTS; do
+  case $p in
+    abfwd)
+      for r in 1 2; do
+        bash scripts/ab_args.sh "" head=scratch_lib/head.so new=paper_2512_05906_b200/lib/libeventq_b200.so
+      done
+      bash scripts/ab_args.sh "--precision 64" head=scratch_lib/head.so new=paper_2512_05906_b200/lib/libeventq_b200.so ;;
+  esac
+done
+for p in $PARTS; do
+  case $p in
+    tlfwd)
+      for lib in scratch_lib/head.so paper_2512_05906_b200/lib/libeventq_b200.so; do
+        echo "== $lib"
+        EQ_LIB_PATH=$lib timeout 600 python scripts/timeline.py --config C3 --trials 24 --steps 1000 2>&1 | tail -16
+      done ;;
+  esac
+done
