@@ -92,3 +92,14 @@ for p in $PARTS; do
       done ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ncu)
+      timeout 900 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+        --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-variants > gpurun_out/${TAG}_ncu_launch.log 2>&1
+      echo "ncu launches rc=$?"
+      timeout 1500 /usr/local/cuda/bin/ncu --set full --import-source on --clock-control none -k regex:"k_forward|k_backward" -s 2 -c 2 \
+        -o gpurun_out/${TAG}_c3x24 -f python bench.py --steps 2 --warmup 1 --no-cpu --no-variants > gpurun_out/${TAG}_ncu_full.log 2>&1
+      echo "ncu full rc=$?"; tail -3 gpurun_out/${TAG}_ncu_full.log ;;
+  esac
+done
