@@ -8,8 +8,11 @@ for the B trials this rank owns (weak scaling: B trials per GPU, trials shard
 across ranks, a final NCCL all-reduce of dL/dw and dL/dd).  `value` is
 synaptic events per second (one event = one (spike, out-edge) pair, counted on
 the device, fwd+bwd counted once) over the whole job; `e2e` is the same metric
-through the public API with the drive mask copied from pinned host memory and
-the loss + gradients read back every step.
+through the public API with the drive mask copied from pinned host memory, the
+(device-resident) network handed to the engine as every training step does
+(validation + edge repack), and the loss + gradients read back every step.
+`variants` adds the same measurement for C3 in fp64 and for the heap and
+sorted queues at C4 (memory pressure, drops), each with its roofline fraction.
 
 --impl reference times the reference's CPU path on the host cores: the
 reference is pure Python and cannot travel to the GPU box, so this runs the
@@ -422,6 +425,10 @@ def run_ours(args):
     # while step k-1 computes, and step k's loss + gradients are read back to
     # pinned host memory while step k+1 computes.  Every copy of every step is
     # inside the timed region (events on the compute stream bracket it all).
+    # the network as a training loop holds it: device-resident parameters,
+    # handed to the engine every step (what RSNNFunction.forward does)
+    net_dev = (torch.from_numpy(net.rowptr).to(dev), torch.from_numpy(net.col).to(dev),
+               torch.from_numpy(net.weight).to(dev, eng.dtype), torch.from_numpy(net.delay).to(dev, eng.dtype))
     mask_host = torch.from_numpy(mask.view(np.int32)).pin_memory()
     md = [mask_dev, torch.empty_like(mask_dev)]
     gwf = [torch.empty(net.n_edges, dtype=torch.float32, device=dev) for _ in range(2)]
@@ -456,6 +463,7 @@ def run_ours(args):
             stream.wait_event(h2d[sl])
             if k >= 2:
                 stream.wait_event(d2h[sl])           # step k-2's read-back of these buffers is done
+            eng.set_network(*net_dev)                 # validation + edge repack, as every training step does
             eng.set_drive(md[sl], amp_dev)
             out = eng.forward()
             lossd[sl].copy_(((out["v"].double() - 0.25) ** 2).sum().reshape(1))

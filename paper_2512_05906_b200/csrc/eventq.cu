@@ -175,6 +175,7 @@ struct eq_handle {
   double* bw_gd = nullptr;
   double* bw_gamp = nullptr;
   void* jvp_buf[24] = {};                         // eq_forward_jvp scratch
+  void *ns_insum = nullptr, *ns_inocc = nullptr, *ns_indeg = nullptr, *ns_stats = nullptr;   // eq_set_network scratch
   std::vector<void*> owned;
   std::vector<std::pair<void*, size_t>> sizes;   // reusable buffers
 };
@@ -1290,11 +1291,13 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   const eq_config& c = h->cfg;
   const int N = c.n_neurons;
   if (n_edges < 1) return fail(h, EQ_ERR_CONFIGURATION, "network has no edges");
-  void *insum = nullptr, *stats = nullptr, *inocc = nullptr, *indeg = nullptr;
-  EQ_CUDA(h, alloc(h, &insum, (size_t)N * sizeof(long long)));
-  EQ_CUDA(h, alloc(h, &inocc, (size_t)N * sizeof(long long)));
-  EQ_CUDA(h, alloc(h, &indeg, (size_t)(N + 1) * sizeof(int)));   // +1: exclusive scan reads n+1
-  EQ_CUDA(h, alloc(h, &stats, 5 * sizeof(long long)));
+  // validation scratch kept in the handle: the autograd shell calls this every
+  // training step (RSNNFunction.forward), so no allocation happens per call
+  EQ_CUDA(h, ensure(h, &h->ns_insum, (size_t)N * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, &h->ns_inocc, (size_t)N * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, &h->ns_indeg, (size_t)(N + 1) * sizeof(int)));   // +1: exclusive scan reads n+1
+  EQ_CUDA(h, ensure(h, &h->ns_stats, 5 * sizeof(long long)));
+  void *insum = h->ns_insum, *stats = h->ns_stats, *inocc = h->ns_inocc, *indeg = h->ns_indeg;
   long long init[5] = {1, -1LL, 0, 0, 1};
   init[1] = (long long)~0ULL;
   EQ_CUDA(h, cudaMemsetAsync(insum, 0, (size_t)N * sizeof(long long), s));
@@ -1316,10 +1319,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   long long st[5];
   EQ_CUDA(h, cudaMemcpyAsync(st, stats, sizeof st, cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));
-  release(h, insum);
-  release(h, inocc);
-  release(h, stats);
-  struct Free { eq_handle* h; void* p; ~Free() { release(h, p); } } free_indeg{h, indeg};
+
   if ((unsigned long long)st[1] != ~0ULL) {
     unsigned long long key = (unsigned long long)st[1];
     long long x = (long long)(key >> 2);
