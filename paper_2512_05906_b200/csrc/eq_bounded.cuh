@@ -282,7 +282,7 @@ template <typename T, int NT>
 __device__ __forceinline__ void bounded_log_fanout(const BndArgs<T>& A, const int m, const int cta, const int tid,
                                                    const int nspk, const int b_first, SpikeRec<T>* s_spk,
                                                    long long* s_r0, int* s_pre, SpikeRec<T>* spill, long long& s_off,
-                                                   unsigned long long (*s_ctr)[3]) {
+                                                   unsigned (*s_ctr)[3]) {
   typedef Prec<T> P;
   constexpr int kCap = FwdShared<NT, T>::kCap;
   constexpr int kTr = FwdShared<NT>::kTrials;
@@ -323,8 +323,8 @@ __device__ __forceinline__ void bounded_log_fanout(const BndArgs<T>& A, const in
         }
         const int tb = b - b_first;
         if (tb < kTr) {
-          atomicAdd(&s_ctr[tb][0], 1ULL);
-          atomicAdd(&s_ctr[tb][1], (unsigned long long)len);
+          atomicAdd(&s_ctr[tb][0], 1u);
+          atomicAdd(&s_ctr[tb][1], (unsigned)len);
         } else {
           atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b), 1ULL);
           atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 1), (unsigned long long)len);
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
   __shared__ int s_pre[kCap + 1];
   __shared__ int s_n;
   __shared__ long long s_off;
-  __shared__ unsigned long long s_ctr[kTr][3];
+  __shared__ unsigned s_ctr[kTr][3];   // per-phase counts (32-bit: native smem atomics), flushed every phase
   FwdArgs<T>& F = A.f;
 
   const int tid = threadIdx.x;
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
   const int b_first = (int)(begin / F.N);
   const StepConsts<T> c = F.c;
   SpikeRec<T>* spill = F.scratch + (size_t)cta * F.per;
-  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
+  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0u;
 
   int m1 = F.m1;   // lowered at a barrier when the spike log could overflow (pause_due)
   for (int m = F.m0; m <= m1; ++m) {
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
           insert_arrivals<T>(A, b, j, idx, m - 1, narr, acs, mt, d);
           const int tb = b - b_first;
           if (d) {
-            if (tb < kTr) atomicAdd(&s_ctr[tb][2], d);
+            if (tb < kTr) atomicAdd(&s_ctr[tb][2], (unsigned)d);
             else atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 2), d);
           }
           dirty = true;
@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
     const int nspk = s_n;
     bounded_log_fanout<T, NT>(A, m, cta, tid, nspk, b_first, s_spk, s_r0, s_pre, spill, s_off, s_ctr);
     __syncthreads();
+    flush_counters<kTr>(s_ctr, F.counters, b_first, F.B, end, F.N);
     tl_mark(F.tl, m, F.G, cta, 2);
     if (!grid_sync(F.bar, F.G, F.err, F.step_start + m + 1, F.log_count)) break;
     tl_mark(F.tl, m, F.G, cta, 3);
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bounded(BndArgs<T> A) {
     int b = b_first + tid;
     if (b < F.B && (long long)b * F.N < end) {
       for (int q = 0; q < 3; ++q)
-        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + q), s_ctr[tid][q]);
+        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + q), (unsigned long long)s_ctr[tid][q]);
     }
   }
 }

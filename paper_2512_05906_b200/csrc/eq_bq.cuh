@@ -238,7 +238,7 @@ struct BqView {                 // the staged-queue arrays of BndArgs, typed
 // staged at sk.  Returns nothing; writes acc[m & 1][idx] when events popped.
 template <typename T>
 __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>& Q, int m, bool last, int idx,
-                                           unsigned* sk, int b_first, unsigned long long (*s_ctr)[3]) {
+                                           unsigned* sk, int b_first, unsigned (*s_ctr)[3]) {
   typedef typename BqPay<T>::type PT;
   const FwdArgs<T>& F = A.f;
   const int C = A.C, kind = F.kind;
@@ -307,7 +307,7 @@ __device__ __forceinline__ void bq_process(const BndArgs<T>& A, const BqView<T>&
     }
     if (drops) {
       const int tb = b - b_first;
-      if (tb < kTr) atomicAdd(&s_ctr[tb][2], drops);
+      if (tb < kTr) atomicAdd(&s_ctr[tb][2], (unsigned)drops);
       else atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + 2), drops);
     }
   }
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bq(BndArgs<T> A) {
   __shared__ SpikeRec<T> s_own[kCapN];            // neuron pass
   __shared__ int s_n;
   __shared__ long long s_off;
-  __shared__ unsigned long long s_ctr[kTr][3];
+  __shared__ unsigned s_ctr[kTr][3];   // per-phase counts (32-bit: native smem atomics), flushed every phase
   __shared__ int s_warp[NT / 32];
   extern __shared__ __align__(16) unsigned s_dyn[];
   int* s_busy = reinterpret_cast<int*>(s_dyn);                 // [kBqChunk]
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bq(BndArgs<T> A) {
   const int C = A.C;
   const int per_round = kBqPoolWords / C < NT ? kBqPoolWords / C : NT;
   unsigned* const sk = s_pool + (tid < per_round ? tid : 0) * C;
-  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
+  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0u;
   if (tid == 0) s_n = 0;
   __syncthreads();
 
@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bq(BndArgs<T> A) {
     // ---------------- 3. fan-out of the crossings of step m
     bq_fanout<T, NT>(A, m, cta, tid, s_spk, s_r0, s_pre);
     __syncthreads();
+    flush_counters<kTr>(s_ctr, F.counters, b_first, F.B, end, F.N);
     tl_mark(F.tl, m, F.G, cta, 2);
     if (!grid_sync(F.bar, F.G, F.err, F.step_start + m + 1, F.log_count)) break;
     tl_mark(F.tl, m, F.G, cta, 3);
@@ -510,7 +511,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward_bq(BndArgs<T> A) {
     const int b = b_first + tid;
     if (b < F.B && (long long)b * F.N < end) {
       for (int q = 0; q < 3; ++q)
-        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + q), s_ctr[tid][q]);
+        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(F.counters + 3 * b + q), (unsigned long long)s_ctr[tid][q]);
     }
   }
 }

@@ -400,6 +400,23 @@ __global__ void __launch_bounds__(NT) k_import_fanout(FwdArgs<T> A) {
   for (int k = threadIdx.x; k < A.NB; k += NT) A.bk_cnt[(size_t)cta * A.NB + k] = s_bin[k];
 }
 
+// Per-trial counters of this CTA (spikes, events, drops) are counted per phase
+// in 32-bit shared memory (64-bit shared atomics are compare-and-swap loops on
+// sm_100a) and flushed into the 64-bit device counters once per phase.
+template <int kTr>
+__device__ __forceinline__ void flush_counters(unsigned (*s_ctr)[3], long long* counters, int b_first, int B,
+                                               long long end, int N) {
+  const int t = threadIdx.x;
+  if (t < kTr * 3) {
+    const int tb = t / 3, q = t % 3;
+    const unsigned v = s_ctr[tb][q];
+    const int b = b_first + tb;
+    if (v && b < B && (long long)b * N < end)
+      atomicAdd(reinterpret_cast<unsigned long long*>(counters + 3 * b + q), (unsigned long long)v);
+    s_ctr[tb][q] = 0u;
+  }
+}
+
 // Neuron side of one forward phase m (network.py:547-580): pop (the slot sums
 // waiting in acc[m&1] when acc_pop — ring, and bounded kinds whose queue stage
 // wrote them), synapse + LIF + exact crossing for the CTA's neuron-trials, clear
@@ -409,7 +426,7 @@ template <typename T, int NT, int U, int NF>
 __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, const int cta, const int gtid,
                                             const long long begin, const long long end, const int b_first,
                                             const bool acc_pop, SpikeRec<T>* s_own, int& s_n, long long& s_off,
-                                            unsigned long long (*s_ctr)[3], SpikeRec<T>* spill, T* s_st = nullptr) {
+                                            unsigned (*s_ctr)[3], SpikeRec<T>* spill, T* s_st = nullptr) {
   // s_st: the CTA's I and V kept in shared memory across the launch ([per] I,
   // then [per] V, indexed by idx - begin), or null (state in HBM)
   T* const gI = s_st ? s_st - begin : A.I;
@@ -686,9 +703,9 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
     }
     const int tb = b - b_first;
     if (tb < kTr) {
-      atomicAdd(&s_ctr[tb][0], 1ULL);
-      atomicAdd(&s_ctr[tb][1], len);
-      if (A.kind == EQ_KIND_DONOTHING) atomicAdd(&s_ctr[tb][2], len);
+      atomicAdd(&s_ctr[tb][0], 1u);
+      atomicAdd(&s_ctr[tb][1], (unsigned)len);
+      if (A.kind == EQ_KIND_DONOTHING) atomicAdd(&s_ctr[tb][2], (unsigned)len);
     } else {
       atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b), 1ULL);
       atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 1), len);
@@ -773,7 +790,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   __shared__ SpikeRec<T> s_own[kCapN];
   __shared__ int s_n;
   __shared__ long long s_off;
-  __shared__ unsigned long long s_ctr[kTr][3];
+  __shared__ unsigned s_ctr[kTr][3];   // per-phase counts (32-bit: native smem atomics), flushed every phase
   __shared__ int s_dq;                            // next unclaimed entry of the bucket being delivered
 
   const int tid = threadIdx.x;
@@ -785,7 +802,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   SpikeRec<T>* spill = A.scratch + (size_t)cta * A.per;
   if (A.no_pause && ld_volatile(A.err) != 0) return;   // an earlier asynchronous window failed
 
-  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0ULL;
+  if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0u;
   if (tid == 0) s_dq = 0;
   if (A.kind == EQ_KIND_RING)
     for (int k = tid; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
@@ -853,6 +870,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
       if (dn > 0 || (m > A.m0 && A.kind == EQ_KIND_RING)) s_bin[(m + 1) % A.NB] = 0;
     }
     if (m == m1) break;
+    flush_counters<kTr>(s_ctr, A.counters, b_first, A.B, end, A.N);
     tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err, A.step_start + m + 1, A.log_count, nullptr,
                    A.kind == EQ_KIND_RING ? A.ring_dirty + m % A.R : nullptr))
@@ -880,7 +898,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
     int b = b_first + tid;
     if (b < A.B && (long long)b * A.N < end) {
       for (int q = 0; q < 3; ++q)
-        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + q), s_ctr[tid][q]);
+        if (s_ctr[tid][q]) atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + q), (unsigned long long)s_ctr[tid][q]);
     }
   }
 }

@@ -103,3 +103,11 @@ for p in $PARTS; do
       echo "ncu full rc=$?"; tail -3 gpurun_out/${TAG}_ncu_full.log ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    abctr)
+      for cfg in "" "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C2 --trials 32 --kind binaryheap --capacity 64"; do
+        bash scripts/ab_args.sh "$cfg" head=scratch_lib/head2.so new=paper_2512_05906_b200/lib/libeventq_b200.so
+      done ;;
+  esac
+done
