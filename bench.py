@@ -281,9 +281,13 @@ def launch_selftest(args):
 VARIANTS = (
     # (label, config, trials, kind, capacity, precision, delays)
     ("C3 ring fp64 (the reference's arithmetic)", "C3", 24, "ring", 0, 64, None),
+    ("C2 binaryheap[64]", "C2", 32, "binaryheap", 64, 32, None),
+    ("C2 fiforing[64] (homogeneous delay 32 steps)", "C2", 32, "fiforing", 64, 32, (32, 32)),
+    ("C4 ring (1M neurons, delays 1..256)", "C4", 4, "ring", 0, 32, None),
     ("C4 binaryheap[16] (memory pressure, drops)", "C4", 4, "binaryheap", 16, 32, None),
     ("C4 sortedarray[16] (memory pressure, drops)", "C4", 4, "sortedarray", 16, 32, None),
 )
+_NETS = {}
 
 
 def measure_variant(label, cfg, trials, kind, capacity, precision, delays, steps, warmup, local, peak):
@@ -294,7 +298,11 @@ def measure_variant(label, cfg, trials, kind, capacity, precision, delays, steps
     from paper_2512_05906_b200.engine import Engine, poisson_drive_device
     from paper_2512_05906_b200 import workload as wl
     n, k, drange, _, T = wl.CONFIGS[cfg]
-    net = wl.random_network(n, k, 0, delay_steps=delays or drange)
+    key = (cfg, delays or drange)
+    if key not in _NETS:
+        _NETS.clear()
+        _NETS[key] = wl.random_network(n, k, 0, delay_steps=delays or drange)
+    net = _NETS[key]
     # drive generated on the device (same PoissonDrive statistics): no host masks at 1M neurons
     mask = poisson_drive_device(n, trials, T, 1e-3, 16e-3, 12e-3, 1000, device=local)
     eng = Engine(n, trials, T, kind=kind, capacity=capacity, precision=precision, device=local)

@@ -111,3 +111,11 @@ for p in $PARTS; do
       done ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    abb)
+      for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 16" "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C2 --trials 32 --kind fiforing --capacity 64 --delays 32,32"; do
+        bash scripts/ab_args.sh "$cfg" head=scratch_lib/head3.so new=paper_2512_05906_b200/lib/libeventq_b200.so
+      done ;;
+  esac
+done
