@@ -119,3 +119,11 @@ for p in $PARTS; do
       done ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    abpf)
+      for r in 1 2; do
+        bash scripts/ab_args.sh "" nopf=scratch_lib/nopf.so pf2=paper_2512_05906_b200/lib/libeventq_b200.so pf1=scratch_lib/pf1.so
+      done ;;
+  esac
+done
