@@ -127,3 +127,12 @@ for p in $PARTS; do
       done ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    abstaged)
+      for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C2 --trials 32 --kind binaryheap --capacity 64"; do
+        bash scripts/ab_args.sh "$cfg" hbm=paper_2512_05906_b200/lib/libeventq_b200.so
+        bash scripts/ab_args.sh "$cfg --staged-queues" staged=paper_2512_05906_b200/lib/libeventq_b200.so
+      done ;;
+  esac
+done
