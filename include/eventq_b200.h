@@ -129,7 +129,7 @@ int eq_forward(eq_handle* h, void* v_out, void* i_out, void* v_trace, void* stre
  * 1 = delay (dir_index = CSR edge), 2 = drive amplitude (dir_index = neuron);
  * host arrays.  Runs the whole drive (t_steps) from rest and writes the final
  * membrane (v_out, double[n_trials][n], may be NULL) and its tangents
- * (v_tangent, double[n_dir][n_trials][n]).  fp64, ring kind, exact delivery.
+ * (v_tangent, double[n_dir][n_trials][n]).  fp64, ring kind, exact or plain delivery.
  * dL/dtheta_d for the reference loss = sum 2 (V - v*) v_tangent[d]. */
 int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const int64_t* dir_index, double* v_out,
                    double* v_tangent, void* stream);

@@ -3,11 +3,13 @@
 // PoissonDrive.materialize seeded_neuron :123-155) for D seeded directions at
 // once, as extra tangent lanes of one primal trajectory.
 //
-// fp64, ring kind, exact delivery.  The primal arithmetic is the engine's
+// fp64, ring kind, exact or plain delivery.  The primal arithmetic is the engine's
 // (lif_step, fixed-point slot sums in the DRAM ring rows), so the raster is
 // the forward kernel's; each direction d carries the reference's dual parts:
 //   synapse    I' += W_s' + Q_s/tau_s; I' *= k_s            (neuro.py:33-47, jumps.py:116-126)
 //   membrane   v' = V' + c (W_m' + Q_m/tau_m - W_s' - Q_s/tau_s)      (network.py:392-401)
+//              (plain delivery: v' = V' - Q_s/tau_m, neuro.py:146-149 delivered_wtt;
+//               payloads w with no phase factor, network.py:403-408, 438)
 //              v_new' = a' + (v' - a') k_m                  (neuro.py:150-154)
 //   crossing   r' = (num' den - num den') / den^2, tdot = -tau_m r'/r (neuro.py:200-210)
 //   reset      v_new' = a' + (-a') ku + (v_r - a) ku tdot / tau_m     (neuro.py:161-175)
@@ -27,6 +29,7 @@ namespace eq {
 
 struct JvpArgs {
   int N, B, D, R, refractory;
+  int exact;              // exact delivery (else plain)
   int* m_dev;             // current step (device-side, so a CUDA graph of steps replays unchanged)
   long long total;
   StepConsts<double> c;
@@ -70,8 +73,8 @@ __global__ void k_jvp_update(JvpArgs A) {
   const double drive = on ? A.net.amp[j] : 0.0;
   int rf = A.refractory ? A.refr[idx] : 0;
   double i, v_new, a, v, t_spk;
-  const bool spike = lif_step<double>(c, true, A.refractory, m, ps, pm, A.I[idx], A.V[idx], drive, rf, i, v_new, a,
-                                      v, t_spk);
+  const bool spike = lif_step<double>(c, A.exact != 0, A.refractory, m, ps, A.exact ? pm : 0.0, A.I[idx], A.V[idx],
+                                      drive, rf, i, v_new, a, v, t_spk);
   if (spike && t_spk != t_spk) {
     raise_error(A.err, EQ_ERR_GRAZING, m + 1, b, j);
     return;
@@ -123,7 +126,8 @@ __global__ void k_jvp_tangent(JvpArgs A) {
   double tI = A.tI[ts];
   tI = (tI + Ws + Qs / c.tau_s) * c.k_s;                    // apply_jump_pulse + dual_exp_decay
   const double ta = tI + ((on && A.dkind[d] == 2 && A.dindex[d] == j) ? 1.0 : 0.0);
-  const double tv = A.tV[ts] + c.cc * (Wm + Qm / c.tau_m - Ws - Qs / c.tau_s);
+  const double tv = A.exact ? A.tV[ts] + c.cc * (Wm + Qm / c.tau_m - Ws - Qs / c.tau_s)
+                            : A.tV[ts] - Qs / c.tau_m;
   double tvn = ta + (tv - ta) * c.k_m;
   if (crossed) {
     const double a = A.pa[idx], v = A.pv[idx], r = A.pr[idx], ku = A.pku[idx];
@@ -163,8 +167,12 @@ __global__ void k_jvp_fanout(JvpArgs A, const long long* n_events_p, const long 
     const double w = A.net.w[x], d = A.net.d[x];
     const double t_post = A.spk_t[k] + d;                   // jumps.py:83-87
     const int ds = delivery_step_coded(t_post, A.net.dcode[x], c.dt, *A.m_dev);
-    const double phi = (double)ds * c.dt - t_post;
-    const double es = eq_exp_t(-phi * c.inv_tau_s), em = eq_exp_t(-phi * c.inv_tau_m);
+    double es = 1.0, em = 0.0;                              // plain delivery: payload w, no twin
+    if (A.exact) {
+      const double phi = (double)ds * c.dt - t_post;
+      es = eq_exp_t(-phi * c.inv_tau_s);
+      em = eq_exp_t(-phi * c.inv_tau_m);
+    }
     const double ws = w * es, wm = w * em;
     if (dd == 0) {
       const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + j;

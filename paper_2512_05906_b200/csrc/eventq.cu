@@ -1531,8 +1531,8 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
                    double* v_tangent, void* stream) {
   if (!h) return EQ_ERR_CONFIGURATION;
   const eq_config& c = h->cfg;
-  if (c.precision != 64 || c.kind != EQ_KIND_RING || !c.exact_delivery)
-    return fail(h, EQ_ERR_CONFIGURATION, "forward-mode runs need precision 64, the ring kind and exact delivery");
+  if (c.precision != 64 || c.kind != EQ_KIND_RING)
+    return fail(h, EQ_ERR_CONFIGURATION, "forward-mode runs need precision 64 and the ring kind");
   if (h->partitioned) return fail(h, EQ_ERR_CONFIGURATION, "forward-mode runs on partitioned networks are not supported");
   if (!h->net_set || !h->drive_set) return fail(h, EQ_ERR_CONFIGURATION, "network and drive must be set");
   if (n_dir < 1 || !dir_kind || !dir_index || !v_tangent)
@@ -1577,6 +1577,7 @@ int eq_forward_jvp(eq_handle* h, int32_t n_dir, const int32_t* dir_kind, const i
   A.D = D;
   A.R = h->R;
   A.refractory = c.refractory_steps;
+  A.exact = c.exact_delivery;
   A.total = h->total;
   A.c = consts<double>(h);
   A.net = netview<double>(h);

@@ -17,7 +17,8 @@ DT = 1e-3
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_refr3_n10"])
+@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_refr3_n10", "dense_ring_plain_n10",
+                                  "sparse_ring_plain_n100"])
 def test_batched_jvp_equals_reference_forward_mode(name):
     from test_network_api import params_for
     from paper_2512_05906_b200.network import SeedDirection, forward_gradients
@@ -29,14 +30,14 @@ def test_batched_jvp_equals_reference_forward_mode(name):
     np.testing.assert_allclose(got, g["jvp"], rtol=1e-7, atol=1e-10)
 
 
-@pytest.mark.parametrize("refractory", [0, 2])
-def test_batched_jvp_equals_reverse_pass(refractory):
+@pytest.mark.parametrize("refractory,exact", [(0, True), (2, True), (0, False)])
+def test_batched_jvp_equals_reverse_pass(refractory, exact):
     from paper_2512_05906_b200.engine import Engine
     net = wl.random_network(300, 25, 8, delay_steps=(1, 14), w_mean=0.04, w_std=0.01)
     B, T = 3, 400
     mask = wl.drive_masks(300, B, T, DT, seed0=55)
     amp = np.full(300, 12.0)
-    eng = Engine(300, B, T, precision=64, lif=wl.LIFConfig(refractory_steps=refractory))
+    eng = Engine(300, B, T, precision=64, lif=wl.LIFConfig(refractory_steps=refractory, exact_delivery=exact))
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     eng.set_drive(mask, amp)
     out = eng.forward()

@@ -25,7 +25,7 @@ def params_for(case):
     w, d = net.dense(DT)
     p = NetworkParams(n=net.n, weights=w, delays=d, tau_m=1.0, tau_syn=0.5, v_th=1.0, v_reset=0.0, dt=DT,
                       queue_kind=case.kind, queue_capacity=case.capacity, refractory_steps=case.refractory,
-                      v_target=np.full(net.n, 0.25))
+                      v_target=np.full(net.n, 0.25), exact_delivery=case.exact)
     from paper_2512_05906_b200.workload import unpack_mask
     return p, (unpack_mask(mask[0], net.n), amp)
 
@@ -93,7 +93,7 @@ def test_poisson_drive_draws_equal_the_reference():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["dense_ring_n8", "dense_heap_cap3_n12", "dense_fifo_cap2_n12",
-                                  "dense_ring_refr3_n10"])
+                                  "dense_ring_refr3_n10", "dense_ring_plain_n10", "dense_lossy_cap6_n10"])
 def test_simulate_matches_reference_fixture(name):
     from paper_2512_05906_b200.network import simulate
     case = BY_NAME[name]
@@ -108,7 +108,9 @@ def test_simulate_matches_reference_fixture(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_refr3_n10"])
+@pytest.mark.parametrize("name", ["dense_ring_n8", "dense_ring_refr3_n10", "dense_ring_plain_n10",
+                                  "dense_sorted_plain_cap3_n12", "dense_lossy_cap6_n10",
+                                  "dense_lossy_cap5_plain_n10"])
 def test_forward_gradient_equals_reference_jvp(name):
     from paper_2512_05906_b200.network import forward_gradient
     case = BY_NAME[name]
