@@ -278,6 +278,8 @@ def launch_selftest(args):
     dist.destroy_process_group()
 
 
+QUEUE_IMPL = {"admission": 0, "smem": 1, "hbm": 2}   # eq_config.staged_queues
+
 VARIANTS = (
     # (label, config, trials, kind, capacity, precision, delays)
     ("C3 ring fp64 (the reference's arithmetic)", "C3", 24, "ring", 0, 64, None),
@@ -359,7 +361,7 @@ def run_ours(args):
         T = args.steps_per_pass
         mask = np.ascontiguousarray(mask[:, :T])
     eng = Engine(net.n, B, T, kind=args.kind, capacity=args.capacity, precision=args.precision, device=local,
-                 staged_queues=args.staged_queues)
+                 staged_queues=QUEUE_IMPL[args.queue_impl])
     eng.set_network(net.rowptr, net.col, net.weight, net.delay)
     mask_dev = torch.from_numpy(mask.view(np.int32)).to(dev)
     amp_dev = torch.from_numpy(amp).to(dev, eng.dtype)
@@ -606,8 +608,9 @@ def main():
     ap.add_argument("--steps-per-pass", type=int, default=0, help="override T (debug)")
     ap.add_argument("--kind", default="ring", choices=["ring", "fiforing", "binaryheap", "sortedarray", "donothing"])
     ap.add_argument("--capacity", type=int, default=0, help="bounded kinds: events per queue")
-    ap.add_argument("--staged-queues", action="store_true",
-                    help="bounded kinds: the shared-memory staged queues with the in-kernel arrival sort")
+    ap.add_argument("--queue-impl", choices=sorted(QUEUE_IMPL), default="admission",
+                    help="bounded kinds: heap/sorted by admission on the calendar (default), the "
+                         "shared-memory staged queues (smem) or the HBM-resident queue structures (hbm)")
     ap.add_argument("--delays", type=lambda s: tuple(int(x) for x in s.split(",")), default=None,
                     help="delay range in steps lo,hi (FIFO needs lo == hi)")
     ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)

@@ -77,10 +77,11 @@ typedef struct eq_config {
   double dt, tau_m, tau_syn, v_th, v_reset;
   int32_t max_ctas;         /* persistent grid size cap (0 = 2 per SM); partitions that run
                                concurrently on one GPU split its SMs this way */
-  int32_t staged_queues;    /* bounded kinds, capacity <= 64: 1 = queues staged in shared
-                               memory per step with an in-kernel counting sort of the
-                               arrivals (eq_bq.cuh); 0 = HBM-resident structures (default,
-                               measured faster) */
+  int32_t staged_queues;    /* bounded-kind implementation (same results):
+                               0 = heap / sorted by admission on the calendar (default;
+                               FIFO keeps 2), 1 = queues staged in shared memory with an
+                               in-kernel counting sort of the arrivals (capacity <= 64,
+                               eq_bq.cuh), 2 = HBM-resident queue structures (eq_bounded.cuh) */
 } eq_config;
 
 typedef struct eq_handle eq_handle;

@@ -102,7 +102,27 @@ struct FwdArgs {
   long long imp_n;
   const long long* imp_dev;  // peer exchange: {first, count} of the import block on the device (overrides imp_n)
   int no_pause;              // asynchronous windows: a full spike log is an error, not a pause
+  int cal;                   // the calendar path runs (ring kind, or a bounded kind by admission)
+  // bounded kinds by admission (binaryheap / sortedarray, eq_adm.cuh): the
+  // calendar carries the accepted events; a per-target record counts them
+  int adm_cap;               // accept while the queue holds fewer events
+  int* arec;                 // [total][8] {E|pc<<16 [2], popped [2], arrivals [3], -}
+  int* fl;                   // [2][G][per] targets whose step needs the reference order
+  int* fl_cnt;               // [2][G]
+  int* lpos;                 // [3][total] log position of the spike of step s (s % 3)
+  const int2* csc;           // [E] in-edges {x, source} by target, ascending x
+  const long long* csc_off;  // [N+1]
+  unsigned* drop_bits;       // event id = log position * maxdeg + row offset
+  long long drop_cap;
+  int maxdeg;
+  FastDiv divPer;            // flat target -> owner CTA
+  int* cring;                // [B][R][N] event counts of the DRAM ring rows (bucket overflow)
+  int2* slots;               // [2][total][kAdmSlots] {x, log position} of a phase's first arrivals
 };
+
+// Arrivals whose key is recorded per target and phase (when 0 < free < kAdmSlots):
+// a fix-up with at most this many arrivals ranks them without the CSC walk.
+constexpr int kAdmSlots = 8;
 
 template <int NT, typename T = float>
 struct FwdShared {
@@ -250,6 +270,242 @@ struct Roles {
   static constexpr int kBarF = 1, kBarN = 2;
 };
 
+// ------------------------------------------------------------------ admission
+//
+// Bounded kinds by admission (BinaryHeapQueue queues.py:481-571, SortedArrayQueue
+// :308-403).  Both drop the INCOMING event when the queue holds `capacity`
+// events and pop every event due now, so a queue's effect on
+// the network is fixed by two numbers per step: how many events it holds and,
+// among a step's arrivals, which come first in the reference order (emit step,
+// then ascending CSR edge index x).  The events themselves ride the ring kind's
+// calendar (buckets + L2 accumulator, fixed point); the structure is replaced by
+// a 32-byte admission record per queue:
+//
+//   words 0,1  E | pc << 16 of the phase with that parity: E = events held
+//              before the phase's admissions, pc = events popped at its step
+//   words 2,3  events accepted for the step with that parity (counted where the
+//              payload is delivered into the accumulator; read and zeroed at pop)
+//   words 4-6  arrivals of the phase (step % 3)
+//
+// Phase m admits the arrivals of step m-1's spikes: an event takes a ticket t
+// (atomic on its target's arrival word); with occ = min(E + n, cap) - pc of phase
+// m-1, the first free = cap - occ tickets are accepted.  Tickets come in
+// arbitrary order, so when 0 < free < n the target goes on its owner's fix-up
+// list: at the start of phase m+1 the owner walks the target's in-edges in
+// ascending x (CSC), ranks the arrivals and swaps any ticket winner that is not
+// among the first `free` in the reference order for the one that is (payload and
+// count moved with the exact fixed-point negation, drop bits flipped).  The
+// accepted SET then equals the reference's; accepted COUNTS never change.
+
+constexpr long long kNegEntry = 1LL << 62;   // bucket entry flag: a withdrawn event (count -1)
+
+__device__ __forceinline__ void red_i32(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// count word of target tgt in DRAM ring row `row` (the ring's [B][R][N] layout)
+template <typename T>
+__device__ __forceinline__ int* cring_at(const FwdArgs<T>& A, int row, long long tgt) {
+  const int b = A.c.divN.div((int)tgt);
+  return A.cring + ((size_t)b * A.R + row) * A.N + (tgt - (long long)b * A.N);
+}
+
+// Occupancy before the admissions of phase m (from phase m-1's record words).
+__device__ __forceinline__ int adm_occ(const int* r, int m, int cap) {
+  const int ep = r[(m - 1) & 1];
+  const int n = r[4 + (m + 2) % 3];
+  const int e = (ep & 0xffff) + n;
+  return (e < cap ? e : cap) - (ep >> 16);
+}
+
+// Add (sign +1) or withdraw (-1) one event's payload and count at due step ds
+// during phase p (in_kernel) or after the launch that ended with phase p-1.
+template <typename T>
+__device__ __forceinline__ void adm_apply(const FwdArgs<T>& A, int p, bool in_kernel, int ds, int tgt, long long q1,
+                                          long long q2, int sign, int* bins, int cta) {
+  typedef Prec<T> P;
+  if (ds == p || (in_kernel && ds == p + 1)) {
+    long long* a = A.acc + (size_t)(ds & 1) * A.total * P::kSlotWords;
+    if (P::kSlotWords == 1) {
+      red_add(a + tgt, pack2(q1, q2));
+    } else {
+      red_add(a + 2 * (size_t)tgt, q1);
+      red_add(a + 2 * (size_t)tgt + 1, q2);
+    }
+    red_i32(A.arec + (size_t)tgt * 8 + 2 + (ds & 1), sign);
+    return;
+  }
+  const int bn = ds % A.NB;
+  const int pos = atomicAdd(bins + bn, 1);
+  if (pos < A.cap_b) {
+    long long* bk = A.bk + (((size_t)cta * A.NB + bn) * A.cap_b + pos) * bk_words<T>();
+    const long long tg = sign < 0 ? (tgt | kNegEntry) : tgt;
+    longlong2* o = reinterpret_cast<longlong2*>(bk);
+    if (P::kSlotWords == 1) {
+      *o = make_longlong2(tg, pack2(q1, q2));
+    } else {
+      o[0] = make_longlong2(tg, q1);
+      o[1] = make_longlong2(q2, 0);
+    }
+  } else {
+    const int b = A.c.divN.div(tgt);
+    const size_t so = ((size_t)b * A.R + (size_t)(ds % A.R)) * A.N + (tgt - b * A.N);
+    if (P::kSlotWords == 1) {
+      red_add(A.ring + so, pack2(q1, q2));
+    } else {
+      red_add(A.ring + 2 * so, q1);
+      red_add(A.ring + 2 * so + 1, q2);
+    }
+    red_i32(cring_at(A, ds % A.R, tgt), sign);
+    if (A.ring_dirty[ds % A.R] == 0) atomicExch(A.ring_dirty + ds % A.R, 1);
+  }
+}
+
+// One arrival of a fix-up target: swap it in (canon) or out of the accepted
+// set if its ticket decided otherwise (drop bit = the ticket's decision).
+template <typename T>
+__device__ __forceinline__ void adm_settle(const FwdArgs<T>& A, const int p, const bool in_kernel, const int tgt,
+                                           const int x, const int pos, const bool canon, int* bins, const int cta) {
+  typedef Prec<T> P;
+  const StepConsts<T>& c = A.c;
+  const long long id = (long long)pos * A.maxdeg + (x - A.log_r0[pos]);
+  const unsigned bit = 1u << (id & 31);
+  const bool tent = !(A.drop_bits[id >> 5] & bit);
+  if (canon == tent) return;
+  const int me = p - 2;
+  const SpikeRec<T> rec = A.log[pos];
+  const EdgeRec<T> ed = ld_edge(A.net.er + x);
+  const T t_post = rec.t + ed.d;
+  const int ds = delivery_step_coded(t_post, (unsigned short)ed.code, c.dt, me);
+  T ws, wm;
+  if (A.exact) {
+    const T phi = (T)ds * c.dt - t_post;
+    ws = ed.w * eq_exp_t(-phi * c.inv_tau_s);
+    wm = ed.w * eq_exp_t(-phi * c.inv_tau_m);
+  } else {
+    ws = ed.w;
+    wm = (T)0;
+  }
+  long long q1 = P::q(ws, c.scale), q2 = A.exact ? P::q(wm, c.scale) : 0;
+  if (canon) {
+    atomicAnd(A.drop_bits + (id >> 5), ~bit);
+  } else {
+    atomicOr(A.drop_bits + (id >> 5), bit);
+    q1 = -q1;
+    q2 = -q2;
+  }
+  adm_apply<T>(A, p, in_kernel, ds, tgt, q1, q2, canon ? 1 : -1, bins, cta);
+}
+
+// Free room and arrival count of a fix-up target's admissions of phase p-1.
+__device__ __forceinline__ int2 adm_room(const int* arec, int cap, int p, int tgt) {
+  const int q = p - 1;
+  const int* r = arec + (size_t)tgt * 8;
+  return make_int2(cap - adm_occ(r, q, cap), r[4 + q % 3]);
+}
+
+// Fix-up from the recorded keys (n <= kAdmSlots arrivals), by one thread:
+// rank = number of arrivals with a smaller x.
+template <typename T>
+__device__ __forceinline__ void adm_fixup_slots(const FwdArgs<T>& A, const int p, const bool in_kernel, const int tgt,
+                                                const int fr, const int n, int* bins, const int cta) {
+  const int2* sl = A.slots + ((size_t)((p - 1) & 1) * A.total + tgt) * kAdmSlots;
+  int2 k[kAdmSlots];
+#pragma unroll
+  for (int e = 0; e < kAdmSlots; ++e)
+    if (e < n) k[e] = sl[e];
+#pragma unroll
+  for (int e = 0; e < kAdmSlots; ++e) {
+    if (e >= n) continue;
+    int rank = 0;
+#pragma unroll
+    for (int g = 0; g < kAdmSlots; ++g) rank += (g < n && k[g].x < k[e].x) ? 1 : 0;
+    adm_settle<T>(A, p, in_kernel, tgt, k[e].x, k[e].y, rank < fr, bins, cta);
+  }
+}
+
+// Reference-order fix-up of one target's admissions of phase p-1 (arrivals from
+// the spikes of step p-2) with more arrivals than recorded keys, by one warp:
+// in-edges in ascending x, 32 per round, arrival = the source's spike of that
+// step is in the log (lpos).
+template <typename T>
+__device__ __forceinline__ void adm_fixup(const FwdArgs<T>& A, const int p, const bool in_kernel, const int tgt,
+                                          const int lane, int* bins, const int cta) {
+  const StepConsts<T>& c = A.c;
+  const int me = p - 2;
+  const int b = c.divN.div(tgt), j = tgt - b * A.N;
+  const int2 rn = adm_room(A.arec, A.adm_cap, p, tgt);
+  const int fr = rn.x, n = rn.y;
+  const long long L0 = A.step_start[me], L1 = A.step_start[me + 1];
+  const int* lp = A.lpos + (size_t)(me % 3) * A.total + (size_t)b * A.N;
+  const long long cs = A.csc_off[j], ce = A.csc_off[j + 1];
+  int rank = 0;
+  for (long long k0 = cs; k0 < ce && rank < n; k0 += 32) {
+    const long long k = k0 + lane;
+    bool arr = false;
+    int2 xi = make_int2(0, 0);
+    int pos = 0;
+    if (k < ce) {
+      xi = A.csc[k];
+      pos = lp[xi.y];
+      arr = pos >= L0 && pos < L1;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, arr);
+    if (arr) adm_settle<T>(A, p, in_kernel, tgt, xi.x, pos, rank + __popc(bal & ((1u << lane) - 1u)) < fr, bins, cta);
+    rank += __popc(bal);
+  }
+}
+
+// The fix-ups listed for this CTA by the admissions of phase p-1, one warp per
+// target; the list is emptied for its next use (phase p+1).
+// Targets with recorded keys: one thread each; the rest (more arrivals than
+// slots, or room beyond the slots) then one warp each over the CSC.
+template <typename T>
+__device__ __noinline__ void adm_fixups(const FwdArgs<T>& A, const int p, const bool in_kernel, const int cta,
+                                        const int gtid, const int nthreads, int* bins) {   // out of line: rare path
+  const int par = (p - 1) & 1;
+  const int n = A.fl_cnt[par * A.G + cta];
+  const int* lst = A.fl + ((size_t)par * A.G + cta) * A.per;
+  bool walk = false;
+  for (int k = gtid; k < n; k += nthreads) {
+    const int tgt = lst[k];
+    const int2 rn = adm_room(A.arec, A.adm_cap, p, tgt);
+    if (rn.x < kAdmSlots && rn.y <= kAdmSlots) adm_fixup_slots<T>(A, p, in_kernel, tgt, rn.x, rn.y, bins, cta);
+    else walk = true;
+  }
+  if (!__any_sync(0xffffffffu, walk)) return;     // warp-uniform: each warp walks the targets of its own lanes
+  const int lane = gtid & 31;
+  for (int k0 = gtid - lane; k0 < n; k0 += nthreads) {
+    const int k = k0 + lane;
+    bool w = false;
+    int tgt = 0;
+    if (k < n) {
+      tgt = lst[k];
+      const int2 rn = adm_room(A.arec, A.adm_cap, p, tgt);
+      w = !(rn.x < kAdmSlots && rn.y <= kAdmSlots);
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, w);
+    while (bal) {
+      const int src = __ffs(bal) - 1;
+      bal &= bal - 1;
+      adm_fixup<T>(A, p, in_kernel, __shfl_sync(0xffffffffu, tgt, src), lane, bins, cta);
+    }
+  }
+}
+
+// After a forward launch: the fix-ups of its last admissions (phase err[4],
+// the step it reached), so the next launch and the queue contents read now see
+// them applied.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) k_adm_fixup(FwdArgs<T> A) {
+  if (ld_volatile(A.err) != 0) return;
+  const int p = ld_volatile(A.err + 4) + 1;
+  const int cta = blockIdx.x;
+  adm_fixups<T>(A, p, false, cta, threadIdx.x, NT, A.bk_cnt + (size_t)cta * A.NB);
+  __syncthreads();
+  if (threadIdx.x == 0) A.fl_cnt[((p - 1) & 1) * A.G + cta] = 0;
+}
+
 // Fan-out (network.py:583-611) of log records [s0, s1): the CTA's share of
 // step m-1's own spikes (kImp = false) or, in a launch's first phase, of the
 // spikes imported from other partitions (kImp = true: per-spike emit steps in
@@ -258,10 +514,12 @@ struct Roles {
 // step (rank from a shared-memory counter).  No read-modify-write touches
 // DRAM; a full bucket spills into the DRAM ring row (flagged), never losing
 // events.  Executed by the event-side warp group.
-template <typename T, int NT, int NF, bool kImp>
+constexpr int kDropTr = 64;   // per-trial drop counts of a phase's admissions kept in smem
+
+template <typename T, int NT, int NF, bool kImp, bool kAdm = false>
 __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, const int cta, const int gtid,
                                            const long long s0, const long long s1, SpikeRec<T>* s_spk,
-                                           long long* s_r0, int* s_pre, int* s_bin) {
+                                           long long* s_r0, int* s_pre, int* s_bin, unsigned* s_drop = nullptr) {
   typedef Prec<T> P;
   typedef Roles<NT, NF> Ro;
   constexpr int kCap = FwdShared<NT, T>::kCap;
@@ -287,11 +545,12 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
 #ifndef EQ_FWD_EV
 #define EQ_FWD_EV 3
 #endif
-    constexpr int EV = EQ_FWD_EV;
+    constexpr int EV = kAdm ? 2 : EQ_FWD_EV;
     for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
       int jj[EV], kk[EV];
       T ww[EV], dd[EV];
       unsigned short cc[EV];
+      int xs[kAdm ? EV : 1];
 #pragma unroll
       for (int e = 0; e < EV; ++e) {
         const int f = f0 + e * Ro::NF;
@@ -300,11 +559,31 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
           const int k = find_row(s_pre, nb, f);
           const long long x = s_r0[k] + (f - s_pre[k]);
           kk[e] = k;
+          if constexpr (kAdm) xs[e] = (int)x;
           const EdgeRec<T> ed = ld_edge(A.net.er + x);   // one 16-byte streamed load per event
           jj[e] = ed.col;
           ww[e] = ed.w;
           dd[e] = ed.d;
           cc[e] = (unsigned short)ed.code;
+        }
+      }
+      // admission: every event's ticket and its target's occupancy, issued
+      // back to back before any is consumed
+      int tk[kAdm ? EV : 1], fr[kAdm ? EV : 1];
+      if constexpr (kAdm) {
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {
+          if (kk[e] < 0) continue;
+          const int tgt = c.divN.div(s_spk[kk[e]].idx) * A.N + jj[e];
+          int* r = A.arec + (size_t)tgt * 8;
+          tk[e] = atomicAdd(r + 4 + m % 3, 1);
+          fr[e] = A.adm_cap - adm_occ(r, m, A.adm_cap);
+        }
+#pragma unroll
+        for (int e = 0; e < EV; ++e) {                      // keys for a possible fix-up
+          if (kk[e] < 0 || fr[e] <= 0 || fr[e] >= kAdmSlots || tk[e] >= kAdmSlots) continue;
+          const int tgt = c.divN.div(s_spk[kk[e]].idx) * A.N + jj[e];
+          A.slots[((size_t)(m & 1) * A.total + tgt) * kAdmSlots + tk[e]] = make_int2(xs[e], (int)(k0 + kk[e]));
         }
       }
 #pragma unroll
@@ -328,6 +607,21 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
         const int tgt = b * A.N + jj[e];                    // flat target
         const long long q1 = P::q(ws, c.scale);
         const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
+        if constexpr (kAdm) {
+          if (tk[e] >= fr[e]) {                             // queue full at this ticket: dropped
+            const int f = f0 + e * Ro::NF;
+            const long long id = (k0 + kk[e]) * (long long)A.maxdeg + (f - s_pre[kk[e]]);
+            atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
+            if (b < kDropTr) atomicAdd(s_drop + b, 1u);
+            else atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * b + 2), 1ULL);
+            if (tk[e] == fr[e] && fr[e] > 0) {              // more arrivals than room: reference order needed
+              const int owner = A.divPer.div(tgt);
+              const int slot = atomicAdd(A.fl_cnt + (m & 1) * A.G + owner, 1);
+              A.fl[((size_t)(m & 1) * A.G + owner) * A.per + slot] = tgt;
+            }
+            continue;
+          }
+        }
         if (ds == m + 1) {
           if (P::kSlotWords == 1) {
             red_add(accn + tgt, pack2(q1, q2));
@@ -335,6 +629,7 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
             red_add(accn + 2 * (size_t)tgt, q1);
             red_add(accn + 2 * (size_t)tgt + 1, q2);
           }
+          if constexpr (kAdm) red_i32(A.arec + (size_t)tgt * 8 + 2 + ((m + 1) & 1), 1);
           continue;
         }
         int bn;
@@ -367,6 +662,7 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
             red_add(A.ring + 2 * so, q1);
             red_add(A.ring + 2 * so + 1, q2);
           }
+          if constexpr (kAdm) red_i32(cring_at(A, ds % A.R, tgt), 1);
           if (A.ring_dirty[ds % A.R] == 0) atomicExch(A.ring_dirty + ds % A.R, 1);
         }
       }
@@ -422,11 +718,12 @@ __device__ __forceinline__ void flush_counters(unsigned (*s_ctr)[3], long long* 
 // wrote them), synapse + LIF + exact crossing for the CTA's neuron-trials, clear
 // the popped slots, then the spike log (one chunk per (step, CTA)) and the
 // per-trial counters.  Executed by the neuron-side warp group (gtid < NN).
-template <typename T, int NT, int U, int NF>
+template <typename T, int NT, int U, int NF, bool kAdm = false>
 __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, const int cta, const int gtid,
                                             const long long begin, const long long end, const int b_first,
                                             const bool acc_pop, SpikeRec<T>* s_own, int& s_n, long long& s_off,
-                                            unsigned (*s_ctr)[3], SpikeRec<T>* spill, T* s_st = nullptr) {
+                                            unsigned (*s_ctr)[3], SpikeRec<T>* spill, T* s_st = nullptr,
+                                            int* s_bin = nullptr) {
   // s_st: the CTA's I and V kept in shared memory across the launch ([per] I,
   // then [per] V, indexed by idx - begin), or null (state in HBM)
   T* const gI = s_st ? s_st - begin : A.I;
@@ -436,7 +733,45 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
   constexpr int kCapN = FwdShared<NT, T>::kCap / 2;
   constexpr int kTr = FwdShared<NT>::kTrials;
   const StepConsts<T>& c = A.c;
-  const bool dirty = A.kind == EQ_KIND_RING && ld_volatile(A.ring_dirty + m % A.R) != 0;
+  const bool dirty = A.cal && ld_volatile(A.ring_dirty + m % A.R) != 0;
+  if constexpr (kAdm) {
+    // (a) reference-order fix-ups of the last phase's admissions (they may
+    // move events due now, so before the pop), then this phase's record words
+    adm_fixups<T>(A, m, true, cta, gtid, Ro::NN, s_bin);
+    __threadfence();   // their reds into acc / counts, before this group's plain loads of them
+    group_sync(Ro::kBarN, Ro::NN);
+    if (gtid == 0) A.fl_cnt[((m - 1) & 1) * A.G + cta] = 0;
+    // four records per thread in flight: loads first, then the stores
+    for (long long i0 = begin + gtid; i0 < end; i0 += 4 * Ro::NN) {
+      int ep[4], np[4], pc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long idx = i0 + u * Ro::NN;
+        if (idx < end) {
+          const int* r = A.arec + (size_t)idx * 8;
+          ep[u] = r[(m - 1) & 1];
+          np[u] = r[4 + (m + 2) % 3];
+          pc[u] = r[2 + (m & 1)];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long idx = i0 + u * Ro::NN;
+        if (idx >= end) continue;
+        int* r = A.arec + (size_t)idx * 8;
+        if (dirty) {                                   // events that overflowed a bucket into ring row m
+          int* cr = cring_at(A, m % A.R, idx);
+          pc[u] += *cr;
+          *cr = 0;
+        }
+        const int e = (ep[u] & 0xffff) + np[u];
+        const int occ = (e < A.adm_cap ? e : A.adm_cap) - (ep[u] >> 16);
+        r[m & 1] = occ | (pc[u] << 16);
+        r[2 + (m & 1)] = 0;
+        r[4 + (m + 1) % 3] = 0;
+      }
+    }
+  }
   // ---------------- (b) neuron update: pop, synapse, membrane, crossing.
   // Walked per trial segment of the owned range so the row pointers are
   // computed once per segment, not per neuron.
@@ -700,6 +1035,7 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
       A.log[s_off + k] = rec;
       A.log_r0[s_off + k] = r0;
       A.log_len[s_off + k] = (int)len;
+      if constexpr (kAdm) A.lpos[(size_t)(m % 3) * A.total + rec.idx] = (int)(s_off + k);
     }
     const int tb = b - b_first;
     if (tb < kTr) {
@@ -725,7 +1061,7 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
 // m), shared by both warp groups: each warp claims 256-entry chunks from a
 // shared counter as soon as its own side's work is done, so the delivery
 // fills whichever side finishes first instead of lengthening the event side.
-template <typename T>
+template <typename T, bool kAdm = false>
 __device__ __forceinline__ void deliver_bucket(const FwdArgs<T>& A, const int m, const int cta, const int n,
                                                int* s_dq) {
   typedef Prec<T> P;
@@ -756,11 +1092,17 @@ __device__ __forceinline__ void deliver_bucket(const FwdArgs<T>& A, const int m,
 #pragma unroll
     for (int e = 0; e < DV; ++e) {
       if (ev[e].x < 0) continue;
+      long long tg = ev[e].x;
+      if constexpr (kAdm) {
+        const int sign = (tg & kNegEntry) ? -1 : 1;
+        tg &= kNegEntry - 1;
+        red_i32(A.arec + (size_t)tg * 8 + 2 + ((m + 1) & 1), sign);
+      }
       if (P::kSlotWords == 1) {
-        red_acc(accn + ev[e].x, ev[e].y);
+        red_acc(accn + tg, ev[e].y);
       } else {
-        red_acc(accn + 2 * (size_t)ev[e].x, ev[e].y);
-        red_acc(accn + 2 * (size_t)ev[e].x + 1, ev2[e].x);
+        red_acc(accn + 2 * (size_t)tg, ev[e].y);
+        red_acc(accn + 2 * (size_t)tg + 1, ev2[e].x);
       }
     }
   }
@@ -774,8 +1116,10 @@ __device__ __forceinline__ bool pause_due(const FwdArgs<T>& A, int m) {
   return ld_published(A.step_start + m + 1) + A.total > A.log_cap;
 }
 
-template <typename T, int NT, int U, int NF = NT / 2>
-__global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
+template <typename T, int NT, int U, int NF = NT / 2, bool kAdm = false>
+__global__ void __launch_bounds__(NT, 2) k_forward(const __grid_constant__ FwdArgs<T> A) {
+  // (__grid_constant__: the out-of-line admission fix-ups take A by reference
+  // without a local copy)
   typedef Prec<T> P;
   typedef Roles<NT, NF> Ro;
   constexpr int kCap = FwdShared<NT, T>::kCap;
@@ -792,6 +1136,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
   __shared__ long long s_off;
   __shared__ unsigned s_ctr[kTr][3];   // per-phase counts (32-bit: native smem atomics), flushed every phase
   __shared__ int s_dq;                            // next unclaimed entry of the bucket being delivered
+  __shared__ unsigned s_drop[kAdm ? kDropTr : 1];  // admission drops per trial, flushed every phase
 
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;
@@ -804,7 +1149,8 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
 
   if (tid < kTr * 3) (&s_ctr[0][0])[tid] = 0u;
   if (tid == 0) s_dq = 0;
-  if (A.kind == EQ_KIND_RING)
+  if (kAdm && tid < kDropTr) s_drop[tid] = 0u;
+  if (A.cal)
     for (int k = tid; k < A.NB; k += NT) s_bin[k] = A.bk_cnt[(size_t)cta * A.NB + k];
   if (tid == 0) s_n = 0;
   // state in shared memory for the launch (A.smem_state): I then V of the owned range
@@ -833,7 +1179,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
     // bucket m+1 (complete: phase m appends only to later buckets), delivered
     // by both sides once their own work is done (deliver_bucket)
     int dn = 0;
-    if (m > A.m0 && A.kind == EQ_KIND_RING) {
+    if (m > A.m0 && A.cal) {
       dn = s_bin[(m + 1) % A.NB];
       dn = dn < A.cap_b ? dn : (int)A.cap_b;
     }
@@ -845,35 +1191,47 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
     if (tid < Ro::NF) {
       // ======================== event side
       const int gtid = tid;
-      if (!kShare) deliver_bucket<T>(A, m, cta, dn, &s_dq);
+      if (!kShare) deliver_bucket<T, kAdm>(A, m, cta, dn, &s_dq);
       // ---------------- fan-out of step m-1: fwd_fanout
-      if (A.kind == EQ_KIND_RING && m > A.m0) {
+      if (A.cal && m > A.m0) {
         const int me = m - 1;                          // emitting step
         const long long L0 = ld_published(A.step_start + me), S = ld_published(A.step_start + me + 1) - L0;
-        fwd_fanout<T, NT, NF, false>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G, s_spk, s_r0,
-                                     s_pre, s_bin);
+        fwd_fanout<T, NT, NF, false, kAdm>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G, s_spk,
+                                           s_r0, s_pre, s_bin, s_drop);
       }
       if (m < m1) tl_mark(A.tl, m, A.G, cta, 1);
-      if (kShare) deliver_bucket<T>(A, m, cta, dn, &s_dq);
+      if (kShare) deliver_bucket<T, kAdm>(A, m, cta, dn, &s_dq);
       if (m < m1) tl_mark(A.tl, m, A.G, cta, 5);
     } else {
       // ======================== neuron side
       const int gtid = tid - Ro::NF;
-      if (m < m1)
-        neuron_side<T, NT, U, NF>(A, m, cta, gtid, begin, end, b_first, A.kind == EQ_KIND_RING, s_own, s_n, s_off,
-                                  s_ctr, spill, s_st);
-      if (kShare) deliver_bucket<T>(A, m, cta, dn, &s_dq);
+      if (m < m1) {
+        neuron_side<T, NT, U, NF, kAdm>(A, m, cta, gtid, begin, end, b_first, A.cal != 0, s_own, s_n, s_off,
+                                        s_ctr, spill, s_st, s_bin);
+      } else if constexpr (kAdm) {                    // last pass: the last phase's fix-ups only
+        adm_fixups<T>(A, m, true, cta, gtid, Ro::NN, s_bin);
+        group_sync(Ro::kBarN, Ro::NN);
+        if (gtid == 0) A.fl_cnt[((m - 1) & 1) * A.G + cta] = 0;
+      }
+      if (kShare) deliver_bucket<T, kAdm>(A, m, cta, dn, &s_dq);
     }
     __syncthreads();
     if (tid == 0) {
       s_dq = 0;
-      if (dn > 0 || (m > A.m0 && A.kind == EQ_KIND_RING)) s_bin[(m + 1) % A.NB] = 0;
+      if (dn > 0 || (m > A.m0 && A.cal)) s_bin[(m + 1) % A.NB] = 0;
+    }
+    if constexpr (kAdm) {
+      if (tid < kDropTr) {
+        if (s_drop[tid] && tid < A.B)
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3 * tid + 2), (unsigned long long)s_drop[tid]);
+        s_drop[tid] = 0u;
+      }
     }
     if (m == m1) break;
     flush_counters<kTr>(s_ctr, A.counters, b_first, A.B, end, A.N);
     tl_mark(A.tl, m, A.G, cta, 2);
     if (!grid_sync(A.bar, A.G, A.err, A.step_start + m + 1, A.log_count, nullptr,
-                   A.kind == EQ_KIND_RING ? A.ring_dirty + m % A.R : nullptr))
+                   A.cal ? A.ring_dirty + m % A.R : nullptr))
       break;
     tl_mark(A.tl, m, A.G, cta, 3);
     if (ld_volatile(A.err) != 0) break;
@@ -892,7 +1250,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(FwdArgs<T> A) {
       A.I[begin + k] = s_st[k];
       A.V[begin + k] = s_st[A.per + k];
     }
-  if (A.kind == EQ_KIND_RING)
+  if (A.cal)
     for (int k = tid; k < A.NB; k += NT) A.bk_cnt[(size_t)cta * A.NB + k] = s_bin[k];
   if (tid < kTr) {
     int b = b_first + tid;

@@ -142,6 +142,17 @@ struct eq_handle {
   int* aoff = nullptr;         // [B*N]
   int* aidx = nullptr;         // [G][in_cap]
   int maxdeg = 1;               // largest CSR row (bounded kinds: event id = log position * maxdeg + row offset)
+  // binaryheap / sortedarray by admission (eq_ring.cuh "admission"): the calendar
+  // path plus one admission record per queue; `cal` = the calendar path runs
+  bool adm = false;
+  bool cal = false;
+  int* arec = nullptr;          // [total][8]
+  int* fl = nullptr;            // [2][G][per]
+  int* fl_cnt = nullptr;        // [2][G]
+  int* lpos = nullptr;          // [3][total]
+  int2* csc = nullptr;          // [E] {x, source} by target, ascending x
+  int2* slots = nullptr;        // [2][total][kAdmSlots]
+  int* cring = nullptr;         // [B][R][N] counts of the DRAM ring rows
   unsigned* drop_bits = nullptr;
   long long drop_cap = 0;
   unsigned long long* tl_f = nullptr;   // debug timelines (EQ_TIMELINE=1)
@@ -413,7 +424,7 @@ __global__ void k_pending_calendar(const long long* acc, const long long* bk,
       const size_t base = ((size_t)cta * NB + bin) * cap_b;
       for (long long k = g0; k < n; k += stride) {
         const long long* ent = bk + (base + k) * bk_words<T>();
-        const long long tg = ent[0];
+        const long long tg = ent[0] & (kNegEntry - 1);   // admission kinds: withdrawn events carry negated payloads
         long long qs, qm;
         const long long* pp = ent + 1;
         if (W == 1) unpack2(pp[0], qs, qm);
@@ -458,6 +469,31 @@ __global__ void k_clear_dirty_rows(long long* ring, int* ring_dirty, int R, long
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < row_words;
        k += (long long)gridDim.x * blockDim.x)
     row[k] = 0;
+}
+
+// Same for the admission kinds' event counts of those rows ([B][R][N] int32).
+__global__ void k_clear_dirty_rows_i32(int* cring, const int* ring_dirty, int R, long long row_words) {
+  const int r = blockIdx.y % R;
+  if (ring_dirty[r] == 0) return;
+  int* row = cring + (size_t)blockIdx.y * row_words;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < row_words;
+       k += (long long)gridDim.x * blockDim.x)
+    row[k] = 0;
+}
+
+// CSC of the admission kinds: source row of every CSR edge, then {x, source}
+// in (target, x) order (a stable radix sort of the edge indices by target).
+__global__ void k_row_src(const int64_t* rowptr, int n_src, int* src) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_src; i += gridDim.x * blockDim.x)
+    for (int64_t x = rowptr[i]; x < rowptr[i + 1]; ++x) src[x] = i;
+}
+__global__ void k_iota_i32(int* p, long long n) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    p[k] = (int)k;
+}
+__global__ void k_csc_pack(const int* xs, const int* src, long long n, int2* csc) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    csc[k] = make_int2(xs[k], src[xs[k]]);
 }
 
 // Lossy ring contents pending at step `now`: slot (now + h) % S holds the
@@ -743,6 +779,8 @@ std::array<long long, 4>* find_block(eq_handle* h, int start) {
 // the first log_used records are kept.
 int grow_log(eq_handle* h, long long need, cudaStream_t s) {
   const long long ncap = std::max<long long>(need, 2 * h->log_cap);
+  if (h->adm && ncap >= (1LL << 31))
+    return fail(h, EQ_ERR_CAPACITY, "spike log beyond 2^31 records (admission kinds keep 32-bit log positions)");
   const size_t rec = h->cfg.precision == 32 ? sizeof(SpikeRec<float>) : sizeof(SpikeRec<double>);
   const long long used = h->log_used;
   void *lg = nullptr, *r0 = nullptr, *len = nullptr, *lt = nullptr, *ltr = nullptr;
@@ -829,6 +867,20 @@ FwdArgs<T> fwd_args(eq_handle* h, int n_steps, void* v_trace) {
   A.imp_n = 0;
   A.imp_dev = nullptr;
   A.no_pause = 0;
+  A.cal = h->cal;
+  A.adm_cap = h->cap;
+  A.arec = h->arec;
+  A.fl = h->fl;
+  A.fl_cnt = h->fl_cnt;
+  A.lpos = h->lpos;
+  A.csc = h->csc;
+  A.csc_off = h->csc_off;
+  A.drop_bits = h->drop_bits;
+  A.drop_cap = h->drop_cap;
+  A.maxdeg = h->maxdeg;
+  A.divPer = FastDiv((unsigned)h->per);
+  A.cring = h->cring;
+  A.slots = h->slots;
   A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
@@ -848,7 +900,7 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
     A.imp_len = h->imp_len + (*blk)[1];
     A.imp_n = (*blk)[2];
   }
-  if (h->bounded || h->lossy) {
+  if ((h->bounded && !h->adm) || h->lossy) {
     BndArgs<T> Bk;
     Bk.f = A;
     Bk.cap = h->lossy ? h->lossy_slots : h->cap;
@@ -891,7 +943,8 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
       h->launches += 1;
       if (n_steps == 0) return check_err(h, s);   // flush: deliver the imports, no step
     }
-    const void* kf = (const void*)k_forward<T, kNT, kU, split_f<T>()>;
+    const void* kf = h->adm ? (const void*)k_forward<T, kNT, kU, split_f<T>(), true>
+                            : (const void*)k_forward<T, kNT, kU, split_f<T>()>;
     // fp32: I and V of each CTA's range in shared memory for the whole launch
     // when two CTAs per SM still fit (state 2 x per x 4 B next to ~39 KB static)
     const size_t st_bytes = (size_t)2 * h->per * sizeof(T);
@@ -905,6 +958,10 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
     FwdArgs<T>* ap = &A;
     ap->smem_state = dyn > 0;
     EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, dyn, s));
+    if (h->adm) {   // reference-order fix-ups of the launch's last admissions (step reached: err[4])
+      k_adm_fixup<T, kNT><<<h->G, kNT, 0, s>>>(A);
+      h->launches += 1;
+    }
   }
   h->launches += 1;
   return check_err(h, s, reached);
@@ -1055,6 +1112,13 @@ int setup_geometry(eq_handle* h) {
   }
   EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf, kNT, 0));
   {
+    int occ_a = 0;
+    const void* ka = h->cfg.precision == 32 ? (const void*)k_forward<float, kNT, kU, kSplitF, true>
+                                            : (const void*)k_forward<double, kNT, kU, split_f<double>(), true>;
+    EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, ka, kNT, 0));
+    occ_f = std::min(occ_f, occ_a);
+  }
+  {
     int occ_q = 0;
     const void* kq = h->cfg.precision == 32 ? (const void*)k_forward_bounded<float, kNT, kU>
                                             : (const void*)k_forward_bounded<double, kNT, kU>;
@@ -1124,12 +1188,57 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   if (cap > (1 << 20)) return fail(h, EQ_ERR_CONFIGURATION, "queue capacity too large; set eq_config.capacity");
   h->cap = (int)cap;
   if (E >= (1LL << 31)) return fail(h, EQ_ERR_CONFIGURATION, "bounded kinds support < 2^31 edges");
+  if (h->adm) {
+    // admission records (16-bit occupancy fields), fix-up lists, spike positions
+    EQ_CUDA(h, ensure(h, (void**)&h->arec, (size_t)h->total * 8 * sizeof(int)));
+    EQ_CUDA(h, ensure(h, (void**)&h->fl, (size_t)2 * h->G * h->per * sizeof(int)));
+    EQ_CUDA(h, ensure(h, (void**)&h->fl_cnt, (size_t)2 * h->G * sizeof(int)));
+    EQ_CUDA(h, ensure(h, (void**)&h->lpos, (size_t)3 * h->total * sizeof(int)));
+    EQ_CUDA(h, ensure(h, (void**)&h->cring, (size_t)B * h->R * N * sizeof(int)));
+    EQ_CUDA(h, ensure(h, (void**)&h->slots, (size_t)2 * h->total * kAdmSlots * sizeof(int2)));
+    // CSC: in-edge segments by exclusive scan of the in-degree, then the edge
+    // indices stably sorted by target (ascending x within a target)
+    size_t tmp_bytes = 0;
+    void* tmp = nullptr;
+    EQ_CUDA(h, ensure(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
+    EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, indeg, h->csc_off, N + 1, s));
+    EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
+    EQ_CUDA(h, cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, indeg, h->csc_off, N + 1, s));
+    release(h, tmp);
+    void *src = nullptr, *xin = nullptr, *xout = nullptr, *kout = nullptr;
+    EQ_CUDA(h, alloc(h, &src, (size_t)E * sizeof(int)));
+    EQ_CUDA(h, alloc(h, &xin, (size_t)E * sizeof(int)));
+    EQ_CUDA(h, alloc(h, &xout, (size_t)E * sizeof(int)));
+    EQ_CUDA(h, alloc(h, &kout, (size_t)E * sizeof(int)));
+    k_row_src<<<(h->n_src + 255) / 256, 256, 0, s>>>(h->rowptr, h->n_src, (int*)src);
+    k_iota_i32<<<1184, 256, 0, s>>>((int*)xin, E);
+    int bits = 1;
+    while ((1LL << bits) < N) ++bits;
+    tmp_bytes = 0;
+    EQ_CUDA(h, cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, h->col, (int*)kout, (const int*)xin, (int*)xout,
+                                               (int)E, 0, bits, s));
+    EQ_CUDA(h, alloc(h, &tmp, tmp_bytes));
+    EQ_CUDA(h, cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, h->col, (int*)kout, (const int*)xin, (int*)xout,
+                                               (int)E, 0, bits, s));
+    EQ_CUDA(h, ensure(h, (void**)&h->csc, (size_t)E * sizeof(int2)));
+    k_csc_pack<<<1184, 256, 0, s>>>((const int*)xout, (const int*)src, E, h->csc);
+    h->launches += 5;
+    EQ_CUDA(h, cudaStreamSynchronize(s));
+    release(h, tmp);
+    release(h, src);
+    release(h, xin);
+    release(h, xout);
+    release(h, kout);
+    h->drop_cap = ((long long)h->log_cap * h->maxdeg + 31) / 32 * 32;
+    EQ_CUDA(h, ensure(h, (void**)&h->drop_bits, (size_t)h->drop_cap / 8));
+    return EQ_OK;
+  }
   size_t qbytes = (size_t)B * N * h->cap * (c.precision == 32 ? sizeof(QEv<float>) : sizeof(QEv<double>));
   if (qbytes > ((size_t)96 << 30))
     return fail(h, EQ_ERR_CONFIGURATION, "queue storage " + std::to_string(qbytes >> 20) +
                                              " MiB exceeds 96 GiB; set eq_config.capacity");
   EQ_CUDA(h, ensure(h, (void**)&h->acnt, (size_t)2 * B * N * sizeof(int)));
-  h->staged = c.staged_queues != 0 && h->cap <= kBqMaxCap;
+  h->staged = c.staged_queues == 1 && h->cap <= kBqMaxCap;
   if (!h->staged) {
     // csc_off = exclusive scan of in-degree: target j's arrival list is its
     // in-edge segment [csc_off[j], csc_off[j+1]) (no step delivers more)
@@ -1214,6 +1323,7 @@ int eq_create(const eq_config* cfg, int device, eq_handle** out) {
     return bad("unknown queue kind " + std::to_string(c.kind));
   if (c.capacity < 0) return bad("capacity must be >= 1, got " + std::to_string(c.capacity));
   if (c.max_ctas < 0) return bad("max_ctas must be >= 0");
+  if (c.staged_queues < 0 || c.staged_queues > 2) return bad("staged_queues must be 0, 1 or 2");
   h->bounded = c.kind == EQ_KIND_FIFORING || c.kind == EQ_KIND_BINARYHEAP || c.kind == EQ_KIND_SORTEDARRAY;
   h->lossy = c.kind == EQ_KIND_LOSSYRING;
   if (c.exact_delivery && std::fabs(c.tau_m - c.tau_syn) < 1e-3 * c.tau_m)
@@ -1386,8 +1496,17 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
     k_pack_edges<double><<<1184, 256, 0, s>>>(col, (const double*)weight, (const double*)delay, n_edges, c.dt,
                                               h->dcode, (EdgeRec<double>*)h->edges);
   h->launches += 1;
+  // heap / sorted run by admission on the calendar (eq_ring.cuh) unless the
+  // queue structures are asked for (staged_queues 1 or 2) or the capacity
+  // needs more than the record's 16-bit occupancy fields
+  h->adm = false;
+  if (h->bounded && c.kind != EQ_KIND_FIFORING && c.staged_queues == 0) {
+    const long long cap_ref = c.capacity > 0 ? c.capacity : (long long)h->horizon * (N - 1) + 1;
+    h->adm = std::min<long long>(cap_ref, std::max<long long>(st[3], 1)) < 32768;
+  }
+  h->cal = c.kind == EQ_KIND_RING || h->adm;
   // queue storage
-  size_t words = c.kind == EQ_KIND_RING ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
+  size_t words = h->cal ? (size_t)c.n_trials * h->R * N * (c.precision == 32 ? 1 : 2) : 1;
   if (h->lossy) {
     // LossyRingQueue capacity as the reference wires it (network.py:327):
     // queue_capacity or horizon*(n-1)+1; >= horizon never aliases
@@ -1401,7 +1520,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
     EQ_CUDA(h, ensure(h, (void**)&h->ring, words * sizeof(long long)));
     if (h->ring != before) h->ring_clean = false;
   }
-  if (c.kind == EQ_KIND_RING) {
+  if (h->cal) {
     const int wd = c.precision == 32 ? 1 : 2;
     h->NB = h->R;
     if (h->NB > 512)
@@ -1443,10 +1562,11 @@ int eq_reset(eq_handle* h, void* stream) {
   DeviceGuard g(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t T = h->tsize;
-  if (h->cfg.kind == EQ_KIND_RING) {
+  if (h->cal) {
     const int wd = h->cfg.precision == 32 ? 1 : 2;
     if (!h->ring_clean) {
       EQ_CUDA(h, cudaMemsetAsync(h->ring, 0, h->ring_words * sizeof(long long), s));
+      if (h->adm) EQ_CUDA(h, cudaMemsetAsync(h->cring, 0, (size_t)h->total * h->R * sizeof(int), s));
       h->ring_clean = true;
     } else {
       const long long row_words = (long long)h->cfg.n_neurons * wd;
@@ -1454,6 +1574,12 @@ int eq_reset(eq_handle* h, void* stream) {
                               (unsigned)(h->cfg.n_trials * h->R)), 256, 0, s>>>(h->ring, h->ring_dirty, h->R,
                                                                                 row_words);
       h->launches += 1;
+      if (h->adm) {
+        k_clear_dirty_rows_i32<<<dim3((unsigned)std::min<long long>((h->cfg.n_neurons + 255) / 256, 64),
+                                      (unsigned)(h->cfg.n_trials * h->R)), 256, 0, s>>>(h->cring, h->ring_dirty, h->R,
+                                                                                        h->cfg.n_neurons);
+        h->launches += 1;
+      }
     }
     EQ_CUDA(h, cudaMemsetAsync(h->acc, 0, (size_t)2 * h->total * wd * sizeof(long long), s));
     EQ_CUDA(h, cudaMemsetAsync(h->bk_cnt, 0, (size_t)h->G * h->NB * sizeof(int), s));
@@ -1474,7 +1600,12 @@ int eq_reset(eq_handle* h, void* stream) {
   EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
   EQ_CUDA(h, cudaMemsetAsync(h->log_count, 0, sizeof(unsigned long long), s));
   EQ_CUDA(h, cudaMemsetAsync(h->step_start, 0, sizeof(long long), s));
-  if (h->bounded) {
+  if (h->adm) {
+    EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
+    EQ_CUDA(h, cudaMemsetAsync(h->arec, 0, (size_t)h->total * 8 * sizeof(int), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->fl_cnt, 0, (size_t)2 * h->G * sizeof(int), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->lpos, 0xFF, (size_t)3 * h->total * sizeof(int), s));
+  } else if (h->bounded) {
     const int B = h->cfg.n_trials, N = h->cfg.n_neurons;
     EQ_CUDA(h, cudaMemsetAsync(h->acnt, 0, (size_t)2 * B * N * sizeof(int), s));
     EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
@@ -2056,7 +2187,7 @@ int eq_get_pending(eq_handle* h, int64_t* host_out, void* stream) {
     else
       k_pending_bq<double><<<592, 256, 0, s>>>(h->qkeys, (const longlong2*)h->qpay, h->meta, h->C,
                                                 (long long)B * N, H, h->steps_done, (long long*)buf);
-  } else if (h->bounded) {
+  } else if (h->bounded && !h->adm) {
     if (h->cfg.precision == 32)
       k_pending_bounded<float><<<592, 256, 0, s>>>((const QEv<float>*)h->q, h->meta, h->cfg.kind, h->cap,
                                                     (long long)B * N, H, h->steps_done, (long long*)buf);
@@ -2099,8 +2230,8 @@ int64_t eq_log_capacity(const eq_handle* h, int32_t* n_grows) {
 
 int eq_debug_set_bucket_capacity(eq_handle* h, int64_t cap) {
   if (!h) return EQ_ERR_CONFIGURATION;
-  if (h->cfg.kind != EQ_KIND_RING || !h->net_set)
-    return fail(h, EQ_ERR_CONFIGURATION, "bucket capacity: ring kind after eq_set_network only");
+  if (!h->cal || !h->net_set)
+    return fail(h, EQ_ERR_CONFIGURATION, "bucket capacity: calendar kinds (ring, heap, sorted) after eq_set_network only");
   if (cap < 1 || cap > h->cap_b_alloc)
     return fail(h, EQ_ERR_CONFIGURATION, "bucket capacity outside [1, " + std::to_string(h->cap_b_alloc) + "]");
   h->cap_b = cap;

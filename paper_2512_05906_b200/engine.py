@@ -33,7 +33,7 @@ class Engine:
                  precision: int = 32, lif: Optional[LIFConfig] = None, capacity: int = 0,
                  max_spikes: int = 0, device: Optional[int] = None,
                  partition: Optional[Tuple[int, int]] = None, max_ctas: int = 0,
-                 stream: Optional[torch.cuda.Stream] = None, staged_queues: bool = False):
+                 stream: Optional[torch.cuda.Stream] = None, staged_queues: int = 0):
         self.L = _native.lib()
         if kind not in _native.KIND_IDS:
             raise ConfigurationError(f"unknown queue kind {kind!r}")
@@ -55,7 +55,7 @@ class Engine:
         cfg.dt, cfg.tau_m, cfg.tau_syn = lif.dt, lif.tau_m, lif.tau_syn
         cfg.v_th, cfg.v_reset = lif.v_th, lif.v_reset
         cfg.max_ctas = max_ctas
-        cfg.staged_queues = int(bool(staged_queues))
+        cfg.staged_queues = int(staged_queues)   # 0 admission, 1 smem-staged, 2 HBM structures
         self.cfg = cfg
         self._stream = stream      # None: the device's current torch stream at each call
         h = ctypes.c_void_p()

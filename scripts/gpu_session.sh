@@ -129,10 +129,21 @@ for p in $PARTS; do
 done
 for p in $PARTS; do
   case $p in
+    adm)
+      timeout 2400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_r2.py -m gpu -x -q -k "bounded or overflow or grows or c4" \
+        > gpurun_out/${TAG}_adm_tests.log 2>&1; tail -3 gpurun_out/${TAG}_adm_tests.log ;;
+    abadm)
+      for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C2 --trials 32 --kind sortedarray --capacity 64" \
+                 "--config C3 --trials 16 --kind binaryheap --capacity 64" "--config C4 --trials 4 --kind binaryheap --capacity 16" \
+                 "--config C4 --trials 4 --kind sortedarray --capacity 32" "--config C2 --trials 32 --kind ring"; do
+        for impl in admission hbm; do
+          bash scripts/ab_args.sh "$cfg --queue-impl $impl" $impl=paper_2512_05906_b200/lib/libeventq_b200.so
+        done
+      done 2>&1 | tee gpurun_out/${TAG}_abadm.txt ;;
     abstaged)
       for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C2 --trials 32 --kind binaryheap --capacity 64"; do
         bash scripts/ab_args.sh "$cfg" hbm=paper_2512_05906_b200/lib/libeventq_b200.so
-        bash scripts/ab_args.sh "$cfg --staged-queues" staged=paper_2512_05906_b200/lib/libeventq_b200.so
+        bash scripts/ab_args.sh "$cfg --queue-impl smem" staged=paper_2512_05906_b200/lib/libeventq_b200.so
       done ;;
   esac
 done

@@ -24,7 +24,7 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-def _engine(net, mask, amp, B, T, precision, kind="ring", refractory=0, capacity=0, exact=True, staged=False):
+def _engine(net, mask, amp, B, T, precision, kind="ring", refractory=0, capacity=0, exact=True, staged=0):
     from paper_2512_05906_b200.engine import Engine
     lif = wl.LIFConfig(refractory_steps=refractory, exact_delivery=exact)
     eng = Engine(net.n, B, T, kind=kind, precision=precision, lif=lif, capacity=capacity or 0, staged_queues=staged)
@@ -206,7 +206,7 @@ BOUNDED = ["dense_heap_n8", "dense_sorted_n8", "dense_fifo_n8", "dense_heap_cap3
            "dense_fifo_cap2_n12", "dense_sorted_plain_cap3_n12"]
 
 
-def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=True, exact=True, staged=False):
+def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=True, exact=True, staged=0):
     eng = _engine(net, mask, amp, B, T, precision, kind=kind, capacity=capacity, exact=exact, staged=staged)
     out = eng.forward()
     s = OracleSession(n=net.n, n_trials=B, t_steps=T, kind=kind, mode="device", precision=precision,
@@ -225,13 +225,17 @@ def _compare_bounded(net, mask, amp, B, T, precision, kind, capacity, backward=T
     return eng, out, ref
 
 
-@pytest.mark.parametrize("staged", [False, True])
+IMPLS = pytest.mark.parametrize("staged", [0, 1, 2], ids=["admission", "smem", "hbm"])
+
+
+@IMPLS
 @pytest.mark.parametrize("precision", [32, 64])
 @pytest.mark.parametrize("name", BOUNDED)
 def test_bounded_kinds_bitwise_vs_oracle(name, precision, staged):
-    """Both implementations of the bounded kinds: HBM-resident structures and
-    (capacity <= 64) the shared-memory staged queues with the in-kernel
-    arrival sort."""
+    """All three implementations of the bounded kinds: heap / sorted by
+    admission on the calendar (default; FIFO falls back to 2), the
+    shared-memory staged queues with the in-kernel arrival sort (capacity
+    <= 64) and the HBM-resident structures."""
     case = BY_NAME[name]
     net, mask, amp = case.inputs()
     eng, out, _ = _compare_bounded(net, mask, amp, 1, case.t_steps, precision, case.kind, case.capacity,
@@ -380,7 +384,7 @@ def test_c3_full_size_trials_are_independent():
     assert np.array_equal(c[0], c[2])
 
 
-@pytest.mark.parametrize("staged", [False, True])
+@IMPLS
 @pytest.mark.parametrize("kind,cap", [("binaryheap", 8), ("sortedarray", 8), ("binaryheap", 64)])
 def test_bounded_c2_size_bitwise_vs_oracle(kind, cap, staged):
     """BASELINE config 2 sizes (10k neurons, K = 100, delays 1..64, T = 1000),

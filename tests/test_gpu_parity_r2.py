@@ -25,7 +25,7 @@ from paper_2512_05906_b200 import workload as wl
 pytestmark = pytest.mark.gpu
 
 
-def _engine(net, mask, amp, B, T, precision=32, kind="ring", capacity=0, max_spikes=0, exact=True, staged=False):
+def _engine(net, mask, amp, B, T, precision=32, kind="ring", capacity=0, max_spikes=0, exact=True, staged=0):
     from paper_2512_05906_b200.engine import Engine
     eng = Engine(net.n, B, T, kind=kind, precision=precision, capacity=capacity, max_spikes=max_spikes,
                  lif=wl.LIFConfig(exact_delivery=exact), staged_queues=staged)
@@ -81,19 +81,22 @@ def _assert_reverse(eng, s, out, B):
 
 # ---------------------------------------------------------------- rare paths
 
+@pytest.mark.parametrize("kind,cap", [("ring", 0), ("binaryheap", 6), ("sortedarray", 6)])
 @pytest.mark.parametrize("precision", [32, 64])
-def test_bucket_overflow_spills_to_dram_ring_bitwise(precision):
+def test_bucket_overflow_spills_to_dram_ring_bitwise(precision, kind, cap):
     """Calendar buckets of 2 events per CTA per step: nearly every event takes
     the spill path (red.add into the DRAM ring row, dirty flag, pop adds the
-    row, row clear) — same raster, state, pending contents and reverse."""
+    row, row clear; the admission kinds also count the row's events and
+    withdraw fix-up losers through it) — same raster, state, pending contents,
+    drops and reverse."""
     net = wl.random_network(2000, 40, 23, delay_steps=(1, 24), w_mean=0.02, w_std=0.01)
     B, T = 2, 300
     mask = wl.drive_masks(2000, B, T, 1e-3, seed0=31)
     amp = np.full(2000, 12.0)
-    eng = _engine(net, mask, amp, B, T, precision)
+    eng = _engine(net, mask, amp, B, T, precision, kind=kind, capacity=cap)
     eng.debug_set_bucket_capacity(2)
     out = eng.forward()
-    s = _oracle(net, mask, amp, B, T, precision, eng.frac_bits)
+    s = _oracle(net, mask, amp, B, T, precision, eng.frac_bits, kind=kind, capacity=cap)
     ref = s.forward()
     _assert_forward_equal(eng, out, ref)
     assert eng.counters()[:, 1].sum() > 50 * eng.geometry[0], "too few events to overflow 2-event buckets"
@@ -103,7 +106,8 @@ def test_bucket_overflow_spills_to_dram_ring_bitwise(precision):
     _assert_forward_equal(eng, out2, ref)
 
 
-@pytest.mark.parametrize("kind,cap,staged", [("ring", 0, False), ("binaryheap", 4, False), ("binaryheap", 4, True)])
+@pytest.mark.parametrize("kind,cap,staged", [("ring", 0, 0), ("binaryheap", 4, 0), ("sortedarray", 4, 0),
+                                              ("binaryheap", 4, 1), ("binaryheap", 4, 2)])
 def test_spike_log_grows_mid_run_bitwise(kind, cap, staged):
     """max_spikes far below the run's spike count: the launch pauses at a step
     boundary whenever one more step could overflow, the log (and for bounded
@@ -210,9 +214,9 @@ def _c4_inputs():
     return _C4["net"]
 
 
-@pytest.mark.parametrize("kind,cap,staged", [("binaryheap", 16, False), ("binaryheap", 32, False),
-                                              ("sortedarray", 16, False), ("sortedarray", 32, False),
-                                              ("binaryheap", 16, True)])
+@pytest.mark.parametrize("kind,cap,staged", [("binaryheap", 16, 0), ("binaryheap", 32, 0),
+                                              ("sortedarray", 16, 0), ("sortedarray", 32, 0),
+                                              ("binaryheap", 16, 1), ("sortedarray", 32, 2)])
 def test_c4_full_size_bounded_with_drops_bitwise(kind, cap, staged):
     """C4 at full size — 1M neurons, K = 100, delays 1..256 — with the heap and
     sorted kinds at capacity 16 / 32 (the memory-pressure regime: most events
