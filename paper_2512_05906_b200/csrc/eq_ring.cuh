@@ -106,7 +106,10 @@ struct FwdArgs {
   // bounded kinds by admission (binaryheap / sortedarray, eq_adm.cuh): the
   // calendar carries the accepted events; a per-target record counts them
   int adm_cap;               // accept while the queue holds fewer events
-  int* arec;                 // [total][8] {E|pc<<16 [2], popped [2], arrivals [3], -}
+  int* aw;                   // [2][totp] E | pc << 16 by phase parity
+  unsigned short* ac;        // [2][totp] events accepted for the step with that parity (popped at it)
+  unsigned short* aa;        // [3][totp] arrivals of the phase (step % 3)
+  long long totp;            // total rounded up to a multiple of 8
   int* fl;                   // [2][G][per] targets whose step needs the reference order
   int* fl_cnt;               // [2][G]
   int* lpos;                 // [3][total] log position of the spike of step s (s % 3)
@@ -279,13 +282,19 @@ struct Roles {
 // among a step's arrivals, which come first in the reference order (emit step,
 // then ascending CSR edge index x).  The events themselves ride the ring kind's
 // calendar (buckets + L2 accumulator, fixed point); the structure is replaced by
-// a 32-byte admission record per queue:
+// admission counters per queue, each in its own array so the owner's per-step
+// pass over them is coalesced (16 bytes per queue and step):
 //
-//   words 0,1  E | pc << 16 of the phase with that parity: E = events held
-//              before the phase's admissions, pc = events popped at its step
-//   words 2,3  events accepted for the step with that parity (counted where the
-//              payload is delivered into the accumulator; read and zeroed at pop)
-//   words 4-6  arrivals of the phase (step % 3)
+//   aw[2]  E | pc << 16 of the phase with that parity: E = events held before
+//          the phase's admissions, pc = events popped at its step
+//   ac[2]  signed 16-bit: events accepted for the step with that parity (counted
+//          where the payload is delivered into the accumulator; read and zeroed
+//          at pop; decoded pairwise with the borrow, like the payload pairs)
+//   aa[3]  16-bit: arrivals of the phase (step % 3)
+//
+// (16-bit counters are updated with 32-bit atomics on the word holding two
+// queues' counters: arrivals stay in [0, 65535]; pop counts in [-cap, cap]
+// are decoded with the borrow.)
 //
 // Phase m admits the arrivals of step m-1's spikes: an event takes a ticket t
 // (atomic on its target's arrival word); with occ = min(E + n, cap) - pc of phase
@@ -310,12 +319,25 @@ __device__ __forceinline__ int* cring_at(const FwdArgs<T>& A, int row, long long
   return A.cring + ((size_t)b * A.R + row) * A.N + (tgt - (long long)b * A.N);
 }
 
-// Occupancy before the admissions of phase m (from phase m-1's record words).
-__device__ __forceinline__ int adm_occ(const int* r, int m, int cap) {
-  const int ep = r[(m - 1) & 1];
-  const int n = r[4 + (m + 2) % 3];
+// Occupancy before the admissions of phase m (from phase m-1's counters).
+template <typename T>
+__device__ __forceinline__ int adm_occ(const FwdArgs<T>& A, int m, long long tgt) {
+  const int ep = A.aw[(size_t)((m - 1) & 1) * A.totp + tgt];
+  const int n = A.aa[(size_t)((m + 2) % 3) * A.totp + tgt];
   const int e = (ep & 0xffff) + n;
-  return (e < cap ? e : cap) - (ep >> 16);
+  return (e < A.adm_cap ? e : A.adm_cap) - (ep >> 16);
+}
+// Ticket of an arrival in phase m (its rank among the target's arrivals so far).
+template <typename T>
+__device__ __forceinline__ int adm_ticket(const FwdArgs<T>& A, int m, long long tgt) {
+  unsigned* w = reinterpret_cast<unsigned*>(A.aa + (size_t)(m % 3) * A.totp) + (tgt >> 1);
+  const int sh = (int)(tgt & 1) * 16;
+  return (int)((atomicAdd(w, 1u << sh) >> sh) & 0xffffu);
+}
+// +-1 accepted event for the step with parity par.
+template <typename T>
+__device__ __forceinline__ void adm_count(const FwdArgs<T>& A, int par, long long tgt, int sign) {
+  red_i32(reinterpret_cast<int*>(A.ac + (size_t)par * A.totp) + (tgt >> 1), sign * (1 << ((int)(tgt & 1) * 16)));
 }
 
 // Add (sign +1) or withdraw (-1) one event's payload and count at due step ds
@@ -332,7 +354,7 @@ __device__ __forceinline__ void adm_apply(const FwdArgs<T>& A, int p, bool in_ke
       red_add(a + 2 * (size_t)tgt, q1);
       red_add(a + 2 * (size_t)tgt + 1, q2);
     }
-    red_i32(A.arec + (size_t)tgt * 8 + 2 + (ds & 1), sign);
+    adm_count(A, ds & 1, tgt, sign);
     return;
   }
   const int bn = ds % A.NB;
@@ -398,10 +420,10 @@ __device__ __forceinline__ void adm_settle(const FwdArgs<T>& A, const int p, con
 }
 
 // Free room and arrival count of a fix-up target's admissions of phase p-1.
-__device__ __forceinline__ int2 adm_room(const int* arec, int cap, int p, int tgt) {
+template <typename T>
+__device__ __forceinline__ int2 adm_room(const FwdArgs<T>& A, int p, int tgt) {
   const int q = p - 1;
-  const int* r = arec + (size_t)tgt * 8;
-  return make_int2(cap - adm_occ(r, q, cap), r[4 + q % 3]);
+  return make_int2(A.adm_cap - adm_occ(A, q, tgt), A.aa[(size_t)(q % 3) * A.totp + tgt]);
 }
 
 // Fix-up from the recorded keys (n <= kAdmSlots arrivals), by one thread:
@@ -434,7 +456,7 @@ __device__ __forceinline__ void adm_fixup(const FwdArgs<T>& A, const int p, cons
   const StepConsts<T>& c = A.c;
   const int me = p - 2;
   const int b = c.divN.div(tgt), j = tgt - b * A.N;
-  const int2 rn = adm_room(A.arec, A.adm_cap, p, tgt);
+  const int2 rn = adm_room(A, p, tgt);
   const int fr = rn.x, n = rn.y;
   const long long L0 = A.step_start[me], L1 = A.step_start[me + 1];
   const int* lp = A.lpos + (size_t)(me % 3) * A.total + (size_t)b * A.N;
@@ -469,7 +491,7 @@ __device__ __noinline__ void adm_fixups(const FwdArgs<T>& A, const int p, const 
   bool walk = false;
   for (int k = gtid; k < n; k += nthreads) {
     const int tgt = lst[k];
-    const int2 rn = adm_room(A.arec, A.adm_cap, p, tgt);
+    const int2 rn = adm_room(A, p, tgt);
     if (rn.x < kAdmSlots && rn.y <= kAdmSlots) adm_fixup_slots<T>(A, p, in_kernel, tgt, rn.x, rn.y, bins, cta);
     else walk = true;
   }
@@ -481,7 +503,7 @@ __device__ __noinline__ void adm_fixups(const FwdArgs<T>& A, const int p, const 
     int tgt = 0;
     if (k < n) {
       tgt = lst[k];
-      const int2 rn = adm_room(A.arec, A.adm_cap, p, tgt);
+      const int2 rn = adm_room(A, p, tgt);
       w = !(rn.x < kAdmSlots && rn.y <= kAdmSlots);
     }
     unsigned bal = __ballot_sync(0xffffffffu, w);
@@ -545,7 +567,10 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
 #ifndef EQ_FWD_EV
 #define EQ_FWD_EV 3
 #endif
-    constexpr int EV = kAdm ? 2 : EQ_FWD_EV;
+#ifndef EQ_ADM_EV
+#define EQ_ADM_EV 2
+#endif
+    constexpr int EV = kAdm ? EQ_ADM_EV : EQ_FWD_EV;
     for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
       int jj[EV], kk[EV];
       T ww[EV], dd[EV];
@@ -575,9 +600,8 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
         for (int e = 0; e < EV; ++e) {
           if (kk[e] < 0) continue;
           const int tgt = c.divN.div(s_spk[kk[e]].idx) * A.N + jj[e];
-          int* r = A.arec + (size_t)tgt * 8;
-          tk[e] = atomicAdd(r + 4 + m % 3, 1);
-          fr[e] = A.adm_cap - adm_occ(r, m, A.adm_cap);
+          tk[e] = adm_ticket(A, m, tgt);
+          fr[e] = A.adm_cap - adm_occ(A, m, tgt);
         }
 #pragma unroll
         for (int e = 0; e < EV; ++e) {                      // keys for a possible fix-up
@@ -629,7 +653,7 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
             red_add(accn + 2 * (size_t)tgt, q1);
             red_add(accn + 2 * (size_t)tgt + 1, q2);
           }
-          if constexpr (kAdm) red_i32(A.arec + (size_t)tgt * 8 + 2 + ((m + 1) & 1), 1);
+          if constexpr (kAdm) adm_count(A, (m + 1) & 1, tgt, 1);
           continue;
         }
         int bn;
@@ -741,36 +765,43 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
     __threadfence();   // their reds into acc / counts, before this group's plain loads of them
     group_sync(Ro::kBarN, Ro::NN);
     if (gtid == 0) A.fl_cnt[((m - 1) & 1) * A.G + cta] = 0;
-    // four records per thread in flight: loads first, then the stores
-    for (long long i0 = begin + gtid; i0 < end; i0 += 4 * Ro::NN) {
-      int ep[4], np[4], pc[4];
+    // E|pc of this phase from the last one's counters, pops of step m read and
+    // zeroed, next phase's arrival counters zeroed: four queues per thread with
+    // 16- / 8-byte accesses (begin and per are multiples of 32)
+    const int* wp = A.aw + (size_t)((m - 1) & 1) * A.totp;
+    int* wc = A.aw + (size_t)(m & 1) * A.totp;
+    const unsigned short* np = A.aa + (size_t)((m + 2) % 3) * A.totp;
+    unsigned short* nz = A.aa + (size_t)((m + 1) % 3) * A.totp;
+    unsigned short* cp = A.ac + (size_t)(m & 1) * A.totp;
+    for (long long i0 = begin + 4 * gtid; i0 < end; i0 += 4 * Ro::NN) {
+      const int4 w4 = *reinterpret_cast<const int4*>(wp + i0);
+      const ushort4 n4 = *reinterpret_cast<const ushort4*>(np + i0);
+      // pop counts: signed 16-bit pairs (a withdrawal may sit here while its
+      // event went to a DRAM ring row: -1 borrows from the pair's other half)
+      const uint2 c2 = *reinterpret_cast<const uint2*>(cp + i0);
+      const int wv[4] = {w4.x, w4.y, w4.z, w4.w};
+      const int nv[4] = {n4.x, n4.y, n4.z, n4.w};
+      int cv[4];
+      cv[0] = (short)(c2.x & 0xffffu);
+      cv[1] = (int)(c2.x - (unsigned)cv[0]) >> 16;
+      cv[2] = (short)(c2.y & 0xffffu);
+      cv[3] = (int)(c2.y - (unsigned)cv[2]) >> 16;
+      int out[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const long long idx = i0 + u * Ro::NN;
-        if (idx < end) {
-          const int* r = A.arec + (size_t)idx * 8;
-          ep[u] = r[(m - 1) & 1];
-          np[u] = r[4 + (m + 2) % 3];
-          pc[u] = r[2 + (m & 1)];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long idx = i0 + u * Ro::NN;
-        if (idx >= end) continue;
-        int* r = A.arec + (size_t)idx * 8;
-        if (dirty) {                                   // events that overflowed a bucket into ring row m
-          int* cr = cring_at(A, m % A.R, idx);
-          pc[u] += *cr;
+        if (dirty && i0 + u < end) {                   // events that overflowed a bucket into ring row m
+          int* cr = cring_at(A, m % A.R, i0 + u);
+          cv[u] += *cr;
           *cr = 0;
         }
-        const int e = (ep[u] & 0xffff) + np[u];
-        const int occ = (e < A.adm_cap ? e : A.adm_cap) - (ep[u] >> 16);
-        r[m & 1] = occ | (pc[u] << 16);
-        r[2 + (m & 1)] = 0;
-        r[4 + (m + 1) % 3] = 0;
+        const int e = (wv[u] & 0xffff) + nv[u];
+        out[u] = ((e < A.adm_cap ? e : A.adm_cap) - (wv[u] >> 16)) | (cv[u] << 16);
       }
+      *reinterpret_cast<int4*>(wc + i0) = make_int4(out[0], out[1], out[2], out[3]);   // (tail lanes past
+      *reinterpret_cast<ushort4*>(cp + i0) = make_ushort4(0, 0, 0, 0);                // `end` are padding)
+      *reinterpret_cast<ushort4*>(nz + i0) = make_ushort4(0, 0, 0, 0);
     }
+    if (gtid == 0) tl_mark_any(A.tl, m, A.G, cta, 7);
   }
   // ---------------- (b) neuron update: pop, synapse, membrane, crossing.
   // Walked per trial segment of the owned range so the row pointers are
@@ -1096,7 +1127,7 @@ __device__ __forceinline__ void deliver_bucket(const FwdArgs<T>& A, const int m,
       if constexpr (kAdm) {
         const int sign = (tg & kNegEntry) ? -1 : 1;
         tg &= kNegEntry - 1;
-        red_i32(A.arec + (size_t)tg * 8 + 2 + ((m + 1) & 1), sign);
+        adm_count(A, (m + 1) & 1, tg, sign);
       }
       if (P::kSlotWords == 1) {
         red_acc(accn + tg, ev[e].y);

@@ -146,7 +146,8 @@ struct eq_handle {
   // path plus one admission record per queue; `cal` = the calendar path runs
   bool adm = false;
   bool cal = false;
-  int* arec = nullptr;          // [total][8]
+  void* adm_ctr = nullptr;      // aw [2][totp] int32, ac [2][totp] u16, aa [3][totp] u16
+  long long totp = 0;
   int* fl = nullptr;            // [2][G][per]
   int* fl_cnt = nullptr;        // [2][G]
   int* lpos = nullptr;          // [3][total]
@@ -336,7 +337,8 @@ __global__ void k_pack_edges(const int32_t* col, const T* w, const T* d, long lo
   }
 }
 
-__global__ void k_max_ll(const long long* a, long long n, long long* out) {
+template <typename E>
+__global__ void k_max_ll(const E* a, long long n, long long* out) {
   long long best = 0;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
        k += (long long)gridDim.x * blockDim.x)
@@ -869,7 +871,10 @@ FwdArgs<T> fwd_args(eq_handle* h, int n_steps, void* v_trace) {
   A.no_pause = 0;
   A.cal = h->cal;
   A.adm_cap = h->cap;
-  A.arec = h->arec;
+  A.totp = h->totp;
+  A.aw = (int*)h->adm_ctr;
+  A.ac = h->adm_ctr ? (unsigned short*)((int*)h->adm_ctr + 2 * h->totp) : nullptr;
+  A.aa = h->adm_ctr ? A.ac + 2 * h->totp : nullptr;
   A.fl = h->fl;
   A.fl_cnt = h->fl_cnt;
   A.lpos = h->lpos;
@@ -1190,7 +1195,8 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
   if (E >= (1LL << 31)) return fail(h, EQ_ERR_CONFIGURATION, "bounded kinds support < 2^31 edges");
   if (h->adm) {
     // admission records (16-bit occupancy fields), fix-up lists, spike positions
-    EQ_CUDA(h, ensure(h, (void**)&h->arec, (size_t)h->total * 8 * sizeof(int)));
+    h->totp = (h->total + 7) / 8 * 8;
+    EQ_CUDA(h, ensure(h, &h->adm_ctr, (size_t)h->totp * (2 * 4 + 2 * 2 + 3 * 2)));
     EQ_CUDA(h, ensure(h, (void**)&h->fl, (size_t)2 * h->G * h->per * sizeof(int)));
     EQ_CUDA(h, ensure(h, (void**)&h->fl_cnt, (size_t)2 * h->G * sizeof(int)));
     EQ_CUDA(h, ensure(h, (void**)&h->lpos, (size_t)3 * h->total * sizeof(int)));
@@ -1406,9 +1412,9 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   EQ_CUDA(h, ensure(h, &h->ns_insum, (size_t)N * sizeof(long long)));
   EQ_CUDA(h, ensure(h, &h->ns_inocc, (size_t)N * sizeof(long long)));
   EQ_CUDA(h, ensure(h, &h->ns_indeg, (size_t)(N + 1) * sizeof(int)));   // +1: exclusive scan reads n+1
-  EQ_CUDA(h, ensure(h, &h->ns_stats, 5 * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, &h->ns_stats, 6 * sizeof(long long)));
   void *insum = h->ns_insum, *stats = h->ns_stats, *inocc = h->ns_inocc, *indeg = h->ns_indeg;
-  long long init[5] = {1, -1LL, 0, 0, 1};
+  long long init[6] = {1, -1LL, 0, 0, 1, 0};
   init[1] = (long long)~0ULL;
   EQ_CUDA(h, cudaMemsetAsync(insum, 0, (size_t)N * sizeof(long long), s));
   EQ_CUDA(h, cudaMemsetAsync(inocc, 0, (size_t)N * sizeof(long long), s));
@@ -1425,8 +1431,9 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
         (long long*)insum, (long long*)stats, (long long*)inocc, (int*)indeg);
   k_max_ll<<<256, 256, 0, s>>>((const long long*)insum, N, (long long*)stats + 2);
   k_max_ll<<<256, 256, 0, s>>>((const long long*)inocc, N, (long long*)stats + 3);
-  h->launches += 3;
-  long long st[5];
+  k_max_ll<<<256, 256, 0, s>>>((const int*)indeg, N, (long long*)stats + 5);
+  h->launches += 4;
+  long long st[6];
   EQ_CUDA(h, cudaMemcpyAsync(st, stats, sizeof st, cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));
 
@@ -1502,7 +1509,9 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   h->adm = false;
   if (h->bounded && c.kind != EQ_KIND_FIFORING && c.staged_queues == 0) {
     const long long cap_ref = c.capacity > 0 ? c.capacity : (long long)h->horizon * (N - 1) + 1;
-    h->adm = std::min<long long>(cap_ref, std::max<long long>(st[3], 1)) < 32768;
+    // 16-bit occupancy fields; 16-bit arrival counters (a step delivers at most
+    // the in-degree to a queue)
+    h->adm = std::min<long long>(cap_ref, std::max<long long>(st[3], 1)) < 32768 && st[5] < 65536;
   }
   h->cal = c.kind == EQ_KIND_RING || h->adm;
   // queue storage
@@ -1602,7 +1611,7 @@ int eq_reset(eq_handle* h, void* stream) {
   EQ_CUDA(h, cudaMemsetAsync(h->step_start, 0, sizeof(long long), s));
   if (h->adm) {
     EQ_CUDA(h, cudaMemsetAsync(h->drop_bits, 0, (size_t)h->drop_cap / 8, s));
-    EQ_CUDA(h, cudaMemsetAsync(h->arec, 0, (size_t)h->total * 8 * sizeof(int), s));
+    EQ_CUDA(h, cudaMemsetAsync(h->adm_ctr, 0, (size_t)h->totp * (2 * 4 + 2 * 2 + 3 * 2), s));
     EQ_CUDA(h, cudaMemsetAsync(h->fl_cnt, 0, (size_t)2 * h->G * sizeof(int), s));
     EQ_CUDA(h, cudaMemsetAsync(h->lpos, 0xFF, (size_t)3 * h->total * sizeof(int), s));
   } else if (h->bounded) {

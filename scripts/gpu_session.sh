@@ -132,6 +132,19 @@ for p in $PARTS; do
     adm)
       timeout 2400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_r2.py -m gpu -x -q -k "bounded or overflow or grows or c4" \
         > gpurun_out/${TAG}_adm_tests.log 2>&1; tail -3 gpurun_out/${TAG}_adm_tests.log ;;
+    admprof)
+      for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C3 --trials 16 --kind binaryheap --capacity 64"; do
+        EQ_TIMELINE=1 timeout 600 python scripts/timeline.py $(echo $cfg | sed 's/--trials 4/--trials 4 --steps 300/;s/--trials 16/--trials 16 --steps 300/') 2>&1 | tee -a gpurun_out/${TAG}_adm_timeline.txt
+        EQ_TIMELINE=1 timeout 600 python scripts/timeline.py $(echo $cfg | sed 's/--trials 4/--trials 4 --steps 300/;s/--trials 16/--trials 16 --steps 300/;s/binaryheap --capacity [0-9]*/ring/') 2>&1 | tee -a gpurun_out/${TAG}_adm_timeline.txt
+      done
+      timeout 1500 /usr/local/cuda/bin/ncu --set full --import-source on --clock-control none -k regex:"k_forward" -s 1 -c 1 \
+        -o gpurun_out/${TAG}_c4heap16 -f python bench.py --config C4 --trials 4 --kind binaryheap --capacity 16 --steps 1 --warmup 3 --no-cpu --no-variants > gpurun_out/${TAG}_ncu_c4.log 2>&1
+      echo "ncu rc=$?" ;;
+    abev)
+      for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
+                 "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
+        bash scripts/ab_args.sh "$cfg" ev2=paper_2512_05906_b200/lib/libeventq_b200.so ev4=scratch_lib/adm_ev4.so
+      done 2>&1 | tee gpurun_out/${TAG}_abev.txt ;;
     abadm)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C2 --trials 32 --kind sortedarray --capacity 64" \
                  "--config C3 --trials 16 --kind binaryheap --capacity 64" "--config C4 --trials 4 --kind binaryheap --capacity 16" \

@@ -18,7 +18,8 @@ from paper_2512_05906_b200.engine import Engine  # noqa: E402
 import bench  # noqa: E402
 
 
-ORDER = {"forward": [(5, "deliver done"), (1, "fan-out done / owner done"), (4, "update done"),
+ORDER = {"forward": [(5, "deliver done"), (1, "fan-out done / owner done"), (7, "admission records done"),
+                     (4, "update done"),
                      (6, "clear+log done"),
                      (2, "both sides done"), (3, "barrier done")],
          "reverse": [(4, "stage done"), (5, "events done"), (1, "R-fanout done"), (6, "R-neuron done"),
