@@ -140,6 +140,23 @@ for p in $PARTS; do
       timeout 1500 /usr/local/cuda/bin/ncu --set full --import-source on --clock-control none -k regex:"k_forward" -s 1 -c 1 \
         -o gpurun_out/${TAG}_c4heap16 -f python bench.py --config C4 --trials 4 --kind binaryheap --capacity 16 --steps 1 --warmup 3 --no-cpu --no-variants > gpurun_out/${TAG}_ncu_c4.log 2>&1
       echo "ncu rc=$?" ;;
+    tladm)
+      for cfg in "--config C4 --trials 4 --steps 300 --kind binaryheap --capacity 16" "--config C4 --trials 4 --steps 300 --kind sortedarray --capacity 32" \
+                 "--config C3 --trials 16 --steps 300 --kind binaryheap --capacity 64" "--config C2 --trials 32 --steps 300 --kind binaryheap --capacity 64" \
+                 "--config C2 --trials 32 --steps 300 --kind ring"; do
+        echo "== $cfg"; EQ_TIMELINE=1 timeout 600 python scripts/timeline.py $cfg 2>&1 | head -9
+      done 2>&1 | tee gpurun_out/${TAG}_tladm.txt ;;
+    abskip)
+      for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
+                 "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
+        bash scripts/ab_args.sh "$cfg" soa=scratch_lib/adm_soa.so skip=paper_2512_05906_b200/lib/libeventq_b200.so
+      done 2>&1 | tee gpurun_out/${TAG}_abskip.txt ;;
+    abknobs)
+      for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C2 --trials 32 --kind binaryheap --capacity 64" \
+                 "--config C3 --trials 16 --kind binaryheap --capacity 64" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
+        bash scripts/ab_args.sh "$cfg" bku2=paper_2512_05906_b200/lib/libeventq_b200.so bku1=scratch_lib/bku1.so ev3=scratch_lib/ev3.so \
+          sp320=scratch_lib/sp320.so sp352=scratch_lib/sp352.so sp256=scratch_lib/sp256.so
+      done 2>&1 | tee gpurun_out/${TAG}_abknobs.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
