@@ -280,6 +280,16 @@ def launch_selftest(args):
 
 QUEUE_IMPL = {"admission": 0, "smem": 1, "hbm": 2}   # eq_config.staged_queues
 
+
+def fwd_kernel(kind, impl):
+    """The forward kernel a kind runs: the ring kernel (heap / sorted by
+    admission too), or a bounded-queue structure kernel."""
+    if kind in ("binaryheap", "sortedarray") and impl == 0:
+        return "k_forward (admission)"
+    if kind in ("fiforing", "binaryheap", "sortedarray", "lossyring"):
+        return "k_forward_bq" if impl == 1 and kind != "lossyring" else "k_forward_bounded"
+    return "k_forward"
+
 VARIANTS = (
     # (label, config, trials, kind, capacity, precision, delays)
     ("C3 ring fp64 (the reference's arithmetic)", "C3", 24, "ring", 0, 64, None),
@@ -330,7 +340,7 @@ def measure_variant(label, cfg, trials, kind, capacity, precision, delays, steps
     fb = alg_bytes(ns, spikes, events, "fwd", bounded, precision)
     bb = alg_bytes(ns, spikes, events, "bwd", False, precision)
     f, b = statistics.mean(fw), statistics.mean(bw)
-    dom = ("k_forward_bounded" if bounded else "k_forward", fb, f) if f >= b else ("k_backward", bb, b)
+    dom = (fwd_kernel(kind, 0), fb, f) if f >= b else ("k_backward", bb, b)
     ach = dom[1] / (dom[2] / 1e3) / 1e9
     del eng
     torch.cuda.empty_cache()
@@ -511,7 +521,7 @@ def run_ours(args):
     bounded = args.kind in ("fiforing", "binaryheap", "sortedarray")
     fwd_bytes = alg_bytes(neuron_steps, spikes, events, "fwd", bounded, args.precision)
     bwd_bytes = alg_bytes(neuron_steps, spikes, events, "bwd", False, args.precision)
-    fwd_name = "k_forward_bounded" if bounded else "k_forward"
+    fwd_name = fwd_kernel(args.kind, QUEUE_IMPL[args.queue_impl])
     dom = (fwd_name, fwd_bytes, fwd_avg) if fwd_avg >= bwd_avg else ("k_backward", bwd_bytes, bwd_avg)
     achieved = dom[1] / (dom[2] / 1e3) / 1e9
     # DRAM bytes per launch of that kernel from the committed ncu --set full capture of this workload
