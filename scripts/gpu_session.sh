@@ -157,6 +157,12 @@ for p in $PARTS; do
         bash scripts/ab_args.sh "$cfg" bku2=paper_2512_05906_b200/lib/libeventq_b200.so bku1=scratch_lib/bku1.so ev3=scratch_lib/ev3.so \
           sp320=scratch_lib/sp320.so sp352=scratch_lib/sp352.so sp256=scratch_lib/sp256.so
       done 2>&1 | tee gpurun_out/${TAG}_abknobs.txt ;;
+    abtail)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for r in 1 2; do
+        bash scripts/ab_env.sh "" base=scratch_lib/base.so=- t0=$L=EQ_REV_TAIL=0 t64=$L=EQ_REV_TAIL=64 t128=$L=EQ_REV_TAIL=128 \
+          t192=$L=EQ_REV_TAIL=192 i128=scratch_lib/inl.so=EQ_REV_TAIL=128 i192=scratch_lib/inl.so=EQ_REV_TAIL=192
+      done 2>&1 | tee gpurun_out/${TAG}_abtail.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
