@@ -238,10 +238,15 @@ int eq_debug_timeline(eq_handle* h, int which, uint64_t* host_out);
  * starts at eq_config.max_spikes (or the default) and doubles whenever one more
  * step could overflow it; the run pauses at that step boundary and resumes. */
 int64_t eq_log_capacity(const eq_handle* h, int32_t* n_grows);
-/* Test hook (ring kind): events per calendar bucket per CTA before a bucket
- * spills into the DRAM overflow ring, 1 <= cap <= the allocated size; takes
- * effect from the next eq_reset.  Small values force the spill path. */
+/* Test hook (calendar kinds: ring, and heap / sorted by admission): events per
+ * calendar bucket per CTA before a bucket spills into the DRAM overflow ring,
+ * 1 <= cap <= the allocated size; takes effect from the next eq_reset.  Small
+ * values force the spill path. */
 int eq_debug_set_bucket_capacity(eq_handle* h, int64_t cap);
+/* Test hook (heap / sorted by admission): arrival keys are recorded for the
+ * reference-order fix-ups while a queue's room is below k (0 <= k <= 8, default
+ * 8); 0 sends every fix-up through the in-edge (CSC) walk. */
+int eq_debug_set_admission_slots(eq_handle* h, int32_t k);
 
 /* ------------------------------------------------------------------------
  * Queue operator API: a batch of Q independent queues of one kind that step

@@ -81,6 +81,7 @@ def lib() -> ctypes.CDLL:
         "eq_debug_timeline": (ctypes.c_int, [H, ctypes.c_int, vp]),
         "eq_log_capacity": (i64, [H, ctypes.POINTER(i32)]),
         "eq_debug_set_bucket_capacity": (ctypes.c_int, [H, i64]),
+        "eq_debug_set_admission_slots": (ctypes.c_int, [H, i32]),
         "eq_queues_create": (ctypes.c_int, [ctypes.c_int] * 6 + [ctypes.POINTER(H)]),
         "eq_queues_destroy": (ctypes.c_int, [H]),
         "eq_queues_last_error": (ctypes.c_char_p, [H]),
@@ -107,6 +108,7 @@ EXPORTED = ("eq_create", "eq_destroy", "eq_last_error", "eq_version", "eq_set_ne
             "eq_backward_window_peer", "eq_sync", "eq_counters", "eq_spike_count",
             "eq_get_spikes", "eq_get_pending", "eq_horizon", "eq_frac_bits", "eq_geometry",
             "eq_launch_count", "eq_debug_timeline", "eq_log_capacity", "eq_debug_set_bucket_capacity",
+            "eq_debug_set_admission_slots",
             "eq_queues_create", "eq_queues_destroy",
             "eq_queues_last_error", "eq_queues_capacity", "eq_queues_now", "eq_queues_enqueue", "eq_queues_pop",
             "eq_queues_occupancy", "eq_queues_lossy_counts", "eq_queues_run_poisson")

@@ -121,6 +121,7 @@ struct FwdArgs {
   FastDiv divPer;            // flat target -> owner CTA
   int* cring;                // [B][R][N] event counts of the DRAM ring rows (bucket overflow)
   int2* slots;               // [2][total][kAdmSlots] {x, log position} of a phase's first arrivals
+  int adm_slots;             // keys recorded while free < adm_slots (<= kAdmSlots; 0: every fix-up walks the CSC)
 };
 
 // Arrivals whose key is recorded per target and phase (when 0 < free < kAdmSlots):
@@ -492,7 +493,7 @@ __device__ __noinline__ void adm_fixups(const FwdArgs<T>& A, const int p, const 
   for (int k = gtid; k < n; k += nthreads) {
     const int tgt = lst[k];
     const int2 rn = adm_room(A, p, tgt);
-    if (rn.x < kAdmSlots && rn.y <= kAdmSlots) adm_fixup_slots<T>(A, p, in_kernel, tgt, rn.x, rn.y, bins, cta);
+    if (rn.x < A.adm_slots && rn.y <= A.adm_slots) adm_fixup_slots<T>(A, p, in_kernel, tgt, rn.x, rn.y, bins, cta);
     else walk = true;
   }
   if (!__any_sync(0xffffffffu, walk)) return;     // warp-uniform: each warp walks the targets of its own lanes
@@ -504,7 +505,7 @@ __device__ __noinline__ void adm_fixups(const FwdArgs<T>& A, const int p, const 
     if (k < n) {
       tgt = lst[k];
       const int2 rn = adm_room(A, p, tgt);
-      w = !(rn.x < kAdmSlots && rn.y <= kAdmSlots);
+      w = !(rn.x < A.adm_slots && rn.y <= A.adm_slots);
     }
     unsigned bal = __ballot_sync(0xffffffffu, w);
     while (bal) {
@@ -605,7 +606,7 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
         }
 #pragma unroll
         for (int e = 0; e < EV; ++e) {                      // keys for a possible fix-up
-          if (kk[e] < 0 || fr[e] <= 0 || fr[e] >= kAdmSlots || tk[e] >= kAdmSlots) continue;
+          if (kk[e] < 0 || fr[e] <= 0 || fr[e] >= A.adm_slots || tk[e] >= A.adm_slots) continue;
           const int tgt = c.divN.div(s_spk[kk[e]].idx) * A.N + jj[e];
           A.slots[((size_t)(m & 1) * A.total + tgt) * kAdmSlots + tk[e]] = make_int2(xs[e], (int)(k0 + kk[e]));
         }

@@ -153,6 +153,7 @@ struct eq_handle {
   int* lpos = nullptr;          // [3][total]
   int2* csc = nullptr;          // [E] {x, source} by target, ascending x
   int2* slots = nullptr;        // [2][total][kAdmSlots]
+  int adm_slots = kAdmSlots;    // eq_debug_set_admission_slots
   int* cring = nullptr;         // [B][R][N] counts of the DRAM ring rows
   unsigned* drop_bits = nullptr;
   long long drop_cap = 0;
@@ -886,6 +887,7 @@ FwdArgs<T> fwd_args(eq_handle* h, int n_steps, void* v_trace) {
   A.divPer = FastDiv((unsigned)h->per);
   A.cring = h->cring;
   A.slots = h->slots;
+  A.adm_slots = h->adm_slots;
   A.tl = (h->tl_f && A.m1 <= h->tl_steps) ? h->tl_f : nullptr;
   A.err = h->err_dev;
   A.bar = h->bar;
@@ -2244,6 +2246,14 @@ int eq_debug_set_bucket_capacity(eq_handle* h, int64_t cap) {
   if (cap < 1 || cap > h->cap_b_alloc)
     return fail(h, EQ_ERR_CONFIGURATION, "bucket capacity outside [1, " + std::to_string(h->cap_b_alloc) + "]");
   h->cap_b = cap;
+  return EQ_OK;
+}
+
+int eq_debug_set_admission_slots(eq_handle* h, int32_t k) {
+  if (!h) return EQ_ERR_CONFIGURATION;
+  if (k < 0 || k > kAdmSlots)
+    return fail(h, EQ_ERR_CONFIGURATION, "admission slots outside [0, " + std::to_string(kAdmSlots) + "]");
+  h->adm_slots = k;
   return EQ_OK;
 }
 

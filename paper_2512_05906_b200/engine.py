@@ -343,6 +343,12 @@ class Engine:
         into the DRAM overflow ring (the rarely-taken path); next reset on."""
         _native.check(self.h, self.L.eq_debug_set_bucket_capacity(self.h, int(cap)))
 
+    def debug_set_admission_slots(self, k: int) -> None:
+        """Test hook (heap / sorted by admission): record arrival keys for the
+        reference-order fix-ups only while a queue's room is below k; 0 sends
+        every fix-up through the in-edge walk."""
+        _native.check(self.h, self.L.eq_debug_set_admission_slots(self.h, int(k)))
+
 
 def poisson_drive_device(n: int, n_trials: int, t_steps: int, dt: float, mean_interval: float,
                          pulse_duration: float, seed: int, device=0, stream=None) -> torch.Tensor:

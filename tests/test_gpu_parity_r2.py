@@ -258,3 +258,28 @@ def test_rsnn_function_rejects_a_stale_backward():
     v2.sum().backward(retain_graph=True)          # the latest run: fine
     with pytest.raises(EventQError, match="ran another forward"):
         v1.sum().backward()
+
+
+# ---------------------------------------------------------------- admission fix-ups
+
+@pytest.mark.parametrize("slots", [0, 2])
+@pytest.mark.parametrize("kind,cap", [("binaryheap", 3), ("sortedarray", 5)])
+def test_admission_fixups_without_recorded_keys_bitwise(kind, cap, slots):
+    """Heap / sorted by admission with the arrival keys recorded only while the
+    queue's room is below `slots` (0: never): the reference-order fix-ups then
+    take the in-edge (CSC) walk, one warp per queue, instead of ranking the
+    recorded keys.  Small capacities on a K = 40 network give many contested
+    steps; forward (raster, state, pending, drops) and reverse = oracle."""
+    net = wl.random_network(3000, 40, 37, delay_steps=(1, 12), w_mean=0.03, w_std=0.01)
+    B, T = 2, 300
+    mask = wl.drive_masks(3000, B, T, 1e-3, seed0=71)
+    amp = np.full(3000, 12.0)
+    eng = _engine(net, mask, amp, B, T, 32, kind=kind, capacity=cap)
+    eng.debug_set_admission_slots(slots)
+    out = eng.forward()
+    s = _oracle(net, mask, amp, B, T, 32, eng.frac_bits, kind=kind, capacity=cap)
+    ref = s.forward()
+    _assert_forward_equal(eng, out, ref)
+    c = eng.counters()
+    assert c[:, 2].sum() > 0.01 * c[:, 1].sum(), "capacity should drop a share of the events"
+    _assert_reverse(eng, s, out, B)
