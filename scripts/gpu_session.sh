@@ -163,6 +163,15 @@ for p in $PARTS; do
         bash scripts/ab_env.sh "" base=scratch_lib/base.so=- t0=$L=EQ_REV_TAIL=0 t64=$L=EQ_REV_TAIL=64 t128=$L=EQ_REV_TAIL=128 \
           t192=$L=EQ_REV_TAIL=192 i128=scratch_lib/inl.so=EQ_REV_TAIL=128 i192=scratch_lib/inl.so=EQ_REV_TAIL=192
       done 2>&1 | tee gpurun_out/${TAG}_abtail.txt ;;
+    tmatest)
+      EQ_NO_SMEM_STATE=1 timeout 1500 python -m pytest tests -m gpu -q -x --deselect tests/test_gpu_parity_r2.py::test_c4_full_size_bounded_with_drops_bitwise \
+        > gpurun_out/${TAG}_tma_tests.log 2>&1; echo "tma tests rc=$?"; tail -2 gpurun_out/${TAG}_tma_tests.log ;;
+    abtma)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for cfg in "--config C4 --trials 4" "--config C4 --trials 4 --kind binaryheap --capacity 16" "" "--config C2 --trials 32"; do
+        bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- tma=$L=- notma=$L=EQ_NO_TMA_STAGE=1
+      done 2>&1 | tee gpurun_out/${TAG}_abtma.txt
+      bash scripts/ab_env.sh "" base_nosmem=scratch_lib/base.so=EQ_NO_SMEM_STATE=1 tma_nosmem=$L=EQ_NO_SMEM_STATE=1 2>&1 | tee -a gpurun_out/${TAG}_abtma.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
