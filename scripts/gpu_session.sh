@@ -172,6 +172,15 @@ for p in $PARTS; do
         bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- tma=$L=- notma=$L=EQ_NO_TMA_STAGE=1
       done 2>&1 | tee gpurun_out/${TAG}_abtma.txt
       bash scripts/ab_env.sh "" base_nosmem=scratch_lib/base.so=EQ_NO_SMEM_STATE=1 tma_nosmem=$L=EQ_NO_SMEM_STATE=1 2>&1 | tee -a gpurun_out/${TAG}_abtma.txt ;;
+    ncufwd)
+      timeout 1200 /usr/local/cuda/bin/ncu --set full --import-source on --clock-control none -k regex:"k_forward" -s 1 -c 1 \
+        -o gpurun_out/${TAG}_fwd -f python bench.py --steps 1 --warmup 3 --no-cpu --no-variants > gpurun_out/${TAG}_ncu_fwd.log 2>&1
+      echo "ncu fwd rc=$?" ;;
+    abrow)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for cfg in "" "--config C4 --trials 4" "--config C2 --trials 32 --kind binaryheap --capacity 64" "--precision 64"; do
+        for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- row=$L=-; done
+      done 2>&1 | tee gpurun_out/${TAG}_abrow.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
