@@ -638,24 +638,9 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
         if (kk[e] < 0) continue;
         const SpikeRec<T> rec = s_spk[kk[e]];
         const int b = c.divN.div(rec.idx);
-        const int me = kImp ? (int)rec.a : me_fixed;
-        const T w = ww[e], d = dd[e];
-        const T t_post = rec.t + d;                              // :588
-        const int ds = delivery_step_coded(t_post, cc[e], c.dt, me);  // jumps.py:96
-        T ws, wm;
-        if (A.exact) {
-          const T phi = (T)ds * c.dt - t_post;              // :599
-          ws = w * eq_exp_t(-phi * c.inv_tau_s);            // :601 (x 1/tau, DESIGN §3)
-          wm = w * eq_exp_t(-phi * c.inv_tau_m);            // :606
-        } else {
-          ws = w;
-          wm = (T)0;
-        }
         const int tgt = b * A.N + jj[e];                    // flat target
-        const long long q1 = P::q(ws, c.scale);
-        const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
         if constexpr (kAdm) {
-          if (tk[e] >= fr[e]) {                             // queue full at this ticket: dropped
+          if (tk[e] >= fr[e]) {                             // queue full at this ticket: dropped (no payload)
             const int f = f0 + e * Ro::NF;
             const long long id = (k0 + kk[e]) * (long long)A.maxdeg + (f - s_pre[kk[e]]);
             atomicOr(A.drop_bits + (id >> 5), 1u << (id & 31));
@@ -669,6 +654,21 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
             continue;
           }
         }
+        const int me = kImp ? (int)rec.a : me_fixed;
+        const T w = ww[e], d = dd[e];
+        const T t_post = rec.t + d;                              // :588
+        const int ds = delivery_step_coded(t_post, cc[e], c.dt, me);  // jumps.py:96
+        T ws, wm;
+        if (A.exact) {
+          const T phi = (T)ds * c.dt - t_post;              // :599
+          ws = w * eq_exp_t(-phi * c.inv_tau_s);            // :601 (x 1/tau, DESIGN §3)
+          wm = w * eq_exp_t(-phi * c.inv_tau_m);            // :606
+        } else {
+          ws = w;
+          wm = (T)0;
+        }
+        const long long q1 = P::q(ws, c.scale);
+        const long long q2 = A.exact ? P::q(wm, c.scale) : 0;
         if (ds == m + 1) {
           if (P::kSlotWords == 1) {
             red_add(accn + tgt, pack2(q1, q2));
