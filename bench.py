@@ -284,8 +284,8 @@ QUEUE_IMPL = {"admission": 0, "smem": 1, "hbm": 2}   # eq_config.staged_queues
 def fwd_kernel(kind, impl):
     """The forward kernel a kind runs: the ring kernel (heap / sorted by
     admission too), or a bounded-queue structure kernel."""
-    if kind in ("binaryheap", "sortedarray") and impl == 0:
-        return "k_forward (admission)"
+    if kind in ("binaryheap", "sortedarray", "fiforing") and impl == 0:
+        return "k_forward (admission)"   # (a FIFO delay off the step grid runs k_forward_bounded)
     if kind in ("fiforing", "binaryheap", "sortedarray", "lossyring"):
         return "k_forward_bq" if impl == 1 and kind != "lossyring" else "k_forward_bounded"
     return "k_forward"

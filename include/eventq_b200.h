@@ -78,8 +78,9 @@ typedef struct eq_config {
   int32_t max_ctas;         /* persistent grid size cap (0 = 2 per SM); partitions that run
                                concurrently on one GPU split its SMs this way */
   int32_t staged_queues;    /* bounded-kind implementation (same results):
-                               0 = heap / sorted by admission on the calendar (default;
-                               FIFO keeps 2), 1 = queues staged in shared memory with an
+                               0 = by admission on the calendar (default; a FIFO whose
+                               homogeneous delay is off the step grid keeps 2),
+                               1 = queues staged in shared memory with an
                                in-kernel counting sort of the arrivals (capacity <= 64,
                                eq_bq.cuh), 2 = HBM-resident queue structures (eq_bounded.cuh) */
 } eq_config;

@@ -760,6 +760,15 @@ int check_err(eq_handle* h, cudaStream_t s, int* reached = nullptr) {
     case EQ_ERR_CUDA:
       snprintf(buf, sizeof buf, "device watchdog: grid barrier timed out");
       break;
+    case EQ_ERR_CAPABILITY:
+      if (h->cfg.kind == EQ_KIND_FIFORING) {   // queues.py:220-224 (the step pair is not kept on the device)
+        snprintf(buf, sizeof buf,
+                 "fiforing supports homogeneous delays only: an event arrived after one due later "
+                 "(enqueued at step %d, trial %d, neuron %d)", e[1], e[2], e[3]);
+        break;
+      }
+      snprintf(buf, sizeof buf, "device error %d at step %d (trial %d, neuron %d)", e[0], e[1], e[2], e[3]);
+      break;
     default:
       snprintf(buf, sizeof buf, "device error %d at step %d (trial %d, neuron %d)", e[0], e[1], e[2], e[3]);
   }
@@ -1509,7 +1518,17 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   // queue structures are asked for (staged_queues 1 or 2) or the capacity
   // needs more than the record's 16-bit occupancy fields
   h->adm = false;
-  if (h->bounded && c.kind != EQ_KIND_FIFORING && c.staged_queues == 0) {
+  // FIFO: with its homogeneous delay on the step grid every event of a step
+  // has the same due step, so dues never decrease and the tail-key check
+  // (queues.py:220-224) cannot fire: its accepted sets and pops are the heap's
+  bool fifo_ok = c.kind != EQ_KIND_FIFORING;
+  if (!fifo_ok && c.staged_queues == 0) {
+    unsigned short code0 = 0x8000;
+    EQ_CUDA(h, cudaMemcpyAsync(&code0, h->dcode, sizeof code0, cudaMemcpyDeviceToHost, s));
+    EQ_CUDA(h, cudaStreamSynchronize(s));
+    fifo_ok = (code0 & 0x8000) == 0;
+  }
+  if (h->bounded && fifo_ok && c.staged_queues == 0) {
     const long long cap_ref = c.capacity > 0 ? c.capacity : (long long)h->horizon * (N - 1) + 1;
     // 16-bit occupancy fields; 16-bit arrival counters (a step delivers at most
     // the in-degree to a queue)

@@ -233,7 +233,7 @@ IMPLS = pytest.mark.parametrize("staged", [0, 1, 2], ids=["admission", "smem", "
 @pytest.mark.parametrize("name", BOUNDED)
 def test_bounded_kinds_bitwise_vs_oracle(name, precision, staged):
     """All three implementations of the bounded kinds: heap / sorted by
-    admission on the calendar (default; FIFO falls back to 2), the
+    admission on the calendar (default; the fixtures' FIFO delay is on the step grid), the
     shared-memory staged queues with the in-kernel arrival sort (capacity
     <= 64) and the HBM-resident structures."""
     case = BY_NAME[name]

@@ -283,3 +283,33 @@ def test_admission_fixups_without_recorded_keys_bitwise(kind, cap, slots):
     c = eng.counters()
     assert c[:, 2].sum() > 0.01 * c[:, 1].sum(), "capacity should drop a share of the events"
     _assert_reverse(eng, s, out, B)
+
+
+@pytest.mark.parametrize("delay_steps,impl", [(7, 0), (7.5, 0), (7.5, 2)])
+def test_fifo_homogeneous_delay_on_and_off_the_step_grid(delay_steps, impl):
+    """FIFO with one homogeneous delay: on the step grid (7 dt) every event of
+    a step has the same due step, so it runs by admission; off the grid
+    (7.5 dt) dues of one step differ by the spike time and the reference's
+    tail-key check (queues.py:220-224) can fire, so it runs the queue
+    structures.  Either way the result equals the oracle: same raster, state,
+    pending queues and drops, or a CapabilityError in both."""
+    from paper_2512_05906_b200.errors import CapabilityError
+    net = wl.random_network(400, 20, 43, delay_steps=(1, 1), w_mean=0.05, w_std=0.01)
+    net.delay[:] = delay_steps * 1e-3
+    B, T = 1, 300
+    mask = wl.drive_masks(400, B, T, 1e-3, seed0=83)
+    amp = np.full(400, 12.0)
+    eng = _engine(net, mask, amp, B, T, 64, kind="fiforing", capacity=6, staged=impl)
+    s = _oracle(net, mask, amp, B, T, 64, eng.frac_bits, kind="fiforing", capacity=6)
+    from oracle.oracle import OracleError
+    try:
+        ref = s.forward()
+    except OracleError as e:
+        assert e.kind == "CapabilityError", str(e)
+        assert delay_steps != int(delay_steps), "an on-grid delay cannot violate the FIFO order"
+        with pytest.raises(CapabilityError, match="homogeneous"):
+            eng.forward()
+        return
+    out = eng.forward()
+    _assert_forward_equal(eng, out, ref)
+    assert eng.counters()[:, 2].sum() > 0
