@@ -186,6 +186,12 @@ for p in $PARTS; do
       for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32" "" ; do
         for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- new=$L=-; done
       done 2>&1 | tee gpurun_out/${TAG}_abdrop.txt ;;
+    abwin)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32" \
+                 "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64"; do
+        for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- win=$L=-; done
+      done 2>&1 | tee gpurun_out/${TAG}_abwin.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
