@@ -1078,6 +1078,7 @@ __device__ __forceinline__ void neuron_side(const FwdArgs<T>& A, const int m, co
     A.chunk_cnt[(size_t)m * A.G + cta] = nspk;
   }
   group_sync(Ro::kBarN, Ro::NN);
+  if (!kAdm && gtid == 0) tl_mark_any(A.tl, m, A.G, cta, 7);
   const bool log_ok = s_off + nspk <= A.log_cap;
   for (int k = gtid; k < nspk; k += Ro::NN) {
     const SpikeRec<T> rec = k < kCapN ? s_own[k] : spill[k - kCapN];

@@ -18,7 +18,7 @@ from paper_2512_05906_b200.engine import Engine  # noqa: E402
 import bench  # noqa: E402
 
 
-ORDER = {"forward": [(5, "deliver done"), (1, "fan-out done / owner done"), (7, "admission records done"),
+ORDER = {"forward": [(5, "deliver done"), (1, "fan-out done / owner done"), (7, "adm records / log reserved"),
                      (4, "update done"),
                      (6, "clear+log done"),
                      (2, "both sides done"), (3, "barrier done")],
