@@ -192,6 +192,15 @@ for p in $PARTS; do
                  "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64"; do
         for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- win=$L=-; done
       done 2>&1 | tee gpurun_out/${TAG}_abwin.txt ;;
+    pipetest)
+      EQ_NO_SMEM_STATE=1 timeout 1500 python -m pytest tests -m gpu -q -x --deselect tests/test_gpu_parity_r2.py::test_c4_full_size_bounded_with_drops_bitwise \
+        > gpurun_out/${TAG}_pipe_tests.log 2>&1; echo "pipe tests rc=$?"; tail -2 gpurun_out/${TAG}_pipe_tests.log ;;
+    abpipe)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for cfg in "--config C4 --trials 4" "--config C4 --trials 4 --kind binaryheap --capacity 16" "" "--config C2 --trials 32"; do
+        for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- pipe=$L=-; done
+      done 2>&1 | tee gpurun_out/${TAG}_abpipe.txt
+      bash scripts/ab_env.sh "" base_nosmem=scratch_lib/base.so=EQ_NO_SMEM_STATE=1 pipe_nosmem=$L=EQ_NO_SMEM_STATE=1 2>&1 | tee -a gpurun_out/${TAG}_abpipe.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
