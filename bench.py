@@ -298,6 +298,9 @@ VARIANTS = (
     ("C4 ring (1M neurons, delays 1..256)", "C4", 4, "ring", 0, 32, None),
     ("C4 binaryheap[16] (memory pressure, drops)", "C4", 4, "binaryheap", 16, 32, None),
     ("C4 sortedarray[16] (memory pressure, drops)", "C4", 4, "sortedarray", 16, 32, None),
+    ("C4 binaryheap[32] (memory pressure, drops)", "C4", 4, "binaryheap", 32, 32, None),
+    ("C4 sortedarray[32] (memory pressure, drops)", "C4", 4, "sortedarray", 32, 32, None),
+    ("C2 sortedarray[64]", "C2", 32, "sortedarray", 64, 32, None),
 )
 _NETS = {}
 
