@@ -321,11 +321,15 @@ struct Roles {
 // (atomic on its target's arrival word); with occ = min(E + n, cap) - pc of phase
 // m-1, the first free = cap - occ tickets are accepted.  Tickets come in
 // arbitrary order, so when 0 < free < n the target goes on its owner's fix-up
-// list: at the start of phase m+1 the owner walks the target's in-edges in
-// ascending x (CSC), ranks the arrivals and swaps any ticket winner that is not
-// among the first `free` in the reference order for the one that is (payload and
-// count moved with the exact fixed-point negation, drop bits flipped).  The
-// accepted SET then equals the reference's; accepted COUNTS never change.
+// list: at the start of phase m+1 the owner ranks the arrivals by x — from the
+// keys {x, log position} they recorded by ticket while free < kAdmSlots, or by
+// walking the target's in-edges in ascending x (CSC, one warp) when there were
+// more arrivals than slots — and swaps any ticket winner that is not among the
+// first `free` in the reference order for the one that is (payload and count
+// moved with the exact fixed-point negation, drop bits flipped).  The accepted
+// SET then equals the reference's; accepted COUNTS never change.  Queue
+// contents, pops and the reverse pass's drop bits are therefore the reference's;
+// a queue full before the phase drops every arrival whatever the ticket order.
 
 constexpr long long kNegEntry = 1LL << 62;   // bucket entry flag: a withdrawn event (count -1)
 
