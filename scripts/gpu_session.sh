@@ -206,6 +206,11 @@ for p in $PARTS; do
       for r in 1 2; do
         bash scripts/ab_env.sh "" base=$L=- fev2=scratch_lib/fev2.so=- fev4=scratch_lib/fev4.so=- rev3=scratch_lib/rev3.so=- rwin2k=scratch_lib/rwin2k.so=-
       done 2>&1 | tee gpurun_out/${TAG}_abknob2.txt ;;
+    abrowst)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for r in 1 2; do
+        bash scripts/ab_env.sh "" base=$L=- plain=scratch_lib/st1.so=- last=scratch_lib/st2.so=-
+      done 2>&1 | tee gpurun_out/${TAG}_abrowst.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
