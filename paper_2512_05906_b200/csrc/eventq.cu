@@ -29,7 +29,10 @@ namespace {
 constexpr int kNT = 512;   // threads per CTA of the persistent kernels
 constexpr int kErrWords = 8;  // device error word: [0] code, [1] step, [2] trial, [3] neuron, [4] step reached
 constexpr int kU = 4;      // neurons per thread in flight per round
-constexpr int kSplitF = 288;  // forward event-side threads per CTA (measured: 224..384, profiles/)
+#ifndef EQ_SPLIT_F32
+#define EQ_SPLIT_F32 288
+#endif
+constexpr int kSplitF = EQ_SPLIT_F32;  // forward event-side threads per CTA (measured: 224..384, profiles/)
 #ifndef EQ_SPLIT_B32
 #define EQ_SPLIT_B32 352
 #endif

@@ -211,6 +211,11 @@ for p in $PARTS; do
       for r in 1 2; do
         bash scripts/ab_env.sh "" base=$L=- plain=scratch_lib/st1.so=- last=scratch_lib/st2.so=-
       done 2>&1 | tee gpurun_out/${TAG}_abrowst.txt ;;
+    absplit)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for cfg in "--config C4 --trials 4" "--config C4 --trials 4 --kind binaryheap --capacity 16" ""; do
+        bash scripts/ab_env.sh "$cfg" base=$L=- f256=scratch_lib/f256.so=- f224=scratch_lib/f224.so=- f192=scratch_lib/f192.so=-
+      done 2>&1 | tee gpurun_out/${TAG}_absplit.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
