@@ -245,7 +245,10 @@ class PartitionedNetwork:
             e.set_frac_bits(fb)
         return fb
 
-    def forward(self, t_steps: int) -> None:
+    def forward(self, t_steps: int, sync: bool = True) -> None:
+        """sync=False (peer exchange): no host wait at the end (errors surface at
+        the next sync) — the whole window loop is then one stream-ordered
+        sequence that a CUDA graph can capture (scripts/c5_partitioned.py --graph)."""
         self.unify_frac_bits()
         for e in self.engines:
             e.reset()
@@ -259,8 +262,9 @@ class PartitionedNetwork:
             for e in self.engines:          # deliver the last window's spikes (queue contents)
                 e.run_window(len(self.win), self.win[-1][0], 0)
             self._order()
-            for e in self.engines:
-                e.sync()
+            if sync:
+                for e in self.engines:
+                    e.sync()
             return
         for a, b in self.win:
             for e in self.engines:
@@ -274,7 +278,7 @@ class PartitionedNetwork:
         for e in self.engines:
             e.run(0)
 
-    def backward(self, v_bars: Sequence[torch.Tensor], want_amp: bool = True):
+    def backward(self, v_bars: Sequence[torch.Tensor], want_amp: bool = True, sync: bool = True):
         grads = [e.backward_begin(vb, None, want_amp) for e, vb in zip(self.engines, v_bars)]
         if self.peer:
             self._order()
@@ -283,8 +287,9 @@ class PartitionedNetwork:
                 for e in self.engines:
                     e.backward_window_peer(w, a, b)
                 self._order()
-            for e in self.engines:
-                e.sync()
+            if sync:
+                for e in self.engines:
+                    e.sync()
             return grads
         for wi in range(len(self.win) - 1, -1, -1):
             a, _ = self.win[wi]

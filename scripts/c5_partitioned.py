@@ -37,6 +37,9 @@ def main():
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="peer exchange: capture the whole partitioned forward + reverse (every window's "
+                         "launches and stream events) in one CUDA graph and time its replays")
     ap.add_argument("--concurrent", action="store_true",
                     help="peer exchange: every partition on its own stream and SM share (grid = 2*SMs/P), "
                          "windows ordered by events — the partitions run side by side as on P GPUs")
@@ -112,7 +115,34 @@ def main():
     if world > 1:
         dist.barrier()
     fw, bw = [], []
-    for _ in range(args.reps):
+    graph = args.graph and world == 1 and args.exchange == "peer"
+    if graph:
+        v_eager = [e.state()["v"].clone() for e in engines]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            cap = torch.cuda.current_stream()
+            pn.forward(args.steps, sync=False)
+            pn.join(cap)
+            vb = [(2.0 * (e.state()["v"].double() - 0.25)).to(e.dtype) for e in engines]
+            pn.backward(vb, want_amp=False, sync=False)
+            pn.join(cap)
+        for _ in range(args.reps + 1):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            fw.append(a.elapsed_time(b))
+            bw.append(0.0)
+        fw, bw = fw[1:], bw[1:]
+        for e in engines:
+            e.sync()
+        same = all(torch.equal(e.state()["v"], v) for e, v in zip(engines, v_eager))
+        print(f"graph replay: V equal to the eager run: {same}", file=sys.stderr)
+        if not same:
+            sys.exit("graph replay differs from the eager run")
+    for _ in range(0 if graph else args.reps):
         f, b = once()
         fw.append(f)
         bw.append(b)

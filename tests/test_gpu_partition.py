@@ -212,3 +212,54 @@ def test_partition_api_rules():
             e0.import_spikes(own)          # own spikes are not remote
     with pytest.raises(ConfigurationError, match="fraction bits"):
         e0.set_frac_bits(e0.frac_bits + 1)
+
+
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_peer_partitions_in_one_cuda_graph_equal_eager(concurrent):
+    """The peer-exchange forward + reverse has no host synchronisation inside
+    (forward/backward with sync=False), so the whole sequence — every
+    window's launches on every partition's stream and the CUDA events that
+    order them — is captured in one CUDA graph.  Two replays give exactly the
+    eager run's state and gradients (scripts/c5_partitioned.py --graph)."""
+    import torch
+    from paper_2512_05906_b200.engine import Engine
+    B, T, P = 1, 200, 4        # one trial: each edge gets at most one gradient term per phase (bitwise)
+    net, mask, amp = _problem(B=B, T=T, seed=13)
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    engines, ranges = [], []
+    for r in range(P):
+        lo, hi = split_range(net.n, P, r)
+        rp, cl, w, d, eid = partition_csr(net.rowptr, net.col, net.weight, net.delay, lo, hi)
+        e = Engine(hi - lo, B, T, precision=32, partition=(net.n, lo),
+                   max_ctas=(2 * sm) // P if concurrent else 0, stream=torch.cuda.Stream() if concurrent else None)
+        e.set_network(rp, cl, w, d)
+        e.set_drive(slice_mask(mask, net.n, lo, hi), amp[lo:hi])
+        engines.append(e)
+        ranges.append((lo, hi))
+    pn = PartitionedNetwork(engines, range(P), PeerTransport(P), window=4)
+
+    def vbars():
+        return [(2.0 * (e.state()["v"].double() - 0.25)).to(torch.float32) for e in engines]
+
+    pn.forward(T)
+    pn.join()
+    v_ref = [e.state()["v"].clone() for e in engines]
+    g_ref = [tuple(x.clone() for x in g[:2]) for g in pn.backward(vbars(), want_amp=False)]
+    pn.join()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cap = torch.cuda.current_stream()
+        pn.forward(T, sync=False)
+        pn.join(cap)
+        grads = pn.backward(vbars(), want_amp=False, sync=False)
+        pn.join(cap)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        for e in engines:
+            e.sync()
+        for e, v in zip(engines, v_ref):
+            assert torch.equal(e.state()["v"], v)
+        for (gw, gd, _), (rw, rd) in zip(grads, g_ref):
+            assert torch.equal(gw, rw) and torch.equal(gd, rd)
