@@ -308,3 +308,36 @@ class PartitionedNetwork:
             for e, r in zip(self.engines, self.ranks):
                 e.add_spike_adjoints(lo_prev, route_adjoints(partials, counts, r))
         return grads
+
+
+class GraphedPass:
+    """One partitioned forward + reverse (peer exchange) captured as a single
+    CUDA graph: every window's launches on every partition's stream and the
+    events that order them are recorded once; `replay()` re-runs the whole
+    pass with no per-launch host work (scripts/c5_partitioned.py --graph;
+    equal to the eager pass, tests/test_gpu_partition.py).
+
+    v_bar_fn(engines) -> list of dL/dV per partition, computed on the device
+    from the forward's final state (it is captured too).  The returned
+    gradient buffers belong to the graph and are overwritten by each replay."""
+
+    def __init__(self, pn: "PartitionedNetwork", t_steps: int, v_bar_fn, want_amp: bool = False):
+        if not pn.peer:
+            raise ValueError("graph capture needs the peer exchange (PeerTransport)")
+        self.pn = pn
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            cap = torch.cuda.current_stream()
+            pn.forward(t_steps, sync=False)
+            pn.join(cap)
+            self.grads = pn.backward(v_bar_fn(pn.engines), want_amp=want_amp, sync=False)
+            pn.join(cap)
+
+    def replay(self, sync: bool = False):
+        """Run the captured pass on the current stream; sync=True waits and
+        raises any device error of the windows."""
+        self.graph.replay()
+        if sync:
+            for e in self.pn.engines:
+                e.sync()
+        return self.grads

@@ -52,7 +52,7 @@ def main():
 
     from paper_2512_05906_b200 import workload as wl
     from paper_2512_05906_b200.engine import Engine
-    from paper_2512_05906_b200.partition import (DistTransport, LocalTransport, PartitionedNetwork, PeerTransport,
+    from paper_2512_05906_b200.partition import (DistTransport, GraphedPass, LocalTransport, PartitionedNetwork, PeerTransport,
                                                  min_delay_steps, partition_csr, slice_mask, split_range)
 
     rank = int(os.environ.get("RANK", "0"))
@@ -118,14 +118,7 @@ def main():
     graph = args.graph and world == 1 and args.exchange == "peer"
     if graph:
         v_eager = [e.state()["v"].clone() for e in engines]
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            cap = torch.cuda.current_stream()
-            pn.forward(args.steps, sync=False)
-            pn.join(cap)
-            vb = [(2.0 * (e.state()["v"].double() - 0.25)).to(e.dtype) for e in engines]
-            pn.backward(vb, want_amp=False, sync=False)
-            pn.join(cap)
+        g = GraphedPass(pn, args.steps, lambda es: [(2.0 * (e.state()["v"].double() - 0.25)).to(e.dtype) for e in es])
         for _ in range(args.reps + 1):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)

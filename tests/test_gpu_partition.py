@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 from paper_2512_05906_b200 import workload as wl
-from paper_2512_05906_b200.partition import (LocalTransport, PartitionedNetwork, PeerTransport, min_delay_steps,
+from paper_2512_05906_b200.partition import (GraphedPass, LocalTransport, PartitionedNetwork, PeerTransport, min_delay_steps,
                                              partition_csr, slice_mask, split_range)
 
 pytestmark = pytest.mark.gpu
@@ -247,18 +247,9 @@ def test_peer_partitions_in_one_cuda_graph_equal_eager(concurrent):
     g_ref = [tuple(x.clone() for x in g[:2]) for g in pn.backward(vbars(), want_amp=False)]
     pn.join()
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        cap = torch.cuda.current_stream()
-        pn.forward(T, sync=False)
-        pn.join(cap)
-        grads = pn.backward(vbars(), want_amp=False, sync=False)
-        pn.join(cap)
+    gp = GraphedPass(pn, T, lambda es: vbars())
     for _ in range(2):
-        g.replay()
-        torch.cuda.synchronize()
-        for e in engines:
-            e.sync()
+        grads = gp.replay(sync=True)
         for e, v in zip(engines, v_ref):
             assert torch.equal(e.state()["v"], v)
         for (gw, gd, _), (rw, rd) in zip(grads, g_ref):
