@@ -216,6 +216,15 @@ for p in $PARTS; do
       for cfg in "--config C4 --trials 4" "--config C4 --trials 4 --kind binaryheap --capacity 16" ""; do
         bash scripts/ab_env.sh "$cfg" base=$L=- f256=scratch_lib/f256.so=- f224=scratch_lib/f224.so=- f192=scratch_lib/f192.so=-
       done 2>&1 | tee gpurun_out/${TAG}_absplit.txt ;;
+    ncuadm)
+      timeout 1200 /usr/local/cuda/bin/ncu --set full --import-source on --clock-control none -k regex:"k_forward" -s 1 -c 1 \
+        -o gpurun_out/${TAG}_adm -f python bench.py --config C4 --trials 4 --kind binaryheap --capacity 16 --steps 1 --warmup 3 --no-cpu --no-variants > gpurun_out/${TAG}_ncu_adm.log 2>&1
+      echo "ncu adm rc=$?" ;;
+    abfbits)
+      L=paper_2512_05906_b200/lib/libeventq_b200.so
+      for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32" "--config C2 --trials 32 --kind binaryheap --capacity 64"; do
+        for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- fbits=$L=-; done
+      done 2>&1 | tee gpurun_out/${TAG}_abfbits.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
