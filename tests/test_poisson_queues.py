@@ -75,3 +75,17 @@ def test_sweeps_and_records():
     assert txt.splitlines()[0].startswith("workload,kind,capacity,max_delay,batch,lambda")
     recs = sweep("pressure", [0.5, 1.0], "fiforing", base, capacity=2, reps=3, warmup=1)
     assert [r.delay_steps for r in recs] == [10, 20]
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_criterion_4_drop_rates():
+    """pkg/tests/test_acceptance.py:167-209 on the GPU queues, with the values the
+    reference's own run printed (pkg/test_output.txt:20-24): DoNothing drops
+    everything, a lossless Ring nothing, FIFORing[4] at queue pressure 0.5
+    (lambda 400, delay 200 steps, 10^6 steps, seed 0) 1.99e-03 over 2511 spikes."""
+    from paper_2512_05906_b200.poisson import measure_drop_rate
+    assert measure_drop_rate("donothing", 400.0, 80, 200_000, 0).drop_rate == 1.0
+    assert measure_drop_rate("ring", 400.0, 80, 200_000, 0, capacity=80).drop_rate == 0.0
+    fifo = measure_drop_rate("fiforing", 400.0, 200, 1_000_000, 0, capacity=4)
+    assert fifo.spikes_in == 2511
+    assert f"{fifo.drop_rate:.2e}" == "1.99e-03"
