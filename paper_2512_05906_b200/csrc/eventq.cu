@@ -155,6 +155,8 @@ struct eq_handle {
   int* fl_cnt = nullptr;        // [2][G]
   int* lpos = nullptr;          // [3][total]
   int2* csc = nullptr;          // [E] {x, source} by target, ascending x
+  unsigned long long csc_fp[2] = {0, 0};   // topology fingerprint the CSC was built for
+  long long csc_E = -1;
   int2* slots = nullptr;        // [2][total][kAdmSlots]
   int adm_slots = kAdmSlots;    // eq_debug_set_admission_slots
   int* cring = nullptr;         // [B][R][N] counts of the DRAM ring rows
@@ -338,6 +340,26 @@ __global__ void k_pack_edges(const int32_t* col, const T* w, const T* d, long lo
     e.d = d[x];
     e.code = cd;
     out[x] = e;
+  }
+}
+
+// Topology fingerprint of a CSR column array: sum of (x+1)*col[x] and of
+// col[x]*col[x] (wrapping): the admission kinds rebuild their CSC only when it
+// changes (set_network runs every training step with new weights and delays).
+__global__ void k_col_fingerprint(const int32_t* col, long long n, unsigned long long* out) {
+  unsigned long long a = 0, b = 0;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long c = (unsigned long long)(unsigned)col[x];
+    a += (unsigned long long)(x + 1) * (c + 1);
+    b += (c + 7) * (c + 7);
+  }
+  for (int off = 16; off; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, a);
+    atomicAdd(out + 1, b);
   }
 }
 
@@ -1198,7 +1220,8 @@ int ensure_chunks(eq_handle* h, int steps_needed) {
 // horizon*(n-1)+1`, network.py:327); the physical array is min(that, the
 // lossless bound max_j sum_{e->j}(ceil(d_e/dt)+1)), which cannot change any
 // accept decision because occupancy never exceeds the bound.
-int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStream_t s) {
+int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStream_t s,
+                  const unsigned long long* col_fp) {
   const eq_config& c = h->cfg;
   const int N = c.n_neurons, B = c.n_trials;
   const long long E = h->E;
@@ -1216,8 +1239,13 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
     EQ_CUDA(h, ensure(h, (void**)&h->lpos, (size_t)3 * h->total * sizeof(int)));
     EQ_CUDA(h, ensure(h, (void**)&h->cring, (size_t)B * h->R * N * sizeof(int)));
     EQ_CUDA(h, ensure(h, (void**)&h->slots, (size_t)2 * h->total * kAdmSlots * sizeof(int2)));
+    h->drop_cap = ((long long)h->log_cap * h->maxdeg + 31) / 32 * 32;
+    EQ_CUDA(h, ensure(h, (void**)&h->drop_bits, (size_t)h->drop_cap / 8));
     // CSC: in-edge segments by exclusive scan of the in-degree, then the edge
-    // indices stably sorted by target (ascending x within a target)
+    // indices stably sorted by target (ascending x within a target).  Only the
+    // topology matters: unchanged (same edge count and column fingerprint, the
+    // usual case of a training step with new weights and delays) -> kept.
+    if (h->csc && h->csc_E == E && h->csc_fp[0] == col_fp[0] && h->csc_fp[1] == col_fp[1]) return EQ_OK;
     size_t tmp_bytes = 0;
     void* tmp = nullptr;
     EQ_CUDA(h, ensure(h, (void**)&h->csc_off, (size_t)(N + 1) * sizeof(long long)));
@@ -1249,8 +1277,9 @@ int setup_bounded(eq_handle* h, const int* indeg, long long occ_bound, cudaStrea
     release(h, xin);
     release(h, xout);
     release(h, kout);
-    h->drop_cap = ((long long)h->log_cap * h->maxdeg + 31) / 32 * 32;
-    EQ_CUDA(h, ensure(h, (void**)&h->drop_bits, (size_t)h->drop_cap / 8));
+    h->csc_E = E;
+    h->csc_fp[0] = col_fp[0];
+    h->csc_fp[1] = col_fp[1];
     return EQ_OK;
   }
   size_t qbytes = (size_t)B * N * h->cap * (c.precision == 32 ? sizeof(QEv<float>) : sizeof(QEv<double>));
@@ -1426,9 +1455,9 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   EQ_CUDA(h, ensure(h, &h->ns_insum, (size_t)N * sizeof(long long)));
   EQ_CUDA(h, ensure(h, &h->ns_inocc, (size_t)N * sizeof(long long)));
   EQ_CUDA(h, ensure(h, &h->ns_indeg, (size_t)(N + 1) * sizeof(int)));   // +1: exclusive scan reads n+1
-  EQ_CUDA(h, ensure(h, &h->ns_stats, 6 * sizeof(long long)));
+  EQ_CUDA(h, ensure(h, &h->ns_stats, 8 * sizeof(long long)));
   void *insum = h->ns_insum, *stats = h->ns_stats, *inocc = h->ns_inocc, *indeg = h->ns_indeg;
-  long long init[6] = {1, -1LL, 0, 0, 1, 0};
+  long long init[8] = {1, -1LL, 0, 0, 1, 0, 0, 0};
   init[1] = (long long)~0ULL;
   EQ_CUDA(h, cudaMemsetAsync(insum, 0, (size_t)N * sizeof(long long), s));
   EQ_CUDA(h, cudaMemsetAsync(inocc, 0, (size_t)N * sizeof(long long), s));
@@ -1446,8 +1475,9 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   k_max_ll<<<256, 256, 0, s>>>((const long long*)insum, N, (long long*)stats + 2);
   k_max_ll<<<256, 256, 0, s>>>((const long long*)inocc, N, (long long*)stats + 3);
   k_max_ll<<<256, 256, 0, s>>>((const int*)indeg, N, (long long*)stats + 5);
-  h->launches += 4;
-  long long st[6];
+  k_col_fingerprint<<<296, 256, 0, s>>>(col, n_edges, (unsigned long long*)stats + 6);
+  h->launches += 5;
+  long long st[8];
   EQ_CUDA(h, cudaMemcpyAsync(st, stats, sizeof st, cudaMemcpyDeviceToHost, s));
   EQ_CUDA(h, cudaStreamSynchronize(s));
 
@@ -1573,7 +1603,7 @@ int eq_set_network(eq_handle* h, const int64_t* rowptr, const int32_t* col, cons
   }
   EQ_CUDA(h, ensure(h, &h->lam, (size_t)c.n_trials * h->R * N * 2 * h->tsize));
   if (h->bounded) {
-    int rc = setup_bounded(h, (const int*)indeg, st[3], s);
+    int rc = setup_bounded(h, (const int*)indeg, st[3], s, reinterpret_cast<const unsigned long long*>(st + 6));
     if (rc) return rc;
   }
   h->net_set = true;

@@ -313,3 +313,24 @@ def test_fifo_homogeneous_delay_on_and_off_the_step_grid(delay_steps, impl):
     out = eng.forward()
     _assert_forward_equal(eng, out, ref)
     assert eng.counters()[:, 2].sum() > 0
+
+
+def test_admission_csc_follows_the_topology_across_set_network():
+    """The admission kinds keep their CSC across set_network calls while the
+    topology is unchanged (training steps change weights and delays only) and
+    rebuild it when the columns change — two networks with the same edge count,
+    then the first network's weights rescaled: each run = oracle, drops included."""
+    B, T, n = 2, 200, 800
+    mask = wl.drive_masks(n, B, T, 1e-3, seed0=5)
+    amp = np.full(n, 12.0)
+    net_a = wl.random_network(n, 30, 51, delay_steps=(1, 10), w_mean=0.04, w_std=0.01)
+    net_b = wl.random_network(n, 30, 52, delay_steps=(1, 10), w_mean=0.04, w_std=0.01)
+    assert net_a.n_edges == net_b.n_edges and not np.array_equal(net_a.col, net_b.col)
+    net_c = wl.Network(net_a.n, net_a.rowptr, net_a.col, net_a.weight * 1.1, net_a.delay)
+    eng = _engine(net_a, mask, amp, B, T, 32, kind="binaryheap", capacity=3)
+    for net in (net_a, net_b, net_c, net_a):
+        eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+        out = eng.forward()
+        s = _oracle(net, mask, amp, B, T, 32, eng.frac_bits, kind="binaryheap", capacity=3)
+        _assert_forward_equal(eng, out, s.forward())
+        assert eng.counters()[:, 2].sum() > 0
