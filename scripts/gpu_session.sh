@@ -225,6 +225,10 @@ for p in $PARTS; do
       for cfg in "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32" "--config C2 --trials 32 --kind binaryheap --capacity 64"; do
         for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- fbits=$L=-; done
       done 2>&1 | tee gpurun_out/${TAG}_abfbits.txt ;;
+    abpfe)
+      for cfg in "" "--config C4 --trials 4" "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C2 --trials 32"; do
+        for r in 1 2; do bash scripts/ab_env.sh "$cfg" base=scratch_lib/base.so=- pf=scratch_lib/pf.so=-; done
+      done 2>&1 | tee gpurun_out/${TAG}_abpfe.txt ;;
     abev)
       for cfg in "--config C2 --trials 32 --kind binaryheap --capacity 64" "--config C3 --trials 16 --kind binaryheap --capacity 64" \
                  "--config C4 --trials 4 --kind binaryheap --capacity 16" "--config C4 --trials 4 --kind sortedarray --capacity 32"; do
