@@ -189,3 +189,24 @@ def test_autograd_function_gradients():
         w2 = (w - 1e-3 * w.grad / w.grad.abs().max()).detach()
     v2 = RSNNFunction.apply(w2, d.detach(), a.detach(), eng, rp, cl, mask)
     assert float(((v2 - 0.25) ** 2).sum()) < float(loss)
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src"), reason="reference not mounted")
+def test_gradcheck_sampling_and_error_rule_equal_the_reference():
+    """paper_2512_05906_b200.gradcheck mirrors eventq.gradcheck: the same random
+    directions for the same Generator, and the same relative-error rule
+    (ensemble floor) on the same (jvp, fd) pairs."""
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import eventq.gradcheck as ref
+    from paper_2512_05906_b200 import gradcheck as ours
+    a = ours.sample_directions(10, 40, np.random.default_rng(11))
+    b = ref.sample_directions(10, 40, np.random.default_rng(11))
+    assert [(d.param, d.i, d.j) for d in a] == [(d.param, d.i, d.j) for d in b]
+    pairs = [(0.5, 0.49), (1e-4, 3e-4), (-0.2, -0.21), (0.01, 0.0)]
+    mk = lambda m: [m.DirectionCheck(None, j, f, None, 1e-3, "ok") for j, f in pairs] + \
+        [m.DirectionCheck(None, 9.0, None, None, 1e-3, "non-smooth")]
+    x, y = mk(ours), mk(ref)
+    ours._fill_relative_errors(x)
+    ref._fill_relative_errors(y)
+    assert [c.rel_err for c in x] == [c.rel_err for c in y]
+    assert ours.direction_epsilon(a[1], small(), 1e-3, 4.0) == ref.direction_epsilon(b[1], small(), 1e-3, 4.0)
