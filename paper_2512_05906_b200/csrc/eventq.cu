@@ -38,9 +38,9 @@ constexpr int kSplitF = EQ_SPLIT_F32;  // forward event-side threads per CTA (me
 #endif
 constexpr int kSplitB = EQ_SPLIT_B32;  // reverse event-side threads per CTA (measured: 224..448, profiles/)
 constexpr size_t kStateSmem = 72 * 1024;   // forward state in shared memory up to this size per CTA
-// fp64: the neuron side is the slower one (scalar paths, 16-byte slots), so it gets more threads
+// fp64 warp-group splits (event side / neuron side), measured per pass
 #ifndef EQ_SPLIT_F64
-#define EQ_SPLIT_F64 288
+#define EQ_SPLIT_F64 320   // fp64 forward event-side threads: 288 -> 320: fwd 76.5-77.1 -> 76.1-76.2 ms (profiles/r2bd_ab_fp64_split.txt)
 #endif
 #ifndef EQ_SPLIT_B64
 #define EQ_SPLIT_B64 288   // 256 -> 288 with EV 2: fp64 bwd 59.6-61.1 -> 59.1 ms (profiles/r1h_ab_4.txt)
