@@ -43,7 +43,7 @@ constexpr size_t kStateSmem = 72 * 1024;   // forward state in shared memory up 
 #define EQ_SPLIT_F64 320   // fp64 forward event-side threads: 288 -> 320: fwd 76.5-77.1 -> 76.1-76.2 ms (profiles/r2bd_ab_fp64_split.txt)
 #endif
 #ifndef EQ_SPLIT_B64
-#define EQ_SPLIT_B64 288   // 256 -> 288 with EV 2: fp64 bwd 59.6-61.1 -> 59.1 ms (profiles/r1h_ab_4.txt)
+#define EQ_SPLIT_B64 320   // 256 -> 288 with EV 2: fp64 bwd 59.6-61.1 -> 59.1 ms (profiles/r1h_ab_4.txt); 288 -> 320: 60.9 -> 60.2 ms (profiles/r2bf_ab_fp64_reverse_split.txt)
 #endif
 template <typename T> constexpr int split_f() { return sizeof(T) == 4 ? kSplitF : EQ_SPLIT_F64; }
 template <typename T> constexpr int split_b() { return sizeof(T) == 4 ? kSplitB : EQ_SPLIT_B64; }
