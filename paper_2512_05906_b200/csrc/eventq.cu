@@ -30,9 +30,17 @@ constexpr int kNT = 512;   // threads per CTA of the persistent kernels
 constexpr int kErrWords = 8;  // device error word: [0] code, [1] step, [2] trial, [3] neuron, [4] step reached
 constexpr int kU = 4;      // neurons per thread in flight per round
 #ifndef EQ_SPLIT_F32
-#define EQ_SPLIT_F32 288
+#define EQ_SPLIT_F32 320
 #endif
-constexpr int kSplitF = EQ_SPLIT_F32;  // forward event-side threads per CTA (measured: 224..384, profiles/)
+#ifndef EQ_SPLIT_F32_HBM
+#define EQ_SPLIT_F32_HBM 288
+#endif
+// forward event-side threads per CTA (fp32): 320 with the neuron state in shared
+// memory and for the admission kinds, 288 for the ring with its state in HBM
+// (the neuron side is heavier there): C3 x 24 fwd 32.62 -> 32.13 ms, C4 ring
+// 76.10 at 288 vs 77.34 at 320 (profiles/r2bi_ab_fp32_split.txt)
+constexpr int kSplitF = EQ_SPLIT_F32;
+constexpr int kSplitFHbm = EQ_SPLIT_F32_HBM;
 #ifndef EQ_SPLIT_B32
 #define EQ_SPLIT_B32 352
 #endif
@@ -46,6 +54,7 @@ constexpr size_t kStateSmem = 72 * 1024;   // forward state in shared memory up 
 #define EQ_SPLIT_B64 320   // 256 -> 288 with EV 2: fp64 bwd 59.6-61.1 -> 59.1 ms (profiles/r1h_ab_4.txt); 288 -> 320: 60.9 -> 60.2 ms (profiles/r2bf_ab_fp64_reverse_split.txt)
 #endif
 template <typename T> constexpr int split_f() { return sizeof(T) == 4 ? kSplitF : EQ_SPLIT_F64; }
+template <typename T> constexpr int split_f_hbm() { return sizeof(T) == 4 ? kSplitFHbm : EQ_SPLIT_F64; }
 template <typename T> constexpr int split_b() { return sizeof(T) == 4 ? kSplitB : EQ_SPLIT_B64; }
 
 
@@ -996,6 +1005,7 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
       EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kNT, st_bytes));
       if ((long long)occ * h->n_sm >= h->G) dyn = st_bytes;
     }
+    if (!h->adm && dyn == 0) kf = (const void*)k_forward<T, kNT, kU, split_f_hbm<T>()>;   // state in HBM
     FwdArgs<T>* ap = &A;
     ap->smem_state = dyn > 0;
     EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, dyn, s));
@@ -1152,6 +1162,12 @@ int setup_geometry(eq_handle* h) {
     kb = (const void*)k_backward<double, kNT, kU, split_b<double>()>;
   }
   EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kf, kNT, 0));
+  if (h->cfg.precision == 32) {   // the state-in-HBM split of the ring kernel too
+    int occ_h = 0;
+    EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, (const void*)k_forward<float, kNT, kU, kSplitFHbm>,
+                                                             kNT, 0));
+    occ_f = std::min(occ_f, occ_h);
+  }
   {
     int occ_a = 0;
     const void* ka = h->cfg.precision == 32 ? (const void*)k_forward<float, kNT, kU, kSplitF, true>
@@ -2139,7 +2155,7 @@ int eq_run_window(eq_handle* h, int32_t w, int32_t a_prev, int32_t n_steps, void
     EQ_CUDA(h, cudaMemsetAsync(h->bar, 0, kBarWords * sizeof(unsigned), s));
     EQ_CUDA(h, cudaMemsetAsync(h->step_start + h->steps_done + 1, 0xFF, (size_t)n_steps * sizeof(long long), s));
     void* args[] = {&A};
-    const void* kf = (const void*)k_forward<T, kNT, kU, split_f<T>()>;
+    const void* kf = (const void*)k_forward<T, kNT, kU, split_f_hbm<T>()>;   // state in HBM
     EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, 0, s));
     h->launches += 1;
     h->steps_done += n_steps;
