@@ -37,7 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
-TRAFFIC_FILE = "r2n_traffic.json"   # DRAM bytes per launch from the committed ncu capture of the default workload
+TRAFFIC_FILE = "r2bl_traffic.json"   # DRAM bytes per launch from the committed ncu capture of the default workload
 
 
 def read_peaks():
