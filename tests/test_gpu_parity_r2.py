@@ -334,3 +334,29 @@ def test_admission_csc_follows_the_topology_across_set_network():
         s = _oracle(net, mask, amp, B, T, 32, eng.frac_bits, kind="binaryheap", capacity=3)
         _assert_forward_equal(eng, out, s.forward())
         assert eng.counters()[:, 2].sum() > 0
+
+
+@pytest.mark.parametrize("kind,cap,refractory", [("binaryheap", 8, 0), ("sortedarray", 8, 3), ("fiforing", 6, 2)])
+def test_admission_fp64_c2_size_with_refractory_bitwise(kind, cap, refractory):
+    """The admission path in fp64 at C2 size (10k neurons, K = 100, two trials;
+    FIFO with one on-grid delay), with refractory neurons: raster, state, pending
+    queues and drops bitwise = the fp64 device-mode oracle, reverse pass within
+    1e-12 of the gradient scale."""
+    delays = (32, 32) if kind == "fiforing" else (1, 64)
+    net = wl.random_network(10_000, 100, 0, delay_steps=delays)
+    B, T = 2, 400
+    mask = wl.drive_masks(10_000, B, T, 1e-3, seed0=1000)
+    amp = np.full(10_000, 12.0)
+    from paper_2512_05906_b200.engine import Engine
+    eng = Engine(net.n, B, T, kind=kind, capacity=cap, precision=64,
+                 lif=wl.LIFConfig(refractory_steps=refractory))
+    eng.set_network(net.rowptr, net.col, net.weight, net.delay)
+    eng.set_drive(mask, amp)
+    out = eng.forward()
+    s = OracleSession(n=net.n, n_trials=B, t_steps=T, kind=kind, mode="device", precision=64,
+                      frac_bits=eng.frac_bits, capacity=cap, refractory_steps=refractory)
+    s.set_network(net.rowptr, net.col, net.weight, net.delay)
+    s.set_drive(mask, amp)
+    _assert_forward_equal(eng, out, s.forward())
+    assert eng.counters()[:, 2].sum() > 0
+    _assert_reverse(eng, s, out, B)
