@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(NT) k_adm_fixup(FwdArgs<T> A) {
 // events.  Executed by the event-side warp group.
 constexpr int kDropTr = 64;   // per-trial drop counts of a phase's admissions kept in smem
 
-template <typename T, int NT, int NF, bool kImp, bool kAdm = false>
+template <typename T, int NT, int NF, bool kImp, bool kAdm = false, int kAdmEv = 2>
 __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, const int cta, const int gtid,
                                            const long long s0, const long long s1, SpikeRec<T>* s_spk,
                                            long long* s_r0, int* s_pre, int* s_bin, unsigned* s_drop = nullptr) {
@@ -592,10 +592,7 @@ __device__ __forceinline__ void fwd_fanout(const FwdArgs<T>& A, const int m, con
 #ifndef EQ_FWD_EV
 #define EQ_FWD_EV 3
 #endif
-#ifndef EQ_ADM_EV
-#define EQ_ADM_EV 2
-#endif
-    constexpr int EV = kAdm ? EQ_ADM_EV : EQ_FWD_EV;
+    constexpr int EV = kAdm ? kAdmEv : EQ_FWD_EV;
     int krow = 0;                                          // row of this thread's last event
     for (int f0 = gtid; f0 < total; f0 += EV * Ro::NF) {
       int jj[EV], kk[EV];
@@ -1175,7 +1172,10 @@ __device__ __forceinline__ bool pause_due(const FwdArgs<T>& A, int m) {
   return ld_published(A.step_start + m + 1) + A.total > A.log_cap;
 }
 
-template <typename T, int NT, int U, int NF = NT / 2, bool kAdm = false>
+// kAdmEv: admission events in flight per thread — 2, or 1 when the neuron state
+// stays in HBM (C4 heap[16] fwd 129.5 -> 127.2-128.3 ms; C2, state in shared
+// memory, prefers 2: profiles/r2bo_ab_admission_ev_split320.txt)
+template <typename T, int NT, int U, int NF = NT / 2, bool kAdm = false, int kAdmEv = 2>
 __global__ void __launch_bounds__(NT, 2) k_forward(const __grid_constant__ FwdArgs<T> A) {
   // (__grid_constant__: the out-of-line admission fix-ups take A by reference
   // without a local copy)
@@ -1255,7 +1255,7 @@ __global__ void __launch_bounds__(NT, 2) k_forward(const __grid_constant__ FwdAr
       if (A.cal && m > A.m0) {
         const int me = m - 1;                          // emitting step
         const long long L0 = ld_published(A.step_start + me), S = ld_published(A.step_start + me + 1) - L0;
-        fwd_fanout<T, NT, NF, false, kAdm>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G, s_spk,
+        fwd_fanout<T, NT, NF, false, kAdm, kAdmEv>(A, m, cta, gtid, L0 + S * cta / A.G, L0 + S * (cta + 1) / A.G, s_spk,
                                            s_r0, s_pre, s_bin, s_drop);
       }
       if (m < m1) tl_mark(A.tl, m, A.G, cta, 1);

@@ -1005,7 +1005,10 @@ int launch_forward_once(eq_handle* h, int n_steps, void* v_trace, cudaStream_t s
       EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kNT, st_bytes));
       if ((long long)occ * h->n_sm >= h->G) dyn = st_bytes;
     }
-    if (!h->adm && dyn == 0) kf = (const void*)k_forward<T, kNT, kU, split_f_hbm<T>()>;   // state in HBM
+    if (dyn == 0) {   // state in HBM: the ring's 288-thread event side; fp32 admission: one event in flight
+      if (!h->adm) kf = (const void*)k_forward<T, kNT, kU, split_f_hbm<T>()>;
+      else if (sizeof(T) == 4) kf = (const void*)k_forward<T, kNT, kU, split_f<T>(), true, 1>;
+    }
     FwdArgs<T>* ap = &A;
     ap->smem_state = dyn > 0;
     EQ_CUDA(h, cudaLaunchCooperativeKernel(kf, dim3(h->G), dim3(kNT), args, dyn, s));
@@ -1173,6 +1176,10 @@ int setup_geometry(eq_handle* h) {
     const void* ka = h->cfg.precision == 32 ? (const void*)k_forward<float, kNT, kU, kSplitF, true>
                                             : (const void*)k_forward<double, kNT, kU, split_f<double>(), true>;
     EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, ka, kNT, 0));
+    occ_f = std::min(occ_f, occ_a);
+    const void* ka1 = h->cfg.precision == 32 ? (const void*)k_forward<float, kNT, kU, kSplitF, true, 1>
+                                             : (const void*)k_forward<double, kNT, kU, split_f<double>(), true, 1>;
+    EQ_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, ka1, kNT, 0));
     occ_f = std::min(occ_f, occ_a);
   }
   {
