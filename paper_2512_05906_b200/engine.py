@@ -25,8 +25,15 @@ def _ptr(t: Optional[torch.Tensor]):
 class Engine:
     """Batched R-SNN simulation of ``n_trials`` trials sharing one network.
 
-    Mirrors ``build_rsnn`` + ``simulate`` (network.py:201-497) for the ring and
-    donothing kinds, plus the reverse pass (``backward``) the reference lacks.
+    Mirrors ``build_rsnn`` + ``simulate`` (network.py:201-497) for every
+    network kind (ring, lossyring, fiforing, binaryheap, sortedarray,
+    donothing), plus the reverse pass (``backward``) the reference lacks.
+
+    staged_queues selects the bounded-kind implementation (same results):
+    0 = by admission on the calendar (default; heap, sorted, and FIFO with its
+    delay on the step grid), 1 = shared-memory staged queues, 2 = HBM-resident
+    queue structures.  max_ctas caps the persistent grid (partitions sharing a
+    GPU); stream = a private stream (ordered after the caller's current one).
     """
 
     def __init__(self, n: int, n_trials: int, t_steps: int, *, kind: str = "ring",
